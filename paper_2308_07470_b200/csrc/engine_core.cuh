@@ -1,0 +1,669 @@
+// engine_core.cuh -- the per-sub-cluster "live-event chain" of the B200
+// scheduler engine.
+//
+// The reference (batchsym simulator.py:191-272) pushes one heap entry per
+// candidate change (~1 per arrival) and discards 92-97 % of them as stale.
+// This engine never materialises stale entries.  Each model keeps at most one
+// live model timer, one live drop timer and its unabsorbed arrival suffix;
+// arrivals of a model that is not registered at the rank plane only touch that
+// model, so they are absorbed *locally* (ahead of global time) until the
+// model's next event that reads or writes shared state.  Only those "chain
+// events" -- live model-timer pops, live drop-timer pops, the live GPU timer,
+// and arrivals of registered models -- are ordered globally.
+//
+// Exact ordering.  The reference orders heap entries by (tick, prio, seq)
+// where seq is a global push counter, and merges arrival i when no entry with
+// (tick, prio) <= (a_i, 4) remains (simulator.py:210).  We replace seq by an
+// order-isomorphic key that can be computed without a global counter:
+//   A   = number of arrivals processed before the event.  Processing order is
+//         non-decreasing in (tick, A); an event pushed at an earlier tick has
+//         A = L(tick) (#arrivals strictly before tick), stored canonically as
+//         BASE (-1); an event pushed during a same-tick cascade inherits the
+//         explicit A of its pusher (> L(tick)).
+//   pusher position (tp, ap, sub): the processing position of the event that
+//         pushed it.  Chain events take sub = a chain counter (monotone in
+//         processing order); arrival g takes (a_g, A'_g, +inf) because it is
+//         processed after every chain event at (a_g, A'_g).
+// Two live events compare by (tick, A', prio, tp, ap, sub); DESIGN.md §3
+// proves this is the reference's pop order among live events.
+//
+// Everything here is __host__ __device__ so tools/hostcheck can run the exact
+// same chain on the CPU against the oracle while iterating; the product only
+// ever runs it inside the CUDA kernels of engine.cu.
+#pragma once
+#include <stdint.h>
+
+#ifndef SYM_HD
+#ifdef __CUDACC__
+#define SYM_HD __host__ __device__ __forceinline__
+#else
+#define SYM_HD inline
+#endif
+#endif
+
+namespace sym {
+
+constexpr int64_t NEG_INF = -(int64_t(1) << 62);  // units.py:17
+constexpr int64_t OUTSTANDING = -1;               // scheduler.py:41
+constexpr int64_t FREE_SENTINEL = INT64_MAX;      // leaf absent from an index
+constexpr int32_t A_BASE = -1;                    // canonical "A = L(tick)"
+constexpr int64_t SUB_ARRIVAL = INT64_MAX;        // arrival pusher sub-rank
+
+enum : int32_t { PR_GPU = 1, PR_MODEL = 2, PR_DROP = 3, PR_ARRIVAL = 4 };
+enum : int32_t { EV_NONE = 0, EV_MT = 1, EV_DT = 2, EV_ARR = 3 };
+enum : int32_t { K_DEFERRED = 0, K_EAGER = 1, K_TIMEOUT = 2 };
+enum : int32_t { G_PREFIX = 0, G_DROP_HEAD = 1 };
+
+struct EvKey {
+  int64_t t;    // tick
+  int64_t tp;   // pusher tick
+  int64_t sub;  // pusher sub-rank (chain counter or SUB_ARRIVAL)
+  int32_t a;    // canonical A'
+  int32_t prio;
+  int32_t ap;   // pusher A'
+  int32_t _pad;
+};
+
+SYM_HD bool key_less(const EvKey& x, const EvKey& y) {
+  if (x.t != y.t) return x.t < y.t;
+  if (x.a != y.a) return x.a < y.a;
+  if (x.prio != y.prio) return x.prio < y.prio;
+  if (x.tp != y.tp) return x.tp < y.tp;
+  if (x.ap != y.ap) return x.ap < y.ap;
+  return x.sub < y.sub;
+}
+
+// Processing position of the event currently being handled; every push made
+// while handling it is stamped with it.
+struct Pusher {
+  int64_t t;
+  int64_t sub;
+  int32_t a_self;   // A' of the pusher itself (ordering)
+  int32_t a_after;  // A' inherited by a push at the same tick
+};
+
+SYM_HD EvKey push_key(int64_t fire, int32_t prio, const Pusher& P) {
+  EvKey k;
+  k.t = fire;
+  k.a = (fire == P.t) ? P.a_after : A_BASE;
+  k.prio = prio;
+  k.tp = P.t;
+  k.ap = P.a_self;
+  k.sub = P.sub;
+  k._pad = 0;
+  return k;
+}
+
+// Static per-model parameters (ModelPlane.__init__, scheduler.py:147-164).
+struct ModelParam {
+  int64_t slo;
+  int64_t timeout_ns;   // resolved (PolicyConfig.resolve_timeout_ns)
+  int64_t base1;        // d_ctrl + d_data + l(1)
+  int32_t off;          // first position of this model in the sorted stream
+  int32_t cnt;          // arrivals of this model
+  int32_t max_batch;
+  int32_t target_batch; // min(policy.target_batch, max_batch)
+};
+
+// Mutable per-model state.
+struct ModelState {
+  int64_t c_exec, c_latest;
+  EvKey mt_key;       // live model timer (valid iff has_mt)
+  EvKey dt_key;       // live drop timer (valid iff dt_head >= 0)
+  EvKey nx_key;       // next chain event of this model
+  int64_t drops;
+  int32_t qh, qt;     // queue = positions [off+qh, off+qt)
+  int32_t has_cand, c_size;
+  int32_t c_head;     // queue position of the candidate head (head rid)
+  int32_t registered; // present in RankPlane.mc
+  int32_t has_mt;
+  int32_t dt_head;    // armed_drop_rid as a position, -1 = disarmed
+  int32_t nx_type;    // EV_*
+  int32_t _pad;
+};
+
+struct BatchRec {
+  int64_t emitted, start, finish;
+  int64_t kt, ksub;   // processing position of the granting event (trace)
+  int32_t ka;
+  int32_t model, gpu, size;
+  int32_t first;      // sorted-stream position of the first member
+  int32_t shrunk_from;// pre-grant candidate size if it shrank, else 0
+};
+
+// All arrays of one sub-cluster.  Pointers may target global or shared
+// memory; the chain is written against this view only.
+struct Shard {
+  // configuration
+  int32_t M, G, Mp, Gp;  // counts and power-of-two tree widths
+  int32_t kind, gather, record_trace, _pad;
+  int64_t d_ctrl, d_data;
+  int32_t lat_stride, _pad2;
+  const int64_t* lat;          // [M * lat_stride]
+  const ModelParam* mp;        // [M]
+  // arrivals, sorted by (model, stream order)
+  const int64_t* s_tick;       // [n] tick of sorted position p
+  const int32_t* s_g;          // [n] stream index of sorted position p
+  const int32_t* s_aself;      // [n] A' of that arrival
+  // mutable
+  ModelState* ms;              // [M]
+  int32_t* pq;                 // [2*Mp] tournament tree of models (next event)
+  int64_t* free_at;            // [G]
+  int32_t* gt;                 // [2*Gp] tournament tree, min (free_at, gid)
+  int32_t* mc_lat_tree;        // [2*Mp] min (latest, mid) over registered
+  int32_t* mc_bs_tree;         // [2*Mp] max (size, mid) over registered
+  int32_t* mc_size;            // [M]
+  int64_t* mc_latest;          // [M]
+  // GPU timer
+  int32_t gt_armed, gt_gid;
+  int64_t gt_fire;
+  EvKey gt_key;
+  // outputs
+  BatchRec* recs;
+  int64_t n_recs, rec_cap;
+  int64_t* drop_t;             // [n] by sorted position (trace only)
+  int64_t* drop_ksub;          // [n]
+  int32_t* drop_ka;            // [n]
+  // counters
+  int64_t chain_events, absorbed, n_dropped;
+  int64_t ops, evictions, registrations, handler_ops_max;
+  int32_t error;
+  int32_t _pad3;
+};
+
+enum : int32_t { ERR_NONE = 0, ERR_REC_OVERFLOW = 1, ERR_STATE = 2 };
+
+SYM_HD int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+SYM_HD int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------ trees -------
+
+// GPU index: min (free_at, gid) (scheduler.py:338, free_idx[0]).
+SYM_HD bool gpu_before(const Shard& S, int32_t x, int32_t y) {
+  if (y < 0) return x >= 0;
+  if (x < 0) return false;
+  int64_t fx = S.free_at[x], fy = S.free_at[y];
+  if (fx != fy) return fx < fy;
+  return x < y;
+}
+
+SYM_HD void gpu_tree_update(Shard& S, int32_t gid) {
+  int32_t i = S.Gp + gid;
+  S.gt[i] = (S.free_at[gid] == OUTSTANDING) ? -1 : gid;
+  for (i >>= 1; i >= 1; i >>= 1) {
+    int32_t l = S.gt[2 * i], r = S.gt[2 * i + 1];
+    S.gt[i] = gpu_before(S, r, l) ? r : l;
+  }
+}
+
+// registered candidates: min (latest, mid) and max (size, mid)
+// (scheduler.py:340-341).
+SYM_HD bool lat_before(const Shard& S, int32_t x, int32_t y) {
+  if (y < 0) return x >= 0;
+  if (x < 0) return false;
+  int64_t lx = S.mc_latest[x], ly = S.mc_latest[y];
+  if (lx != ly) return lx < ly;
+  return x < y;
+}
+SYM_HD bool bs_before(const Shard& S, int32_t x, int32_t y) {
+  if (y < 0) return x >= 0;
+  if (x < 0) return false;
+  int32_t sx = S.mc_size[x], sy = S.mc_size[y];
+  if (sx != sy) return sx > sy;
+  return x > y;
+}
+
+SYM_HD void mc_tree_update(Shard& S, int32_t mid) {
+  int32_t i = S.Mp + mid;
+  int32_t v = S.ms[mid].registered ? mid : -1;
+  S.mc_lat_tree[i] = v;
+  S.mc_bs_tree[i] = v;
+  for (i >>= 1; i >= 1; i >>= 1) {
+    int32_t l = S.mc_lat_tree[2 * i], r = S.mc_lat_tree[2 * i + 1];
+    S.mc_lat_tree[i] = lat_before(S, r, l) ? r : l;
+    l = S.mc_bs_tree[2 * i];
+    r = S.mc_bs_tree[2 * i + 1];
+    S.mc_bs_tree[i] = bs_before(S, r, l) ? r : l;
+  }
+}
+
+// model priority queue: min next chain-event key.
+SYM_HD bool model_before(const Shard& S, int32_t x, int32_t y) {
+  if (y < 0) return x >= 0 && S.ms[x].nx_type != EV_NONE;
+  if (x < 0 || S.ms[x].nx_type == EV_NONE) return false;
+  if (S.ms[y].nx_type == EV_NONE) return true;
+  return key_less(S.ms[x].nx_key, S.ms[y].nx_key);
+}
+
+SYM_HD void pq_update(Shard& S, int32_t mid) {
+  int32_t i = S.Mp + mid;
+  S.pq[i] = S.ms[mid].nx_type != EV_NONE ? mid : -1;
+  for (i >>= 1; i >= 1; i >>= 1) {
+    int32_t l = S.pq[2 * i], r = S.pq[2 * i + 1];
+    S.pq[i] = model_before(S, r, l) ? r : l;
+  }
+}
+
+// ------------------------------------------------------- ModelPlane -------
+
+SYM_HD int64_t lat_of(const Shard& S, int32_t m, int32_t b) {
+  return S.lat[(int64_t)m * S.lat_stride + (b - 1)];
+}
+SYM_HD int64_t deadline_at(const Shard& S, const ModelParam& P, int32_t q) {
+  return S.s_tick[P.off + q] + P.slo;
+}
+
+// Record one dropped head (scheduler.py:213-216, simulator.py:175-182).
+SYM_HD void drop_head(Shard& S, ModelState& st, const ModelParam& P,
+                      int64_t now, const Pusher& who) {
+  int32_t pos = P.off + st.qh;
+  st.qh += 1;
+  st.drops += 1;
+  S.n_dropped += 1;
+  if (S.record_trace) {
+    S.drop_t[pos] = now;
+    S.drop_ka[pos] = who.a_self;
+    S.drop_ksub[pos] = who.sub;
+  }
+}
+
+// scheduler.py:301-315
+SYM_HD void arm_drop_timer(Shard& S, ModelState& st, const ModelParam& P,
+                           int32_t m, int64_t now, const Pusher& who) {
+  if (st.qh == st.qt) {
+    st.dt_head = -1;
+    return;
+  }
+  if (st.qh == st.dt_head) return;
+  st.dt_head = st.qh;
+  int64_t fire = deadline_at(S, P, st.qh) - P.base1 + 1;
+  st.dt_key = push_key(imax(fire, now), PR_DROP, who);
+}
+
+// scheduler.py:277-299.  The predicate is monotone in b, so the answer is
+// unique; this is a branch-light binary search over the l(b) row.
+SYM_HD int32_t max_feasible(const Shard& S, int32_t m, int64_t now,
+                            int64_t floor, int32_t cap, int64_t d) {
+  const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
+  const int64_t dc = S.d_ctrl, dd = S.d_data;
+  if (imax(now + dc + dd, floor) + lat[0] > d) return 0;
+  int32_t lo = 1, hi = cap;
+  while (lo < hi) {
+    int32_t mid = (lo + hi + 1) >> 1;
+    if (imax(now + dc + dd * mid, floor) + lat[mid - 1] <= d)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// scheduler.py:218-275.  Returns true when the candidate changed.
+SYM_HD bool update_candidate(Shard& S, int32_t m, int64_t now,
+                             int64_t gpu_floor, const Pusher& who) {
+  ModelState& st = S.ms[m];
+  const ModelParam& P = S.mp[m];
+  while (st.qh < st.qt && now + P.base1 > deadline_at(S, P, st.qh))
+    drop_head(S, st, P, now, who);
+  if (S.kind == K_TIMEOUT) {
+    const int64_t l1 = lat_of(S, m, 1);
+    // arrival + k + l(1) > deadline  <=>  k + l(1) > slo (scheduler.py:229)
+    while (st.qh < st.qt && P.timeout_ns + l1 > P.slo)
+      drop_head(S, st, P, now, who);
+  }
+  if (S.gather == G_DROP_HEAD && st.qt - st.qh > P.target_batch) {
+    const int32_t tb = P.target_batch;
+    const int64_t need = now + S.d_ctrl + S.d_data * tb + lat_of(S, m, tb);
+    while (st.qt - st.qh > tb && need > deadline_at(S, P, st.qh))
+      drop_head(S, st, P, now, who);
+  }
+  if (st.qh == st.qt) {
+    arm_drop_timer(S, st, P, m, now, who);
+    if (st.has_cand) {
+      st.has_cand = 0;
+      return true;
+    }
+    return false;
+  }
+  const int64_t d = deadline_at(S, P, st.qh);
+  int32_t cap = st.qt - st.qh;
+  if (cap > P.max_batch) cap = P.max_batch;
+  if (S.gather == G_DROP_HEAD && cap > P.target_batch) cap = P.target_batch;
+  const int64_t pol_floor =
+      S.kind == K_TIMEOUT ? S.s_tick[P.off + st.qh] + P.timeout_ns : NEG_INF;
+  const int64_t floor2 = imax(pol_floor, gpu_floor);
+  const int32_t b = max_feasible(S, m, now, floor2, cap, d);
+  if (b == 0) {
+    arm_drop_timer(S, st, P, m, now, who);
+    if (st.has_cand) {
+      st.has_cand = 0;
+      return true;
+    }
+    return false;
+  }
+  const int64_t l_next =
+      b < P.max_batch ? lat_of(S, m, b + 1) : lat_of(S, m, P.max_batch);
+  int64_t exec_at = now + S.d_ctrl + S.d_data * b;
+  if (S.kind == K_DEFERRED && d - l_next > exec_at) exec_at = d - l_next;
+  if (floor2 > exec_at) exec_at = floor2;
+  const int64_t latest = d - lat_of(S, m, b);
+  arm_drop_timer(S, st, P, m, now, who);
+  if (st.has_cand && st.c_size == b && st.c_exec == exec_at &&
+      st.c_latest == latest && st.c_head == st.qh)
+    return false;
+  st.has_cand = 1;
+  st.c_size = b;
+  st.c_exec = exec_at;
+  st.c_latest = latest;
+  st.c_head = st.qh;
+  return true;
+}
+
+// ------------------------------------------------------- RankPlane --------
+
+SYM_HD void unregister(Shard& S, int32_t m) {  // scheduler.py:430-436
+  if (S.ms[m].registered) {
+    S.ms[m].registered = 0;
+    mc_tree_update(S, m);
+    S.ops += 2;
+  }
+}
+
+// scheduler.py:438-457
+SYM_HD void set_gpu_timer(Shard& S, int64_t now, const Pusher& who) {
+  const int32_t gid = S.gt[1];
+  const int32_t bm = S.mc_bs_tree[1];
+  if (bm < 0 || gid < 0) {
+    S.gt_armed = 0;
+    return;
+  }
+  S.ops += 2;
+  int64_t fire = S.free_at[gid] - (S.d_ctrl + S.d_data * S.mc_size[bm]);
+  if (fire < now) fire = now;
+  if (S.gt_armed && S.gt_fire == fire && S.gt_gid == gid) return;
+  S.gt_armed = 1;
+  S.gt_fire = fire;
+  S.gt_gid = gid;
+  S.gt_key = push_key(fire, PR_GPU, who);
+}
+
+// scheduler.py:354-365
+SYM_HD void inform_candidate(Shard& S, int32_t m, int64_t now,
+                             const Pusher& who) {
+  ModelState& st = S.ms[m];
+  st.has_mt = 0;  // model_gen[m] += 1
+  unregister(S, m);
+  if (st.has_cand) {
+    int64_t fire = st.c_exec - (S.d_ctrl + S.d_data * st.c_size);
+    if (fire < now) fire = now;
+    st.mt_key = push_key(fire, PR_MODEL, who);
+    st.has_mt = 1;
+  }
+}
+
+// scheduler.py:367-377 (the GPU is always OUTSTANDING here: grants resolve
+// inline, so the only caller re-inserts the granted GPU)
+SYM_HD void inform_gpu(Shard& S, int32_t gid, int64_t free_at, int64_t now,
+                       const Pusher& who) {
+  if (S.free_at[gid] != OUTSTANDING) S.ops += 1;
+  S.free_at[gid] = free_at;
+  gpu_tree_update(S, gid);
+  S.ops += 1;
+  set_gpu_timer(S, now, who);
+}
+
+// scheduler.py:180-209 (jitterless network: start = exec_at)
+SYM_HD void granted_gpu(Shard& S, int32_t m, int32_t gid, int64_t gpu_free_at,
+                        int64_t now, const Pusher& who) {
+  ModelState& st = S.ms[m];
+  const int32_t pre_size = st.has_cand ? st.c_size : 0;
+  update_candidate(S, m, now, imax(gpu_free_at, 0), who);
+  if (!st.has_cand) {
+    inform_gpu(S, gid, imax(now, gpu_free_at), now, who);
+    update_candidate(S, m, now, NEG_INF, who);
+    inform_candidate(S, m, now, who);
+    return;
+  }
+  const int32_t b = st.c_size;
+  const int64_t lat_b = lat_of(S, m, b);
+  if (S.n_recs < S.rec_cap) {
+    BatchRec& r = S.recs[S.n_recs];
+    r.emitted = now;
+    r.start = st.c_exec;
+    r.finish = st.c_exec + lat_b;
+    r.kt = who.t;
+    r.ka = who.a_self;
+    r.ksub = who.sub;
+    r.model = m;
+    r.gpu = gid;
+    r.size = b;
+    r.first = S.mp[m].off + st.qh;
+    r.shrunk_from = b < pre_size ? pre_size : 0;
+  } else {
+    S.error = ERR_REC_OVERFLOW;
+  }
+  S.n_recs += 1;
+  st.qh += b;
+  const int64_t believed_free = st.c_exec + lat_b;
+  st.has_cand = 0;
+  update_candidate(S, m, now, NEG_INF, who);
+  inform_gpu(S, gid, believed_free, now, who);
+  inform_candidate(S, m, now, who);
+}
+
+// scheduler.py:381-399 (always live here: only live timers exist)
+SYM_HD void on_model_timer(Shard& S, int32_t m, int64_t now,
+                           const Pusher& who) {
+  ModelState& st = S.ms[m];
+  st.has_mt = 0;
+  const int32_t gid = S.gt[1];
+  if (gid >= 0) {
+    const int64_t fa = S.free_at[gid];
+    S.ops += 1;
+    if (fa <= st.c_exec) {
+      S.ops += 1;
+      S.free_at[gid] = OUTSTANDING;
+      gpu_tree_update(S, gid);
+      granted_gpu(S, m, gid, fa, now, who);
+      return;
+    }
+  }
+  st.registered = 1;
+  S.mc_size[m] = st.c_size;
+  S.mc_latest[m] = st.c_latest;
+  mc_tree_update(S, m);
+  S.ops += 2;
+  S.registrations += 1;
+  set_gpu_timer(S, now, who);
+}
+
+// scheduler.py:173-178
+SYM_HD void on_drop_timer(Shard& S, int32_t m, int64_t now,
+                          const Pusher& who) {
+  S.ms[m].dt_head = -1;
+  if (update_candidate(S, m, now, NEG_INF, who))
+    inform_candidate(S, m, now, who);
+}
+
+// scheduler.py:168-171 for the arrival at sorted position off+qt.
+SYM_HD void on_arrival(Shard& S, int32_t m) {
+  ModelState& st = S.ms[m];
+  const int32_t pos = S.mp[m].off + st.qt;
+  const int64_t now = S.s_tick[pos];
+  Pusher who;
+  who.t = now;
+  who.a_self = S.s_aself[pos];
+  who.a_after = S.s_g[pos] + 1;
+  who.sub = SUB_ARRIVAL;
+  st.qt += 1;
+  if (update_candidate(S, m, now, NEG_INF, who))
+    inform_candidate(S, m, now, who);
+}
+
+// ----------------------------------------------- local absorption scan ----
+// Absorb this model's arrivals until its next chain event, which is stored
+// in nx_key/nx_type.  Valid because an unregistered model's arrivals touch
+// nothing but the model itself, and no other chain event touches it.
+SYM_HD void scan_model(Shard& S, int32_t m) {
+  ModelState& st = S.ms[m];
+  const ModelParam& P = S.mp[m];
+  for (;;) {
+    int32_t type = EV_NONE;
+    EvKey best;
+    if (st.has_mt) {
+      best = st.mt_key;
+      type = EV_MT;
+    }
+    if (st.dt_head >= 0 && (type == EV_NONE || key_less(st.dt_key, best))) {
+      best = st.dt_key;
+      type = EV_DT;
+    }
+    if (st.qt < P.cnt) {
+      const int32_t pos = P.off + st.qt;
+      EvKey ka;
+      ka.t = S.s_tick[pos];
+      ka.a = S.s_aself[pos];
+      ka.prio = PR_ARRIVAL;
+      ka.tp = 0;
+      ka.ap = 0;
+      ka.sub = 0;
+      ka._pad = 0;
+      if (type == EV_NONE || key_less(ka, best)) {
+        if (st.registered) {
+          best = ka;
+          type = EV_ARR;
+        } else {
+          on_arrival(S, m);
+          S.absorbed += 1;
+          continue;
+        }
+      }
+    }
+    st.nx_type = type;
+    if (type != EV_NONE) st.nx_key = best;
+    return;
+  }
+}
+
+// ------------------------------------------------------------ chain -------
+
+SYM_HD void on_gpu_timer(Shard& S, const Pusher& who, int32_t* dirty,
+                         int32_t& nd) {
+  S.gt_armed = 0;
+  const int32_t gid = S.gt_gid;
+  const int64_t fa = S.free_at[gid];
+  const int64_t now = who.t;
+  if (fa == OUTSTANDING) {
+    set_gpu_timer(S, now, who);
+    return;
+  }
+  for (;;) {
+    const int32_t m = S.mc_lat_tree[1];
+    if (m < 0 || S.mc_latest[m] >= fa) break;
+    S.ms[m].registered = 0;
+    mc_tree_update(S, m);
+    S.ops += 2;
+    S.evictions += 1;
+    dirty[nd++] = m;
+  }
+  const int32_t m = S.mc_lat_tree[1];
+  if (m >= 0) {
+    S.ops += 1;
+    unregister(S, m);
+    S.ops += 1;
+    S.free_at[gid] = OUTSTANDING;
+    gpu_tree_update(S, gid);
+    granted_gpu(S, m, gid, fa, now, who);
+    dirty[nd++] = m;
+  }
+  set_gpu_timer(S, now, who);
+}
+
+// Process one chain event; returns false when the sub-cluster is drained.
+// dirty must hold M+1 entries.
+SYM_HD bool chain_step(Shard& S, int32_t* dirty) {
+  const int32_t m = S.pq[1];
+  const bool have_m = m >= 0;
+  if (!have_m && !S.gt_armed) return false;
+  int32_t nd = 0;
+  const int64_t ops0 = S.ops, ev0 = S.evictions;
+  bool timer_event = true;
+  if (S.gt_armed && (!have_m || key_less(S.gt_key, S.ms[m].nx_key))) {
+    Pusher who;
+    who.t = S.gt_key.t;
+    who.a_self = who.a_after = S.gt_key.a;
+    who.sub = S.chain_events;
+    on_gpu_timer(S, who, dirty, nd);
+  } else {
+    ModelState& st = S.ms[m];
+    Pusher who;
+    who.t = st.nx_key.t;
+    who.a_self = who.a_after = st.nx_key.a;
+    who.sub = S.chain_events;
+    switch (st.nx_type) {
+      case EV_MT: on_model_timer(S, m, who.t, who); break;
+      case EV_DT: on_drop_timer(S, m, who.t, who); break;
+      case EV_ARR:
+        on_arrival(S, m);
+        timer_event = false;
+        break;
+      default: S.error = ERR_STATE; return false;
+    }
+    dirty[nd++] = m;
+  }
+  S.chain_events += 1;
+  if (timer_event) {
+    const int64_t ops = (S.ops - ops0) - 2 * (S.evictions - ev0);
+    if (ops > S.handler_ops_max) S.handler_ops_max = ops;
+  }
+  for (int32_t i = 0; i < nd; i++) {
+    scan_model(S, dirty[i]);
+    pq_update(S, dirty[i]);
+  }
+  return true;
+}
+
+// Initialise trees and absorb every model's leading arrivals.
+SYM_HD void chain_init(Shard& S) {
+  for (int32_t g = 0; g < S.G; g++) S.free_at[g] = 0;
+  for (int32_t i = 0; i < 2 * S.Gp; i++) S.gt[i] = -1;
+  for (int32_t g = 0; g < S.G; g++) S.gt[S.Gp + g] = g;
+  for (int32_t i = S.Gp - 1; i >= 1; i--) {
+    int32_t l = S.gt[2 * i], r = S.gt[2 * i + 1];
+    S.gt[i] = gpu_before(S, r, l) ? r : l;
+  }
+  for (int32_t i = 0; i < 2 * S.Mp; i++) {
+    S.pq[i] = -1;
+    S.mc_lat_tree[i] = -1;
+    S.mc_bs_tree[i] = -1;
+  }
+  for (int32_t m = 0; m < S.M; m++) {
+    ModelState& st = S.ms[m];
+    st.qh = st.qt = 0;
+    st.has_cand = 0;
+    st.c_size = 0;
+    st.c_head = -1;
+    st.registered = 0;
+    st.has_mt = 0;
+    st.dt_head = -1;
+    st.nx_type = EV_NONE;
+    st.drops = 0;
+    S.mc_size[m] = 0;
+    S.mc_latest[m] = 0;
+  }
+  S.gt_armed = 0;
+  S.n_recs = 0;
+  S.chain_events = S.absorbed = S.n_dropped = 0;
+  S.ops = S.evictions = S.registrations = S.handler_ops_max = 0;
+  S.error = ERR_NONE;
+  for (int32_t m = 0; m < S.M; m++) {
+    scan_model(S, m);
+    S.pq[S.Mp + m] = S.ms[m].nx_type != EV_NONE ? m : -1;
+  }
+  for (int32_t i = S.Mp - 1; i >= 1; i--) {
+    int32_t l = S.pq[2 * i], r = S.pq[2 * i + 1];
+    S.pq[i] = model_before(S, r, l) ? r : l;
+  }
+}
+
+}  // namespace sym
