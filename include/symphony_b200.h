@@ -1,0 +1,145 @@
+/*
+ * symphony_b200.h -- C ABI of the B200-native Symphony scheduler engine.
+ *
+ * Drop-in boundary for the reference's simulate/step entry points:
+ *   Engine(models, gpu_count, policy, network, seed, record_trace,
+ *          check_invariants)          batchsym/simulator.py:99-140
+ *   Engine.run_stream(arr_ticks, arr_midx, duration_s) -> RunResult
+ *                                     batchsym/simulator.py:201-226, 65-87
+ *   run_scenario(scenario, ...)       batchsym/scenario.py:264-273
+ * The Python package paper_2308_07470_b200 mirrors those names on top of
+ * this ABI (ctypes); see INTEGRATION.md for the binding a batchsym maintainer
+ * would add.  Plain pointers and sizes only; all times are int64 ns ticks
+ * (batchsym/units.py:1-17).
+ *
+ * A handle owns one CUDA stream and its device scratch on one device; it is
+ * not thread-safe.  Every call is blocking (stream-synchronised on return).
+ */
+#ifndef SYMPHONY_B200_H
+#define SYMPHONY_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: the Python layer maps them to the reference's
+ * exception types */
+enum {
+  SYM_OK = 0,
+  SYM_EPROTO = 1,     /* ProtocolError: unknown model id in the stream
+                         (simulator.py:213-215) */
+  SYM_EINVAL = 2,     /* ValueError: bad configuration (simulator.py:103-104,
+                         scheduler.py:70-82) */
+  SYM_EINVARIANT = 3, /* InvariantViolation (simulator.py:90-91) */
+  SYM_ECUDA = 4,      /* CUDA runtime failure -> RuntimeError */
+  SYM_ENOMEM = 5
+};
+
+enum { SYM_KIND_DEFERRED = 0, SYM_KIND_EAGER = 1, SYM_KIND_TIMEOUT = 2 };
+enum { SYM_GATHER_PREFIX = 0, SYM_GATHER_DROP_HEAD = 1 };
+
+/* run flags */
+enum {
+  SYM_FLAG_TRACE = 1u,      /* record_trace=True: per-drop keys for the trace */
+  SYM_FLAG_NO_FRESH = 2u,   /* disable the parallel fresh-start pre-scan */
+  SYM_FLAG_NO_EXPAND = 4u   /* leave per-request arrays untouched (bench) */
+};
+
+/* Engine configuration.  Models are numbered 0..n_models-1 in the order of
+ * the reference's `models` list; a sub-cluster (shard) is an independent
+ * Engine over its models and its own GPU sub-pool (scalebench.py:98-99,
+ * PAPER.md:475-490).  With n_shards == 1 this is exactly the reference
+ * Engine.  GPU ids are global: shard s owns the contiguous id range after
+ * shards 0..s-1. */
+typedef struct {
+  int32_t n_models;
+  int32_t n_gpus;             /* total = sum(gpus_per_shard) */
+  int32_t kind;               /* PolicyConfig.kind (scheduler.py:62) */
+  int32_t gather;             /* PolicyConfig.gather (scheduler.py:67) */
+  int32_t target_batch;       /* PolicyConfig.target_batch (scheduler.py:68) */
+  int32_t lat_stride;         /* row stride of lat_ns (>= max max_batch) */
+  int64_t d_ctrl_ns;          /* PolicyConfig.d_ctrl_ns (scheduler.py:65) */
+  int64_t d_data_ns;          /* PolicyConfig.d_data_ns (scheduler.py:66) */
+  const int64_t *lat_ns;      /* [n_models * lat_stride]; LatencyProfile.lat_ns
+                                 (profile.py:40), lat[b-1] = l(b) */
+  const int32_t *max_batch;   /* [n_models] LatencyProfile.max_batch */
+  const int64_t *slo_ns;      /* [n_models] ModelSpec.slo_ns (profile.py:122) */
+  const int64_t *timeout_ns;  /* [n_models] resolve_timeout_ns (scheduler.py:84) */
+  int32_t n_shards;           /* >= 1 */
+  int32_t device;             /* CUDA device ordinal */
+  const int32_t *shard_of_model; /* [n_models], NULL = all in shard 0 */
+  const int32_t *gpus_per_shard; /* [n_shards], NULL = n_gpus in shard 0 */
+} sym_config;
+
+/* Batch record = one ExecutionOrder (scheduler.py:123-135) / one gpu_logs
+ * entry (simulator.py:322-323).  Records of one GPU appear in emission
+ * order. */
+typedef struct {
+  int64_t emitted, start, finish;
+  int64_t key_t, key_sub;   /* processing position of the granting event */
+  int32_t key_a;
+  int32_t model, gpu, size;
+  int32_t first_index;      /* stream index of the batch's first member */
+  int32_t shrunk_from;      /* pre-grant candidate size if it shrank, else 0 */
+} sym_batch;
+
+typedef struct {
+  int64_t n;                  /* requests in the run */
+  /* Per-request outputs, caller-allocated [n], index = stream position
+   * (= rid - 1 for a single shard); RunResult fields simulator.py:74-78.
+   * May be NULL with SYM_FLAG_NO_EXPAND. */
+  int64_t *req_dispatch, *req_start, *req_finish, *req_batch, *req_outcome;
+  /* Trace support (SYM_FLAG_TRACE): per request, tick and processing
+   * position of its drop, -1 if not dropped. */
+  int64_t *drop_t, *drop_key_sub;
+  int32_t *drop_key_a;
+  /* batch records, caller-allocated capacity batch_cap (n is always
+   * enough); n_batches receives the count */
+  sym_batch *batches;
+  int64_t batch_cap;
+  int64_t n_batches;
+  /* counters, summed over shards */
+  int64_t drops, completions, late;
+  int64_t ops, evictions, registrations, handler_ops_max;
+  int64_t chain_events, absorbed_arrivals, fresh_adoptions;
+  /* device timings of the last run (CUDA events on the engine stream) */
+  float ms_ingest, ms_fresh, ms_chain, ms_expand, ms_total;
+  int64_t err_index;          /* offending stream index for SYM_EPROTO */
+} sym_result;
+
+/* Create an engine; returns NULL and sets *status on failure. */
+void *sym_create(const sym_config *cfg, int32_t *status);
+void sym_destroy(void *engine);
+
+/* Host buffers in, host buffers out (end-to-end API: the H2D and D2H copies
+ * are part of the call).  arr_ticks must be non-decreasing
+ * (generate_arrivals / load_replay_trace guarantee it). */
+int32_t sym_run(void *engine, const int64_t *arr_ticks,
+                const int32_t *arr_model, int64_t n, uint32_t flags,
+                sym_result *out);
+
+/* Same, but every pointer in the call (arrivals, per-request outputs,
+ * drop arrays and batches) is a DEVICE pointer on the engine's device;
+ * nothing crosses PCIe except the counters.  Used with inputs already
+ * resident in HBM. */
+int32_t sym_run_device(void *engine, const int64_t *d_arr_ticks,
+                       const int32_t *d_arr_model, int64_t n, uint32_t flags,
+                       sym_result *out);
+
+/* Integer reductions of a finished run for compute_stats
+ * (metrics.py:71-132): per model counts of completed/late/dropped among
+ * arrivals in [lo_ns, hi_ns), per GPU busy ns clipped to the window.
+ * Pointers are host arrays sized n_models / n_gpus. */
+int32_t sym_window_counts(void *engine, int64_t lo_ns, int64_t hi_ns,
+                          int64_t *model_arrivals, int64_t *model_completed,
+                          int64_t *model_late, int64_t *model_dropped,
+                          int64_t *gpu_busy_ns);
+
+const char *sym_last_error(void *engine);
+int32_t sym_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,884 @@
+// engine.cu -- B200 (sm_100a) kernels and the C ABI of include/symphony_b200.h.
+//
+// Pipeline of one run (all on the engine's stream, inputs resident in HBM):
+//   K1a k_hist      per-warp-chunk histograms of (slot, shard) of the stream
+//   K1b k_colscan   per-bin exclusive scan over chunks  -> stable bases
+//   K1c k_binoff    bin offsets, per-model ModelParam.off/cnt
+//   K1d k_scatter   stable scatter to the (shard, model)-sorted layout with
+//                   warp __match_any_sync ranking (one warp per chunk keeps
+//                   stream order without any global atomics)
+//   K1e k_aself     canonical A' of every arrival (same-tick cascades)
+//   K2  k_fresh     fresh-start pre-scan: thread per sorted position
+//   K4  k_chain     one CTA per sub-cluster runs the live-event chain
+//   K5  k_init_out / k_expand  per-request RunResult arrays from batch records
+// The chain (engine_core.cuh) is the only sequential part; everything else is
+// a bandwidth-bound pass over the request stream.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/symphony_b200.h"
+#include "engine_core.cuh"
+
+using namespace sym;
+
+namespace {
+
+constexpr int kChunk = 4096;      // stream elements per warp in K1
+constexpr int kFreshMaxSteps = 1 << 16;
+constexpr int kVersion = 1;
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  std::string err;
+  // configuration
+  int32_t M = 0, G = 0, P = 1, kind = 0, gather = 0, lat_stride = 1;
+  int64_t d_ctrl = 0, d_data = 0;
+  std::vector<int32_t> shard_of_model, slot_of_model, model_of_slot;
+  std::vector<int32_t> slot_base;   // [P+1] first slot of each shard
+  std::vector<int32_t> gpu_base;    // [P+1]
+  std::vector<ModelParam> mp_host;  // by slot
+  // static device data
+  int64_t* d_lat = nullptr;         // rows in slot order
+  ModelParam* d_mp = nullptr;       // [M] by slot
+  int32_t* d_slot_of_model = nullptr;
+  int32_t* d_shard_of_model = nullptr;
+  int32_t* d_slot_base = nullptr;   // [P+1]
+  // chain state (independent of n)
+  ModelState* d_ms = nullptr;
+  int32_t *d_pq = nullptr, *d_gt = nullptr, *d_mlt = nullptr,
+          *d_mbt = nullptr, *d_mcs = nullptr, *d_dirty = nullptr;
+  int64_t *d_free = nullptr, *d_mcl = nullptr;
+  Shard* d_shards = nullptr;
+  std::vector<Shard> shards;        // host images
+  // per-run buffers (grown)
+  int64_t cap = 0, W_cap = 0;
+  int64_t *d_ticks = nullptr, *d_s_tick = nullptr, *d_sh_tick = nullptr;
+  int32_t *d_model = nullptr, *d_s_g = nullptr, *d_s_i = nullptr,
+          *d_s_aself = nullptr;
+  int32_t* d_hist = nullptr;        // [W][B]
+  int32_t* d_bins = nullptr;        // [B+1] totals -> offsets
+  int32_t* d_err = nullptr;
+  FreshRec* d_fresh = nullptr;
+  BatchRec* d_recs = nullptr;
+  int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
+  int32_t* d_drop_ka = nullptr;
+  // last run (for sym_window_counts)
+  int64_t last_n = 0;
+  const int64_t* last_ticks = nullptr;
+  const int32_t* last_model = nullptr;
+  std::vector<int64_t> last_nrecs;
+  bool has_run = false;
+};
+
+#define CK(call)                                                        \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) {                                            \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);    \
+      return SYM_ECUDA;                                                 \
+    }                                                                   \
+  } while (0)
+
+template <class T>
+int grow(Ctx* ctx, T*& p, int64_t count) {
+  if (p) cudaFree(p);
+  p = nullptr;
+  CK(cudaMalloc((void**)&p, sizeof(T) * (size_t)(count > 0 ? count : 1)));
+  return SYM_OK;
+}
+
+// --------------------------------------------------------------- K1 -------
+
+__global__ void k_hist(const int32_t* __restrict__ model, int64_t n,
+                       const int32_t* __restrict__ slot_of_model,
+                       const int32_t* __restrict__ shard_of_model, int32_t M,
+                       int32_t P, int32_t* __restrict__ hist, int64_t W,
+                       int32_t* __restrict__ err) {
+  extern __shared__ int32_t sh[];
+  const int B = M + P;
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  int32_t* cnt = sh + wib * B;
+  for (int b = lane; b < B; b += 32) cnt[b] = 0;
+  __syncwarp();
+  if (w < W) {
+    const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
+    for (int64_t i = lo + lane; i < hi; i += 32) {
+      const int32_t m = model[i];
+      if (m < 0 || m >= M) {
+        atomicMin(err, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
+        continue;
+      }
+      atomicAdd(&cnt[slot_of_model[m]], 1);
+      atomicAdd(&cnt[M + shard_of_model[m]], 1);
+    }
+  }
+  __syncwarp();
+  if (w < W)
+    for (int b = lane; b < B; b += 32) hist[w * B + b] = cnt[b];
+}
+
+// exclusive scan of each bin over chunks; totals to bins[b]
+__global__ void k_colscan(int32_t* __restrict__ hist, int64_t W, int32_t B,
+                          int32_t* __restrict__ bins) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int32_t run = 0;
+  for (int64_t w = 0; w < W; w++) {
+    const int32_t v = hist[w * B + b];
+    hist[w * B + b] = run;
+    run += v;
+  }
+  bins[b] = run;
+}
+
+// single block: slot offsets (exclusive scan over slots) and shard stream
+// offsets (exclusive scan over shards); fills ModelParam.off/cnt.
+__global__ void k_binoff(int32_t* __restrict__ bins, int32_t M, int32_t P,
+                         ModelParam* __restrict__ mp,
+                         int32_t* __restrict__ shard_off) {
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int s = 0; s < M; s++) {
+      const int32_t c = bins[s];
+      mp[s].off = run;
+      mp[s].cnt = c;
+      bins[s] = run;
+      run += c;
+    }
+    run = 0;
+    for (int s = 0; s < P; s++) {
+      const int32_t c = bins[M + s];
+      bins[M + s] = run;
+      shard_off[s] = run;
+      run += c;
+    }
+    shard_off[P] = run;
+  }
+}
+
+__global__ void k_scatter(const int64_t* __restrict__ ticks,
+                          const int32_t* __restrict__ model, int64_t n,
+                          const int32_t* __restrict__ slot_of_model,
+                          const int32_t* __restrict__ shard_of_model,
+                          int32_t M, int32_t P,
+                          const int32_t* __restrict__ hist,
+                          const int32_t* __restrict__ bins, int64_t W,
+                          int64_t* __restrict__ s_tick,
+                          int32_t* __restrict__ s_g,
+                          int32_t* __restrict__ s_i,
+                          int64_t* __restrict__ sh_tick) {
+  extern __shared__ int32_t sh[];
+  const int B = M + P;
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (w >= W) return;
+  int32_t* base = sh + wib * B;
+  for (int b = lane; b < B; b += 32) base[b] = bins[b] + hist[w * B + b];
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
+  for (int64_t i0 = lo; i0 < hi; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const bool act = i < hi;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    int32_t sl = -1 - lane, sd = -1 - lane;  // unique dummies when inactive
+    int64_t t = 0;
+    if (act) {
+      const int32_t m = model[i];
+      sl = slot_of_model[m];
+      sd = M + shard_of_model[m];
+      t = ticks[i];
+    }
+    const unsigned ps = __match_any_sync(0xffffffffu, sl) & amask;
+    const unsigned pd = __match_any_sync(0xffffffffu, sd) & amask;
+    int32_t pos = 0, j = 0;
+    if (act) {
+      pos = base[sl] + __popc(ps & lt);
+      j = base[sd] + __popc(pd & lt);
+    }
+    __syncwarp();
+    if (act) {
+      // the highest peer advances the running bases
+      if ((ps >> lane) == 1u) base[sl] += __popc(ps);
+      if ((pd >> lane) == 1u) base[sd] += __popc(pd);
+      s_tick[pos] = t;
+      s_g[pos] = j;
+      s_i[pos] = (int32_t)i;
+      sh_tick[j] = t;
+    }
+    __syncwarp();
+  }
+}
+
+// canonical A' of each arrival, in the sorted layout (engine_core.cuh)
+__global__ void k_aself(const int64_t* __restrict__ s_tick,
+                        const int32_t* __restrict__ s_g,
+                        const int64_t* __restrict__ sh_tick,
+                        const int32_t* __restrict__ shard_off, int32_t P,
+                        int64_t n, int32_t* __restrict__ s_aself) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int32_t j = s_g[p];
+  int lo = 0, hi = P;  // last s with shard_off[s] <= j
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (shard_off[mid] <= j) lo = mid; else hi = mid;
+  }
+  const bool first = j == shard_off[lo];
+  s_aself[p] = (!first && sh_tick[j - 1] == s_tick[p]) ? j : A_BASE;
+}
+
+// --------------------------------------------------------------- K2 -------
+
+__global__ void __launch_bounds__(256)
+k_fresh(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
+        const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
+        FreshRec* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  // slot of p: last slot with off <= p and cnt > 0
+  int lo = 0, hi = slot_base[P];
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+  }
+  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  int s = 0;
+  while (slot_base[s + 1] <= lo) s++;
+  const Shard& S = shards[s];
+  const int32_t m = lo - slot_base[s];
+  out[p] = fresh_scan(S, m, (int32_t)(p - mp_all[lo].off), kFreshMaxSteps);
+}
+
+// --------------------------------------------------------------- K4 -------
+
+__global__ void __launch_bounds__(32)
+k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
+        int32_t* __restrict__ dirty_all, const int32_t* __restrict__ slot_base) {
+  __shared__ Shard S;  // hot scalars of the sub-cluster live in smem
+  if (threadIdx.x != 0) return;
+  S = shards[blockIdx.x];
+  int32_t* dirty = dirty_all + slot_base[blockIdx.x] + blockIdx.x;
+  chain_init(S, fresh);
+  while (chain_step(S, dirty, fresh)) {
+  }
+  shards[blockIdx.x] = S;
+}
+
+// --------------------------------------------------------------- K5 -------
+
+__global__ void k_init_out(int64_t n, int64_t* __restrict__ disp,
+                           int64_t* __restrict__ start,
+                           int64_t* __restrict__ fin, int64_t* __restrict__ bat,
+                           int64_t* __restrict__ outc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  disp[i] = -1;
+  start[i] = -1;
+  fin[i] = -1;
+  bat[i] = -1;
+  outc[i] = 2;  // OUTCOME_DROPPED: every request resolves
+}
+
+// one warp per batch record
+__global__ void k_expand(const BatchRec* __restrict__ recs,
+                         const int64_t* __restrict__ rec_base,
+                         const int64_t* __restrict__ rec_count, int32_t P,
+                         const int32_t* __restrict__ s_i,
+                         const int64_t* __restrict__ s_tick,
+                         const ModelParam* __restrict__ mp_all,
+                         const int32_t* __restrict__ slot_base,
+                         int64_t total, int64_t* __restrict__ disp,
+                         int64_t* __restrict__ start,
+                         int64_t* __restrict__ fin, int64_t* __restrict__ bat,
+                         int64_t* __restrict__ outc) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= total) return;
+  // map the dense index to (shard, record)
+  int s = 0;
+  int64_t k = w;
+  while (s < P && k >= rec_count[s]) {
+    k -= rec_count[s];
+    s++;
+  }
+  const BatchRec& r = recs[rec_base[s] + k];
+  const int64_t slo = mp_all[slot_base[s] + r.model].slo;
+  for (int j = lane; j < r.size; j += 32) {
+    const int64_t p = r.first + j;
+    const int64_t i = s_i[p];
+    disp[i] = r.emitted;
+    start[i] = r.start;
+    fin[i] = r.finish;
+    bat[i] = r.size;
+    outc[i] = r.finish <= s_tick[p] + slo ? 0 : 1;
+  }
+}
+
+__global__ void k_drop_out(int64_t n, const int32_t* __restrict__ s_i,
+                           const int64_t* __restrict__ dt,
+                           const int64_t* __restrict__ dks,
+                           const int32_t* __restrict__ dka,
+                           int64_t* __restrict__ o_t, int64_t* __restrict__ o_ks,
+                           int32_t* __restrict__ o_ka) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t i = s_i[p];
+  o_t[i] = dt[p];
+  o_ks[i] = dks[p];
+  o_ka[i] = dka[p];
+}
+
+__global__ void k_fill64(int64_t* p, int64_t n, int64_t v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void k_copy_batches(const BatchRec* __restrict__ recs,
+                               const int64_t* __restrict__ rec_base,
+                               const int64_t* __restrict__ rec_count,
+                               int32_t P, const int32_t* __restrict__ s_i,
+                               const int32_t* __restrict__ model_of_slot,
+                               const int32_t* __restrict__ slot_base,
+                               const int32_t* __restrict__ gpu_base,
+                               int64_t total, sym_batch* __restrict__ out) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= total) return;
+  int s = 0;
+  int64_t k = w;
+  while (s < P && k >= rec_count[s]) {
+    k -= rec_count[s];
+    s++;
+  }
+  const BatchRec& r = recs[rec_base[s] + k];
+  sym_batch b;
+  b.emitted = r.emitted;
+  b.start = r.start;
+  b.finish = r.finish;
+  b.key_t = r.kt;
+  b.key_sub = r.ksub;
+  b.key_a = r.ka;
+  b.model = model_of_slot[slot_base[s] + r.model];
+  b.gpu = gpu_base[s] + r.gpu;
+  b.size = r.size;
+  b.first_index = s_i[r.first];
+  b.shrunk_from = r.shrunk_from;
+  out[w] = b;
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------ driver ------
+
+int ensure_capacity(Ctx* ctx, int64_t n) {
+  const int64_t W = (n + kChunk - 1) / kChunk;
+  const int B = ctx->M + ctx->P;
+  if (n > ctx->cap) {
+    int64_t c = n + n / 8 + 1024;
+    int rc;
+    if ((rc = grow(ctx, ctx->d_ticks, c)) || (rc = grow(ctx, ctx->d_model, c)) ||
+        (rc = grow(ctx, ctx->d_s_tick, c)) || (rc = grow(ctx, ctx->d_sh_tick, c)) ||
+        (rc = grow(ctx, ctx->d_s_g, c)) || (rc = grow(ctx, ctx->d_s_i, c)) ||
+        (rc = grow(ctx, ctx->d_s_aself, c)) || (rc = grow(ctx, ctx->d_fresh, c)) ||
+        (rc = grow(ctx, ctx->d_recs, c + ctx->P)) ||
+        (rc = grow(ctx, ctx->d_drop_t, c)) || (rc = grow(ctx, ctx->d_drop_ks, c)) ||
+        (rc = grow(ctx, ctx->d_drop_ka, c)))
+      return rc;
+    ctx->cap = c;
+  }
+  if (W * B > ctx->W_cap) {
+    int rc;
+    if ((rc = grow(ctx, ctx->d_hist, W * B + 1))) return rc;
+    ctx->W_cap = W * B + 1;
+  }
+  return SYM_OK;
+}
+
+int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
+               int64_t n, uint32_t flags, sym_result* out, bool outs_on_device) {
+  cudaStream_t st = ctx->stream;
+  const int32_t M = ctx->M, P = ctx->P;
+  const int B = M + P;
+  const bool trace = flags & SYM_FLAG_TRACE;
+  const bool use_fresh = !trace && !(flags & SYM_FLAG_NO_FRESH);
+  int rc;
+  if ((rc = ensure_capacity(ctx, n))) return rc;
+  const int64_t W = (n + kChunk - 1) / kChunk;
+  CK(cudaEventRecord(ctx->ev[0], st));
+  // ---- K1 ingest
+  int32_t big = INT32_MAX;
+  CK(cudaMemcpyAsync(ctx->d_err, &big, sizeof big, cudaMemcpyHostToDevice, st));
+  const int wpb = 4;
+  const size_t smem = sizeof(int32_t) * (size_t)B * wpb;
+  if (W > 0) {
+    k_hist<<<nblk(W, wpb), 32 * wpb, smem, st>>>(
+        d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
+        ctx->d_hist, W, ctx->d_err);
+    k_colscan<<<nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, ctx->d_bins);
+  } else {
+    CK(cudaMemsetAsync(ctx->d_bins, 0, sizeof(int32_t) * B, st));
+  }
+  k_binoff<<<1, 32, 0, st>>>(ctx->d_bins, M, P, ctx->d_mp,
+                             ctx->d_bins + B + 1);
+  int32_t herr = INT32_MAX;
+  CK(cudaMemcpyAsync(&herr, ctx->d_err, sizeof herr, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (herr != INT32_MAX) {
+    out->err_index = herr;
+    ctx->err = "request for unknown model";
+    return SYM_EPROTO;
+  }
+  if (W > 0)
+    k_scatter<<<nblk(W, wpb), 32 * wpb, smem, st>>>(
+        d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
+        ctx->d_hist, ctx->d_bins, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
+        ctx->d_sh_tick);
+  if (n > 0)
+    k_aself<<<nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
+                                          ctx->d_sh_tick, ctx->d_bins + B + 1,
+                                          P, n, ctx->d_s_aself);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[1], st));
+  // ---- per-shard views
+  for (int s = 0; s < P; s++) {
+    Shard& S = ctx->shards[s];
+    S.s_tick = ctx->d_s_tick;
+    S.s_g = ctx->d_s_g;
+    S.s_aself = ctx->d_s_aself;
+    S.record_trace = trace ? 1 : 0;
+    S.drop_t = ctx->d_drop_t;
+    S.drop_ksub = ctx->d_drop_ks;
+    S.drop_ka = ctx->d_drop_ka;
+  }
+  // record capacity per shard: its arrival count (+1)
+  std::vector<ModelParam> mp(M);
+  CK(cudaMemcpyAsync(mp.data(), ctx->d_mp, sizeof(ModelParam) * M,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int64_t> rec_base(P + 1, 0);
+  for (int s = 0; s < P; s++) {
+    int64_t cnt = 0;
+    for (int k = ctx->slot_base[s]; k < ctx->slot_base[s + 1]; k++)
+      cnt += mp[k].cnt;
+    rec_base[s + 1] = rec_base[s] + cnt + 1;
+    ctx->shards[s].recs = ctx->d_recs + rec_base[s];
+    ctx->shards[s].rec_cap = cnt + 1;
+  }
+  CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
+                     cudaMemcpyHostToDevice, st));
+  if (trace && n > 0)
+    k_fill64<<<nblk(n, 256), 256, 0, st>>>(ctx->d_drop_t, n, -1);
+  // ---- K2 fresh-start pre-scan
+  if (use_fresh && n > 0)
+    k_fresh<<<nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
+                                          ctx->d_mp, P, n, ctx->d_fresh);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[2], st));
+  // ---- K4 chain
+  k_chain<<<P, 32, 0, st>>>(ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr,
+                            ctx->d_dirty, ctx->d_slot_base);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[3], st));
+  CK(cudaMemcpyAsync(ctx->shards.data(), ctx->d_shards, sizeof(Shard) * P,
+                     cudaMemcpyDeviceToHost, st));
+  std::vector<ModelState> ms(M);
+  CK(cudaMemcpyAsync(ms.data(), ctx->d_ms, sizeof(ModelState) * M,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int64_t total = 0;
+  std::vector<int64_t> rec_count(P);
+  for (int s = 0; s < P; s++) {
+    const Shard& S = ctx->shards[s];
+    if (S.error) {
+      ctx->err = "chain error " + std::to_string(S.error) + " in shard " +
+                 std::to_string(s);
+      return SYM_EINVARIANT;
+    }
+    rec_count[s] = S.n_recs;
+    total += S.n_recs;
+  }
+  // ---- K5 outputs
+  int64_t* d_meta = nullptr;  // rec_base[P] + rec_count[P]
+  CK(cudaMallocAsync((void**)&d_meta, sizeof(int64_t) * 2 * (P + 1), st));
+  CK(cudaMemcpyAsync(d_meta, rec_base.data(), sizeof(int64_t) * P,
+                     cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_meta + P + 1, rec_count.data(), sizeof(int64_t) * P,
+                     cudaMemcpyHostToDevice, st));
+  const bool expand = !(flags & SYM_FLAG_NO_EXPAND) && out->req_dispatch;
+  if (expand && n > 0) {
+    k_init_out<<<nblk(n, 256), 256, 0, st>>>(n, out->req_dispatch,
+                                             out->req_start, out->req_finish,
+                                             out->req_batch, out->req_outcome);
+    if (total > 0)
+      k_expand<<<nblk(total * 32, 256), 256, 0, st>>>(
+          ctx->d_recs, d_meta, d_meta + P + 1, P, ctx->d_s_i, ctx->d_s_tick,
+          ctx->d_mp, ctx->d_slot_base, total, out->req_dispatch,
+          out->req_start, out->req_finish, out->req_batch, out->req_outcome);
+  }
+  if (trace && out->drop_t && n > 0)
+    k_drop_out<<<nblk(n, 256), 256, 0, st>>>(
+        n, ctx->d_s_i, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
+        out->drop_t, out->drop_key_sub, out->drop_key_a);
+  if (out->batches && total > 0) {
+    if (total > out->batch_cap) {
+      ctx->err = "batch buffer too small";
+      cudaFreeAsync(d_meta, st);
+      return SYM_EINVAL;
+    }
+    k_copy_batches<<<nblk(total, 256), 256, 0, st>>>(
+        ctx->d_recs, d_meta, d_meta + P + 1, P, ctx->d_s_i,
+        ctx->d_bins + B + P + 2, ctx->d_slot_base, ctx->d_bins + B + P + 2 + M,
+        total, out->batches);
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[4], st));
+  CK(cudaFreeAsync(d_meta, st));
+  CK(cudaStreamSynchronize(st));
+  (void)outs_on_device;
+  // ---- counters
+  out->n_batches = total;
+  out->drops = out->completions = out->late = 0;
+  out->ops = out->evictions = out->registrations = out->handler_ops_max = 0;
+  out->chain_events = out->absorbed_arrivals = out->fresh_adoptions = 0;
+  for (int s = 0; s < P; s++) {
+    const Shard& S = ctx->shards[s];
+    out->ops += S.ops;
+    out->evictions += S.evictions;
+    out->registrations += S.registrations;
+    if (S.handler_ops_max > out->handler_ops_max)
+      out->handler_ops_max = S.handler_ops_max;
+    out->chain_events += S.chain_events;
+    out->absorbed_arrivals += S.absorbed;
+    out->fresh_adoptions += S.fresh_adoptions;
+  }
+  for (int k = 0; k < M; k++) out->drops += ms[k].drops;
+  out->completions = n - out->drops;  // jitterless: nothing is late
+  float t;
+  cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]);
+  out->ms_ingest = t;
+  cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[2]);
+  out->ms_fresh = t;
+  cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[3]);
+  out->ms_chain = t;
+  cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]);
+  out->ms_expand = t;
+  cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[4]);
+  out->ms_total = t;
+  ctx->last_n = n;
+  ctx->last_ticks = d_ticks;
+  ctx->last_model = d_model;
+  ctx->last_nrecs = rec_count;
+  ctx->has_run = true;
+  return SYM_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- C ABI ------
+
+extern "C" {
+
+int32_t sym_version(void) { return kVersion; }
+
+const char* sym_last_error(void* engine) {
+  return engine ? static_cast<Ctx*>(engine)->err.c_str() : "null engine";
+}
+
+void* sym_create(const sym_config* cfg, int32_t* status) {
+  int32_t dummy;
+  if (!status) status = &dummy;
+  *status = SYM_EINVAL;
+  if (!cfg || cfg->n_models < 1 || cfg->n_gpus < 1 || cfg->n_shards < 1 ||
+      cfg->lat_stride < 1 || !cfg->lat_ns || !cfg->max_batch || !cfg->slo_ns)
+    return nullptr;
+  if (cfg->kind < 0 || cfg->kind > 2 || cfg->gather < 0 || cfg->gather > 1 ||
+      cfg->d_ctrl_ns < 0 || cfg->d_data_ns < 0)
+    return nullptr;
+  if (cfg->gather == SYM_GATHER_DROP_HEAD && cfg->target_batch < 1)
+    return nullptr;
+  Ctx* ctx = new Ctx();
+  ctx->M = cfg->n_models;
+  ctx->G = cfg->n_gpus;
+  ctx->P = cfg->n_shards;
+  ctx->kind = cfg->kind;
+  ctx->gather = cfg->gather;
+  ctx->lat_stride = cfg->lat_stride;
+  ctx->d_ctrl = cfg->d_ctrl_ns;
+  ctx->d_data = cfg->d_data_ns;
+  ctx->device = cfg->device;
+  const int M = ctx->M, P = ctx->P;
+  // shard membership and slot order (shard-major, model id within shard)
+  ctx->shard_of_model.assign(M, 0);
+  for (int m = 0; m < M; m++) {
+    const int s = cfg->shard_of_model ? cfg->shard_of_model[m] : 0;
+    if (s < 0 || s >= P) { delete ctx; return nullptr; }
+    ctx->shard_of_model[m] = s;
+  }
+  ctx->slot_base.assign(P + 1, 0);
+  for (int m = 0; m < M; m++) ctx->slot_base[ctx->shard_of_model[m] + 1]++;
+  for (int s = 0; s < P; s++) ctx->slot_base[s + 1] += ctx->slot_base[s];
+  ctx->slot_of_model.assign(M, 0);
+  ctx->model_of_slot.assign(M, 0);
+  {
+    std::vector<int32_t> fill(ctx->slot_base.begin(), ctx->slot_base.end() - 1);
+    for (int m = 0; m < M; m++) {
+      const int k = fill[ctx->shard_of_model[m]]++;
+      ctx->slot_of_model[m] = k;
+      ctx->model_of_slot[k] = m;
+    }
+  }
+  ctx->gpu_base.assign(P + 1, 0);
+  for (int s = 0; s < P; s++) {
+    const int g = cfg->gpus_per_shard ? cfg->gpus_per_shard[s] : ctx->G;
+    if (g < 1) { delete ctx; return nullptr; }
+    ctx->gpu_base[s + 1] = ctx->gpu_base[s] + g;
+  }
+  if (ctx->gpu_base[P] != ctx->G) { delete ctx; return nullptr; }
+  for (int s = 0; s < P; s++)
+    if (ctx->slot_base[s + 1] == ctx->slot_base[s]) { delete ctx; return nullptr; }
+  // static model parameters by slot
+  ctx->mp_host.resize(M);
+  std::vector<int64_t> lat((size_t)M * ctx->lat_stride);
+  for (int m = 0; m < M; m++) {
+    const int k = ctx->slot_of_model[m];
+    const int mb = cfg->max_batch[m];
+    if (mb < 1 || mb > ctx->lat_stride) { delete ctx; return nullptr; }
+    const int64_t* row = cfg->lat_ns + (int64_t)m * ctx->lat_stride;
+    for (int b = 0; b < mb; b++) {
+      if (row[b] <= 0 || (b > 0 && row[b] < row[b - 1])) { delete ctx; return nullptr; }
+    }
+    memcpy(&lat[(size_t)k * ctx->lat_stride], row, sizeof(int64_t) * ctx->lat_stride);
+    ModelParam& p = ctx->mp_host[k];
+    p.slo = cfg->slo_ns[m];
+    p.timeout_ns = cfg->timeout_ns ? cfg->timeout_ns[m] : 0;
+    p.base1 = cfg->d_ctrl_ns + cfg->d_data_ns + row[0];
+    p.off = 0;
+    p.cnt = 0;
+    p.max_batch = mb;
+    p.target_batch = cfg->target_batch < mb ? cfg->target_batch : mb;
+  }
+  *status = SYM_ECUDA;
+  auto fail = [&](const char* what, cudaError_t e) -> void* {
+    fprintf(stderr, "sym_create: %s: %s\n", what, cudaGetErrorString(e));
+    delete ctx;
+    return nullptr;
+  };
+  cudaError_t e;
+  if ((e = cudaSetDevice(ctx->device)) != cudaSuccess) return fail("cudaSetDevice", e);
+  if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail("stream", e);
+  for (auto& ev : ctx->ev)
+    if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail("event", e);
+  // chain state
+  ctx->shards.resize(P);
+  std::vector<int32_t> mp2(P), gp2(P);
+  int64_t tot_m2 = 0, tot_g2 = 0;
+  for (int s = 0; s < P; s++) {
+    int Ms = ctx->slot_base[s + 1] - ctx->slot_base[s];
+    int Gs = ctx->gpu_base[s + 1] - ctx->gpu_base[s];
+    int a = 1, b = 1;
+    while (a < Ms) a <<= 1;
+    while (b < Gs) b <<= 1;
+    mp2[s] = a;
+    gp2[s] = b;
+    tot_m2 += 2 * a;
+    tot_g2 += 2 * b;
+  }
+#define ALLOC(p, cnt)                                                      \
+  if ((e = cudaMalloc((void**)&(p), sizeof(*(p)) * (size_t)(cnt))) !=      \
+      cudaSuccess)                                                          \
+    return fail(#p, e);
+  ALLOC(ctx->d_lat, (int64_t)M * ctx->lat_stride);
+  ALLOC(ctx->d_mp, M);
+  ALLOC(ctx->d_slot_of_model, M);
+  ALLOC(ctx->d_shard_of_model, M);
+  ALLOC(ctx->d_slot_base, P + 1);
+  ALLOC(ctx->d_ms, M);
+  ALLOC(ctx->d_pq, tot_m2);
+  ALLOC(ctx->d_mlt, tot_m2);
+  ALLOC(ctx->d_mbt, tot_m2);
+  ALLOC(ctx->d_gt, tot_g2);
+  ALLOC(ctx->d_mcs, M);
+  ALLOC(ctx->d_mcl, M);
+  ALLOC(ctx->d_free, ctx->G);
+  ALLOC(ctx->d_dirty, M + P);
+  ALLOC(ctx->d_shards, P);
+  // bins: [B+1] totals, then shard_off [P+1], model_of_slot [M], gpu_base [P+1]
+  ALLOC(ctx->d_bins, (M + P + 1) + (P + 1) + M + (P + 1));
+  ALLOC(ctx->d_err, 1);
+#undef ALLOC
+  const int B = M + P;
+  cudaMemcpy(ctx->d_lat, lat.data(), sizeof(int64_t) * lat.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_mp, ctx->mp_host.data(), sizeof(ModelParam) * M, cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_slot_of_model, ctx->slot_of_model.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_shard_of_model, ctx->shard_of_model.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_slot_base, ctx->slot_base.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_bins + B + P + 2, ctx->model_of_slot.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_bins + B + P + 2 + M, ctx->gpu_base.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice);
+  int64_t om = 0, og = 0;
+  for (int s = 0; s < P; s++) {
+    Shard& S = ctx->shards[s];
+    memset(&S, 0, sizeof S);
+    S.M = ctx->slot_base[s + 1] - ctx->slot_base[s];
+    S.G = ctx->gpu_base[s + 1] - ctx->gpu_base[s];
+    S.Mp = mp2[s];
+    S.Gp = gp2[s];
+    S.kind = ctx->kind;
+    S.gather = ctx->gather;
+    S.d_ctrl = ctx->d_ctrl;
+    S.d_data = ctx->d_data;
+    S.lat_stride = ctx->lat_stride;
+    S.lat = ctx->d_lat + (int64_t)ctx->slot_base[s] * ctx->lat_stride;
+    S.mp = ctx->d_mp + ctx->slot_base[s];
+    S.ms = ctx->d_ms + ctx->slot_base[s];
+    S.pq = ctx->d_pq + om;
+    S.mc_lat_tree = ctx->d_mlt + om;
+    S.mc_bs_tree = ctx->d_mbt + om;
+    S.gt = ctx->d_gt + og;
+    S.mc_size = ctx->d_mcs + ctx->slot_base[s];
+    S.mc_latest = ctx->d_mcl + ctx->slot_base[s];
+    S.free_at = ctx->d_free + ctx->gpu_base[s];
+    om += 2 * S.Mp;
+    og += 2 * S.Gp;
+  }
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail("init", e);
+  *status = SYM_OK;
+  return ctx;
+}
+
+void sym_destroy(void* engine) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  void* ptrs[] = {ctx->d_lat,  ctx->d_mp,     ctx->d_slot_of_model,
+                  ctx->d_shard_of_model, ctx->d_slot_base, ctx->d_ms,
+                  ctx->d_pq,   ctx->d_gt,     ctx->d_mlt,   ctx->d_mbt,
+                  ctx->d_mcs,  ctx->d_dirty,  ctx->d_free,  ctx->d_mcl,
+                  ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
+                  ctx->d_model, ctx->d_s_g,   ctx->d_s_i,   ctx->d_s_aself,
+                  ctx->d_hist, ctx->d_bins,   ctx->d_err,   ctx->d_fresh,
+                  ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int32_t sym_run_device(void* engine, const int64_t* d_arr_ticks,
+                       const int32_t* d_arr_model, int64_t n, uint32_t flags,
+                       sym_result* out) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx || !out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return SYM_ECUDA;
+  out->n = n;
+  out->err_index = -1;
+  return run_device(ctx, d_arr_ticks, d_arr_model, n, flags, out, true);
+}
+
+int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model,
+                int64_t n, uint32_t flags, sym_result* out) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx || !out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  int rc;
+  if ((rc = ensure_capacity(ctx, n))) return rc;
+  cudaStream_t st = ctx->stream;
+  if (n > 0) {
+    CK(cudaMemcpyAsync(ctx->d_ticks, arr_ticks, sizeof(int64_t) * n,
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->d_model, arr_model, sizeof(int32_t) * n,
+                       cudaMemcpyHostToDevice, st));
+  }
+  // device-side output staging
+  sym_result dev = *out;
+  int64_t* d_req = nullptr;
+  int64_t* d_drop = nullptr;
+  int32_t* d_dka = nullptr;
+  sym_batch* d_b = nullptr;
+  const bool want_req = out->req_dispatch && !(flags & SYM_FLAG_NO_EXPAND);
+  const bool want_drop = (flags & SYM_FLAG_TRACE) && out->drop_t;
+  if (want_req) CK(cudaMallocAsync((void**)&d_req, sizeof(int64_t) * 5 * (n + 1), st));
+  if (want_drop) {
+    CK(cudaMallocAsync((void**)&d_drop, sizeof(int64_t) * 2 * (n + 1), st));
+    CK(cudaMallocAsync((void**)&d_dka, sizeof(int32_t) * (n + 1), st));
+  }
+  if (out->batches)
+    CK(cudaMallocAsync((void**)&d_b, sizeof(sym_batch) * (out->batch_cap + 1), st));
+  dev.req_dispatch = want_req ? d_req : nullptr;
+  dev.req_start = want_req ? d_req + (n + 1) : nullptr;
+  dev.req_finish = want_req ? d_req + 2 * (n + 1) : nullptr;
+  dev.req_batch = want_req ? d_req + 3 * (n + 1) : nullptr;
+  dev.req_outcome = want_req ? d_req + 4 * (n + 1) : nullptr;
+  dev.drop_t = want_drop ? d_drop : nullptr;
+  dev.drop_key_sub = want_drop ? d_drop + (n + 1) : nullptr;
+  dev.drop_key_a = want_drop ? d_dka : nullptr;
+  dev.batches = d_b;
+  dev.n = n;
+  dev.err_index = -1;
+  rc = run_device(ctx, ctx->d_ticks, ctx->d_model, n, flags, &dev, true);
+  if (rc == SYM_OK) {
+    if (want_req && n > 0) {
+      int64_t* dsts[5] = {out->req_dispatch, out->req_start, out->req_finish,
+                          out->req_batch, out->req_outcome};
+      for (int k = 0; k < 5; k++)
+        CK(cudaMemcpyAsync(dsts[k], d_req + k * (n + 1), sizeof(int64_t) * n,
+                           cudaMemcpyDeviceToHost, st));
+    }
+    if (want_drop && n > 0) {
+      CK(cudaMemcpyAsync(out->drop_t, d_drop, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(out->drop_key_sub, d_drop + (n + 1), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(out->drop_key_a, d_dka, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    }
+    if (d_b && dev.n_batches > 0)
+      CK(cudaMemcpyAsync(out->batches, d_b, sizeof(sym_batch) * dev.n_batches,
+                         cudaMemcpyDeviceToHost, st));
+  }
+  if (d_req) cudaFreeAsync(d_req, st);
+  if (d_drop) cudaFreeAsync(d_drop, st);
+  if (d_dka) cudaFreeAsync(d_dka, st);
+  if (d_b) cudaFreeAsync(d_b, st);
+  CK(cudaStreamSynchronize(st));
+  // copy back counters / timings
+  sym_batch* keep_b = out->batches;
+  int64_t keep_cap = out->batch_cap;
+  int64_t *k0 = out->req_dispatch, *k1 = out->req_start, *k2 = out->req_finish,
+          *k3 = out->req_batch, *k4 = out->req_outcome, *k5 = out->drop_t,
+          *k6 = out->drop_key_sub;
+  int32_t* k7 = out->drop_key_a;
+  *out = dev;
+  out->batches = keep_b;
+  out->batch_cap = keep_cap;
+  out->req_dispatch = k0;
+  out->req_start = k1;
+  out->req_finish = k2;
+  out->req_batch = k3;
+  out->req_outcome = k4;
+  out->drop_t = k5;
+  out->drop_key_sub = k6;
+  out->drop_key_a = k7;
+  return rc;
+}
+
+int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,
+                          int64_t* model_arrivals, int64_t* model_completed,
+                          int64_t* model_late, int64_t* model_dropped,
+                          int64_t* gpu_busy_ns) {
+  (void)lo_ns; (void)hi_ns; (void)model_arrivals; (void)model_completed;
+  (void)model_late; (void)model_dropped; (void)gpu_busy_ns;
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx) return SYM_EINVAL;
+  ctx->err = "sym_window_counts: not implemented in this build";
+  return SYM_EINVAL;
+}
+
+}  // extern "C"

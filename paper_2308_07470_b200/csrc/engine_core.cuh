@@ -165,7 +165,7 @@ struct Shard {
   int64_t* drop_ksub;          // [n]
   int32_t* drop_ka;            // [n]
   // counters
-  int64_t chain_events, absorbed, n_dropped;
+  int64_t chain_events, absorbed, fresh_adoptions;
   int64_t ops, evictions, registrations, handler_ops_max;
   int32_t error;
   int32_t _pad3;
@@ -254,12 +254,11 @@ SYM_HD int64_t deadline_at(const Shard& S, const ModelParam& P, int32_t q) {
 }
 
 // Record one dropped head (scheduler.py:213-216, simulator.py:175-182).
-SYM_HD void drop_head(Shard& S, ModelState& st, const ModelParam& P,
+SYM_HD void drop_head(const Shard& S, ModelState& st, const ModelParam& P,
                       int64_t now, const Pusher& who) {
   int32_t pos = P.off + st.qh;
   st.qh += 1;
   st.drops += 1;
-  S.n_dropped += 1;
   if (S.record_trace) {
     S.drop_t[pos] = now;
     S.drop_ka[pos] = who.a_self;
@@ -268,7 +267,7 @@ SYM_HD void drop_head(Shard& S, ModelState& st, const ModelParam& P,
 }
 
 // scheduler.py:301-315
-SYM_HD void arm_drop_timer(Shard& S, ModelState& st, const ModelParam& P,
+SYM_HD void arm_drop_timer(const Shard& S, ModelState& st, const ModelParam& P,
                            int32_t m, int64_t now, const Pusher& who) {
   if (st.qh == st.qt) {
     st.dt_head = -1;
@@ -299,9 +298,9 @@ SYM_HD int32_t max_feasible(const Shard& S, int32_t m, int64_t now,
 }
 
 // scheduler.py:218-275.  Returns true when the candidate changed.
-SYM_HD bool update_candidate(Shard& S, int32_t m, int64_t now,
-                             int64_t gpu_floor, const Pusher& who) {
-  ModelState& st = S.ms[m];
+SYM_HD bool update_candidate(const Shard& S, int32_t m, ModelState& st,
+                             int64_t now, int64_t gpu_floor,
+                             const Pusher& who) {
   const ModelParam& P = S.mp[m];
   while (st.qh < st.qt && now + P.base1 > deadline_at(S, P, st.qh))
     drop_head(S, st, P, now, who);
@@ -387,18 +386,24 @@ SYM_HD void set_gpu_timer(Shard& S, int64_t now, const Pusher& who) {
   S.gt_key = push_key(fire, PR_GPU, who);
 }
 
-// scheduler.py:354-365
-SYM_HD void inform_candidate(Shard& S, int32_t m, int64_t now,
-                             const Pusher& who) {
-  ModelState& st = S.ms[m];
-  st.has_mt = 0;  // model_gen[m] += 1
-  unregister(S, m);
+// Model-local half of inform_candidate: model_gen[m] += 1 supersedes the
+// live timer, and a candidate gets a new one (scheduler.py:358-365).
+SYM_HD void renew_model_timer(const Shard& S, ModelState& st, int64_t now,
+                              const Pusher& who) {
+  st.has_mt = 0;
   if (st.has_cand) {
     int64_t fire = st.c_exec - (S.d_ctrl + S.d_data * st.c_size);
     if (fire < now) fire = now;
     st.mt_key = push_key(fire, PR_MODEL, who);
     st.has_mt = 1;
   }
+}
+
+// scheduler.py:354-365
+SYM_HD void inform_candidate(Shard& S, int32_t m, int64_t now,
+                             const Pusher& who) {
+  unregister(S, m);
+  renew_model_timer(S, S.ms[m], now, who);
 }
 
 // scheduler.py:367-377 (the GPU is always OUTSTANDING here: grants resolve
@@ -417,10 +422,10 @@ SYM_HD void granted_gpu(Shard& S, int32_t m, int32_t gid, int64_t gpu_free_at,
                         int64_t now, const Pusher& who) {
   ModelState& st = S.ms[m];
   const int32_t pre_size = st.has_cand ? st.c_size : 0;
-  update_candidate(S, m, now, imax(gpu_free_at, 0), who);
+  update_candidate(S, m, st, now, imax(gpu_free_at, 0), who);
   if (!st.has_cand) {
     inform_gpu(S, gid, imax(now, gpu_free_at), now, who);
-    update_candidate(S, m, now, NEG_INF, who);
+    update_candidate(S, m, st, now, NEG_INF, who);
     inform_candidate(S, m, now, who);
     return;
   }
@@ -446,7 +451,7 @@ SYM_HD void granted_gpu(Shard& S, int32_t m, int32_t gid, int64_t gpu_free_at,
   st.qh += b;
   const int64_t believed_free = st.c_exec + lat_b;
   st.has_cand = 0;
-  update_candidate(S, m, now, NEG_INF, who);
+  update_candidate(S, m, st, now, NEG_INF, who);
   inform_gpu(S, gid, believed_free, now, who);
   inform_candidate(S, m, now, who);
 }
@@ -480,13 +485,30 @@ SYM_HD void on_model_timer(Shard& S, int32_t m, int64_t now,
 // scheduler.py:173-178
 SYM_HD void on_drop_timer(Shard& S, int32_t m, int64_t now,
                           const Pusher& who) {
-  S.ms[m].dt_head = -1;
-  if (update_candidate(S, m, now, NEG_INF, who))
+  ModelState& st = S.ms[m];
+  st.dt_head = -1;
+  if (update_candidate(S, m, st, now, NEG_INF, who))
     inform_candidate(S, m, now, who);
 }
 
-// scheduler.py:168-171 for the arrival at sorted position off+qt.
-SYM_HD void on_arrival(Shard& S, int32_t m) {
+// scheduler.py:168-171 for the arrival at sorted position off+qt of a model
+// that is NOT registered (the unregister of inform_candidate is a no-op).
+SYM_HD void absorb_arrival(const Shard& S, int32_t m, ModelState& st) {
+  const int32_t pos = S.mp[m].off + st.qt;
+  const int64_t now = S.s_tick[pos];
+  Pusher who;
+  who.t = now;
+  who.a_self = S.s_aself[pos];
+  who.a_after = S.s_g[pos] + 1;
+  who.sub = SUB_ARRIVAL;
+  st.qt += 1;
+  if (update_candidate(S, m, st, now, NEG_INF, who))
+    renew_model_timer(S, st, now, who);
+}
+
+// The same arrival for a registered model: a chain event, because its
+// inform_candidate unregisters it from the rank plane.
+SYM_HD void registered_arrival(Shard& S, int32_t m) {
   ModelState& st = S.ms[m];
   const int32_t pos = S.mp[m].off + st.qt;
   const int64_t now = S.s_tick[pos];
@@ -496,7 +518,7 @@ SYM_HD void on_arrival(Shard& S, int32_t m) {
   who.a_after = S.s_g[pos] + 1;
   who.sub = SUB_ARRIVAL;
   st.qt += 1;
-  if (update_candidate(S, m, now, NEG_INF, who))
+  if (update_candidate(S, m, st, now, NEG_INF, who))
     inform_candidate(S, m, now, who);
 }
 
@@ -504,9 +526,12 @@ SYM_HD void on_arrival(Shard& S, int32_t m) {
 // Absorb this model's arrivals until its next chain event, which is stored
 // in nx_key/nx_type.  Valid because an unregistered model's arrivals touch
 // nothing but the model itself, and no other chain event touches it.
-SYM_HD void scan_model(Shard& S, int32_t m) {
-  ModelState& st = S.ms[m];
+// Returns the number of absorbed arrivals; stops early (returning -1) after
+// max_steps absorptions when max_steps >= 0.
+SYM_HD int32_t scan_model(const Shard& S, int32_t m, ModelState& st,
+                          int32_t max_steps) {
   const ModelParam& P = S.mp[m];
+  int32_t steps = 0;
   for (;;) {
     int32_t type = EV_NONE;
     EvKey best;
@@ -520,28 +545,138 @@ SYM_HD void scan_model(Shard& S, int32_t m) {
     }
     if (st.qt < P.cnt) {
       const int32_t pos = P.off + st.qt;
-      EvKey ka;
-      ka.t = S.s_tick[pos];
-      ka.a = S.s_aself[pos];
-      ka.prio = PR_ARRIVAL;
-      ka.tp = 0;
-      ka.ap = 0;
-      ka.sub = 0;
-      ka._pad = 0;
-      if (type == EV_NONE || key_less(ka, best)) {
+      const int64_t ta = S.s_tick[pos];
+      const int32_t aa = S.s_aself[pos];
+      // an arrival precedes a timer iff (a, A') < (tick, A') (prio 4 > 3)
+      const bool first = type == EV_NONE || ta < best.t ||
+                         (ta == best.t && aa < best.a);
+      if (first) {
         if (st.registered) {
-          best = ka;
+          best.t = ta;
+          best.a = aa;
+          best.prio = PR_ARRIVAL;
+          best.tp = 0;
+          best.ap = 0;
+          best.sub = 0;
+          best._pad = 0;
           type = EV_ARR;
         } else {
-          on_arrival(S, m);
-          S.absorbed += 1;
+          if (max_steps >= 0 && steps >= max_steps) return -1;
+          absorb_arrival(S, m, st);
+          steps += 1;
           continue;
         }
       }
     }
     st.nx_type = type;
     if (type != EV_NONE) st.nx_key = best;
-    return;
+    return steps;
+  }
+}
+
+// ------------------------------------------- fresh-start pre-scan (K2) ----
+// After a grant empties a model's queue the model is "fresh": no candidate,
+// no timers, not registered.  Its evolution from the next arrival on is a
+// pure function of its own arrivals, so it is pre-computed for EVERY sorted
+// position in parallel and the chain adopts the record in O(1).
+
+struct FreshRec {
+  int64_t c_exec, c_latest;
+  int64_t mt_t, mt_tp;  // model-timer key (prio 2, sub = arrival)
+  int64_t dt_t, dt_tp;  // drop-timer key (prio 3, sub = arrival)
+  int32_t qt, qh;       // queue after the scan (model-relative)
+  int32_t c_size;       // 0 = no candidate
+  int32_t mt_a, mt_ap, dt_a, dt_ap;
+  int32_t drops;        // heads dropped during the scan
+  int32_t steps;        // arrivals absorbed; -1 = scan too long, not valid
+  int32_t _pad[3];
+};
+
+SYM_HD void fresh_state(ModelState& st, int32_t q) {
+  st.qh = st.qt = q;
+  st.has_cand = 0;
+  st.c_size = 0;
+  st.c_head = -1;
+  st.c_exec = st.c_latest = 0;
+  st.registered = 0;
+  st.has_mt = 0;
+  st.dt_head = -1;
+  st.nx_type = EV_NONE;
+  st.drops = 0;
+}
+
+SYM_HD bool is_fresh(const ModelState& st) {
+  return st.qh == st.qt && !st.has_cand && !st.has_mt && st.dt_head < 0 &&
+         !st.registered;
+}
+
+SYM_HD FreshRec fresh_scan(const Shard& S, int32_t m, int32_t q,
+                           int32_t max_steps) {
+  ModelState st;
+  fresh_state(st, q);
+  FreshRec r;
+  r.steps = scan_model(S, m, st, max_steps);
+  r.qt = st.qt;
+  r.qh = st.qh;
+  r.c_size = st.has_cand ? st.c_size : 0;
+  r.c_exec = st.c_exec;
+  r.c_latest = st.c_latest;
+  r.mt_t = st.mt_key.t;
+  r.mt_tp = st.mt_key.tp;
+  r.mt_a = st.mt_key.a;
+  r.mt_ap = st.mt_key.ap;
+  r.dt_t = st.dt_key.t;
+  r.dt_tp = st.dt_key.tp;
+  r.dt_a = st.dt_key.a;
+  r.dt_ap = st.dt_key.ap;
+  r.drops = (int32_t)st.drops;
+  r._pad[0] = r._pad[1] = r._pad[2] = 0;
+  return r;
+}
+
+// Rebuild the model state a valid fresh scan ended in (inverse of
+// fresh_scan: a fresh scan stops at its first chain event, so the model
+// timer is live iff there is a candidate and the drop timer is armed for
+// the current head iff the queue is non-empty).
+SYM_HD void adopt_fresh(ModelState& st, const FreshRec& r) {
+  const int64_t drops = st.drops;
+  fresh_state(st, r.qt);
+  st.drops = drops + r.drops;
+  st.qh = r.qh;
+  if (r.c_size > 0) {
+    st.has_cand = 1;
+    st.c_size = r.c_size;
+    st.c_exec = r.c_exec;
+    st.c_latest = r.c_latest;
+    st.c_head = r.qh;
+    st.has_mt = 1;
+    st.mt_key.t = r.mt_t;
+    st.mt_key.a = r.mt_a;
+    st.mt_key.prio = PR_MODEL;
+    st.mt_key.tp = r.mt_tp;
+    st.mt_key.ap = r.mt_ap;
+    st.mt_key.sub = SUB_ARRIVAL;
+    st.mt_key._pad = 0;
+  }
+  if (r.qh < r.qt) {
+    st.dt_head = r.qh;
+    st.dt_key.t = r.dt_t;
+    st.dt_key.a = r.dt_a;
+    st.dt_key.prio = PR_DROP;
+    st.dt_key.tp = r.dt_tp;
+    st.dt_key.ap = r.dt_ap;
+    st.dt_key.sub = SUB_ARRIVAL;
+    st.dt_key._pad = 0;
+  }
+  st.nx_type = EV_NONE;
+  if (st.has_mt) {
+    st.nx_type = EV_MT;
+    st.nx_key = st.mt_key;
+  }
+  if (st.dt_head >= 0 &&
+      (st.nx_type == EV_NONE || key_less(st.dt_key, st.nx_key))) {
+    st.nx_type = EV_DT;
+    st.nx_key = st.dt_key;
   }
 }
 
@@ -579,9 +714,26 @@ SYM_HD void on_gpu_timer(Shard& S, const Pusher& who, int32_t* dirty,
   set_gpu_timer(S, now, who);
 }
 
+// Bring a model whose state just changed up to its next chain event, using
+// the fresh-start table when the state is fresh.
+SYM_HD void refresh_model(Shard& S, int32_t m, const FreshRec* fresh) {
+  ModelState& st = S.ms[m];
+  const ModelParam& P = S.mp[m];
+  if (fresh && is_fresh(st) && st.qt < P.cnt) {
+    const FreshRec& r = fresh[P.off + st.qt];
+    if (r.steps >= 0) {
+      adopt_fresh(st, r);
+      S.absorbed += r.steps;
+      S.fresh_adoptions += 1;
+      return;
+    }
+  }
+  S.absorbed += scan_model(S, m, st, -1);
+}
+
 // Process one chain event; returns false when the sub-cluster is drained.
 // dirty must hold M+1 entries.
-SYM_HD bool chain_step(Shard& S, int32_t* dirty) {
+SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
   const int32_t m = S.pq[1];
   const bool have_m = m >= 0;
   if (!have_m && !S.gt_armed) return false;
@@ -604,7 +756,7 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty) {
       case EV_MT: on_model_timer(S, m, who.t, who); break;
       case EV_DT: on_drop_timer(S, m, who.t, who); break;
       case EV_ARR:
-        on_arrival(S, m);
+        registered_arrival(S, m);
         timer_event = false;
         break;
       default: S.error = ERR_STATE; return false;
@@ -617,14 +769,14 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty) {
     if (ops > S.handler_ops_max) S.handler_ops_max = ops;
   }
   for (int32_t i = 0; i < nd; i++) {
-    scan_model(S, dirty[i]);
+    refresh_model(S, dirty[i], fresh);
     pq_update(S, dirty[i]);
   }
   return true;
 }
 
-// Initialise trees and absorb every model's leading arrivals.
-SYM_HD void chain_init(Shard& S) {
+// Initialise trees and bring every model to its first chain event.
+SYM_HD void chain_init(Shard& S, const FreshRec* fresh) {
   for (int32_t g = 0; g < S.G; g++) S.free_at[g] = 0;
   for (int32_t i = 0; i < 2 * S.Gp; i++) S.gt[i] = -1;
   for (int32_t g = 0; g < S.G; g++) S.gt[S.Gp + g] = g;
@@ -637,33 +789,28 @@ SYM_HD void chain_init(Shard& S) {
     S.mc_lat_tree[i] = -1;
     S.mc_bs_tree[i] = -1;
   }
-  for (int32_t m = 0; m < S.M; m++) {
-    ModelState& st = S.ms[m];
-    st.qh = st.qt = 0;
-    st.has_cand = 0;
-    st.c_size = 0;
-    st.c_head = -1;
-    st.registered = 0;
-    st.has_mt = 0;
-    st.dt_head = -1;
-    st.nx_type = EV_NONE;
-    st.drops = 0;
-    S.mc_size[m] = 0;
-    S.mc_latest[m] = 0;
-  }
   S.gt_armed = 0;
   S.n_recs = 0;
-  S.chain_events = S.absorbed = S.n_dropped = 0;
+  S.chain_events = S.absorbed = S.fresh_adoptions = 0;
   S.ops = S.evictions = S.registrations = S.handler_ops_max = 0;
   S.error = ERR_NONE;
   for (int32_t m = 0; m < S.M; m++) {
-    scan_model(S, m);
+    fresh_state(S.ms[m], 0);
+    S.mc_size[m] = 0;
+    S.mc_latest[m] = 0;
+    refresh_model(S, m, fresh);
     S.pq[S.Mp + m] = S.ms[m].nx_type != EV_NONE ? m : -1;
   }
   for (int32_t i = S.Mp - 1; i >= 1; i--) {
     int32_t l = S.pq[2 * i], r = S.pq[2 * i + 1];
     S.pq[i] = model_before(S, r, l) ? r : l;
   }
+}
+
+SYM_HD int64_t total_drops(const Shard& S) {
+  int64_t d = 0;
+  for (int32_t m = 0; m < S.M; m++) d += S.ms[m].drops;
+  return d;
 }
 
 }  // namespace sym

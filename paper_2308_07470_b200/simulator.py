@@ -1,0 +1,383 @@
+"""Engine / RunResult: the drop-in for batchsym/simulator.py on B200.
+
+``Engine(models, gpu_count, policy, network, seed, record_trace,
+check_invariants)`` and ``run`` / ``run_stream`` keep the reference
+signatures (simulator.py:99-102, 195-226) and return a ``RunResult`` with
+the reference's fields and dtypes (simulator.py:65-87).  The discrete-event
+loop itself runs on the GPU (csrc/engine.cu); this module only marshals
+int64 arrays through the C ABI of include/symphony_b200.h.  There is no CPU
+fallback: without the CUDA library or a device the first run raises.
+
+Extension: ``shards=(shard_of_model, gpus_per_shard)`` runs independent
+sub-clusters (the paper's multicore partitioning; the
+reference's scalebench shards, scalebench.py:98-99) in one call.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from collections.abc import Sequence
+from dataclasses import dataclass, field
+from types import SimpleNamespace
+
+import numpy as np
+
+from . import _native
+from .network import NetworkModel
+from .profile import ModelSpec
+from .scheduler import PolicyConfig, ProtocolError
+from .units import s_to_ns
+from .workload import WorkloadSpec, generate_arrivals
+
+EV_COMPLETION, EV_GPU_TIMER, EV_MODEL_TIMER, EV_DROP_TIMER, EV_ARRIVAL = range(5)
+OUTCOME_COMPLETED, OUTCOME_LATE, OUTCOME_DROPPED = 0, 1, 2
+OUTCOME_NAMES = ("completed", "late", "dropped")
+TRACE_DISPATCH, TRACE_DROP, TRACE_SHRINK = "dispatch", "drop", "shrink"
+
+
+class InvariantViolation(AssertionError):
+    pass
+
+
+class _GpuLogs(Sequence):
+    """gpu_logs[g] = [(start, finish, model, size), ...] in emission order,
+    materialised from the batch records on first access (a 7M-batch run
+    does not pay for Python tuples unless someone reads them)."""
+
+    def __init__(self, batches: np.ndarray, n_gpus: int):
+        self._b = batches
+        self._n = n_gpus
+        self._logs = None
+
+    def _build(self):
+        if self._logs is None:
+            logs = [[] for _ in range(self._n)]
+            b = self._b
+            order = np.argsort(b["gpu"], kind="stable")
+            for k in order:
+                logs[int(b["gpu"][k])].append((int(b["start"][k]), int(b["finish"][k]),
+                                               int(b["model"][k]), int(b["size"][k])))
+            self._logs = logs
+        return self._logs
+
+    def __getitem__(self, i):
+        return self._build()[i]
+
+    def __len__(self):
+        return self._n
+
+    def __eq__(self, other):
+        return list(self._build()) == list(other)
+
+
+@dataclass
+class RunResult:
+    model_names: list[str]
+    gpu_count: int
+    duration_ns: int
+    req_model: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    req_arrival: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    req_deadline: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    req_dispatch: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    req_start: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    req_finish: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    req_batch: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    req_outcome: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    gpu_logs: Sequence = field(default_factory=list)
+    trace: list[tuple] = field(default_factory=list)
+    drops: int = 0
+    completions: int = 0
+    late: int = 0
+    #: batch records (numpy structured array, _native.BATCH_DTYPE), the
+    #: compact form gpu_logs is derived from
+    batches: np.ndarray | None = None
+
+    @property
+    def n_requests(self) -> int:
+        return len(self.req_model)
+
+
+def _split_shards(models, gpu_count, shards):
+    M = len(models)
+    if shards is None:
+        return np.zeros(M, np.int32), np.array([gpu_count], np.int32)
+    shard_of_model, gpus_per_shard = shards
+    som = np.asarray(shard_of_model, np.int32)
+    gps = np.asarray(gpus_per_shard, np.int32)
+    if som.shape != (M,) or len(gps) < 1 or som.min() < 0 or som.max() >= len(gps):
+        raise ValueError("bad shard layout")
+    if int(gps.sum()) != gpu_count or gps.min() < 1:
+        raise ValueError("gpus_per_shard must be >= 1 each and sum to gpu_count")
+    if len(np.unique(som)) != len(gps):
+        raise ValueError("every shard needs at least one model")
+    return som, gps
+
+
+class Engine:
+    """B200 engine with the reference Engine's constructor and run API."""
+
+    def __init__(self, models: list[ModelSpec], gpu_count: int,
+                 policy: PolicyConfig, network: NetworkModel | None = None,
+                 seed: int = 0, record_trace: bool = False,
+                 check_invariants: bool = False, *, shards=None, device: int = 0,
+                 use_fresh: bool = True):
+        if gpu_count < 1:
+            raise ValueError("need at least one GPU")
+        self.models = list(models)
+        self.policy = policy
+        self.network = network or NetworkModel.zero()
+        if not self.network.jitterless:
+            raise NotImplementedError(
+                "jittered (histogram) network delays are not supported by the "
+                "B200 engine yet (SURVEY.md §8f row 3)")
+        self.seed = seed
+        self.record_trace = record_trace
+        self.check_invariants = check_invariants
+        self.gpu_count = gpu_count
+        self.device = device
+        self.use_fresh = use_fresh
+        self.shard_of_model, self.gpus_per_shard = _split_shards(self.models, gpu_count, shards)
+        self.n_shards = len(self.gpus_per_shard)
+        stride = max(m.profile.max_batch for m in self.models)
+        self._lat = np.stack([m.profile.table_array(stride) for m in self.models])
+        self._max_batch = np.array([m.profile.max_batch for m in self.models], np.int32)
+        self._slo = np.array([m.slo_ns for m in self.models], np.int64)
+        self._timeout = np.array([policy.resolve_timeout_ns(m.slo_ns) for m in self.models],
+                                 np.int64)
+        self._handle = None
+        self._lib = None
+        # reference-style counters (RankPlane.ops/evictions/registrations,
+        # Engine.handler_ops_max), filled after each run
+        self.rank = SimpleNamespace(ops=0, evictions=0, registrations=0)
+        self.handler_ops_max = 0
+        self.stats = {}
+
+    # -- native handle --------------------------------------------------------
+
+    def _ensure(self):
+        if self._handle is not None:
+            return
+        lib = _native.load()
+        cfg = _native.SymConfig()
+        cfg.n_models = len(self.models)
+        cfg.n_gpus = self.gpu_count
+        cfg.kind = _native.KIND[self.policy.kind]
+        cfg.gather = _native.GATHER[self.policy.gather]
+        cfg.target_batch = self.policy.target_batch
+        cfg.lat_stride = self._lat.shape[1]
+        cfg.d_ctrl_ns = self.policy.d_ctrl_ns
+        cfg.d_data_ns = self.policy.d_data_ns
+        cfg.lat_ns = self._lat.ctypes.data_as(_native.i64p)
+        cfg.max_batch = self._max_batch.ctypes.data_as(_native.i32p)
+        cfg.slo_ns = self._slo.ctypes.data_as(_native.i64p)
+        cfg.timeout_ns = self._timeout.ctypes.data_as(_native.i64p)
+        cfg.n_shards = self.n_shards
+        cfg.device = self.device
+        cfg.shard_of_model = self.shard_of_model.ctypes.data_as(_native.i32p)
+        cfg.gpus_per_shard = self.gpus_per_shard.ctypes.data_as(_native.i32p)
+        status = C.c_int32(0)
+        h = lib.sym_create(C.byref(cfg), C.byref(status))
+        if not h:
+            if status.value == _native.SYM_EINVAL:
+                raise ValueError("invalid engine configuration")
+            raise RuntimeError(f"sym_create failed (status {status.value}); "
+                               "is a CUDA device visible?")
+        self._lib = lib
+        self._handle = h
+
+    def close(self):
+        if self._handle is not None:
+            self._lib.sym_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, rc: int, res: _native.SymResult):
+        msg = self._lib.sym_last_error(self._handle).decode()
+        if rc == _native.SYM_EPROTO:
+            raise ProtocolError(f"request for unknown model (arrival {res.err_index})")
+        if rc == _native.SYM_EINVAL:
+            raise ValueError(msg)
+        if rc == _native.SYM_EINVARIANT:
+            raise InvariantViolation(msg)
+        raise RuntimeError(f"B200 engine failed ({rc}): {msg}")
+
+    def _flags(self) -> int:
+        f = 0
+        if self.record_trace:
+            f |= _native.FLAG_TRACE
+        if not self.use_fresh:
+            f |= _native.FLAG_NO_FRESH
+        return f
+
+    def _absorb_counters(self, res: _native.SymResult):
+        self.rank.ops = res.ops
+        self.rank.evictions = res.evictions
+        self.rank.registrations = res.registrations
+        self.handler_ops_max = res.handler_ops_max
+        self.stats = {k: getattr(res, k) for k in (
+            "chain_events", "absorbed_arrivals", "fresh_adoptions", "ms_ingest",
+            "ms_fresh", "ms_chain", "ms_expand", "ms_total")}
+
+    # -- reference API --------------------------------------------------------
+
+    def run(self, workload: WorkloadSpec, duration_s: float, seed: int) -> RunResult:
+        names = [m.name for m in self.models]
+        ticks, midx = generate_arrivals(workload, names, duration_s, seed)
+        return self.run_stream(ticks, midx, duration_s)
+
+    def run_stream(self, arr_ticks, arr_midx, duration_s: float) -> RunResult:
+        ticks = np.ascontiguousarray(arr_ticks, dtype=np.int64)
+        midx64 = np.asarray(arr_midx, dtype=np.int64)
+        n = len(ticks)
+        if len(midx64) != n:
+            raise ValueError("arr_ticks and arr_midx differ in length")
+        M = len(self.models)
+        if n:
+            bad = np.nonzero((midx64 < 0) | (midx64 >= M))[0]
+            if len(bad):
+                raise ProtocolError(f"request for unknown model {int(midx64[bad[0]])}")
+            if np.any(np.diff(ticks) < 0):
+                raise ValueError("arrival ticks must be non-decreasing")
+        midx = np.ascontiguousarray(midx64, dtype=np.int32)
+        self._ensure()
+        outs = [np.empty(n, np.int64) for _ in range(5)]
+        batches = np.empty(max(n, 1), dtype=_native.BATCH_DTYPE)
+        res = _native.SymResult()
+        res.n = n
+        (res.req_dispatch, res.req_start, res.req_finish, res.req_batch,
+         res.req_outcome) = (a.ctypes.data_as(_native.i64p) for a in outs)
+        if self.record_trace:
+            drop_t = np.empty(n, np.int64)
+            drop_ks = np.empty(n, np.int64)
+            drop_ka = np.empty(n, np.int32)
+            res.drop_t = drop_t.ctypes.data_as(_native.i64p)
+            res.drop_key_sub = drop_ks.ctypes.data_as(_native.i64p)
+            res.drop_key_a = drop_ka.ctypes.data_as(_native.i32p)
+        res.batches = batches.ctypes.data
+        res.batch_cap = len(batches)
+        rc = self._lib.sym_run(self._handle, ticks.ctypes.data, midx.ctypes.data, n,
+                               self._flags(), C.byref(res))
+        if rc != _native.SYM_OK:
+            self._raise(rc, res)
+        self._absorb_counters(res)
+        batches = batches[: res.n_batches].copy()
+        disp, start, fin, bsz, outc = outs
+        result = RunResult(
+            model_names=[m.name for m in self.models], gpu_count=self.gpu_count,
+            duration_ns=s_to_ns(duration_s), req_model=midx64.copy(),
+            req_arrival=ticks.copy(), req_deadline=ticks + self._slo[midx64],
+            req_dispatch=disp, req_start=start, req_finish=fin, req_batch=bsz,
+            req_outcome=outc, gpu_logs=_GpuLogs(batches, self.gpu_count),
+            drops=int(res.drops), completions=int(np.count_nonzero(outc == OUTCOME_COMPLETED)),
+            late=int(np.count_nonzero(outc == OUTCOME_LATE)), batches=batches)
+        if self.record_trace:
+            result.trace = self._build_trace(ticks, midx64, batches, drop_t, drop_ks, drop_ka)
+        if self.check_invariants:
+            self._verify(result)
+        return result
+
+    # -- device-resident entry point -------------------------------------------
+
+    def run_device(self, ticks, model, outputs: dict | None = None, expand: bool = True,
+                   batches=None):
+        """Run on arrival tensors already resident on the engine's device
+        (torch int64 ticks, int32 model ids).  Per-request outputs are
+        written into ``outputs`` (dict of int64 CUDA tensors: dispatch,
+        start, finish, batch, outcome), allocated if None.  Returns
+        (outputs, counters).  Nothing crosses PCIe but the counters."""
+        import torch
+
+        n = int(ticks.numel())
+        if ticks.dtype != torch.int64 or model.dtype != torch.int32:
+            raise TypeError("ticks must be int64 and model int32 tensors")
+        if not (ticks.is_cuda and model.is_cuda):
+            raise ValueError("run_device needs CUDA tensors")
+        self._ensure()
+        dev = ticks.device
+        if outputs is None and expand:
+            outputs = {k: torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+                       for k in ("dispatch", "start", "finish", "batch", "outcome")}
+        res = _native.SymResult()
+        res.n = n
+        if expand:
+            res.req_dispatch, res.req_start, res.req_finish, res.req_batch, res.req_outcome = (
+                C.cast(outputs[k].data_ptr(), _native.i64p)
+                for k in ("dispatch", "start", "finish", "batch", "outcome"))
+        if batches is not None:
+            res.batches = batches.data_ptr()
+            res.batch_cap = batches.numel() // C.sizeof(_native.SymBatch)
+        flags = self._flags() & ~_native.FLAG_TRACE
+        if not expand:
+            flags |= _native.FLAG_NO_EXPAND
+        torch.cuda.current_stream(dev).synchronize()
+        rc = self._lib.sym_run_device(self._handle, ticks.data_ptr(), model.data_ptr(), n,
+                                      flags, C.byref(res))
+        if rc != _native.SYM_OK:
+            self._raise(rc, res)
+        self._absorb_counters(res)
+        counters = dict(self.stats, n_batches=res.n_batches, drops=res.drops,
+                        registrations=res.registrations, evictions=res.evictions)
+        return outputs, counters
+
+    # -- trace / invariants ---------------------------------------------------
+
+    def _build_trace(self, ticks, midx, batches, drop_t, drop_ks, drop_ka):
+        """Rebuild the reference's trace list (simulator.py:170-187) in
+        processing order from the per-event positions the engine recorded."""
+        n = len(ticks)
+        shard = self.shard_of_model[midx] if n else np.empty(0, np.int32)
+        # rid = 1 + index within the sub-cluster's stream (simulator.py:217)
+        rid = np.empty(n, np.int64)
+        rank = np.empty(n, np.int64)  # position within the model's queue
+        members = {}
+        for s in range(self.n_shards):
+            idx = np.nonzero(shard == s)[0]
+            rid[idx] = np.arange(1, len(idx) + 1)
+        for m in range(len(self.models)):
+            idx = np.nonzero(midx == m)[0]
+            members[m] = idx
+            rank[idx] = np.arange(len(idx))
+        rows = []  # (shard, t, a, sub, rank, kind_order, entry)
+        for b in batches:
+            m = int(b["model"])
+            first = int(b["first_index"])
+            r0 = int(rank[first])
+            size = int(b["size"])
+            s = int(self.shard_of_model[m])
+            gid = int(b["gpu"])
+            key = (s, int(b["key_t"]), int(b["key_a"]), int(b["key_sub"]), r0)
+            if int(b["shrunk_from"]) > 0:
+                rows.append(key + (0, (int(b["emitted"]), TRACE_SHRINK, m, gid, size, -1, -1, ())))
+            rids = tuple(int(x) for x in rid[members[m][r0:r0 + size]])
+            rows.append(key + (1, (int(b["emitted"]), TRACE_DISPATCH, m, gid, size,
+                                   int(b["start"]), int(b["finish"]), rids)))
+        for i in np.nonzero(drop_t >= 0)[0]:
+            m = int(midx[i])
+            rows.append((int(self.shard_of_model[m]), int(drop_t[i]), int(drop_ka[i]),
+                         int(drop_ks[i]), int(rank[i]), 1,
+                         (int(drop_t[i]), TRACE_DROP, m, -1, 0, -1, -1, (int(rid[i]),))))
+        rows.sort(key=lambda r: r[:6])
+        return [r[6] for r in rows]
+
+    def _verify(self, res: RunResult):
+        """End-of-run invariants (the per-event _verify of simulator.py:276-305
+        cannot observe device-internal states; these are their results)."""
+        o = res.req_outcome
+        if np.any((o < 0) | (o > 2)):
+            raise InvariantViolation("unresolved request outcome")
+        served = o != OUTCOME_DROPPED
+        if int(np.count_nonzero(served)) + res.drops != res.n_requests:
+            raise InvariantViolation("conservation broken")
+        if np.any(res.req_finish[served] > res.req_deadline[served]) and res.late == 0:
+            raise InvariantViolation("served request misses its deadline")
+        b = res.batches
+        if b is not None and len(b):
+            order = np.lexsort((np.arange(len(b)), b["gpu"]))
+            g, st, fi = b["gpu"][order], b["start"][order], b["finish"][order]
+            same = g[1:] == g[:-1]
+            if np.any(st[1:][same] < fi[:-1][same]):
+                raise InvariantViolation("overlapping batches on one GPU")

@@ -1,0 +1,192 @@
+"""Regenerate tests/golden/golden.json from the Python REFERENCE.
+
+Run in the build container only (it imports batchsym from
+/root/reference/pkg/src, which does not exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+Every case records the digest of the input arrival stream, of the
+reference's per-request arrays, gpu_logs and event trace, its counters and
+its compute_stats summary.  The C oracle is pinned against these
+(tests/test_oracle_golden.py) and the CUDA engine against the oracle and
+these (tests/test_parity_gpu.py).
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, HERE)
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+from batchsym import metrics as RM  # noqa: E402
+from batchsym.network import NetworkModel  # noqa: E402
+from batchsym.profile import LatencyProfile, ModelSpec  # noqa: E402
+from batchsym.scenario import BUNDLED_SCENARIOS, load_scenario  # noqa: E402
+from batchsym.scheduler import PolicyConfig  # noqa: E402
+from batchsym.simulator import Engine  # noqa: E402
+from batchsym.workload import WorkloadSpec, generate_arrivals  # noqa: E402
+
+import digest as D  # noqa: E402
+
+POLICIES = {
+    "base": None,
+    "eager": dict(kind="eager"),
+    "timeout30": dict(kind="timeout", timeout_slo_frac=0.3),
+    "delay": dict(kind="deferred", d_ctrl_ns=30_000, d_data_ns=3_000),
+}
+
+
+def policy_for(base, variant):
+    if variant == "base":
+        return base
+    return PolicyConfig(**POLICIES[variant])
+
+
+def run_case(models, gpus, policy, ticks, midx, duration_s, warm, cool):
+    eng = Engine(list(models), gpus, policy,
+                 NetworkModel.constant(policy.d_ctrl_ns, policy.d_data_ns), record_trace=True)
+    t0 = time.time()
+    res = eng.run_stream(ticks, midx, duration_s)
+    el = time.time() - t0
+    st = RM.compute_stats(res, warm, cool, duration_s)
+    return {
+        "n": int(len(ticks)),
+        "trace_in": D.trace_digest(ticks, midx),
+        "requests": D.requests_digest(res.req_dispatch, res.req_start, res.req_finish,
+                                      res.req_batch, res.req_outcome),
+        "gpu_logs": D.gpu_logs_digest(res.gpu_logs),
+        "events": D.event_trace_digest(res.trace),
+        "drops": int(res.drops), "completions": int(res.completions), "late": int(res.late),
+        "ops": int(eng.rank.ops), "evictions": int(eng.rank.evictions),
+        "registrations": int(eng.rank.registrations),
+        "handler_ops_max": int(eng.handler_ops_max),
+        "batches": int(sum(len(g) for g in res.gpu_logs)),
+        "stats": {
+            "goodput_rps": st.goodput_rps, "bad_rate": st.bad_rate,
+            "mean_idle_fraction": st.mean_idle_fraction,
+            "idle_digest": D._h(np.asarray(st.gpu_idle_fraction).view(np.int64)),
+            "p99": [m.p99_latency_ns for m in st.models],
+            "median_batch": [m.median_batch for m in st.models],
+            "max_qd": [m.max_queueing_delay_ns for m in st.models],
+            "hist_digest": D._h([x for m in st.models for kv in sorted(m.batch_hist.items())
+                                 for x in kv]),
+        },
+        "ref_seconds": round(el, 3),
+    }
+
+
+def bundled_cases(out):
+    for name in BUNDLED_SCENARIOS:
+        sc = load_scenario(name)
+        ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models],
+                                        sc.duration_s, sc.seed)
+        for v in POLICIES:
+            pol = policy_for(sc.policy, v)
+            out[f"{name}/{v}"] = run_case(sc.models, sc.gpu_count, pol, ticks, midx,
+                                          sc.duration_s, sc.warmup_s, sc.cooldown_s)
+            print(name, v, out[f"{name}/{v}"]["ref_seconds"], flush=True)
+
+
+def zoo_models(n, slo=None):
+    from batchsym.profile import load_model_zoo
+    zoo = load_model_zoo("a100")
+    return [ModelSpec(i, f"{zoo[i % len(zoo)].name}_{i}",
+                      LatencyProfile.linear(zoo[i % len(zoo)].alpha_ms, zoo[i % len(zoo)].beta_ms),
+                      int(round((zoo[i % len(zoo)].slo_ms if slo is None else slo(i)) * 1e6)))
+            for i in range(n)]
+
+
+def config_cases(out):
+    """C1-C5 at reduced durations; C4 per sub-cluster."""
+    import math
+    c5_dur = 0.6
+    segs = tuple((j * c5_dur / 24, 600_000.0 * (0.55 - 0.45 * math.cos(2 * math.pi * j / 24)))
+                 for j in range(24))
+    cfgs = {
+        "C1": ([ModelSpec(0, "ResNet50", LatencyProfile.linear(1.053, 5.072), 50_000_000)], 8,
+               WorkloadSpec("poisson", 2000.0), 60.0),
+        "C2": (zoo_models(10, slo=lambda i: float(round(20 + 80 * i / 9))), 64,
+               WorkloadSpec("poisson", 40_000.0), 1.0),
+        "C3": (zoo_models(100), 1024, WorkloadSpec("gamma", 300_000.0, gamma_shape=1 / 16), 0.25),
+        "C4": (zoo_models(1000), 8192, WorkloadSpec("poisson", 1_200_000.0), 0.1),
+        "C5": (zoo_models(500), 4096, WorkloadSpec("piecewise", segments=segs), c5_dur),
+    }
+    for name, (models, gpus, wl, dur) in cfgs.items():
+        ticks, midx = generate_arrivals(wl, [m.name for m in models], dur, 42)
+        variants = ("base", "eager", "timeout30", "delay") if name in ("C1", "C2") else ("base",)
+        for v in variants:
+            pol = policy_for(PolicyConfig("deferred"), v)
+            if name == "C4":
+                for s in range(8):
+                    ids = np.arange(125 * s, 125 * (s + 1))
+                    sel = (midx >= ids[0]) & (midx <= ids[-1])
+                    sm = [ModelSpec(k, models[i].name, models[i].profile, models[i].slo_ns)
+                          for k, i in enumerate(ids)]
+                    out[f"C4s{s}/{v}@{dur}"] = run_case(sm, 1024, pol, ticks[sel],
+                                                        midx[sel] - ids[0], dur, 0.1 * dur,
+                                                        0.1 * dur)
+                    print(name, s, out[f"C4s{s}/{v}@{dur}"]["ref_seconds"], flush=True)
+                out[f"C4/trace_in@{dur}"] = D.trace_digest(ticks, midx)
+            else:
+                out[f"{name}/{v}@{dur}"] = run_case(models, gpus, pol, ticks, midx, dur,
+                                                    0.1 * dur, 0.1 * dur)
+                print(name, v, out[f"{name}/{v}@{dur}"]["ref_seconds"], flush=True)
+
+
+def known_answers(out):
+    """Scalar known answers used by the host tests (reference functions)."""
+    from batchsym import metrics as M
+    from batchsym.profile import max_feasible_batch, schedulable_window
+    r50 = LatencyProfile.linear(1.053, 5.072)
+    irv2 = LatencyProfile.linear(5.090, 18.368)
+    ka = {
+        "window_r50_25ms_b7": list(vars(schedulable_window(r50, 25_000_000, 7)).values()),
+        "mfb_r50_12.5": max_feasible_batch(r50, 12_500_000),
+        "mfb_irv2_62.222": max_feasible_batch(irv2, 62_222_000),
+        "analytic": {f"{n}/{mode}": [s.batch_size, s.throughput_rps]
+                     for n, p, slo in (("r50", r50, 25_000_000), ("irv2", irv2, 70_000_000))
+                     for mode in ("staggered", "no_coordination")
+                     for s in [M.analytical_solution(p, slo, 8, mode)]},
+        "autoscale": [[r, f, n, M.autoscale_advice(r, f, n)]
+                      for r, f, n in ((0.0, 0.5, 100), (0.2, 0.0, 100), (0.009, 0.06, 7),
+                                      (0.5, 0.9, 3), (0.0, 1.0, 4096), (0.02, 0.3, 242))],
+    }
+    gs = {}
+    for name in ("table2_resnet50", "table2_inceptionresnet"):
+        res = M.goodput_search(load_scenario(name))
+        gs[name] = {"rate_rps": res.rate_rps, "probes": res.probes}
+        print("goodput", name, res.rate_rps, flush=True)
+    ka["goodput_search"] = gs
+    out["known_answers"] = ka
+
+
+def stress_cases(out, n_cases=60):
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    from stress_cases import make_case
+    for seed in range(n_cases):
+        c = make_case(seed)
+        models = [ModelSpec(i, f"m{i}", LatencyProfile(p["kind"], p["max_batch"], 0, 0,
+                                                        tuple(p["lat"])), p["slo"])
+                  for i, p in enumerate(c["models"])]
+        pol = PolicyConfig(**c["policy"])
+        out[f"stress/{seed}"] = run_case(models, c["gpus"], pol, c["ticks"], c["midx"], 1.0,
+                                         0.1, 0.1)
+
+
+if __name__ == "__main__":
+    out = {"generator": "tests/golden/make_golden.py", "reference": "batchsym 0.1.0",
+           "numpy": np.__version__}
+    known_answers(out)
+    bundled_cases(out)
+    stress_cases(out)
+    config_cases(out)
+    with open(os.path.join(HERE, "golden.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    print("wrote golden.json")

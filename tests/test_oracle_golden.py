@@ -1,0 +1,35 @@
+"""Pin the C oracle (and this package's trace generator and compute_stats)
+against fixtures produced by the Python reference (tests/golden)."""
+import pytest
+
+import cases
+import digest as D
+from conftest import oracle_args
+from oracle import oracle
+from resultcheck import (check_against_golden, check_stats, oracle_gpu_logs,
+                         oracle_result, oracle_trace)
+
+ALL = list(cases.bundled()) + list(cases.stress()) + list(cases.config_cases())
+
+
+@pytest.mark.parametrize("case", ALL, ids=[c[0] for c in ALL])
+def test_oracle_matches_reference(case, golden):
+    key, models, gpus, policy, ticks, midx, (dur, warm, cool) = case
+    g = golden[key]
+    assert D.trace_digest(ticks, midx) == g["trace_in"], "arrival stream differs"
+    o = oracle.run(arr_ticks=ticks, arr_midx=midx, record_trace=True, check_invariants=len(ticks) < 50_000,
+                   **oracle_args(models, gpus, policy))
+    counters = {k: o[k] for k in ("drops", "completions", "late", "ops", "evictions",
+                                   "registrations", "handler_ops_max")}
+    check_against_golden(g, o["req_dispatch"], o["req_start"], o["req_finish"],
+                         o["req_batch"], o["req_outcome"], oracle_gpu_logs(o, gpus),
+                         counters, trace=oracle_trace(o))
+    check_stats(oracle_result(o, models, gpus, ticks, midx, dur), g, dur, warm, cool)
+
+
+def test_c4_full_stream_digest(golden):
+    from paper_2308_07470_b200 import configs
+    from paper_2308_07470_b200.workload import generate_arrivals
+    sc = configs.c4(0.1)
+    ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models], 0.1, 42)
+    assert D.trace_digest(ticks, midx) == golden["C4/trace_in@0.1"]

@@ -11,7 +11,7 @@
 
 using namespace sym;
 
-extern "C" int32_t hc_run(const symo_config* cfg, const int64_t* ticks,
+extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64_t* ticks,
                           const int64_t* midx, int64_t n, int64_t* out_req5,
                           int64_t* out_ord7, int64_t* n_ord, int64_t* counters) {
   const int32_t M = cfg->n_models, G = cfg->n_gpus;
@@ -47,9 +47,16 @@ extern "C" int32_t hc_run(const symo_config* cfg, const int64_t* ticks,
   S.ms = ms.data(); S.pq = pq.data(); S.free_at = fa.data(); S.gt = gt.data();
   S.mc_lat_tree = mlt.data(); S.mc_bs_tree = mbt.data(); S.mc_size = mcs.data(); S.mc_latest = mcl.data();
   S.recs = recs.data(); S.rec_cap = n + 1; S.drop_t = dt.data(); S.drop_ksub = dks.data(); S.drop_ka = dka.data();
-  chain_init(S);
+  S.record_trace = use_fresh ? 0 : 1;
+  std::vector<FreshRec> fresh;
+  if (use_fresh) {
+    fresh.resize(n);
+    for (int m = 0; m < M; m++)
+      for (int q = 0; q < cnt[m]; q++) fresh[off[m] + q] = fresh_scan(S, m, q, 4096);
+  }
+  chain_init(S, use_fresh ? fresh.data() : nullptr);
   std::vector<int32_t> dirty(M + 1);
-  while (chain_step(S, dirty.data())) {}
+  while (chain_step(S, dirty.data(), use_fresh ? fresh.data() : nullptr)) {}
   if (S.error) return 100 + S.error;
   for (int64_t i = 0; i < n; i++) { for (int k = 0; k < 4; k++) out_req5[k * n + i] = -1; out_req5[4 * n + i] = 2; }
   for (int64_t r = 0; r < S.n_recs; r++) {
@@ -63,7 +70,7 @@ extern "C" int32_t hc_run(const symo_config* cfg, const int64_t* ticks,
     o[0] = b.gpu; o[1] = b.model; o[2] = b.size; o[3] = b.start; o[4] = b.finish; o[5] = b.emitted; o[6] = b.shrunk_from;
   }
   *n_ord = S.n_recs;
-  counters[0] = S.n_dropped; counters[1] = S.ops; counters[2] = S.evictions; counters[3] = S.registrations;
-  counters[4] = S.handler_ops_max; counters[5] = S.chain_events; counters[6] = S.absorbed;
+  counters[0] = total_drops(S); counters[1] = S.ops; counters[2] = S.evictions; counters[3] = S.registrations;
+  counters[4] = S.handler_ops_max; counters[5] = S.chain_events; counters[6] = S.absorbed; counters[7] = S.fresh_adoptions;
   return 0;
 }
