@@ -103,6 +103,7 @@ typedef struct {
   int64_t drops, completions, late;
   int64_t ops, evictions, registrations, handler_ops_max;
   int64_t chain_events, absorbed_arrivals, fresh_adoptions;
+  int64_t launches;           /* kernels this call launched */
   /* device timings of the last run (CUDA events on the engine stream) */
   float ms_ingest, ms_fresh, ms_chain, ms_expand, ms_total;
   int64_t err_index;          /* offending stream index for SYM_EPROTO */

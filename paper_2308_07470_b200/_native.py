@@ -59,7 +59,7 @@ class SymResult(C.Structure):
         ("ops", C.c_int64), ("evictions", C.c_int64), ("registrations", C.c_int64),
         ("handler_ops_max", C.c_int64),
         ("chain_events", C.c_int64), ("absorbed_arrivals", C.c_int64),
-        ("fresh_adoptions", C.c_int64),
+        ("fresh_adoptions", C.c_int64), ("launches", C.c_int64),
         ("ms_ingest", C.c_float), ("ms_fresh", C.c_float), ("ms_chain", C.c_float),
         ("ms_expand", C.c_float), ("ms_total", C.c_float),
         ("err_index", C.c_int64),

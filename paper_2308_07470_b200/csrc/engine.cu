@@ -405,6 +405,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
 int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                int64_t n, uint32_t flags, sym_result* out, bool outs_on_device) {
   cudaStream_t st = ctx->stream;
+  int64_t launches = 0;
   const int32_t M = ctx->M, P = ctx->P;
   const int B = M + P;
   const bool trace = flags & SYM_FLAG_TRACE;
@@ -419,14 +420,14 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const int wpb = 4;
   const size_t smem = sizeof(int32_t) * (size_t)B * wpb;
   if (W > 0) {
-    k_hist<<<nblk(W, wpb), 32 * wpb, smem, st>>>(
+    ++launches, k_hist<<<nblk(W, wpb), 32 * wpb, smem, st>>>(
         d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_err);
-    k_colscan<<<nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, ctx->d_bins);
+    ++launches, k_colscan<<<nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, ctx->d_bins);
   } else {
     CK(cudaMemsetAsync(ctx->d_bins, 0, sizeof(int32_t) * B, st));
   }
-  k_binoff<<<1, 32, 0, st>>>(ctx->d_bins, M, P, ctx->d_mp,
+  ++launches, k_binoff<<<1, 32, 0, st>>>(ctx->d_bins, M, P, ctx->d_mp,
                              ctx->d_bins + B + 1);
   int32_t herr = INT32_MAX;
   CK(cudaMemcpyAsync(&herr, ctx->d_err, sizeof herr, cudaMemcpyDeviceToHost, st));
@@ -437,12 +438,12 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     return SYM_EPROTO;
   }
   if (W > 0)
-    k_scatter<<<nblk(W, wpb), 32 * wpb, smem, st>>>(
+    ++launches, k_scatter<<<nblk(W, wpb), 32 * wpb, smem, st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, ctx->d_bins, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
         ctx->d_sh_tick);
   if (n > 0)
-    k_aself<<<nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
+    ++launches, k_aself<<<nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
                                           ctx->d_sh_tick, ctx->d_bins + B + 1,
                                           P, n, ctx->d_s_aself);
   CK(cudaGetLastError());
@@ -475,15 +476,15 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
                      cudaMemcpyHostToDevice, st));
   if (trace && n > 0)
-    k_fill64<<<nblk(n, 256), 256, 0, st>>>(ctx->d_drop_t, n, -1);
+    ++launches, k_fill64<<<nblk(n, 256), 256, 0, st>>>(ctx->d_drop_t, n, -1);
   // ---- K2 fresh-start pre-scan
   if (use_fresh && n > 0)
-    k_fresh<<<nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
+    ++launches, k_fresh<<<nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
                                           ctx->d_mp, P, n, ctx->d_fresh);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
   // ---- K4 chain
-  k_chain<<<P, 32, 0, st>>>(ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr,
+  ++launches, k_chain<<<P, 32, 0, st>>>(ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr,
                             ctx->d_dirty, ctx->d_slot_base);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[3], st));
@@ -514,17 +515,17 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                      cudaMemcpyHostToDevice, st));
   const bool expand = !(flags & SYM_FLAG_NO_EXPAND) && out->req_dispatch;
   if (expand && n > 0) {
-    k_init_out<<<nblk(n, 256), 256, 0, st>>>(n, out->req_dispatch,
+    ++launches, k_init_out<<<nblk(n, 256), 256, 0, st>>>(n, out->req_dispatch,
                                              out->req_start, out->req_finish,
                                              out->req_batch, out->req_outcome);
     if (total > 0)
-      k_expand<<<nblk(total * 32, 256), 256, 0, st>>>(
+      ++launches, k_expand<<<nblk(total * 32, 256), 256, 0, st>>>(
           ctx->d_recs, d_meta, d_meta + P + 1, P, ctx->d_s_i, ctx->d_s_tick,
           ctx->d_mp, ctx->d_slot_base, total, out->req_dispatch,
           out->req_start, out->req_finish, out->req_batch, out->req_outcome);
   }
   if (trace && out->drop_t && n > 0)
-    k_drop_out<<<nblk(n, 256), 256, 0, st>>>(
+    ++launches, k_drop_out<<<nblk(n, 256), 256, 0, st>>>(
         n, ctx->d_s_i, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
         out->drop_t, out->drop_key_sub, out->drop_key_a);
   if (out->batches && total > 0) {
@@ -533,7 +534,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
       cudaFreeAsync(d_meta, st);
       return SYM_EINVAL;
     }
-    k_copy_batches<<<nblk(total, 256), 256, 0, st>>>(
+    ++launches, k_copy_batches<<<nblk(total, 256), 256, 0, st>>>(
         ctx->d_recs, d_meta, d_meta + P + 1, P, ctx->d_s_i,
         ctx->d_bins + B + P + 2, ctx->d_slot_base, ctx->d_bins + B + P + 2 + M,
         total, out->batches);
@@ -545,6 +546,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   (void)outs_on_device;
   // ---- counters
   out->n_batches = total;
+  out->launches = launches;
   out->drops = out->completions = out->late = 0;
   out->ops = out->evictions = out->registrations = out->handler_ops_max = 0;
   out->chain_events = out->absorbed_arrivals = out->fresh_adoptions = 0;

@@ -219,7 +219,7 @@ class Engine:
         self.rank.registrations = res.registrations
         self.handler_ops_max = res.handler_ops_max
         self.stats = {k: getattr(res, k) for k in (
-            "chain_events", "absorbed_arrivals", "fresh_adoptions", "ms_ingest",
+            "chain_events", "absorbed_arrivals", "fresh_adoptions", "launches", "ms_ingest",
             "ms_fresh", "ms_chain", "ms_expand", "ms_total")}
 
     # -- reference API --------------------------------------------------------
