@@ -18,7 +18,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/symphony_b200.h"
@@ -57,6 +59,7 @@ struct Ctx {
   int64_t *d_free = nullptr, *d_mcl = nullptr;
   Shard* d_shards = nullptr;
   std::vector<Shard> shards;        // host images
+  size_t chain_smem = 0;            // dynamic smem of k_chain
   // per-run buffers (grown)
   int64_t cap = 0, W_cap = 0;
   int64_t *d_ticks = nullptr, *d_s_tick = nullptr, *d_sh_tick = nullptr;
@@ -260,16 +263,61 @@ k_fresh(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
 
 // --------------------------------------------------------------- K4 -------
 
+// Shared-memory plan of one sub-cluster's chain state.  Arrays are placed in
+// smem in order of how often the chain touches them; whatever does not fit
+// stays in its global scratch (the chain is agnostic: it only sees pointers).
+struct SmemPlan {
+  static SYM_HD size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+  static SYM_HD size_t need(const Shard& S) {
+    return al(sizeof(int32_t) * 2 * S.Gp) + al(sizeof(int64_t) * S.G) +
+           al(sizeof(int32_t) * 2 * S.Mp) + al(sizeof(ModelState) * S.M) +
+           al(sizeof(ModelParam) * S.M) + 2 * al(sizeof(int32_t) * 2 * S.Mp) +
+           al(sizeof(int32_t) * S.M) + al(sizeof(int64_t) * S.M);
+  }
+};
+
 __global__ void __launch_bounds__(32)
 k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
-        int32_t* __restrict__ dirty_all, const int32_t* __restrict__ slot_base) {
+        int32_t* __restrict__ dirty_all, const int32_t* __restrict__ slot_base,
+        size_t smem_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Shard S;  // hot scalars of the sub-cluster live in smem
   if (threadIdx.x != 0) return;
   S = shards[blockIdx.x];
+  ModelState* const ms_global = S.ms;
+  size_t used = 0;
+  auto place = [&](auto*& ptr, size_t bytes, bool copy_in) {
+    bytes = SmemPlan::al(bytes);
+    if (used + bytes > smem_bytes) return false;
+    using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
+    T* dst = reinterpret_cast<T*>(smem + used);
+    if (copy_in) {
+      const uint4* src = reinterpret_cast<const uint4*>(ptr);
+      uint4* d = reinterpret_cast<uint4*>(dst);
+      for (size_t k = 0; k < bytes / 16; k++) d[k] = src[k];
+    }
+    ptr = dst;
+    used += bytes;
+    return true;
+  };
+  place(S.gt, sizeof(int32_t) * 2 * S.Gp, false);
+  place(S.free_at, sizeof(int64_t) * S.G, false);
+  place(S.pq, sizeof(int32_t) * 2 * S.Mp, false);
+  const bool ms_in_smem = place(S.ms, sizeof(ModelState) * S.M, false);
+  const ModelParam* mp = S.mp;
+  ModelParam* mp_s = const_cast<ModelParam*>(mp);
+  if (place(mp_s, sizeof(ModelParam) * S.M, true)) S.mp = mp_s;
+  place(S.mc_lat_tree, sizeof(int32_t) * 2 * S.Mp, false);
+  place(S.mc_bs_tree, sizeof(int32_t) * 2 * S.Mp, false);
+  place(S.mc_size, sizeof(int32_t) * S.M, false);
+  place(S.mc_latest, sizeof(int64_t) * S.M, false);
   int32_t* dirty = dirty_all + slot_base[blockIdx.x] + blockIdx.x;
   chain_init(S, fresh);
   while (chain_step(S, dirty, fresh)) {
   }
+  if (ms_in_smem)
+    for (int32_t k = 0; k < S.M; k++) ms_global[k] = S.ms[k];
+  S.ms = ms_global;
   shards[blockIdx.x] = S;
 }
 
@@ -484,8 +532,9 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
   // ---- K4 chain
-  ++launches, k_chain<<<P, 32, 0, st>>>(ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr,
-                            ctx->d_dirty, ctx->d_slot_base);
+  ++launches, k_chain<<<P, 32, ctx->chain_smem, st>>>(
+      ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr, ctx->d_dirty,
+      ctx->d_slot_base, ctx->chain_smem);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[3], st));
   CK(cudaMemcpyAsync(ctx->shards.data(), ctx->d_shards, sizeof(Shard) * P,
@@ -733,6 +782,10 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     S.G = ctx->gpu_base[s + 1] - ctx->gpu_base[s];
     S.Mp = mp2[s];
     S.Gp = gp2[s];
+    S.Mlog = 0;
+    while ((1 << S.Mlog) < S.Mp) S.Mlog++;
+    S.Glog = 0;
+    while ((1 << S.Glog) < S.Gp) S.Glog++;
     S.kind = ctx->kind;
     S.gather = ctx->gather;
     S.d_ctrl = ctx->d_ctrl;
@@ -750,6 +803,17 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     S.free_at = ctx->d_free + ctx->gpu_base[s];
     om += 2 * S.Mp;
     og += 2 * S.Gp;
+  }
+  {
+    int dev_max = 0;
+    cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    size_t want = 0;
+    for (const Shard& S : ctx->shards) want = std::max(want, SmemPlan::need(S));
+    const size_t cap = dev_max > 4096 ? (size_t)dev_max - 2048 : 0;  // room for static S
+    ctx->chain_smem = std::min(want, cap);
+    if ((e = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ctx->chain_smem)) != cudaSuccess)
+      return fail("smem attribute", e);
   }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail("init", e);
   *status = SYM_OK;

@@ -108,6 +108,9 @@ struct ModelParam {
 // Mutable per-model state.
 struct ModelState {
   int64_t c_exec, c_latest;
+  int64_t c_d;        // candidate head deadline
+  int64_t c_lb;       // l(c_size)
+  int64_t c_lb1;      // l(c_size+1), or l(max_batch) at the cap (l_next)
   EvKey mt_key;       // live model timer (valid iff has_mt)
   EvKey dt_key;       // live drop timer (valid iff dt_head >= 0)
   EvKey nx_key;       // next chain event of this model
@@ -136,6 +139,7 @@ struct BatchRec {
 struct Shard {
   // configuration
   int32_t M, G, Mp, Gp;  // counts and power-of-two tree widths
+  int32_t Mlog, Glog;    // log2(Mp), log2(Gp)
   int32_t kind, gather, record_trace, _pad;
   int64_t d_ctrl, d_data;
   int32_t lat_stride, _pad2;
@@ -187,12 +191,38 @@ SYM_HD bool gpu_before(const Shard& S, int32_t x, int32_t y) {
   return x < y;
 }
 
+// Leaf-to-root update of a tournament tree along one path.  The siblings of
+// the path are not modified by the update, so all of them (and their keys)
+// are loaded up front -- two waves of independent loads instead of
+// log2(width) dependent round trips -- and the winners are then resolved in
+// registers.  kMaxLevels bounds the width at 2^14 leaves.
+constexpr int kMaxLevels = 14;
+
 SYM_HD void gpu_tree_update(Shard& S, int32_t gid) {
-  int32_t i = S.Gp + gid;
-  S.gt[i] = (S.free_at[gid] == OUTSTANDING) ? -1 : gid;
-  for (i >>= 1; i >= 1; i >>= 1) {
-    int32_t l = S.gt[2 * i], r = S.gt[2 * i + 1];
-    S.gt[i] = gpu_before(S, r, l) ? r : l;
+  const int32_t L = S.Glog;
+  const int32_t node = S.Gp + gid;
+  int32_t sib[kMaxLevels];
+  int64_t sk[kMaxLevels];
+#pragma unroll
+  for (int l = 0; l < kMaxLevels; l++)
+    if (l < L) sib[l] = S.gt[(node >> l) ^ 1];
+#pragma unroll
+  for (int l = 0; l < kMaxLevels; l++)
+    if (l < L) sk[l] = sib[l] >= 0 ? S.free_at[sib[l]] : 0;
+  const int64_t f = S.free_at[gid];
+  int32_t cur = f == OUTSTANDING ? -1 : gid;
+  int64_t ck = f;
+  S.gt[node] = cur;
+#pragma unroll
+  for (int l = 0; l < kMaxLevels; l++) {
+    if (l < L) {
+      const int32_t o = sib[l];
+      if (o >= 0 && (cur < 0 || sk[l] < ck || (sk[l] == ck && o < cur))) {
+        cur = o;
+        ck = sk[l];
+      }
+      S.gt[node >> (l + 1)] = cur;
+    }
   }
 }
 
@@ -236,11 +266,31 @@ SYM_HD bool model_before(const Shard& S, int32_t x, int32_t y) {
 }
 
 SYM_HD void pq_update(Shard& S, int32_t mid) {
-  int32_t i = S.Mp + mid;
-  S.pq[i] = S.ms[mid].nx_type != EV_NONE ? mid : -1;
-  for (i >>= 1; i >= 1; i >>= 1) {
-    int32_t l = S.pq[2 * i], r = S.pq[2 * i + 1];
-    S.pq[i] = model_before(S, r, l) ? r : l;
+  const int32_t L = S.Mlog;
+  const int32_t node = S.Mp + mid;
+  int32_t sib[kMaxLevels];
+  int64_t st[kMaxLevels];
+#pragma unroll
+  for (int l = 0; l < kMaxLevels; l++)
+    if (l < L) sib[l] = S.pq[(node >> l) ^ 1];
+#pragma unroll
+  for (int l = 0; l < kMaxLevels; l++)
+    if (l < L) st[l] = sib[l] >= 0 ? S.ms[sib[l]].nx_key.t : 0;
+  int32_t cur = S.ms[mid].nx_type != EV_NONE ? mid : -1;
+  int64_t ck = S.ms[mid].nx_key.t;
+  S.pq[node] = cur;
+#pragma unroll
+  for (int l = 0; l < kMaxLevels; l++) {
+    if (l < L) {
+      const int32_t o = sib[l];
+      // leaves of models without a next event are -1, so o >= 0 has one
+      if (o >= 0 && (cur < 0 || st[l] < ck ||
+                     (st[l] == ck && key_less(S.ms[o].nx_key, S.ms[cur].nx_key)))) {
+        cur = o;
+        ck = st[l];
+      }
+      S.pq[node >> (l + 1)] = cur;
+    }
   }
 }
 
@@ -298,23 +348,39 @@ SYM_HD int32_t max_feasible(const Shard& S, int32_t m, int64_t now,
 }
 
 // scheduler.py:218-275.  Returns true when the candidate changed.
+// The candidate caches its head deadline, l(b) and l(b+1): when the head is
+// unchanged, the reference's bisection is replaced by the two probes that
+// certify the same answer (the predicate is monotone in b, so b is the
+// unique maximum iff ok(b) and not ok(b+1) or b == cap).
 SYM_HD bool update_candidate(const Shard& S, int32_t m, ModelState& st,
                              int64_t now, int64_t gpu_floor,
                              const Pusher& who) {
   const ModelParam& P = S.mp[m];
-  while (st.qh < st.qt && now + P.base1 > deadline_at(S, P, st.qh))
+  bool hc = st.has_cand && st.c_head == st.qh;  // cache valid for the head
+  int64_t dh = 0;
+  if (st.qh < st.qt) dh = hc ? st.c_d : deadline_at(S, P, st.qh);
+  while (st.qh < st.qt && now + P.base1 > dh) {
     drop_head(S, st, P, now, who);
+    hc = false;
+    if (st.qh < st.qt) dh = deadline_at(S, P, st.qh);
+  }
   if (S.kind == K_TIMEOUT) {
-    const int64_t l1 = lat_of(S, m, 1);
     // arrival + k + l(1) > deadline  <=>  k + l(1) > slo (scheduler.py:229)
-    while (st.qh < st.qt && P.timeout_ns + l1 > P.slo)
+    const int64_t l1 = P.base1 - S.d_ctrl - S.d_data;
+    while (st.qh < st.qt && P.timeout_ns + l1 > P.slo) {
       drop_head(S, st, P, now, who);
+      hc = false;
+    }
+    if (st.qh < st.qt && !hc) dh = deadline_at(S, P, st.qh);
   }
   if (S.gather == G_DROP_HEAD && st.qt - st.qh > P.target_batch) {
     const int32_t tb = P.target_batch;
     const int64_t need = now + S.d_ctrl + S.d_data * tb + lat_of(S, m, tb);
-    while (st.qt - st.qh > tb && need > deadline_at(S, P, st.qh))
+    while (st.qt - st.qh > tb && need > dh) {
       drop_head(S, st, P, now, who);
+      hc = false;
+      dh = deadline_at(S, P, st.qh);
+    }
   }
   if (st.qh == st.qt) {
     arm_drop_timer(S, st, P, m, now, who);
@@ -324,28 +390,39 @@ SYM_HD bool update_candidate(const Shard& S, int32_t m, ModelState& st,
     }
     return false;
   }
-  const int64_t d = deadline_at(S, P, st.qh);
+  const int64_t d = dh;
   int32_t cap = st.qt - st.qh;
   if (cap > P.max_batch) cap = P.max_batch;
   if (S.gather == G_DROP_HEAD && cap > P.target_batch) cap = P.target_batch;
-  const int64_t pol_floor =
-      S.kind == K_TIMEOUT ? S.s_tick[P.off + st.qh] + P.timeout_ns : NEG_INF;
+  // timeout floor = head arrival + k = (deadline - slo) + k
+  const int64_t pol_floor = S.kind == K_TIMEOUT ? d - P.slo + P.timeout_ns : NEG_INF;
   const int64_t floor2 = imax(pol_floor, gpu_floor);
-  const int32_t b = max_feasible(S, m, now, floor2, cap, d);
-  if (b == 0) {
-    arm_drop_timer(S, st, P, m, now, who);
-    if (st.has_cand) {
-      st.has_cand = 0;
-      return true;
+  const int64_t dc = S.d_ctrl, dd = S.d_data;
+  int32_t b;
+  int64_t lb, lnext;
+  const int32_t cb = st.c_size;
+  if (hc && cb <= cap && imax(now + dc + dd * cb, floor2) + st.c_lb <= d &&
+      (cb == cap || imax(now + dc + dd * (cb + 1), floor2) + st.c_lb1 > d)) {
+    b = cb;
+    lb = st.c_lb;
+    lnext = st.c_lb1;
+  } else {
+    b = max_feasible(S, m, now, floor2, cap, d);
+    if (b == 0) {
+      arm_drop_timer(S, st, P, m, now, who);
+      if (st.has_cand) {
+        st.has_cand = 0;
+        return true;
+      }
+      return false;
     }
-    return false;
+    lb = lat_of(S, m, b);
+    lnext = b < P.max_batch ? lat_of(S, m, b + 1) : lat_of(S, m, P.max_batch);
   }
-  const int64_t l_next =
-      b < P.max_batch ? lat_of(S, m, b + 1) : lat_of(S, m, P.max_batch);
-  int64_t exec_at = now + S.d_ctrl + S.d_data * b;
-  if (S.kind == K_DEFERRED && d - l_next > exec_at) exec_at = d - l_next;
+  int64_t exec_at = now + dc + dd * b;
+  if (S.kind == K_DEFERRED && d - lnext > exec_at) exec_at = d - lnext;
   if (floor2 > exec_at) exec_at = floor2;
-  const int64_t latest = d - lat_of(S, m, b);
+  const int64_t latest = d - lb;
   arm_drop_timer(S, st, P, m, now, who);
   if (st.has_cand && st.c_size == b && st.c_exec == exec_at &&
       st.c_latest == latest && st.c_head == st.qh)
@@ -355,6 +432,9 @@ SYM_HD bool update_candidate(const Shard& S, int32_t m, ModelState& st,
   st.c_exec = exec_at;
   st.c_latest = latest;
   st.c_head = st.qh;
+  st.c_d = d;
+  st.c_lb = lb;
+  st.c_lb1 = lnext;
   return true;
 }
 
@@ -430,7 +510,7 @@ SYM_HD void granted_gpu(Shard& S, int32_t m, int32_t gid, int64_t gpu_free_at,
     return;
   }
   const int32_t b = st.c_size;
-  const int64_t lat_b = lat_of(S, m, b);
+  const int64_t lat_b = st.c_lb;
   if (S.n_recs < S.rec_cap) {
     BatchRec& r = S.recs[S.n_recs];
     r.emitted = now;
@@ -467,8 +547,7 @@ SYM_HD void on_model_timer(Shard& S, int32_t m, int64_t now,
     S.ops += 1;
     if (fa <= st.c_exec) {
       S.ops += 1;
-      S.free_at[gid] = OUTSTANDING;
-      gpu_tree_update(S, gid);
+      S.free_at[gid] = OUTSTANDING;  // tree refreshed by inform_gpu
       granted_gpu(S, m, gid, fa, now, who);
       return;
     }
@@ -580,8 +659,9 @@ SYM_HD int32_t scan_model(const Shard& S, int32_t m, ModelState& st,
 // pure function of its own arrivals, so it is pre-computed for EVERY sorted
 // position in parallel and the chain adopts the record in O(1).
 
-struct FreshRec {
+struct alignas(128) FreshRec {
   int64_t c_exec, c_latest;
+  int64_t c_d, c_lb, c_lb1;
   int64_t mt_t, mt_tp;  // model-timer key (prio 2, sub = arrival)
   int64_t dt_t, dt_tp;  // drop-timer key (prio 3, sub = arrival)
   int32_t qt, qh;       // queue after the scan (model-relative)
@@ -589,7 +669,6 @@ struct FreshRec {
   int32_t mt_a, mt_ap, dt_a, dt_ap;
   int32_t drops;        // heads dropped during the scan
   int32_t steps;        // arrivals absorbed; -1 = scan too long, not valid
-  int32_t _pad[3];
 };
 
 SYM_HD void fresh_state(ModelState& st, int32_t q) {
@@ -598,6 +677,7 @@ SYM_HD void fresh_state(ModelState& st, int32_t q) {
   st.c_size = 0;
   st.c_head = -1;
   st.c_exec = st.c_latest = 0;
+  st.c_d = st.c_lb = st.c_lb1 = 0;
   st.registered = 0;
   st.has_mt = 0;
   st.dt_head = -1;
@@ -621,6 +701,9 @@ SYM_HD FreshRec fresh_scan(const Shard& S, int32_t m, int32_t q,
   r.c_size = st.has_cand ? st.c_size : 0;
   r.c_exec = st.c_exec;
   r.c_latest = st.c_latest;
+  r.c_d = st.c_d;
+  r.c_lb = st.c_lb;
+  r.c_lb1 = st.c_lb1;
   r.mt_t = st.mt_key.t;
   r.mt_tp = st.mt_key.tp;
   r.mt_a = st.mt_key.a;
@@ -630,7 +713,6 @@ SYM_HD FreshRec fresh_scan(const Shard& S, int32_t m, int32_t q,
   r.dt_a = st.dt_key.a;
   r.dt_ap = st.dt_key.ap;
   r.drops = (int32_t)st.drops;
-  r._pad[0] = r._pad[1] = r._pad[2] = 0;
   return r;
 }
 
@@ -649,6 +731,9 @@ SYM_HD void adopt_fresh(ModelState& st, const FreshRec& r) {
     st.c_exec = r.c_exec;
     st.c_latest = r.c_latest;
     st.c_head = r.qh;
+    st.c_d = r.c_d;
+    st.c_lb = r.c_lb;
+    st.c_lb1 = r.c_lb1;
     st.has_mt = 1;
     st.mt_key.t = r.mt_t;
     st.mt_key.a = r.mt_a;
@@ -706,12 +791,25 @@ SYM_HD void on_gpu_timer(Shard& S, const Pusher& who, int32_t* dirty,
     S.ops += 1;
     unregister(S, m);
     S.ops += 1;
-    S.free_at[gid] = OUTSTANDING;
-    gpu_tree_update(S, gid);
+    S.free_at[gid] = OUTSTANDING;  // tree refreshed by inform_gpu
     granted_gpu(S, m, gid, fa, now, who);
     dirty[nd++] = m;
   }
   set_gpu_timer(S, now, who);
+}
+
+// The record this model will most likely adopt next (its queue drains at
+// its next grant) is pulled into L2 now, long before that grant.
+SYM_HD void prefetch_fresh(const FreshRec* fresh, const ModelParam& P,
+                           const ModelState& st) {
+#ifdef __CUDA_ARCH__
+  if (fresh && st.qt < P.cnt)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(fresh + P.off + st.qt));
+#else
+  (void)fresh;
+  (void)P;
+  (void)st;
+#endif
 }
 
 // Bring a model whose state just changed up to its next chain event, using
@@ -725,10 +823,12 @@ SYM_HD void refresh_model(Shard& S, int32_t m, const FreshRec* fresh) {
       adopt_fresh(st, r);
       S.absorbed += r.steps;
       S.fresh_adoptions += 1;
+      prefetch_fresh(fresh, P, st);
       return;
     }
   }
   S.absorbed += scan_model(S, m, st, -1);
+  prefetch_fresh(fresh, P, st);
 }
 
 // Process one chain event; returns false when the sub-cluster is drained.

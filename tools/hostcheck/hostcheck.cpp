@@ -40,7 +40,7 @@ extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64
   std::vector<BatchRec> recs(n + 1);
   std::vector<int64_t> dt(n, -1), dks(n); std::vector<int32_t> dka(n);
   Shard S; memset(&S, 0, sizeof S);
-  S.M = M; S.G = G; S.Mp = Mp; S.Gp = Gp; S.kind = cfg->kind; S.gather = cfg->gather;
+  S.M = M; S.G = G; S.Mp = Mp; S.Gp = Gp; while ((1 << S.Mlog) < Mp) S.Mlog++; while ((1 << S.Glog) < Gp) S.Glog++; S.kind = cfg->kind; S.gather = cfg->gather;
   S.record_trace = 1; S.d_ctrl = cfg->d_ctrl_ns; S.d_data = cfg->d_data_ns;
   S.lat_stride = cfg->lat_stride; S.lat = cfg->lat_ns; S.mp = mp.data();
   S.s_tick = s_tick.data(); S.s_g = s_g.data(); S.s_aself = s_as.data();
