@@ -43,7 +43,8 @@ enum { SYM_GATHER_PREFIX = 0, SYM_GATHER_DROP_HEAD = 1 };
 enum {
   SYM_FLAG_TRACE = 1u,      /* record_trace=True: per-drop keys for the trace */
   SYM_FLAG_NO_FRESH = 2u,   /* disable the parallel fresh-start pre-scan */
-  SYM_FLAG_NO_EXPAND = 4u   /* leave per-request arrays untouched (bench) */
+  SYM_FLAG_NO_EXPAND = 4u,  /* leave per-request arrays untouched (bench) */
+  SYM_FLAG_NO_FAST = 8u     /* always run the sequential live-event chain */
 };
 
 /* Engine configuration.  Models are numbered 0..n_models-1 in the order of
@@ -104,8 +105,9 @@ typedef struct {
   int64_t ops, evictions, registrations, handler_ops_max;
   int64_t chain_events, absorbed_arrivals, fresh_adoptions;
   int64_t launches;           /* kernels this call launched */
+  int64_t fast_shards;        /* sub-clusters resolved by the parallel path */
   /* device timings of the last run (CUDA events on the engine stream) */
-  float ms_ingest, ms_fresh, ms_chain, ms_expand, ms_total;
+  float ms_ingest, ms_fresh, ms_fast, ms_chain, ms_expand, ms_total;
   int64_t err_index;          /* offending stream index for SYM_EPROTO */
 } sym_result;
 

@@ -14,7 +14,7 @@ LIB_NAME = "libsymphony_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 
 SYM_OK, SYM_EPROTO, SYM_EINVAL, SYM_EINVARIANT, SYM_ECUDA, SYM_ENOMEM = range(6)
-FLAG_TRACE, FLAG_NO_FRESH, FLAG_NO_EXPAND = 1, 2, 4
+FLAG_TRACE, FLAG_NO_FRESH, FLAG_NO_EXPAND, FLAG_NO_FAST = 1, 2, 4, 8
 KIND = {"deferred": 0, "eager": 1, "timeout": 2}
 GATHER = {"prefix": 0, "drop_head": 1}
 
@@ -60,7 +60,9 @@ class SymResult(C.Structure):
         ("handler_ops_max", C.c_int64),
         ("chain_events", C.c_int64), ("absorbed_arrivals", C.c_int64),
         ("fresh_adoptions", C.c_int64), ("launches", C.c_int64),
-        ("ms_ingest", C.c_float), ("ms_fresh", C.c_float), ("ms_chain", C.c_float),
+        ("fast_shards", C.c_int64),
+        ("ms_ingest", C.c_float), ("ms_fresh", C.c_float), ("ms_fast", C.c_float),
+        ("ms_chain", C.c_float),
         ("ms_expand", C.c_float), ("ms_total", C.c_float),
         ("err_index", C.c_int64),
     ]

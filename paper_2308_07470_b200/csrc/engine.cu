@@ -25,6 +25,7 @@
 
 #include "../../include/symphony_b200.h"
 #include "engine_core.cuh"
+#include "fastpath.cuh"
 
 using namespace sym;
 
@@ -70,6 +71,15 @@ struct Ctx {
   int32_t* d_err = nullptr;
   FreshRec* d_fresh = nullptr;
   BatchRec* d_recs = nullptr;
+  // fast path scratch
+  EvBatch* d_evb = nullptr;
+  uint64_t *d_bkA = nullptr, *d_bkB = nullptr, *d_tkA = nullptr, *d_tkB = nullptr;
+  uint32_t *d_bvA = nullptr, *d_bvB = nullptr, *d_tvA = nullptr, *d_tvB = nullptr;
+  int32_t *d_ptrA = nullptr, *d_ptrB = nullptr, *d_rhist = nullptr;
+  int32_t *d_nb = nullptr, *d_bbase = nullptr, *d_changed = nullptr;
+  int64_t *d_mdrops = nullptr, *d_sbase = nullptr;
+  uint32_t* d_fail = nullptr;
+  int32_t* d_skip = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
   int32_t* d_drop_ka = nullptr;
   // last run (for sym_window_counts)
@@ -77,6 +87,7 @@ struct Ctx {
   const int64_t* last_ticks = nullptr;
   const int32_t* last_model = nullptr;
   std::vector<int64_t> last_nrecs;
+  std::vector<uint32_t> last_fast_fail;
   bool has_run = false;
 };
 
@@ -279,22 +290,22 @@ struct SmemPlan {
 __global__ void __launch_bounds__(32)
 k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
         int32_t* __restrict__ dirty_all, const int32_t* __restrict__ slot_base,
-        size_t smem_bytes) {
+        size_t smem_bytes, const int32_t* __restrict__ skip) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Shard S;  // hot scalars of the sub-cluster live in smem
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x != 0 || skip[blockIdx.x]) return;
   S = shards[blockIdx.x];
+  const Shard orig = S;  // global pointers, restored before the write-back
   ModelState* const ms_global = S.ms;
   size_t used = 0;
-  auto place = [&](auto*& ptr, size_t bytes, bool copy_in) {
-    bytes = SmemPlan::al(bytes);
+  auto place = [&](auto*& ptr, size_t exact, bool copy_in) {
+    const size_t bytes = SmemPlan::al(exact);
     if (used + bytes > smem_bytes) return false;
     using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
     T* dst = reinterpret_cast<T*>(smem + used);
-    if (copy_in) {
-      const uint4* src = reinterpret_cast<const uint4*>(ptr);
-      uint4* d = reinterpret_cast<uint4*>(dst);
-      for (size_t k = 0; k < bytes / 16; k++) d[k] = src[k];
+    if (copy_in) {  // element-wise: sources need not be 16-byte aligned
+      const size_t cnt = exact / sizeof(T);
+      for (size_t k = 0; k < cnt; k++) dst[k] = ptr[k];
     }
     ptr = dst;
     used += bytes;
@@ -317,7 +328,15 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
   }
   if (ms_in_smem)
     for (int32_t k = 0; k < S.M; k++) ms_global[k] = S.ms[k];
-  S.ms = ms_global;
+  S.ms = orig.ms;
+  S.mp = orig.mp;
+  S.gt = orig.gt;
+  S.free_at = orig.free_at;
+  S.pq = orig.pq;
+  S.mc_lat_tree = orig.mc_lat_tree;
+  S.mc_bs_tree = orig.mc_bs_tree;
+  S.mc_size = orig.mc_size;
+  S.mc_latest = orig.mc_latest;
   shards[blockIdx.x] = S;
 }
 
@@ -424,6 +443,272 @@ __global__ void k_copy_batches(const BatchRec* __restrict__ recs,
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+
+// --------------------------------------------------------- K3 fast path ---
+// (fastpath.cuh).  All sub-clusters are processed together: sort keys carry
+// the shard id in bits [kTickBits, 64).
+
+constexpr int kTickBits = 40;  // event ticks < 2^40 ns (~18 minutes)
+
+__device__ __forceinline__ int shard_of_slot(const int32_t* slot_base, int32_t P,
+                                             int32_t k) {
+  int s = 0;
+  while (s + 1 < P && slot_base[s + 1] <= k) s++;
+  return s;
+}
+
+// K3a: one thread per model: its unconstrained batch sequence
+__global__ void __launch_bounds__(64)
+k_evolve(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
+         int32_t P, int32_t M, const FreshRec* __restrict__ fresh,
+         EvBatch* __restrict__ evb, int32_t* __restrict__ nb,
+         int64_t* __restrict__ mdrops, uint32_t* __restrict__ fail) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  const int s = shard_of_slot(slot_base, P, k);
+  const Shard& S = shards[s];
+  const int32_t m = k - slot_base[s];
+  const ModelParam& mp = S.mp[m];
+  uint32_t f = 0;
+  int64_t dr = 0;
+  const int32_t c = evolve_model(S, m, fresh, evb + mp.off, mp.cnt, &dr, &f);
+  nb[k] = c < 0 ? 0 : c;
+  mdrops[k] = dr;
+  if (f) atomicOr(&fail[s], f);
+}
+
+// K3b: dense batch numbering: bbase[k] per model, sbase[s] per shard
+__global__ void k_nb_scan(const int32_t* __restrict__ nb, int32_t M, int32_t P,
+                          const int32_t* __restrict__ slot_base,
+                          int32_t* __restrict__ bbase, int64_t* __restrict__ sbase) {
+  if (threadIdx.x != 0) return;
+  int64_t run = 0;
+  for (int s = 0; s < P; s++) {
+    sbase[s] = run;
+    for (int k = slot_base[s]; k < slot_base[s + 1]; k++) {
+      bbase[k] = (int32_t)run;
+      run += nb[k];
+    }
+  }
+  sbase[P] = run;
+}
+
+// K3c: (shard|tick) keys of every batch, value = its EvBatch index
+__global__ void k_batch_keys(const Shard* __restrict__ shards,
+                             const int32_t* __restrict__ slot_base, int32_t P,
+                             const ModelParam* __restrict__ mp_all,
+                             const int32_t* __restrict__ nb,
+                             const int32_t* __restrict__ bbase,
+                             const EvBatch* __restrict__ evb, int64_t n,
+                             uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                             uint32_t* __restrict__ fail) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int lo = 0, hi = slot_base[P];
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+  }
+  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  const int32_t j = (int32_t)(p - mp_all[lo].off);
+  if (j >= nb[lo]) return;
+  const int s = shard_of_slot(slot_base, P, lo);
+  const int64_t t = evb[p].t;
+  if (t < 0 || t >= (int64_t(1) << kTickBits)) atomicOr(&fail[s], FP_CAPACITY);
+  const int64_t d = bbase[lo] + j;
+  keys[d] = ((uint64_t)s << kTickBits) | (uint64_t)(t & ((int64_t(1) << kTickBits) - 1));
+  vals[d] = (uint32_t)p;
+}
+
+// --- LSD radix sort of (u64 key, u32 value) pairs, 8-bit digits, stable ---
+
+__global__ void k_rhist(const uint64_t* __restrict__ keys, int64_t n, int shift,
+                        int32_t* __restrict__ hist, int64_t W) {
+  __shared__ int32_t cnt[4][256];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * 4 + wib;
+  for (int b = lane; b < 256; b += 32) cnt[wib][b] = 0;
+  __syncwarp();
+  if (w < W) {
+    const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
+    for (int64_t i = lo + lane; i < hi; i += 32)
+      atomicAdd(&cnt[wib][(keys[i] >> shift) & 255], 1);
+  }
+  __syncwarp();
+  if (w < W)
+    for (int b = lane; b < 256; b += 32) hist[w * 256 + b] = cnt[wib][b];
+}
+
+__global__ void k_binscan256(int32_t* __restrict__ bins) {
+  if (threadIdx.x != 0) return;
+  int32_t run = 0;
+  for (int b = 0; b < 256; b++) {
+    const int32_t c = bins[b];
+    bins[b] = run;
+    run += c;
+  }
+}
+
+__global__ void k_rscatter(const uint64_t* __restrict__ kin,
+                           const uint32_t* __restrict__ vin, int64_t n, int shift,
+                           const int32_t* __restrict__ hist,
+                           const int32_t* __restrict__ bins, int64_t W,
+                           uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+  __shared__ int32_t base_s[4][256];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * 4 + wib;
+  if (w >= W) return;
+  int32_t* base = base_s[wib];
+  for (int b = lane; b < 256; b += 32) base[b] = bins[b] + hist[w * 256 + b];
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
+  for (int64_t i0 = lo; i0 < hi; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const bool act = i < hi;
+    const unsigned amask = __ballot_sync(0xffffffffu, act);
+    uint64_t k = 0;
+    uint32_t v = 0;
+    int32_t dg = -1 - lane;
+    if (act) {
+      k = kin[i];
+      v = vin[i];
+      dg = (int32_t)((k >> shift) & 255);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, dg) & amask;
+    int32_t pos = 0;
+    if (act) pos = base[dg] + __popc(peers & lt);
+    __syncwarp();
+    if (act) {
+      if ((peers >> lane) == 1u) base[dg] += __popc(peers);
+      kout[pos] = k;
+      vout[pos] = v;
+    }
+    __syncwarp();
+  }
+}
+
+// K3d: order runs of equal (shard, tick) by the full event key
+__global__ void k_runfix(const uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                         int64_t nt, const EvBatch* __restrict__ evb,
+                         uint32_t* __restrict__ fail) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  if (i > 0 && keys[i - 1] == keys[i]) return;        // not a run start
+  if (i + 1 >= nt || keys[i + 1] != keys[i]) return;  // singleton
+  int64_t e = i + 1;
+  while (e < nt && keys[e] == keys[i]) e++;
+  for (int64_t a = i + 1; a < e; a++) {  // insertion sort, runs are tiny
+    const uint32_t v = vals[a];
+    int64_t b = a;
+    while (b > i && batch_cmp(evb[v], evb[vals[b - 1]]) < 0) {
+      vals[b] = vals[b - 1];
+      b--;
+    }
+    vals[b] = v;
+  }
+  for (int64_t a = i + 1; a < e; a++)
+    if (batch_cmp(evb[vals[a - 1]], evb[vals[a]]) == 0)
+      atomicOr(&fail[keys[i] >> kTickBits], FP_KEY_TIE);
+}
+
+// K3e: finish-time token of every sorted batch: key (shard|finish),
+// value = the batch's rank within its shard
+__global__ void k_token_keys(const uint32_t* __restrict__ bvals, int64_t nt,
+                             const uint64_t* __restrict__ bkeys,
+                             const EvBatch* __restrict__ evb,
+                             const int64_t* __restrict__ sbase,
+                             uint64_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
+                             uint32_t* __restrict__ fail) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const int s = (int)(bkeys[i] >> kTickBits);
+  const EvBatch& e = evb[bvals[i]];
+  const int64_t fin = e.exec + e.lat;
+  if (fin < 0 || fin >= (int64_t(1) << kTickBits)) atomicOr(&fail[s], FP_CAPACITY);
+  tkeys[i] = ((uint64_t)s << kTickBits) | (uint64_t)(fin & ((int64_t(1) << kTickBits) - 1));
+  tvals[i] = (uint32_t)(i - sbase[s]);
+}
+
+// K3f: batch of shard-rank r pops token rank r: initial (0, r) for r < G,
+// else the (r-G)-th finish token; ptr = creator rank (or r itself if initial)
+__global__ void k_match(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bvals,
+                        int64_t nt, const EvBatch* __restrict__ evb,
+                        const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
+                        const uint64_t* __restrict__ tkeys,
+                        const uint32_t* __restrict__ tvals, int32_t* __restrict__ ptr,
+                        uint32_t* __restrict__ fail) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const int s = (int)(bkeys[i] >> kTickBits);
+  const int64_t r = i - sbase[s];
+  const int32_t G = shards[s].G;
+  if (r < G) {
+    ptr[i] = (int32_t)r;  // terminal: gid r
+    return;
+  }
+  const int64_t ti = sbase[s] + (r - G);
+  const int64_t fa = (int64_t)(tkeys[ti] & ((uint64_t(1) << kTickBits) - 1));
+  const int64_t c = tvals[ti];
+  if (fa > evb[bvals[i]].exec) atomicOr(&fail[s], FP_NO_GPU);
+  if (c >= r) atomicOr(&fail[s], FP_LATE_TOKEN);
+  ptr[i] = (int32_t)(G + c);  // encoded: >= G means "same gid as rank c"
+}
+
+// pointer jumping: ptr >= G refers to rank ptr-G of the same shard
+__global__ void k_jump(const int32_t* __restrict__ pin, int32_t* __restrict__ pout,
+                       int64_t nt, const uint64_t* __restrict__ bkeys,
+                       const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
+                       int32_t* __restrict__ changed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const int32_t v = pin[i];
+  const int s = (int)(bkeys[i] >> kTickBits);
+  const int32_t G = shards[s].G;
+  if (v < G) {
+    pout[i] = v;
+    return;
+  }
+  const int32_t w = pin[sbase[s] + (v - G)];
+  pout[i] = w;
+  if (w >= G) *changed = 1;
+}
+
+// K3g: token ties must pop in gid order; emit the BatchRec of every batch
+__global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
+                            const uint32_t* __restrict__ bvals, int64_t nt,
+                            const EvBatch* __restrict__ evb,
+                            const int64_t* __restrict__ sbase,
+                            const uint64_t* __restrict__ tkeys,
+                            const uint32_t* __restrict__ tvals,
+                            const int32_t* __restrict__ gid,
+                            const int64_t* __restrict__ rec_base,
+                            BatchRec* __restrict__ recs, uint32_t* __restrict__ fail) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const int s = (int)(bkeys[i] >> kTickBits);
+  const int64_t r = i - sbase[s];
+  // token i (shard order) vs token i+1: equal finish => gid order
+  if (i + 1 < nt && tkeys[i + 1] == tkeys[i]) {
+    const int32_t g0 = gid[sbase[s] + tvals[i]];
+    const int32_t g1 = gid[sbase[s] + tvals[i + 1]];
+    if (g0 > g1) atomicOr(&fail[s], FP_TOKEN_TIE);
+  }
+  const EvBatch& e = evb[bvals[i]];
+  BatchRec& o = recs[rec_base[s] + r];
+  o.emitted = e.t;
+  o.start = e.exec;
+  o.finish = e.exec + e.lat;
+  o.kt = e.t;
+  o.ka = e.a;
+  o.ksub = r;  // processing order = rank (the chain counter of the chain)
+  o.model = e.model;
+  o.gpu = gid[i];
+  o.size = e.size;
+  o.first = e.first;
+  o.shrunk_from = 0;
+}
+
 // ------------------------------------------------------------ driver ------
 
 int ensure_capacity(Ctx* ctx, int64_t n) {
@@ -438,7 +723,13 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_s_aself, c)) || (rc = grow(ctx, ctx->d_fresh, c)) ||
         (rc = grow(ctx, ctx->d_recs, c + ctx->P)) ||
         (rc = grow(ctx, ctx->d_drop_t, c)) || (rc = grow(ctx, ctx->d_drop_ks, c)) ||
-        (rc = grow(ctx, ctx->d_drop_ka, c)))
+        (rc = grow(ctx, ctx->d_drop_ka, c)) || (rc = grow(ctx, ctx->d_evb, c)) ||
+        (rc = grow(ctx, ctx->d_bkA, c)) || (rc = grow(ctx, ctx->d_bkB, c)) ||
+        (rc = grow(ctx, ctx->d_tkA, c)) || (rc = grow(ctx, ctx->d_tkB, c)) ||
+        (rc = grow(ctx, ctx->d_bvA, c)) || (rc = grow(ctx, ctx->d_bvB, c)) ||
+        (rc = grow(ctx, ctx->d_tvA, c)) || (rc = grow(ctx, ctx->d_tvB, c)) ||
+        (rc = grow(ctx, ctx->d_ptrA, c)) || (rc = grow(ctx, ctx->d_ptrB, c)) ||
+        (rc = grow(ctx, ctx->d_rhist, ((c + kChunk - 1) / kChunk) * 256 + 256)))
       return rc;
     ctx->cap = c;
   }
@@ -531,10 +822,112 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                                           ctx->d_mp, P, n, ctx->d_fresh);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
-  // ---- K4 chain
-  ++launches, k_chain<<<P, 32, ctx->chain_smem, st>>>(
-      ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr, ctx->d_dirty,
-      ctx->d_slot_base, ctx->chain_smem);
+  // ---- K3 parallel fast path (validated regime), K4 chain for the rest
+  std::vector<uint32_t> fail(P, 0);
+  std::vector<int64_t> sbase(P + 1, 0);
+  std::vector<int64_t> mdrops(M, 0);
+  const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
+  if (fast) {
+    CK(cudaMemsetAsync(ctx->d_fail, 0, sizeof(uint32_t) * P, st));
+    ++launches, k_evolve<<<nblk(M, 64), 64, 0, st>>>(ctx->d_shards, ctx->d_slot_base, P, M,
+                                                     ctx->d_fresh, ctx->d_evb, ctx->d_nb,
+                                                     ctx->d_mdrops, ctx->d_fail);
+    ++launches, k_nb_scan<<<1, 32, 0, st>>>(ctx->d_nb, M, P, ctx->d_slot_base, ctx->d_bbase,
+                                            ctx->d_sbase);
+    CK(cudaMemcpyAsync(sbase.data(), ctx->d_sbase, sizeof(int64_t) * (P + 1),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t nt = sbase[P];
+    if (nt > 0) {
+      ++launches, k_batch_keys<<<nblk(n, 256), 256, 0, st>>>(
+          ctx->d_shards, ctx->d_slot_base, P, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
+          ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail);
+      int bits = kTickBits;
+      while ((1 << (bits - kTickBits)) < P) bits++;
+      const int64_t Wr = (nt + kChunk - 1) / kChunk;
+      auto radix = [&](uint64_t*& ka, uint32_t*& va, uint64_t*& kb, uint32_t*& vb) {
+        for (int shift = 0; shift < bits; shift += 8) {
+          ++launches, k_rhist<<<nblk(Wr, 4), 128, 0, st>>>(ka, nt, shift, ctx->d_rhist, Wr);
+          ++launches, k_colscan<<<nblk(256, 128), 128, 0, st>>>(ctx->d_rhist, Wr, 256,
+                                                                ctx->d_rhist + Wr * 256);
+          ++launches, k_binscan256<<<1, 32, 0, st>>>(ctx->d_rhist + Wr * 256);
+          ++launches, k_rscatter<<<nblk(Wr, 4), 128, 0, st>>>(
+              ka, va, nt, shift, ctx->d_rhist, ctx->d_rhist + Wr * 256, Wr, kb, vb);
+          std::swap(ka, kb);
+          std::swap(va, vb);
+        }
+      };
+      radix(ctx->d_bkA, ctx->d_bvA, ctx->d_bkB, ctx->d_bvB);
+      ++launches, k_runfix<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_bkA, ctx->d_bvA, nt,
+                                                          ctx->d_evb, ctx->d_fail);
+      ++launches, k_token_keys<<<nblk(nt, 256), 256, 0, st>>>(
+          ctx->d_bvA, nt, ctx->d_bkA, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
+          ctx->d_fail);
+      radix(ctx->d_tkA, ctx->d_tvA, ctx->d_tkB, ctx->d_tvB);
+      ++launches, k_match<<<nblk(nt, 256), 256, 0, st>>>(
+          ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_shards, ctx->d_tkA,
+          ctx->d_tvA, ctx->d_ptrA, ctx->d_fail);
+      for (int round = 0; round < 64; round += 2) {
+        CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
+        ++launches, k_jump<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
+                                                          ctx->d_bkA, ctx->d_sbase,
+                                                          ctx->d_shards, ctx->d_changed);
+        ++launches, k_jump<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
+                                                          ctx->d_bkA, ctx->d_sbase,
+                                                          ctx->d_shards, ctx->d_changed);
+        int32_t changed = 0;
+        CK(cudaMemcpyAsync(&changed, ctx->d_changed, sizeof changed, cudaMemcpyDeviceToHost,
+                           st));
+        CK(cudaStreamSynchronize(st));
+        if (!changed) break;
+      }
+      int64_t* d_rb = nullptr;
+      CK(cudaMallocAsync((void**)&d_rb, sizeof(int64_t) * (P + 1), st));
+      CK(cudaMemcpyAsync(d_rb, rec_base.data(), sizeof(int64_t) * (P + 1),
+                         cudaMemcpyHostToDevice, st));
+      ++launches, k_fast_emit<<<nblk(nt, 256), 256, 0, st>>>(
+          ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
+          ctx->d_ptrA, d_rb, ctx->d_recs, ctx->d_fail);
+      CK(cudaFreeAsync(d_rb, st));
+    }
+    CK(cudaMemcpyAsync(fail.data(), ctx->d_fail, sizeof(uint32_t) * P,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(mdrops.data(), ctx->d_mdrops, sizeof(int64_t) * M,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaEventRecord(ctx->ev[5], st));
+  std::vector<int32_t> skip(P, 0);
+  int32_t n_chain = 0;
+  for (int s = 0; s < P; s++) {
+    skip[s] = fast && fail[s] == 0;
+    n_chain += !skip[s];
+    if (skip[s]) {  // counters the chain would have produced
+      Shard& S = ctx->shards[s];
+      const int64_t nbs = sbase[s + 1] - sbase[s];
+      S.n_recs = nbs;
+      S.ops = 3 * nbs;
+      S.handler_ops_max = nbs > 0 ? 3 : 0;
+      S.registrations = S.evictions = 0;
+      S.chain_events = nbs;
+      S.absorbed = rec_base[s + 1] - rec_base[s] - 1;
+      S.fresh_adoptions = 0;
+      S.error = ERR_NONE;
+    }
+  }
+  ctx->last_fast_fail = fail;
+  if (n_chain > 0) {
+    CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->d_skip, skip.data(), sizeof(int32_t) * P,
+                       cudaMemcpyHostToDevice, st));
+    ++launches, k_chain<<<P, 32, ctx->chain_smem, st>>>(
+        ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr, ctx->d_dirty,
+        ctx->d_slot_base, ctx->chain_smem, ctx->d_skip);
+  } else {
+    CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
+                       cudaMemcpyHostToDevice, st));
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[3], st));
   CK(cudaMemcpyAsync(ctx->shards.data(), ctx->d_shards, sizeof(Shard) * P,
@@ -610,14 +1003,19 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     out->absorbed_arrivals += S.absorbed;
     out->fresh_adoptions += S.fresh_adoptions;
   }
-  for (int k = 0; k < M; k++) out->drops += ms[k].drops;
+  for (int s = 0; s < P; s++)
+    for (int k = ctx->slot_base[s]; k < ctx->slot_base[s + 1]; k++)
+      out->drops += skip[s] ? mdrops[k] : ms[k].drops;
+  out->fast_shards = P - n_chain;
   out->completions = n - out->drops;  // jitterless: nothing is late
   float t;
   cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]);
   out->ms_ingest = t;
   cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[2]);
   out->ms_fresh = t;
-  cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[5]);
+  out->ms_fast = t;
+  cudaEventElapsedTime(&t, ctx->ev[5], ctx->ev[3]);
   out->ms_chain = t;
   cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]);
   out->ms_expand = t;
@@ -765,6 +1163,13 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   // bins: [B+1] totals, then shard_off [P+1], model_of_slot [M], gpu_base [P+1]
   ALLOC(ctx->d_bins, (M + P + 1) + (P + 1) + M + (P + 1));
   ALLOC(ctx->d_err, 1);
+  ALLOC(ctx->d_nb, M);
+  ALLOC(ctx->d_bbase, M);
+  ALLOC(ctx->d_mdrops, M);
+  ALLOC(ctx->d_sbase, P + 1);
+  ALLOC(ctx->d_fail, P);
+  ALLOC(ctx->d_skip, P);
+  ALLOC(ctx->d_changed, 1);
 #undef ALLOC
   const int B = M + P;
   cudaMemcpy(ctx->d_lat, lat.data(), sizeof(int64_t) * lat.size(), cudaMemcpyHostToDevice);
@@ -831,7 +1236,12 @@ void sym_destroy(void* engine) {
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,   ctx->d_s_aself,
                   ctx->d_hist, ctx->d_bins,   ctx->d_err,   ctx->d_fresh,
-                  ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka};
+                  ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
+                  ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
+                  ctx->d_bvA, ctx->d_bvB, ctx->d_tvA, ctx->d_tvB, ctx->d_ptrA,
+                  ctx->d_ptrB, ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
+                  ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
+                  ctx->d_skip};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& ev : ctx->ev)

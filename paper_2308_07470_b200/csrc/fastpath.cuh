@@ -1,0 +1,142 @@
+// fastpath.cuh -- the parallel "validated regime" of a sub-cluster.
+//
+// Observation.  While every live model timer finds the
+// earliest-free GPU free by its exec_at (scheduler.py:385-393 never takes
+// the registration branch), the rank plane never feeds anything back into a
+// model: the revalidation in granted_gpu (scheduler.py:185) reproduces the
+// candidate unchanged, and no GPU timer is ever armed (mc stays empty,
+// scheduler.py:442).  Each model's batch sequence is then a pure function of
+// its own arrivals ("unconstrained evolution", k_evolve), and the whole
+// sub-cluster reduces to
+//   (1) sort all batches of the sub-cluster by their event key,
+//   (2) batch i pops the smallest (free_at, gid) of the GPU index and pushes
+//       (exec_i + l(b_i), same gid).  The index is a monotone priority queue
+//       (every push exceeds the popped key), so batch i pops the i-th
+//       smallest token overall -- initial tokens (0, g) first, in gid
+//       order, then the finish times -- provided that token was created
+//       before batch i.  A token's gid is its creator batch's gid, resolved
+//       by pointer jumping.
+// Every assumption is checked (flags below); a sub-cluster that violates any
+// of them is re-run by the exact sequential chain (k_chain).
+#pragma once
+#include "engine_core.cuh"
+
+namespace sym {
+
+// validation failure reasons (bit flags per sub-cluster)
+enum : uint32_t {
+  FP_DROP_TIMER = 1u,      // a drop timer would pop before the model timer
+  FP_SAME_TICK_GRANT = 2u, // a grant pushes a timer firing at its own tick
+  FP_REVALIDATE = 4u,      // revalidation at the pop changed the candidate
+  FP_KEY_TIE = 8u,         // two batch keys tie up to the chain counter
+  FP_NO_GPU = 16u,         // popped token free after exec_at (registration)
+  FP_LATE_TOKEN = 32u,     // token created after the batch that pops it
+  FP_TOKEN_TIE = 64u,      // equal finish times popped out of gid order
+  FP_CAPACITY = 128u,      // scratch exhausted / scan too long
+};
+
+// One batch of a model's unconstrained evolution.
+struct EvBatch {
+  int64_t t;       // model-timer tick (the grant's processing tick)
+  int64_t tp;      // pusher tick
+  int64_t exec;    // exec_at = start
+  int64_t lat;     // l(size)
+  int32_t a;       // canonical A' of the timer
+  int32_t ap;      // pusher A'
+  int32_t size;
+  int32_t first;   // sorted-stream position of the first member
+  int32_t model;   // shard-local model id
+  int32_t chain;   // 1 = pushed by the model's previous grant, 0 = arrival
+};
+
+// Strict weak order of two batch events of one sub-cluster, excluding the
+// chain-counter tie-break (ties there are rejected with FP_KEY_TIE).
+SYM_HD int batch_cmp(const EvBatch& x, const EvBatch& y) {
+  if (x.t != y.t) return x.t < y.t ? -1 : 1;
+  if (x.a != y.a) return x.a < y.a ? -1 : 1;
+  if (x.tp != y.tp) return x.tp < y.tp ? -1 : 1;
+  if (x.ap != y.ap) return x.ap < y.ap ? -1 : 1;
+  // at an equal pusher position a chain event precedes the arrival
+  if (x.chain != y.chain) return x.chain ? -1 : 1;
+  return 0;
+}
+
+// Unconstrained evolution of model m of shard S: emits its batches in event
+// order into out[0..), returns their count (or -1 on a validation failure
+// recorded in *fail).  The model-side effect of a grant is exactly
+// granted_gpu (scheduler.py:180-209) with the GPU floor elided: the floor is
+// <= exec_at in the validated regime and leaves the candidate unchanged,
+// which is asserted (FP_REVALIDATE).
+SYM_HD int32_t evolve_model(const Shard& S, int32_t m, const FreshRec* fresh,
+                            EvBatch* out, int32_t cap, int64_t* drops,
+                            uint32_t* fail) {
+  const ModelParam& P = S.mp[m];
+  ModelState st;
+  fresh_state(st, 0);
+  int32_t nb = 0;
+  bool first_refresh = true;
+  for (;;) {
+    // bring the model to its next event (fresh-start table when possible)
+    if (first_refresh || is_fresh(st)) {
+      first_refresh = false;
+      if (st.qt < P.cnt && fresh) {
+        const FreshRec& r = fresh[P.off + st.qt];
+        if (r.steps >= 0) {
+          adopt_fresh(st, r);
+        } else {
+          scan_model(S, m, st, -1);
+        }
+      } else {
+        scan_model(S, m, st, -1);
+      }
+    } else {
+      scan_model(S, m, st, -1);
+    }
+    if (st.nx_type == EV_NONE) break;
+    if (st.nx_type != EV_MT) {
+      *fail |= FP_DROP_TIMER;
+      return -1;
+    }
+    if (nb >= cap) {
+      *fail |= FP_CAPACITY;
+      return -1;
+    }
+    const EvKey k = st.mt_key;
+    const int64_t now = k.t;
+    Pusher who;
+    who.t = now;
+    who.a_self = who.a_after = k.a;
+    who.sub = 0;  // placeholder: the chain counter is never compared here
+    // granted_gpu: revalidation with a floor <= exec_at
+    const int32_t b0 = st.c_size;
+    const int64_t e0 = st.c_exec, l0 = st.c_latest;
+    update_candidate(S, m, st, now, 0, who);
+    if (!st.has_cand || st.c_size != b0 || st.c_exec != e0 || st.c_latest != l0) {
+      *fail |= FP_REVALIDATE;
+      return -1;
+    }
+    EvBatch& e = out[nb++];
+    e.t = now;
+    e.a = k.a;
+    e.tp = k.tp;
+    e.ap = k.ap;
+    e.chain = k.sub != SUB_ARRIVAL;
+    e.exec = st.c_exec;
+    e.lat = st.c_lb;
+    e.size = st.c_size;
+    e.first = P.off + st.qh;
+    e.model = m;
+    st.qh += st.c_size;
+    st.has_cand = 0;
+    update_candidate(S, m, st, now, NEG_INF, who);
+    renew_model_timer(S, st, now, who);
+    if (st.has_mt && st.mt_key.t == now) {
+      *fail |= FP_SAME_TICK_GRANT;
+      return -1;
+    }
+  }
+  *drops = st.drops;
+  return nb;
+}
+
+}  // namespace sym

@@ -119,7 +119,7 @@ class Engine:
                  policy: PolicyConfig, network: NetworkModel | None = None,
                  seed: int = 0, record_trace: bool = False,
                  check_invariants: bool = False, *, shards=None, device: int = 0,
-                 use_fresh: bool = True):
+                 use_fresh: bool = True, use_fast: bool = True):
         if gpu_count < 1:
             raise ValueError("need at least one GPU")
         self.models = list(models)
@@ -135,6 +135,7 @@ class Engine:
         self.gpu_count = gpu_count
         self.device = device
         self.use_fresh = use_fresh
+        self.use_fast = use_fast
         self.shard_of_model, self.gpus_per_shard = _split_shards(self.models, gpu_count, shards)
         self.n_shards = len(self.gpus_per_shard)
         stride = max(m.profile.max_batch for m in self.models)
@@ -211,6 +212,8 @@ class Engine:
             f |= _native.FLAG_TRACE
         if not self.use_fresh:
             f |= _native.FLAG_NO_FRESH
+        if not self.use_fast:
+            f |= _native.FLAG_NO_FAST
         return f
 
     def _absorb_counters(self, res: _native.SymResult):
@@ -219,8 +222,8 @@ class Engine:
         self.rank.registrations = res.registrations
         self.handler_ops_max = res.handler_ops_max
         self.stats = {k: getattr(res, k) for k in (
-            "chain_events", "absorbed_arrivals", "fresh_adoptions", "launches", "ms_ingest",
-            "ms_fresh", "ms_chain", "ms_expand", "ms_total")}
+            "chain_events", "absorbed_arrivals", "fresh_adoptions", "launches", "fast_shards",
+            "ms_ingest", "ms_fresh", "ms_fast", "ms_chain", "ms_expand", "ms_total")}
 
     # -- reference API --------------------------------------------------------
 

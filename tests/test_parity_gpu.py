@@ -45,12 +45,14 @@ def test_engine_trace_parity(case, golden):
     eng.close()
 
 
+@pytest.mark.parametrize("use_fast", [True, False], ids=["fast", "chain"])
 @pytest.mark.parametrize("case", SMALL + CONFIGS, ids=[c[0] for c in SMALL + CONFIGS])
-def test_engine_fresh_path_parity(case, golden):
-    """Default (fresh-start pre-scan) path vs the reference digests and the
-    oracle's arrays, plus compute_stats on the engine's RunResult."""
+def test_engine_default_path_parity(case, use_fast, golden):
+    """Default path (fresh-start pre-scan + parallel validated fast path, with
+    the chain as fallback) and the chain alone, vs the reference digests and
+    the oracle's arrays, plus compute_stats on the engine's RunResult."""
     key, models, gpus, policy, ticks, midx, (dur, warm, cool) = case
-    eng = _engine(models, gpus, policy)
+    eng = _engine(models, gpus, policy, use_fast=use_fast)
     res = eng.run_stream(ticks, midx, dur)
     g = golden[key]
     check_against_golden(g, res.req_dispatch, res.req_start, res.req_finish, res.req_batch,
@@ -59,6 +61,9 @@ def test_engine_fresh_path_parity(case, golden):
     for k in ("req_dispatch", "req_start", "req_finish", "req_batch", "req_outcome"):
         np.testing.assert_array_equal(getattr(res, k), o[k], err_msg=k)
     check_stats(res, g, dur, warm, cool)
+    if use_fast and key.split("/")[0].split("@")[0] in ("C1", "C2", "C3") or key.startswith("C4s"):
+        if use_fast and "base" in key:
+            assert eng.stats["fast_shards"] == 1, "underload config must take the fast path"
     eng.close()
 
 
@@ -73,6 +78,7 @@ def test_c4_sharded_single_call(golden):
     ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models], dur, 42)
     eng = Engine(list(sc.models), sc.gpu_count, sc.policy, shards=sc.shards)
     res = eng.run_stream(ticks, midx, dur)
+    assert eng.stats["fast_shards"] == 8
     for s, (ms, g, ids) in enumerate(configs.shard_scenarios(sc)):
         sel = (midx >= ids[0]) & (midx <= ids[-1])
         gk = golden[f"C4s{s}/base@{dur}"]
