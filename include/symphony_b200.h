@@ -106,6 +106,7 @@ typedef struct {
   int64_t chain_events, absorbed_arrivals, fresh_adoptions;
   int64_t launches;           /* kernels this call launched */
   int64_t fast_shards;        /* sub-clusters resolved by the parallel path */
+  int64_t fast_fail_mask;     /* OR of the validation failures (fastpath.cuh) */
   /* device timings of the last run (CUDA events on the engine stream) */
   float ms_ingest, ms_fresh, ms_fast, ms_chain, ms_expand, ms_total;
   int64_t err_index;          /* offending stream index for SYM_EPROTO */

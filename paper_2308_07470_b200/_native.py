@@ -60,7 +60,7 @@ class SymResult(C.Structure):
         ("handler_ops_max", C.c_int64),
         ("chain_events", C.c_int64), ("absorbed_arrivals", C.c_int64),
         ("fresh_adoptions", C.c_int64), ("launches", C.c_int64),
-        ("fast_shards", C.c_int64),
+        ("fast_shards", C.c_int64), ("fast_fail_mask", C.c_int64),
         ("ms_ingest", C.c_float), ("ms_fresh", C.c_float), ("ms_fast", C.c_float),
         ("ms_chain", C.c_float),
         ("ms_expand", C.c_float), ("ms_total", C.c_float),

@@ -648,11 +648,38 @@ __global__ void k_match(const uint64_t* __restrict__ bkeys, const uint32_t* __re
     return;
   }
   const int64_t ti = sbase[s] + (r - G);
-  const int64_t fa = (int64_t)(tkeys[ti] & ((uint64_t(1) << kTickBits) - 1));
   const int64_t c = tvals[ti];
-  if (fa > evb[bvals[i]].exec) atomicOr(&fail[s], FP_NO_GPU);
-  if (c >= r) atomicOr(&fail[s], FP_LATE_TOKEN);
-  ptr[i] = (int32_t)(G + c);  // encoded: >= G means "same gid as rank c"
+  // a token created at or after its consumer would loop; validated in emit
+  ptr[i] = c < r ? (int32_t)(G + c) : 0;  // >= G: "same gid as rank c"
+}
+
+// Equal-finish tokens pop in gid order (scheduler.py:338: min (free_at,
+// gid)).  Re-sort each tie group by the gids just resolved; a token's gid
+// only depends on strictly earlier tokens, so iterating match -> jump ->
+// tiefix reaches the fixed point the sequential index produces.
+__global__ void k_tiefix(const uint64_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
+                         int64_t nt, const int64_t* __restrict__ sbase,
+                         const int32_t* __restrict__ gid, int32_t* __restrict__ changed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  if (i > 0 && tkeys[i - 1] == tkeys[i]) return;
+  if (i + 1 >= nt || tkeys[i + 1] != tkeys[i]) return;
+  const int64_t base = sbase[tkeys[i] >> kTickBits];
+  int64_t e = i + 1;
+  while (e < nt && tkeys[e] == tkeys[i]) e++;
+  bool moved = false;
+  for (int64_t a = i + 1; a < e; a++) {
+    const uint32_t v = tvals[a];
+    const int32_t gv = gid[base + v];
+    int64_t b = a;
+    while (b > i && gid[base + tvals[b - 1]] > gv) {
+      tvals[b] = tvals[b - 1];
+      b--;
+      moved = true;
+    }
+    tvals[b] = v;
+  }
+  if (moved) *changed = 1;
 }
 
 // pointer jumping: ptr >= G refers to rank ptr-G of the same shard
@@ -683,6 +710,7 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
                             const uint32_t* __restrict__ tvals,
                             const int32_t* __restrict__ gid,
                             const int64_t* __restrict__ rec_base,
+                            const Shard* __restrict__ shards,
                             BatchRec* __restrict__ recs, uint32_t* __restrict__ fail) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
@@ -695,6 +723,13 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
     if (g0 > g1) atomicOr(&fail[s], FP_TOKEN_TIE);
   }
   const EvBatch& e = evb[bvals[i]];
+  const int32_t G = shards[s].G;
+  if (r >= G) {  // popped token: free by exec_at, created before this batch
+    const int64_t ti = sbase[s] + (r - G);
+    const int64_t fa = (int64_t)(tkeys[ti] & ((uint64_t(1) << kTickBits) - 1));
+    if (fa > e.exec) atomicOr(&fail[s], FP_NO_GPU);
+    if ((int64_t)tvals[ti] >= r) atomicOr(&fail[s], FP_LATE_TOKEN);
+  }
   BatchRec& o = recs[rec_base[s] + r];
   o.emitted = e.t;
   o.start = e.exec;
@@ -864,22 +899,32 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
           ctx->d_bvA, nt, ctx->d_bkA, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
           ctx->d_fail);
       radix(ctx->d_tkA, ctx->d_tvA, ctx->d_tkB, ctx->d_tvB);
-      ++launches, k_match<<<nblk(nt, 256), 256, 0, st>>>(
-          ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_shards, ctx->d_tkA,
-          ctx->d_tvA, ctx->d_ptrA, ctx->d_fail);
-      for (int round = 0; round < 64; round += 2) {
+      for (int it = 0; it < 16; it++) {
+        ++launches, k_match<<<nblk(nt, 256), 256, 0, st>>>(
+            ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_shards, ctx->d_tkA,
+            ctx->d_tvA, ctx->d_ptrA, ctx->d_fail);
+        for (int round = 0; round < 64; round += 2) {
+          CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
+          ++launches, k_jump<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
+                                                            ctx->d_bkA, ctx->d_sbase,
+                                                            ctx->d_shards, ctx->d_changed);
+          ++launches, k_jump<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
+                                                            ctx->d_bkA, ctx->d_sbase,
+                                                            ctx->d_shards, ctx->d_changed);
+          int32_t changed = 0;
+          CK(cudaMemcpyAsync(&changed, ctx->d_changed, sizeof changed,
+                             cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          if (!changed) break;
+        }
         CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
-        ++launches, k_jump<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
-                                                          ctx->d_bkA, ctx->d_sbase,
-                                                          ctx->d_shards, ctx->d_changed);
-        ++launches, k_jump<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
-                                                          ctx->d_bkA, ctx->d_sbase,
-                                                          ctx->d_shards, ctx->d_changed);
-        int32_t changed = 0;
-        CK(cudaMemcpyAsync(&changed, ctx->d_changed, sizeof changed, cudaMemcpyDeviceToHost,
-                           st));
+        ++launches, k_tiefix<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_tkA, ctx->d_tvA, nt,
+                                                            ctx->d_sbase, ctx->d_ptrA,
+                                                            ctx->d_changed);
+        int32_t moved = 0;
+        CK(cudaMemcpyAsync(&moved, ctx->d_changed, sizeof moved, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (!changed) break;
+        if (!moved) break;
       }
       int64_t* d_rb = nullptr;
       CK(cudaMallocAsync((void**)&d_rb, sizeof(int64_t) * (P + 1), st));
@@ -887,7 +932,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                          cudaMemcpyHostToDevice, st));
       ++launches, k_fast_emit<<<nblk(nt, 256), 256, 0, st>>>(
           ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
-          ctx->d_ptrA, d_rb, ctx->d_recs, ctx->d_fail);
+          ctx->d_ptrA, d_rb, ctx->d_shards, ctx->d_recs, ctx->d_fail);
       CK(cudaFreeAsync(d_rb, st));
     }
     CK(cudaMemcpyAsync(fail.data(), ctx->d_fail, sizeof(uint32_t) * P,
@@ -1007,6 +1052,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     for (int k = ctx->slot_base[s]; k < ctx->slot_base[s + 1]; k++)
       out->drops += skip[s] ? mdrops[k] : ms[k].drops;
   out->fast_shards = P - n_chain;
+  out->fast_fail_mask = 0;
+  for (int s = 0; s < P; s++) out->fast_fail_mask |= fail[s];
   out->completions = n - out->drops;  // jitterless: nothing is late
   float t;
   cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]);

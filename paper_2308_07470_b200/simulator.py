@@ -222,7 +222,7 @@ class Engine:
         self.rank.registrations = res.registrations
         self.handler_ops_max = res.handler_ops_max
         self.stats = {k: getattr(res, k) for k in (
-            "chain_events", "absorbed_arrivals", "fresh_adoptions", "launches", "fast_shards",
+            "chain_events", "absorbed_arrivals", "fresh_adoptions", "launches", "fast_shards", "fast_fail_mask",
             "ms_ingest", "ms_fresh", "ms_fast", "ms_chain", "ms_expand", "ms_total")}
 
     # -- reference API --------------------------------------------------------

@@ -61,9 +61,10 @@ def test_engine_default_path_parity(case, use_fast, golden):
     for k in ("req_dispatch", "req_start", "req_finish", "req_batch", "req_outcome"):
         np.testing.assert_array_equal(getattr(res, k), o[k], err_msg=k)
     check_stats(res, g, dur, warm, cool)
-    if use_fast and key.split("/")[0].split("@")[0] in ("C1", "C2", "C3") or key.startswith("C4s"):
-        if use_fast and "base" in key:
-            assert eng.stats["fast_shards"] == 1, "underload config must take the fast path"
+    if use_fast and key[:2] in ("C1", "C2", "C3", "C4", "C5") and "/base" in key:
+        assert eng.stats["fast_shards"] == 1, "underload config must take the fast path"
+    if not use_fast:
+        assert eng.stats["fast_shards"] == 0
     eng.close()
 
 
