@@ -80,6 +80,8 @@ struct Ctx {
   int64_t *d_mdrops = nullptr, *d_sbase = nullptr;
   uint32_t* d_fail = nullptr;
   int32_t* d_skip = nullptr;
+  int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
+          *d_cp_model = nullptr, *d_special = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
   int32_t* d_drop_ka = nullptr;
   // last run (for sym_window_counts)
@@ -252,10 +254,29 @@ __global__ void k_aself(const int64_t* __restrict__ s_tick,
 
 // --------------------------------------------------------------- K2 -------
 
+// Batch-chain pointer of a fresh start at position p (fastpath.cuh):
+//   >= 0  a batch starts at p and drains the queue; the model is fresh again
+//         at that absolute position
+//   NX_LAST  a batch starts at p, drains the queue, no arrivals remain
+//   NX_NONE  no batch: every queued request was dropped, none remain
+//   NX_SPECIAL  anything else (non-draining grant, drop timer first, scan cap)
+constexpr int32_t NX_LAST = -1, NX_NONE = -2, NX_SPECIAL = -3;
+
+SYM_HD int32_t chain_next(const FreshRec& r, const ModelParam& mp) {
+  if (r.steps < 0) return NX_SPECIAL;
+  if (r.c_size == 0) return r.qh == r.qt && r.qt == mp.cnt ? NX_NONE : NX_SPECIAL;
+  if (r.c_size != r.qt - r.qh) return NX_SPECIAL;  // grant would leave a remainder
+  // the model timer must be the next event (it precedes the drop timer in a
+  // fresh scan, fastpath.cuh FP_DROP_TIMER)
+  const bool mt_first = r.mt_t < r.dt_t || (r.mt_t == r.dt_t && r.mt_a <= r.dt_a);
+  if (!mt_first) return NX_SPECIAL;
+  return r.qt == mp.cnt ? NX_LAST : mp.off + r.qt;
+}
+
 __global__ void __launch_bounds__(256)
 k_fresh(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
         const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
-        FreshRec* __restrict__ out) {
+        FreshRec* __restrict__ out, int32_t* __restrict__ nxt) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   // slot of p: last slot with off <= p and cnt > 0
@@ -269,7 +290,9 @@ k_fresh(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
   while (slot_base[s + 1] <= lo) s++;
   const Shard& S = shards[s];
   const int32_t m = lo - slot_base[s];
-  out[p] = fresh_scan(S, m, (int32_t)(p - mp_all[lo].off), kFreshMaxSteps);
+  const FreshRec r = fresh_scan(S, m, (int32_t)(p - mp_all[lo].off), kFreshMaxSteps);
+  out[p] = r;
+  if (nxt) nxt[p] = chain_next(r, mp_all[lo]);
 }
 
 // --------------------------------------------------------------- K4 -------
@@ -462,9 +485,10 @@ __global__ void __launch_bounds__(64)
 k_evolve(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
          int32_t P, int32_t M, const FreshRec* __restrict__ fresh,
          EvBatch* __restrict__ evb, int32_t* __restrict__ nb,
-         int64_t* __restrict__ mdrops, uint32_t* __restrict__ fail) {
+         int64_t* __restrict__ mdrops, uint32_t* __restrict__ fail,
+         const int32_t* __restrict__ only) {
   const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= M) return;
+  if (k >= M || (only && !only[k])) return;
   const int s = shard_of_slot(slot_base, P, k);
   const Shard& S = shards[s];
   const int32_t m = k - slot_base[s];
@@ -475,6 +499,107 @@ k_evolve(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base
   nb[k] = c < 0 ? 0 : c;
   mdrops[k] = dr;
   if (f) atomicOr(&fail[s], f);
+}
+
+
+// K3a' (parallel unconstrained evolution).  J1 = the chain pointer where it
+// continues; J_{2k}[p] = J_k[J_k[p]]: the position 2k batches after p, or -1
+// if the chain ends (or needs the sequential path) within 2k batches.
+__global__ void k_double(const int32_t* __restrict__ jin, int32_t* __restrict__ jout,
+                         int64_t n, int first) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int32_t v = jin[p];
+  if (first) {
+    jout[p] = v >= 0 ? v : -1;
+    return;
+  }
+  jout[p] = v >= 0 ? jin[v] : -1;
+}
+
+constexpr int kJump = 64;  // batches per checkpoint (J_64)
+
+// One thread per model: follow J_64 from the model's first position,
+// recording a checkpoint every 64 batches; then count the tail with the
+// single-step pointers.  Models whose chain meets NX_SPECIAL are left to
+// the sequential k_evolve (special[k] = 1).
+__global__ void k_walk(const ModelParam* __restrict__ mp_all, int32_t M,
+                       const int32_t* __restrict__ nxt, const int32_t* __restrict__ j64,
+                       int32_t* __restrict__ cp_pos, int32_t* __restrict__ cp_model,
+                       int32_t* __restrict__ nb, int32_t* __restrict__ special) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  const ModelParam& mp = mp_all[k];
+  int32_t count = 0, sp = 0;
+  if (mp.cnt > 0) {
+    const int64_t cbase = mp.off / kJump + k;  // disjoint per-model slots
+    int32_t p = mp.off, c = 0;
+    while (j64[p] >= 0) {
+      cp_pos[cbase + c] = p;
+      cp_model[cbase + c] = k;
+      c++;
+      p = j64[p];
+    }
+    cp_pos[cbase + c] = p;
+    cp_model[cbase + c] = k;
+    count = c * kJump;
+    for (;;) {  // tail: < 64 batches
+      const int32_t v = nxt[p];
+      if (v == NX_SPECIAL) {
+        sp = 1;
+        break;
+      }
+      if (v == NX_NONE) break;
+      count++;
+      if (v == NX_LAST) break;
+      p = v;
+    }
+  }
+  nb[k] = sp ? 0 : count;
+  special[k] = sp;
+}
+
+// One thread per checkpoint: materialise up to 64 batches (EvBatch) from
+// the fresh-start records along the chain, and add their drops.
+__global__ void k_walk_expand(const int32_t* __restrict__ cp_pos,
+                              const int32_t* __restrict__ cp_model, int64_t ncp,
+                              const ModelParam* __restrict__ mp_all,
+                              const int32_t* __restrict__ slot_base, int32_t P,
+                              const int32_t* __restrict__ nxt,
+                              const int32_t* __restrict__ special,
+                              const FreshRec* __restrict__ fresh,
+                              EvBatch* __restrict__ evb,
+                              unsigned long long* __restrict__ mdrops) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= ncp) return;
+  const int32_t k = cp_model[q];
+  if (k < 0 || special[k]) return;
+  const ModelParam& mp = mp_all[k];
+  const int64_t c = q - (mp.off / kJump + k);  // checkpoint ordinal
+  const int s = shard_of_slot(slot_base, P, k);
+  int32_t p = cp_pos[q];
+  int64_t out = mp.off + c * kJump;
+  unsigned long long dr = 0;
+  for (int j = 0; j < kJump && p >= 0; j++) {
+    const FreshRec& r = fresh[p];
+    const int32_t v = nxt[p];
+    dr += (unsigned long long)r.drops;
+    if (v == NX_NONE || v == NX_SPECIAL) break;
+    EvBatch& e = evb[out++];
+    e.t = r.mt_t;
+    e.a = r.mt_a;
+    e.tp = r.mt_tp;
+    e.ap = r.mt_ap;
+    e.chain = 0;  // fresh scans only hold arrival-pushed timers
+    e.exec = r.c_exec;
+    e.lat = r.c_lb;
+    e.size = r.c_size;
+    e.first = mp.off + r.qh;
+    e.model = k - slot_base[s];
+    if (v == NX_LAST) break;
+    p = v;
+  }
+  atomicAdd(&mdrops[k], dr);
 }
 
 // K3b: dense batch numbering: bbase[k] per model, sbase[s] per shard
@@ -764,7 +889,11 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_bvA, c)) || (rc = grow(ctx, ctx->d_bvB, c)) ||
         (rc = grow(ctx, ctx->d_tvA, c)) || (rc = grow(ctx, ctx->d_tvB, c)) ||
         (rc = grow(ctx, ctx->d_ptrA, c)) || (rc = grow(ctx, ctx->d_ptrB, c)) ||
-        (rc = grow(ctx, ctx->d_rhist, ((c + kChunk - 1) / kChunk) * 256 + 256)))
+        (rc = grow(ctx, ctx->d_rhist, ((c + kChunk - 1) / kChunk) * 256 + 256)) ||
+        (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
+        (rc = grow(ctx, ctx->d_jB, c)) ||
+        (rc = grow(ctx, ctx->d_cp_pos, c / kJump + ctx->M + 2)) ||
+        (rc = grow(ctx, ctx->d_cp_model, c / kJump + ctx->M + 2)))
       return rc;
     ctx->cap = c;
   }
@@ -854,7 +983,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   // ---- K2 fresh-start pre-scan
   if (use_fresh && n > 0)
     ++launches, k_fresh<<<nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
-                                          ctx->d_mp, P, n, ctx->d_fresh);
+                                          ctx->d_mp, P, n, ctx->d_fresh,
+                                          (flags & SYM_FLAG_NO_FAST) ? nullptr : ctx->d_nxt);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
   // ---- K3 parallel fast path (validated regime), K4 chain for the rest
@@ -864,9 +994,26 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
   if (fast) {
     CK(cudaMemsetAsync(ctx->d_fail, 0, sizeof(uint32_t) * P, st));
+    CK(cudaMemsetAsync(ctx->d_mdrops, 0, sizeof(int64_t) * M, st));
+    const int64_t ncp = n / kJump + M + 2;
+    CK(cudaMemsetAsync(ctx->d_cp_model, 0xff, sizeof(int32_t) * ncp, st));
+    // J_64 by six doublings of the chain pointer
+    ++launches, k_double<<<nblk(n, 256), 256, 0, st>>>(ctx->d_nxt, ctx->d_jA, n, 1);
+    for (int d = 0; d < 6; d++) {
+      ++launches, k_double<<<nblk(n, 256), 256, 0, st>>>(ctx->d_jA, ctx->d_jB, n, 0);
+      std::swap(ctx->d_jA, ctx->d_jB);
+    }
+    ++launches, k_walk<<<nblk(M, 64), 64, 0, st>>>(ctx->d_mp, M, ctx->d_nxt, ctx->d_jA,
+                                                   ctx->d_cp_pos, ctx->d_cp_model, ctx->d_nb,
+                                                   ctx->d_special);
+    ++launches, k_walk_expand<<<nblk(ncp, 128), 128, 0, st>>>(
+        ctx->d_cp_pos, ctx->d_cp_model, ncp, ctx->d_mp, ctx->d_slot_base, P, ctx->d_nxt,
+        ctx->d_special, ctx->d_fresh, ctx->d_evb, (unsigned long long*)ctx->d_mdrops);
+    // models whose chain needs the general (non-draining) evolution
     ++launches, k_evolve<<<nblk(M, 64), 64, 0, st>>>(ctx->d_shards, ctx->d_slot_base, P, M,
                                                      ctx->d_fresh, ctx->d_evb, ctx->d_nb,
-                                                     ctx->d_mdrops, ctx->d_fail);
+                                                     ctx->d_mdrops, ctx->d_fail,
+                                                     ctx->d_special);
     ++launches, k_nb_scan<<<1, 32, 0, st>>>(ctx->d_nb, M, P, ctx->d_slot_base, ctx->d_bbase,
                                             ctx->d_sbase);
     CK(cudaMemcpyAsync(sbase.data(), ctx->d_sbase, sizeof(int64_t) * (P + 1),
@@ -1217,6 +1364,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_fail, P);
   ALLOC(ctx->d_skip, P);
   ALLOC(ctx->d_changed, 1);
+  ALLOC(ctx->d_special, M);
 #undef ALLOC
   const int B = M + P;
   cudaMemcpy(ctx->d_lat, lat.data(), sizeof(int64_t) * lat.size(), cudaMemcpyHostToDevice);
@@ -1288,7 +1436,8 @@ void sym_destroy(void* engine) {
                   ctx->d_bvA, ctx->d_bvB, ctx->d_tvA, ctx->d_tvB, ctx->d_ptrA,
                   ctx->d_ptrB, ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
-                  ctx->d_skip};
+                  ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_cp_pos,
+                  ctx->d_cp_model, ctx->d_special};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& ev : ctx->ev)
