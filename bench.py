@@ -7,8 +7,10 @@ partitioned into P=8 sub-clusters of 125 contiguous models and 1024 GPUs
 per-GPU work is fixed (weak scaling) and N=8 is exactly C4 on 8 B200s.
 
 A step is one pass of the hot path over the rank's whole sub-cluster trace
-(~9.0M requests): ingest -> fresh-start pre-scan -> live-event chain ->
-per-request RunResult arrays, inputs resident in HBM.  `value` is the
+(~9.0M requests): ingest -> fresh-start pre-scan -> batch chains ->
+per-request RunResult arrays, inputs resident in HBM (the parallel
+validated fast path resolves the sub-cluster; the sequential live-event
+chain takes over for any sub-cluster that fails validation).  `value` is the
 whole-job throughput; `e2e` is the same metric through the public API
 (Engine.run_stream: host arrays in, RunResult out, H2D/D2H inside).
 
@@ -33,8 +35,34 @@ sys.path.insert(0, ROOT)
 
 METRIC = "requests scheduled/sec (device-timed) at 1/2/4/8 B200; goodput bit-exact vs CPU ref"
 UNIT = "requests/s"
-FRESH_REC_BYTES = 96   # sizeof(FreshRec) read per adopted fresh start
-BATCH_REC_BYTES = 64   # sizeof(BatchRec) written per dispatched batch
+FRESH_REC_BYTES = 128  # sizeof(FreshRec)
+BATCH_REC_BYTES = 64   # sizeof(BatchRec) / sizeof(sym_batch)
+EV_BATCH_BYTES = 56    # sizeof(EvBatch)
+
+
+def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
+    """Minimal DRAM bytes one launch of `kernel` must move for n requests and
+    nb batches (DESIGN.md §5 derives each line)."""
+    table = {
+        # stable partition: read tick+model, write s_tick, s_g, s_i, sh_tick
+        "k_scatter": n * (8 + 4 + 8 + 4 + 4 + 8),
+        "k_hist": n * 4,
+        "k_aself": n * (4 + 8 + 8 + 4),
+        # fresh-start pre-scan: read each sorted arrival once (tick, A', g),
+        # write one FreshRec and one chain pointer per position
+        "k_fresh": n * (8 + 4 + 4 + FRESH_REC_BYTES + 4),
+        "k_double": n * (4 + 4),
+        "k_walk_expand": nb * (FRESH_REC_BYTES + 4 + EV_BATCH_BYTES),
+        "k_batch_keys": nb * (8 + 8 + 4),
+        "k_rscatter": nb * (12 + 12),
+        "k_rhist": nb * 8,
+        "k_fast_emit": nb * (EV_BATCH_BYTES + 12 + 4 + 8 + BATCH_REC_BYTES),
+        # per-request RunResult arrays from batch records
+        "k_init_out": n * 5 * 8,
+        "k_expand": nb * BATCH_REC_BYTES + n * (4 + 8 + 5 * 8),
+        "k_copy_batches": nb * (BATCH_REC_BYTES + 4 + 64),
+    }
+    return table.get(kernel)
 
 
 def dist_env():
@@ -182,14 +210,13 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    dev_ms, chain_ms, batches, launches = 0.0, 0.0, 0, 0
+    dev_ms, batches, launches = 0.0, 0, 0
     with ClockSampler(local_rank) as clk:
         t0 = time.perf_counter()
         for _ in range(args.steps):
             flush.fill_(1)
             _, cnt = eng.run_device(t_dev, m_dev, outs)
             dev_ms += cnt["ms_total"]
-            chain_ms += cnt["ms_chain"]
             batches += cnt["n_batches"]
             launches += cnt["launches"] + 1  # + the L2 flush
         torch.cuda.synchronize()
@@ -197,6 +224,13 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     stats = dict(cnt)
+    # per-kernel device time: the same K steps again with every launch
+    # bracketed by CUDA events on the engine's stream
+    eng.kernel_times(reset=True)
+    for _ in range(args.steps):
+        flush.fill_(1)
+        eng.run_device(t_dev, m_dev, outs, kernel_times=True)
+    ktimes = eng.kernel_times(reset=True)
 
     # end to end through the public API: pinned host arrays in, RunResult out
     pin_t = torch.from_numpy(ticks).pin_memory().numpy()
@@ -215,23 +249,33 @@ def run_b200(args, rank, world, local_rank):
         if not np.array_equal(outs[k].cpu().numpy(), ref):
             raise SystemExit(f"device-resident and API outputs differ on {k}")
 
-    t = torch.tensor([dev_ms, e2e_time, wall, chain_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([dev_ms, e2e_time, wall], dtype=torch.float64, device=dev)
     tot = torch.tensor([n, batches], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    dev_ms, e2e_time, wall, chain_ms = t.tolist()
+    dev_ms, e2e_time, wall = t.tolist()
     n_all = int(tot[0].item())
     if rank != 0:
         return
     value = n_all * args.steps / (dev_ms / 1e3)
     peak, peak_kind = measured_peak_hbm()
-    # dominant kernel = the live-event chain (k_chain): algorithmic bytes are
-    # one FreshRec read + one BatchRec write per dispatched batch
-    per_launch_batches = batches / args.steps
-    chain_ms_launch = chain_ms / args.steps
-    alg_bytes = per_launch_batches * (FRESH_REC_BYTES + BATCH_REC_BYTES)
-    achieved = alg_bytes / (chain_ms_launch / 1e3) / 1e9
+    nb_step = batches // args.steps
+    kern = {}
+    for name, (cnt_l, ms) in ktimes.items():
+        per_launch_ms = ms / cnt_l
+        ab = algorithmic_bytes(name, n, nb_step)
+        kern[name] = {"launches_per_step": cnt_l / args.steps, "ms_per_launch": per_launch_ms,
+                      "share": ms / sum(v[1] for v in ktimes.values()),
+                      "gbs": (ab / (per_launch_ms / 1e3) / 1e9) if ab else None}
+    dom = max(kern, key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches_per_step"])
+    ab = algorithmic_bytes(dom, n, nb_step)
+    achieved = kern[dom]["gbs"]
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -244,14 +288,16 @@ def run_b200(args, rank, world, local_rank):
                    "parallelism": f"sub-cluster-per-gpu x{world}"},
         "e2e": {"value": n_all / e2e_time, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                 "d2h_bytes_per_step": d2h * world},
-        "roofline": {"bound": "hbm", "kernel": "k_chain", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None,
-                     "note": "latency-bound dependent event chain; bytes = 160 B per batch"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": ab},
+        "kernels": {k: kern[k] for k in sorted(kern, key=lambda k: -kern[k]["share"])[:8]},
         "gpu_launches": launches,
-        "phases_ms": {k: stats[k] for k in ("ms_ingest", "ms_fresh", "ms_chain", "ms_expand")},
-        "chain": {"events": stats["chain_events"], "batches": stats["n_batches"],
-                  "ns_per_event": 1e6 * stats["ms_chain"] / max(1, stats["chain_events"])},
+        "phases_ms": {k: stats[k] for k in ("ms_ingest", "ms_fresh", "ms_fast", "ms_chain",
+                                            "ms_expand")},
+        "path": {"fast_shards": stats["fast_shards"], "batches": stats["n_batches"],
+                 "chain_events": stats["chain_events"]},
         "clocks": clk.summary(),
         "wall_ms_per_step": 1e3 * wall / args.steps,
     }

@@ -44,7 +44,8 @@ enum {
   SYM_FLAG_TRACE = 1u,      /* record_trace=True: per-drop keys for the trace */
   SYM_FLAG_NO_FRESH = 2u,   /* disable the parallel fresh-start pre-scan */
   SYM_FLAG_NO_EXPAND = 4u,  /* leave per-request arrays untouched (bench) */
-  SYM_FLAG_NO_FAST = 8u     /* always run the sequential live-event chain */
+  SYM_FLAG_NO_FAST = 8u,    /* always run the sequential live-event chain */
+  SYM_FLAG_KERNEL_TIMES = 16u /* CUDA-event time every kernel (profiling) */
 };
 
 /* Engine configuration.  Models are numbered 0..n_models-1 in the order of
@@ -141,6 +142,11 @@ int32_t sym_window_counts(void *engine, int64_t lo_ns, int64_t hi_ns,
                           int64_t *gpu_busy_ns);
 
 const char *sym_last_error(void *engine);
+
+/* JSON object {"kernel": [launches, total_ms], ...} accumulated over runs
+ * made with SYM_FLAG_KERNEL_TIMES; reset != 0 clears the table.  The string
+ * lives until the next call on the handle. */
+const char *sym_kernel_times(void *engine, int32_t reset);
 int32_t sym_version(void);
 
 #ifdef __cplusplus

@@ -14,7 +14,7 @@ LIB_NAME = "libsymphony_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 
 SYM_OK, SYM_EPROTO, SYM_EINVAL, SYM_EINVARIANT, SYM_ECUDA, SYM_ENOMEM = range(6)
-FLAG_TRACE, FLAG_NO_FRESH, FLAG_NO_EXPAND, FLAG_NO_FAST = 1, 2, 4, 8
+FLAG_TRACE, FLAG_NO_FRESH, FLAG_NO_EXPAND, FLAG_NO_FAST, FLAG_KERNEL_TIMES = 1, 2, 4, 8, 16
 KIND = {"deferred": 0, "eager": 1, "timeout": 2}
 GATHER = {"prefix": 0, "drop_head": 1}
 
@@ -69,7 +69,7 @@ class SymResult(C.Structure):
 
 
 EXPORTS = ("sym_create", "sym_destroy", "sym_run", "sym_run_device",
-           "sym_window_counts", "sym_last_error", "sym_version")
+           "sym_window_counts", "sym_last_error", "sym_version", "sym_kernel_times")
 
 _lib = None
 
@@ -101,5 +101,7 @@ def load(path: str | None = None):
     lib.sym_last_error.argtypes = [C.c_void_p]
     lib.sym_last_error.restype = C.c_char_p
     lib.sym_version.restype = C.c_int32
+    lib.sym_kernel_times.argtypes = [C.c_void_p, C.c_int32]
+    lib.sym_kernel_times.restype = C.c_char_p
     _lib = lib
     return lib

@@ -19,6 +19,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <chrono>
+#include <cstdlib>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -80,6 +83,12 @@ struct Ctx {
   int64_t *d_mdrops = nullptr, *d_sbase = nullptr;
   uint32_t* d_fail = nullptr;
   int32_t* d_skip = nullptr;
+  int64_t* d_meta = nullptr;       // [3*(P+1)]: rec_base | rec_count | spare
+  // staging for the host-buffer entry point (grown, never freed per call)
+  int64_t *d_req = nullptr, *d_drop = nullptr;
+  int32_t* d_dka = nullptr;
+  sym_batch* d_bat = nullptr;
+  int64_t stage_cap = 0, bat_cap = 0;
   int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
           *d_cp_model = nullptr, *d_special = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
@@ -91,6 +100,8 @@ struct Ctx {
   std::vector<int64_t> last_nrecs;
   std::vector<uint32_t> last_fast_fail;
   bool has_run = false;
+  std::map<std::string, std::pair<int64_t, double>> ktimes;  // name -> (launches, ms)
+  std::string ktimes_json;
 };
 
 #define CK(call)                                                        \
@@ -905,10 +916,95 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
   return SYM_OK;
 }
 
+// Opt-in host-side phase timing (SYM_DEBUG_TIMING=1): synchronises the
+// stream at each mark and prints the wall time since the previous mark.
+struct PhaseClock {
+  int mode;  // 0 off, 1 host wall time with syncs, 2 device events (no syncs)
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0, h0;
+  std::vector<std::pair<const char*, cudaEvent_t>> evs;
+  std::vector<double> host_ms;
+  explicit PhaseClock(cudaStream_t s) : st(s) {
+    const char* e = getenv("SYM_DEBUG_TIMING");
+    mode = e ? atoi(e) : 0;
+    t0 = h0 = std::chrono::steady_clock::now();
+    if (mode == 2) mark("start");
+  }
+  void mark(const char* what) {
+    if (mode == 1) {
+      cudaStreamSynchronize(st);
+      auto t = std::chrono::steady_clock::now();
+      fprintf(stderr, "[sym] %-14s %9.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(t - t0).count());
+      t0 = t;
+    } else if (mode == 2) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      cudaEventRecord(ev, st);
+      evs.push_back({what, ev});
+      host_ms.push_back(std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now() - h0).count());
+    }
+  }
+  ~PhaseClock() {
+    if (mode != 2 || evs.empty()) return;
+    cudaEventSynchronize(evs.back().second);
+    for (size_t i = 1; i < evs.size(); i++) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, evs[i - 1].second, evs[i].second);
+      fprintf(stderr, "[sym] %-14s gpu %9.3f ms   host-enqueued at %9.3f ms\n",
+              evs[i].first, ms, host_ms[i]);
+    }
+    for (auto& e : evs) cudaEventDestroy(e.second);
+  }
+};
+
+// Per-kernel device time (SYM_FLAG_KERNEL_TIMES): CUDA events on the engine
+// stream bracket every launch; accumulated per kernel name in the context.
+struct KernelTimer {
+  Ctx* ctx;
+  cudaStream_t st;
+  bool on;
+  std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  void begin(const char* name) {
+    if (!on) return;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    marks.push_back({name, {a, b}});
+  }
+  void end() {
+    if (on) cudaEventRecord(marks.back().second.second, st);
+  }
+  ~KernelTimer() {
+    for (auto& m : marks) {
+      cudaEventSynchronize(m.second.second);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, m.second.first, m.second.second);
+      auto& acc = ctx->ktimes[m.first];
+      acc.first += 1;
+      acc.second += ms;
+      cudaEventDestroy(m.second.first);
+      cudaEventDestroy(m.second.second);
+    }
+  }
+};
+
+#define KL(name, ...)          \
+  do {                         \
+    kt.begin(#name);           \
+    ++launches;                \
+    name<<<__VA_ARGS__;        \
+    kt.end();                  \
+  } while (0)
+
 int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                int64_t n, uint32_t flags, sym_result* out, bool outs_on_device) {
   cudaStream_t st = ctx->stream;
   int64_t launches = 0;
+  PhaseClock pc(st);
+  KernelTimer kt{ctx, st, (flags & SYM_FLAG_KERNEL_TIMES) != 0, {}};
   const int32_t M = ctx->M, P = ctx->P;
   const int B = M + P;
   const bool trace = flags & SYM_FLAG_TRACE;
@@ -923,15 +1019,15 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const int wpb = 4;
   const size_t smem = sizeof(int32_t) * (size_t)B * wpb;
   if (W > 0) {
-    ++launches, k_hist<<<nblk(W, wpb), 32 * wpb, smem, st>>>(
+    KL(k_hist, nblk(W, wpb), 32 * wpb, smem, st>>>(
         d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
-        ctx->d_hist, W, ctx->d_err);
-    ++launches, k_colscan<<<nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, ctx->d_bins);
+        ctx->d_hist, W, ctx->d_err));
+    KL(k_colscan, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, ctx->d_bins));
   } else {
     CK(cudaMemsetAsync(ctx->d_bins, 0, sizeof(int32_t) * B, st));
   }
-  ++launches, k_binoff<<<1, 32, 0, st>>>(ctx->d_bins, M, P, ctx->d_mp,
-                             ctx->d_bins + B + 1);
+  KL(k_binoff, 1, 32, 0, st>>>(ctx->d_bins, M, P, ctx->d_mp,
+                             ctx->d_bins + B + 1));
   int32_t herr = INT32_MAX;
   CK(cudaMemcpyAsync(&herr, ctx->d_err, sizeof herr, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -941,15 +1037,16 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     return SYM_EPROTO;
   }
   if (W > 0)
-    ++launches, k_scatter<<<nblk(W, wpb), 32 * wpb, smem, st>>>(
+    KL(k_scatter, nblk(W, wpb), 32 * wpb, smem, st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, ctx->d_bins, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
-        ctx->d_sh_tick);
+        ctx->d_sh_tick));
   if (n > 0)
-    ++launches, k_aself<<<nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
+    KL(k_aself, nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
                                           ctx->d_sh_tick, ctx->d_bins + B + 1,
-                                          P, n, ctx->d_s_aself);
+                                          P, n, ctx->d_s_aself));
   CK(cudaGetLastError());
+  pc.mark("ingest");
   CK(cudaEventRecord(ctx->ev[1], st));
   // ---- per-shard views
   for (int s = 0; s < P; s++) {
@@ -979,13 +1076,14 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
                      cudaMemcpyHostToDevice, st));
   if (trace && n > 0)
-    ++launches, k_fill64<<<nblk(n, 256), 256, 0, st>>>(ctx->d_drop_t, n, -1);
+    KL(k_fill64, nblk(n, 256), 256, 0, st>>>(ctx->d_drop_t, n, -1));
   // ---- K2 fresh-start pre-scan
   if (use_fresh && n > 0)
-    ++launches, k_fresh<<<nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
+    KL(k_fresh, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
                                           ctx->d_mp, P, n, ctx->d_fresh,
-                                          (flags & SYM_FLAG_NO_FAST) ? nullptr : ctx->d_nxt);
+                                          (flags & SYM_FLAG_NO_FAST) ? nullptr : ctx->d_nxt));
   CK(cudaGetLastError());
+  pc.mark("fresh");
   CK(cudaEventRecord(ctx->ev[2], st));
   // ---- K3 parallel fast path (validated regime), K4 chain for the rest
   std::vector<uint32_t> fail(P, 0);
@@ -998,66 +1096,71 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     const int64_t ncp = n / kJump + M + 2;
     CK(cudaMemsetAsync(ctx->d_cp_model, 0xff, sizeof(int32_t) * ncp, st));
     // J_64 by six doublings of the chain pointer
-    ++launches, k_double<<<nblk(n, 256), 256, 0, st>>>(ctx->d_nxt, ctx->d_jA, n, 1);
+    KL(k_double, nblk(n, 256), 256, 0, st>>>(ctx->d_nxt, ctx->d_jA, n, 1));
     for (int d = 0; d < 6; d++) {
-      ++launches, k_double<<<nblk(n, 256), 256, 0, st>>>(ctx->d_jA, ctx->d_jB, n, 0);
+      KL(k_double, nblk(n, 256), 256, 0, st>>>(ctx->d_jA, ctx->d_jB, n, 0));
       std::swap(ctx->d_jA, ctx->d_jB);
     }
-    ++launches, k_walk<<<nblk(M, 64), 64, 0, st>>>(ctx->d_mp, M, ctx->d_nxt, ctx->d_jA,
+    KL(k_walk, nblk(M, 64), 64, 0, st>>>(ctx->d_mp, M, ctx->d_nxt, ctx->d_jA,
                                                    ctx->d_cp_pos, ctx->d_cp_model, ctx->d_nb,
-                                                   ctx->d_special);
-    ++launches, k_walk_expand<<<nblk(ncp, 128), 128, 0, st>>>(
+                                                   ctx->d_special));
+    KL(k_walk_expand, nblk(ncp, 128), 128, 0, st>>>(
         ctx->d_cp_pos, ctx->d_cp_model, ncp, ctx->d_mp, ctx->d_slot_base, P, ctx->d_nxt,
-        ctx->d_special, ctx->d_fresh, ctx->d_evb, (unsigned long long*)ctx->d_mdrops);
+        ctx->d_special, ctx->d_fresh, ctx->d_evb, (unsigned long long*)ctx->d_mdrops));
     // models whose chain needs the general (non-draining) evolution
-    ++launches, k_evolve<<<nblk(M, 64), 64, 0, st>>>(ctx->d_shards, ctx->d_slot_base, P, M,
+    KL(k_evolve, nblk(M, 64), 64, 0, st>>>(ctx->d_shards, ctx->d_slot_base, P, M,
                                                      ctx->d_fresh, ctx->d_evb, ctx->d_nb,
                                                      ctx->d_mdrops, ctx->d_fail,
-                                                     ctx->d_special);
-    ++launches, k_nb_scan<<<1, 32, 0, st>>>(ctx->d_nb, M, P, ctx->d_slot_base, ctx->d_bbase,
-                                            ctx->d_sbase);
+                                                     ctx->d_special));
+  pc.mark("evolve");
+    KL(k_nb_scan, 1, 32, 0, st>>>(ctx->d_nb, M, P, ctx->d_slot_base, ctx->d_bbase,
+                                            ctx->d_sbase));
     CK(cudaMemcpyAsync(sbase.data(), ctx->d_sbase, sizeof(int64_t) * (P + 1),
                        cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const int64_t nt = sbase[P];
     if (nt > 0) {
-      ++launches, k_batch_keys<<<nblk(n, 256), 256, 0, st>>>(
+      KL(k_batch_keys, nblk(n, 256), 256, 0, st>>>(
           ctx->d_shards, ctx->d_slot_base, P, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
-          ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail);
+          ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail));
       int bits = kTickBits;
       while ((1 << (bits - kTickBits)) < P) bits++;
       const int64_t Wr = (nt + kChunk - 1) / kChunk;
       auto radix = [&](uint64_t*& ka, uint32_t*& va, uint64_t*& kb, uint32_t*& vb) {
         for (int shift = 0; shift < bits; shift += 8) {
-          ++launches, k_rhist<<<nblk(Wr, 4), 128, 0, st>>>(ka, nt, shift, ctx->d_rhist, Wr);
-          ++launches, k_colscan<<<nblk(256, 128), 128, 0, st>>>(ctx->d_rhist, Wr, 256,
-                                                                ctx->d_rhist + Wr * 256);
-          ++launches, k_binscan256<<<1, 32, 0, st>>>(ctx->d_rhist + Wr * 256);
-          ++launches, k_rscatter<<<nblk(Wr, 4), 128, 0, st>>>(
-              ka, va, nt, shift, ctx->d_rhist, ctx->d_rhist + Wr * 256, Wr, kb, vb);
+          KL(k_rhist, nblk(Wr, 4), 128, 0, st>>>(ka, nt, shift, ctx->d_rhist, Wr));
+          KL(k_colscan, nblk(256, 128), 128, 0, st>>>(ctx->d_rhist, Wr, 256,
+                                                                ctx->d_rhist + Wr * 256));
+          KL(k_binscan256, 1, 32, 0, st>>>(ctx->d_rhist + Wr * 256));
+          KL(k_rscatter, nblk(Wr, 4), 128, 0, st>>>(
+              ka, va, nt, shift, ctx->d_rhist, ctx->d_rhist + Wr * 256, Wr, kb, vb));
           std::swap(ka, kb);
           std::swap(va, vb);
         }
       };
+  pc.mark("batch_keys");
       radix(ctx->d_bkA, ctx->d_bvA, ctx->d_bkB, ctx->d_bvB);
-      ++launches, k_runfix<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_bkA, ctx->d_bvA, nt,
-                                                          ctx->d_evb, ctx->d_fail);
-      ++launches, k_token_keys<<<nblk(nt, 256), 256, 0, st>>>(
+  pc.mark("sort_batches");
+      KL(k_runfix, nblk(nt, 256), 256, 0, st>>>(ctx->d_bkA, ctx->d_bvA, nt,
+                                                          ctx->d_evb, ctx->d_fail));
+      KL(k_token_keys, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_bvA, nt, ctx->d_bkA, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
-          ctx->d_fail);
+          ctx->d_fail));
+  pc.mark("token_keys");
       radix(ctx->d_tkA, ctx->d_tvA, ctx->d_tkB, ctx->d_tvB);
+  pc.mark("sort_tokens");
       for (int it = 0; it < 16; it++) {
-        ++launches, k_match<<<nblk(nt, 256), 256, 0, st>>>(
+        KL(k_match, nblk(nt, 256), 256, 0, st>>>(
             ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_shards, ctx->d_tkA,
-            ctx->d_tvA, ctx->d_ptrA, ctx->d_fail);
+            ctx->d_tvA, ctx->d_ptrA, ctx->d_fail));
         for (int round = 0; round < 64; round += 2) {
           CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
-          ++launches, k_jump<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
+          KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
                                                             ctx->d_bkA, ctx->d_sbase,
-                                                            ctx->d_shards, ctx->d_changed);
-          ++launches, k_jump<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
+                                                            ctx->d_shards, ctx->d_changed));
+          KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
                                                             ctx->d_bkA, ctx->d_sbase,
-                                                            ctx->d_shards, ctx->d_changed);
+                                                            ctx->d_shards, ctx->d_changed));
           int32_t changed = 0;
           CK(cudaMemcpyAsync(&changed, ctx->d_changed, sizeof changed,
                              cudaMemcpyDeviceToHost, st));
@@ -1065,22 +1168,21 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
           if (!changed) break;
         }
         CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
-        ++launches, k_tiefix<<<nblk(nt, 256), 256, 0, st>>>(ctx->d_tkA, ctx->d_tvA, nt,
+        KL(k_tiefix, nblk(nt, 256), 256, 0, st>>>(ctx->d_tkA, ctx->d_tvA, nt,
                                                             ctx->d_sbase, ctx->d_ptrA,
-                                                            ctx->d_changed);
+                                                            ctx->d_changed));
         int32_t moved = 0;
         CK(cudaMemcpyAsync(&moved, ctx->d_changed, sizeof moved, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (!moved) break;
       }
-      int64_t* d_rb = nullptr;
-      CK(cudaMallocAsync((void**)&d_rb, sizeof(int64_t) * (P + 1), st));
+  pc.mark("match_loop");
+      int64_t* d_rb = ctx->d_meta + 2 * (P + 1);
       CK(cudaMemcpyAsync(d_rb, rec_base.data(), sizeof(int64_t) * (P + 1),
                          cudaMemcpyHostToDevice, st));
-      ++launches, k_fast_emit<<<nblk(nt, 256), 256, 0, st>>>(
+      KL(k_fast_emit, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
-          ctx->d_ptrA, d_rb, ctx->d_shards, ctx->d_recs, ctx->d_fail);
-      CK(cudaFreeAsync(d_rb, st));
+          ctx->d_ptrA, d_rb, ctx->d_shards, ctx->d_recs, ctx->d_fail));
     }
     CK(cudaMemcpyAsync(fail.data(), ctx->d_fail, sizeof(uint32_t) * P,
                        cudaMemcpyDeviceToHost, st));
@@ -1088,6 +1190,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                        cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
+  pc.mark("fast_tail");
   CK(cudaEventRecord(ctx->ev[5], st));
   std::vector<int32_t> skip(P, 0);
   int32_t n_chain = 0;
@@ -1113,14 +1216,15 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                        cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(ctx->d_skip, skip.data(), sizeof(int32_t) * P,
                        cudaMemcpyHostToDevice, st));
-    ++launches, k_chain<<<P, 32, ctx->chain_smem, st>>>(
+    KL(k_chain, P, 32, ctx->chain_smem, st>>>(
         ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr, ctx->d_dirty,
-        ctx->d_slot_base, ctx->chain_smem, ctx->d_skip);
+        ctx->d_slot_base, ctx->chain_smem, ctx->d_skip));
   } else {
     CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
                        cudaMemcpyHostToDevice, st));
   }
   CK(cudaGetLastError());
+  pc.mark("chain");
   CK(cudaEventRecord(ctx->ev[3], st));
   CK(cudaMemcpyAsync(ctx->shards.data(), ctx->d_shards, sizeof(Shard) * P,
                      cudaMemcpyDeviceToHost, st));
@@ -1141,41 +1245,39 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     total += S.n_recs;
   }
   // ---- K5 outputs
-  int64_t* d_meta = nullptr;  // rec_base[P] + rec_count[P]
-  CK(cudaMallocAsync((void**)&d_meta, sizeof(int64_t) * 2 * (P + 1), st));
+  int64_t* d_meta = ctx->d_meta;  // rec_base[P] + rec_count[P]
   CK(cudaMemcpyAsync(d_meta, rec_base.data(), sizeof(int64_t) * P,
                      cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_meta + P + 1, rec_count.data(), sizeof(int64_t) * P,
                      cudaMemcpyHostToDevice, st));
   const bool expand = !(flags & SYM_FLAG_NO_EXPAND) && out->req_dispatch;
   if (expand && n > 0) {
-    ++launches, k_init_out<<<nblk(n, 256), 256, 0, st>>>(n, out->req_dispatch,
+    KL(k_init_out, nblk(n, 256), 256, 0, st>>>(n, out->req_dispatch,
                                              out->req_start, out->req_finish,
-                                             out->req_batch, out->req_outcome);
+                                             out->req_batch, out->req_outcome));
     if (total > 0)
-      ++launches, k_expand<<<nblk(total * 32, 256), 256, 0, st>>>(
+      KL(k_expand, nblk(total * 32, 256), 256, 0, st>>>(
           ctx->d_recs, d_meta, d_meta + P + 1, P, ctx->d_s_i, ctx->d_s_tick,
           ctx->d_mp, ctx->d_slot_base, total, out->req_dispatch,
-          out->req_start, out->req_finish, out->req_batch, out->req_outcome);
+          out->req_start, out->req_finish, out->req_batch, out->req_outcome));
   }
   if (trace && out->drop_t && n > 0)
-    ++launches, k_drop_out<<<nblk(n, 256), 256, 0, st>>>(
+    KL(k_drop_out, nblk(n, 256), 256, 0, st>>>(
         n, ctx->d_s_i, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
-        out->drop_t, out->drop_key_sub, out->drop_key_a);
+        out->drop_t, out->drop_key_sub, out->drop_key_a));
   if (out->batches && total > 0) {
     if (total > out->batch_cap) {
       ctx->err = "batch buffer too small";
-      cudaFreeAsync(d_meta, st);
       return SYM_EINVAL;
     }
-    ++launches, k_copy_batches<<<nblk(total, 256), 256, 0, st>>>(
+    KL(k_copy_batches, nblk(total, 256), 256, 0, st>>>(
         ctx->d_recs, d_meta, d_meta + P + 1, P, ctx->d_s_i,
         ctx->d_bins + B + P + 2, ctx->d_slot_base, ctx->d_bins + B + P + 2 + M,
-        total, out->batches);
+        total, out->batches));
   }
   CK(cudaGetLastError());
+  pc.mark("outputs");
   CK(cudaEventRecord(ctx->ev[4], st));
-  CK(cudaFreeAsync(d_meta, st));
   CK(cudaStreamSynchronize(st));
   (void)outs_on_device;
   // ---- counters
@@ -1230,6 +1332,24 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
 extern "C" {
 
 int32_t sym_version(void) { return kVersion; }
+
+const char* sym_kernel_times(void* engine, int32_t reset) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx) return "{}";
+  std::string j = "{";
+  bool first = true;
+  for (auto& kv : ctx->ktimes) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "%s\"%s\": [%lld, %.6f]", first ? "" : ", ", kv.first.c_str(),
+             (long long)kv.second.first, kv.second.second);
+    j += buf;
+    first = false;
+  }
+  j += "}";
+  ctx->ktimes_json = j;
+  if (reset) ctx->ktimes.clear();
+  return ctx->ktimes_json.c_str();
+}
 
 const char* sym_last_error(void* engine) {
   return engine ? static_cast<Ctx*>(engine)->err.c_str() : "null engine";
@@ -1365,7 +1485,15 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_skip, P);
   ALLOC(ctx->d_changed, 1);
   ALLOC(ctx->d_special, M);
+  ALLOC(ctx->d_meta, 3 * (P + 1));
 #undef ALLOC
+  {  // keep pool memory mapped across synchronisations (no remap stalls)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   const int B = M + P;
   cudaMemcpy(ctx->d_lat, lat.data(), sizeof(int64_t) * lat.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(ctx->d_mp, ctx->mp_host.data(), sizeof(ModelParam) * M, cudaMemcpyHostToDevice);
@@ -1437,7 +1565,8 @@ void sym_destroy(void* engine) {
                   ctx->d_ptrB, ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
                   ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_cp_pos,
-                  ctx->d_cp_model, ctx->d_special};
+                  ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
+                  ctx->d_drop, ctx->d_dka, ctx->d_bat};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& ev : ctx->ev)
@@ -1471,28 +1600,32 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model
     CK(cudaMemcpyAsync(ctx->d_model, arr_model, sizeof(int32_t) * n,
                        cudaMemcpyHostToDevice, st));
   }
-  // device-side output staging
+  // device-side output staging (persistent, grown on demand)
   sym_result dev = *out;
-  int64_t* d_req = nullptr;
-  int64_t* d_drop = nullptr;
-  int32_t* d_dka = nullptr;
-  sym_batch* d_b = nullptr;
   const bool want_req = out->req_dispatch && !(flags & SYM_FLAG_NO_EXPAND);
   const bool want_drop = (flags & SYM_FLAG_TRACE) && out->drop_t;
-  if (want_req) CK(cudaMallocAsync((void**)&d_req, sizeof(int64_t) * 5 * (n + 1), st));
-  if (want_drop) {
-    CK(cudaMallocAsync((void**)&d_drop, sizeof(int64_t) * 2 * (n + 1), st));
-    CK(cudaMallocAsync((void**)&d_dka, sizeof(int32_t) * (n + 1), st));
+  if (n + 1 > ctx->stage_cap) {
+    if ((rc = grow(ctx, ctx->d_req, 5 * (n + 1))) || (rc = grow(ctx, ctx->d_drop, 2 * (n + 1))) ||
+        (rc = grow(ctx, ctx->d_dka, n + 1)))
+      return rc;
+    ctx->stage_cap = n + 1;
   }
-  if (out->batches)
-    CK(cudaMallocAsync((void**)&d_b, sizeof(sym_batch) * (out->batch_cap + 1), st));
+  if (out->batches && out->batch_cap + 1 > ctx->bat_cap) {
+    if ((rc = grow(ctx, ctx->d_bat, out->batch_cap + 1))) return rc;
+    ctx->bat_cap = out->batch_cap + 1;
+  }
+  const int64_t sc = ctx->stage_cap;
+  int64_t* d_req = ctx->d_req;
+  int64_t* d_drop = ctx->d_drop;
+  int32_t* d_dka = ctx->d_dka;
+  sym_batch* d_b = out->batches ? ctx->d_bat : nullptr;
   dev.req_dispatch = want_req ? d_req : nullptr;
-  dev.req_start = want_req ? d_req + (n + 1) : nullptr;
-  dev.req_finish = want_req ? d_req + 2 * (n + 1) : nullptr;
-  dev.req_batch = want_req ? d_req + 3 * (n + 1) : nullptr;
-  dev.req_outcome = want_req ? d_req + 4 * (n + 1) : nullptr;
+  dev.req_start = want_req ? d_req + sc : nullptr;
+  dev.req_finish = want_req ? d_req + 2 * sc : nullptr;
+  dev.req_batch = want_req ? d_req + 3 * sc : nullptr;
+  dev.req_outcome = want_req ? d_req + 4 * sc : nullptr;
   dev.drop_t = want_drop ? d_drop : nullptr;
-  dev.drop_key_sub = want_drop ? d_drop + (n + 1) : nullptr;
+  dev.drop_key_sub = want_drop ? d_drop + sc : nullptr;
   dev.drop_key_a = want_drop ? d_dka : nullptr;
   dev.batches = d_b;
   dev.n = n;
@@ -1503,22 +1636,18 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model
       int64_t* dsts[5] = {out->req_dispatch, out->req_start, out->req_finish,
                           out->req_batch, out->req_outcome};
       for (int k = 0; k < 5; k++)
-        CK(cudaMemcpyAsync(dsts[k], d_req + k * (n + 1), sizeof(int64_t) * n,
+        CK(cudaMemcpyAsync(dsts[k], d_req + k * sc, sizeof(int64_t) * n,
                            cudaMemcpyDeviceToHost, st));
     }
     if (want_drop && n > 0) {
       CK(cudaMemcpyAsync(out->drop_t, d_drop, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(out->drop_key_sub, d_drop + (n + 1), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(out->drop_key_sub, d_drop + sc, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(out->drop_key_a, d_dka, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     }
     if (d_b && dev.n_batches > 0)
       CK(cudaMemcpyAsync(out->batches, d_b, sizeof(sym_batch) * dev.n_batches,
                          cudaMemcpyDeviceToHost, st));
   }
-  if (d_req) cudaFreeAsync(d_req, st);
-  if (d_drop) cudaFreeAsync(d_drop, st);
-  if (d_dka) cudaFreeAsync(d_dka, st);
-  if (d_b) cudaFreeAsync(d_b, st);
   CK(cudaStreamSynchronize(st));
   // copy back counters / timings
   sym_batch* keep_b = out->batches;

@@ -285,8 +285,16 @@ class Engine:
 
     # -- device-resident entry point -------------------------------------------
 
+    def kernel_times(self, reset: bool = True) -> dict:
+        """{kernel: (launches, total_ms)} from runs made with kernel_times=True."""
+        import json
+        if self._handle is None:
+            return {}
+        raw = self._lib.sym_kernel_times(self._handle, int(reset)).decode()
+        return {k: (int(v[0]), float(v[1])) for k, v in json.loads(raw).items()}
+
     def run_device(self, ticks, model, outputs: dict | None = None, expand: bool = True,
-                   batches=None):
+                   batches=None, kernel_times: bool = False):
         """Run on arrival tensors already resident on the engine's device
         (torch int64 ticks, int32 model ids).  Per-request outputs are
         written into ``outputs`` (dict of int64 CUDA tensors: dispatch,
@@ -316,6 +324,8 @@ class Engine:
         flags = self._flags() & ~_native.FLAG_TRACE
         if not expand:
             flags |= _native.FLAG_NO_EXPAND
+        if kernel_times:
+            flags |= _native.FLAG_KERNEL_TIMES
         torch.cuda.current_stream(dev).synchronize()
         rc = self._lib.sym_run_device(self._handle, ticks.data_ptr(), model.data_ptr(), n,
                                       flags, C.byref(res))
