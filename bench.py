@@ -262,11 +262,12 @@ def run_b200(args, rank, world, local_rank):
     peak, peak_kind = measured_peak_hbm()
     nb_step = batches // args.steps
     kern = {}
-    for name, (cnt_l, ms) in ktimes.items():
-        per_launch_ms = ms / cnt_l
+    k_total = sum(v[1] for v in ktimes.values())
+    for name, (cnt_l, k_ms) in ktimes.items():
+        per_launch_ms = k_ms / cnt_l
         ab = algorithmic_bytes(name, n, nb_step)
         kern[name] = {"launches_per_step": cnt_l / args.steps, "ms_per_launch": per_launch_ms,
-                      "share": ms / sum(v[1] for v in ktimes.values()),
+                      "share": k_ms / k_total,
                       "gbs": (ab / (per_launch_ms / 1e3) / 1e9) if ab else None}
     dom = max(kern, key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches_per_step"])
     ab = algorithmic_bytes(dom, n, nb_step)
@@ -314,8 +315,8 @@ def run_b200(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--duration", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
