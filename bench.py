@@ -249,6 +249,22 @@ def run_b200(args, rank, world, local_rank):
         if not np.array_equal(outs[k].cpu().numpy(), ref):
             raise SystemExit(f"device-resident and API outputs differ on {k}")
 
+    # end of run: the one collective -- per-sub-cluster integer summaries
+    # reduced over NCCL into the cluster's goodput / idle / autoscale view
+    from paper_2308_07470_b200.parallel import SummaryLayout, cluster_stats, reduce_summaries
+    layout = SummaryLayout(len(sc.models), sc.gpu_count)
+    lo, hi = int(0.1 * args.duration * 1e9), int(0.9 * args.duration * 1e9)
+    ids = np.arange(125 * rank, 125 * (rank + 1))
+    vec = layout.empty()
+    layout.put(vec, ids, np.arange(1024 * rank, 1024 * (rank + 1)), eng.window_counts(lo, hi))
+    t_red = time.perf_counter()
+    vec = reduce_summaries(vec)
+    red_ms = 1e3 * (time.perf_counter() - t_red)
+    world_layout = SummaryLayout(125 * world, 1024 * world)
+    cstats = cluster_stats(np.concatenate([vec[k * layout.M:k * layout.M + 125 * world]
+                                           for k in range(4)] + [vec[4 * layout.M:4 * layout.M
+                                                                      + 1024 * world]]),
+                           world_layout, lo, hi)
     t = torch.tensor([dev_ms, e2e_time, wall], dtype=torch.float64, device=dev)
     tot = torch.tensor([n, batches], dtype=torch.float64, device=dev)
     if world > 1:
@@ -301,6 +317,8 @@ def run_b200(args, rank, world, local_rank):
                  "chain_events": stats["chain_events"]},
         "clocks": clk.summary(),
         "wall_ms_per_step": 1e3 * wall / args.steps,
+        "cluster": dict(cstats, summary_allreduce_ms=red_ms,
+                        scope=f"sub-clusters 0..{world - 1}, window [10%, 90%) of the trace"),
     }
     if world == 1 and not args.no_cpu_baseline:
         t0 = time.perf_counter()

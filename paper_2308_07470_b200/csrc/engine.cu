@@ -97,7 +97,8 @@ struct Ctx {
   int64_t last_n = 0;
   const int64_t* last_ticks = nullptr;
   const int32_t* last_model = nullptr;
-  std::vector<int64_t> last_nrecs;
+  std::vector<int64_t> last_nrecs, last_rec_base;
+  const int64_t* last_outcome = nullptr;
   std::vector<uint32_t> last_fast_fail;
   bool has_run = false;
   std::map<std::string, std::pair<int64_t, double>> ktimes;  // name -> (launches, ms)
@@ -880,6 +881,45 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
   o.shrunk_from = 0;
 }
 
+
+// ------------------------------------------------ window reductions (K5) --
+// Integer parts of compute_stats (metrics.py:79-94) over the last run:
+// per-model outcome counts of arrivals in [lo, hi) and per-GPU busy time
+// clipped to the window.
+__global__ void k_window_req(const int64_t* __restrict__ ticks,
+                             const int32_t* __restrict__ model,
+                             const int64_t* __restrict__ outcome, int64_t n, int64_t lo,
+                             int64_t hi, unsigned long long* __restrict__ cnt /*[4][M]*/,
+                             int32_t M) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t t = ticks[i];
+  if (t < lo || t >= hi) return;
+  const int32_t m = model[i];
+  atomicAdd(&cnt[m], 1ull);
+  const int64_t o = outcome[i];
+  if (o >= 0 && o <= 2) atomicAdd(&cnt[(1 + o) * M + m], 1ull);
+}
+
+__global__ void k_window_busy(const BatchRec* __restrict__ recs,
+                              const int64_t* __restrict__ rec_base,
+                              const int64_t* __restrict__ rec_count, int32_t P,
+                              const int32_t* __restrict__ gpu_base, int64_t total,
+                              int64_t lo, int64_t hi, unsigned long long* __restrict__ busy) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= total) return;
+  int s = 0;
+  int64_t k = w;
+  while (s < P && k >= rec_count[s]) {
+    k -= rec_count[s];
+    s++;
+  }
+  const BatchRec& r = recs[rec_base[s] + k];
+  const int64_t a = r.start > lo ? r.start : lo;
+  const int64_t b = r.finish < hi ? r.finish : hi;
+  if (b > a) atomicAdd(&busy[gpu_base[s] + r.gpu], (unsigned long long)(b - a));
+}
+
 // ------------------------------------------------------------ driver ------
 
 int ensure_capacity(Ctx* ctx, int64_t n) {
@@ -1320,7 +1360,9 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   ctx->last_n = n;
   ctx->last_ticks = d_ticks;
   ctx->last_model = d_model;
+  ctx->last_outcome = expand ? out->req_outcome : nullptr;
   ctx->last_nrecs = rec_count;
+  ctx->last_rec_base = rec_base;
   ctx->has_run = true;
   return SYM_OK;
 }
@@ -1674,12 +1716,48 @@ int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,
                           int64_t* model_arrivals, int64_t* model_completed,
                           int64_t* model_late, int64_t* model_dropped,
                           int64_t* gpu_busy_ns) {
-  (void)lo_ns; (void)hi_ns; (void)model_arrivals; (void)model_completed;
-  (void)model_late; (void)model_dropped; (void)gpu_busy_ns;
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx) return SYM_EINVAL;
-  ctx->err = "sym_window_counts: not implemented in this build";
-  return SYM_EINVAL;
+  if (!ctx->has_run || !ctx->last_outcome) {
+    ctx->err = "sym_window_counts: no expanded run to reduce";
+    return SYM_EINVAL;
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int32_t M = ctx->M, P = ctx->P, G = ctx->G;
+  const int64_t n = ctx->last_n;
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc((void**)&d, sizeof(unsigned long long) * (4 * (size_t)M + G)));
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * (4 * (size_t)M + G), st));
+  if (n > 0)
+    k_window_req<<<nblk(n, 256), 256, 0, st>>>(ctx->last_ticks, ctx->last_model,
+                                               ctx->last_outcome, n, lo_ns, hi_ns, d, M);
+  int64_t total = 0;
+  for (int64_t c : ctx->last_nrecs) total += c;
+  if (total > 0) {
+    int64_t* meta = ctx->d_meta;
+    CK(cudaMemcpyAsync(meta, ctx->last_rec_base.data(), sizeof(int64_t) * P,
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(meta + P + 1, ctx->last_nrecs.data(), sizeof(int64_t) * P,
+                       cudaMemcpyHostToDevice, st));
+    const int32_t B = M + P;
+    k_window_busy<<<nblk(total, 256), 256, 0, st>>>(
+        ctx->d_recs, meta, meta + P + 1, P, ctx->d_bins + B + P + 2 + M, total, lo_ns, hi_ns,
+        d + 4 * (size_t)M);
+  }
+  std::vector<unsigned long long> h(4 * (size_t)M + G);
+  CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(d);
+  for (int32_t m = 0; m < M; m++) {
+    model_arrivals[m] = (int64_t)h[m];
+    model_completed[m] = (int64_t)h[M + m];
+    model_late[m] = (int64_t)h[2 * M + m];
+    model_dropped[m] = (int64_t)h[3 * M + m];
+  }
+  for (int32_t g = 0; g < G; g++) gpu_busy_ns[g] = (int64_t)h[4 * (size_t)M + g];
+  return SYM_OK;
 }
 
 }  // extern "C"

@@ -285,6 +285,26 @@ class Engine:
 
     # -- device-resident entry point -------------------------------------------
 
+    def window_counts(self, lo_ns: int, hi_ns: int) -> dict:
+        """Integer window reductions of the last run on the device (the
+        counting part of compute_stats, metrics.py:79-94): per model
+        arrivals/completed/late/dropped among arrivals in [lo, hi), per GPU
+        busy ns clipped to the window."""
+        if self._handle is None:
+            raise RuntimeError("no run to reduce")
+        M, G = len(self.models), self.gpu_count
+        out = {k: np.zeros(M, np.int64) for k in ("arrivals", "completed", "late", "dropped")}
+        busy = np.zeros(G, np.int64)
+        rc = self._lib.sym_window_counts(
+            self._handle, int(lo_ns), int(hi_ns),
+            *(out[k].ctypes.data_as(_native.i64p) for k in ("arrivals", "completed", "late",
+                                                               "dropped")),
+            busy.ctypes.data_as(_native.i64p))
+        if rc != _native.SYM_OK:
+            self._raise(rc, _native.SymResult())
+        out["gpu_busy_ns"] = busy
+        return out
+
     def kernel_times(self, reset: bool = True) -> dict:
         """{kernel: (launches, total_ms)} from runs made with kernel_times=True."""
         import json

@@ -167,6 +167,27 @@ def known_answers(out):
     out["known_answers"] = ka
 
 
+def autoscale_cases(out):
+    """C5 active-GPU series: reference compute_stats per 25 ms epoch of the
+    0.6 s diurnal run + autoscale_advice."""
+    import math
+    dur = 0.6
+    segs = tuple((j * dur / 24, 600_000.0 * (0.55 - 0.45 * math.cos(2 * math.pi * j / 24)))
+                 for j in range(24))
+    models = zoo_models(500)
+    ticks, midx = generate_arrivals(WorkloadSpec("piecewise", segments=segs),
+                                    [m.name for m in models], dur, 42)
+    eng = Engine(models, 4096, PolicyConfig("deferred"), NetworkModel.zero())
+    res = eng.run_stream(ticks, midx, dur)
+    series = []
+    for e in range(24):
+        st = RM.compute_stats(res, e * dur / 24, dur - (e + 1) * dur / 24, dur)
+        r = min(st.bad_rate, math.nextafter(1.0, 0.0))
+        series.append(4096 + RM.autoscale_advice(r, st.mean_idle_fraction, 4096))
+    out["C5/autoscale_series@0.6"] = series
+    print("autoscale", series, flush=True)
+
+
 def stress_cases(out, n_cases=60):
     sys.path.insert(0, os.path.join(REPO, "tests"))
     from stress_cases import make_case
@@ -184,6 +205,7 @@ if __name__ == "__main__":
     out = {"generator": "tests/golden/make_golden.py", "reference": "batchsym 0.1.0",
            "numpy": np.__version__}
     known_answers(out)
+    autoscale_cases(out)
     bundled_cases(out)
     stress_cases(out)
     config_cases(out)

@@ -33,3 +33,20 @@ def test_c4_full_stream_digest(golden):
     sc = configs.c4(0.1)
     ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models], 0.1, 42)
     assert D.trace_digest(ticks, midx) == golden["C4/trace_in@0.1"]
+
+
+def test_autoscale_series_c5(golden):
+    """C5 active-GPU series from the oracle run, with the
+    package's epoch reductions, equals the reference's compute_stats +
+    autoscale_advice per epoch."""
+    import numpy as np
+    from conftest import oracle_args
+    from paper_2308_07470_b200 import configs
+    from paper_2308_07470_b200.metrics import autoscale_series
+    from paper_2308_07470_b200.workload import generate_arrivals
+    from resultcheck import oracle_result
+    sc = configs.c5(0.6)
+    ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models], 0.6, 42)
+    o = oracle.run(arr_ticks=ticks, arr_midx=midx, **oracle_args(list(sc.models), 4096, sc.policy))
+    res = oracle_result(o, list(sc.models), 4096, ticks, midx, 0.6)
+    assert autoscale_series(res, 0.025, 0.6) == golden["C5/autoscale_series@0.6"]

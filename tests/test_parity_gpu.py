@@ -150,3 +150,26 @@ def test_goodput_search_known_answers(golden):
         res = goodput_search(load_scenario(name))
         assert res.rate_rps == want["rate_rps"]
         assert [list(p) for p in res.probes] == [list(p) for p in want["probes"]]
+
+
+def test_window_counts_and_autoscale_on_device(golden):
+    """sym_window_counts (device reductions) equals the host reductions, and
+    the C5 active-GPU series from the engine's result equals the reference."""
+    from paper_2308_07470_b200 import configs
+    from paper_2308_07470_b200.metrics import autoscale_series
+    from paper_2308_07470_b200.parallel import window_counts_host
+    from paper_2308_07470_b200.simulator import Engine
+    from paper_2308_07470_b200.workload import generate_arrivals
+    sc = configs.c5(0.6)
+    ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models], 0.6, 42)
+    eng = Engine(list(sc.models), sc.gpu_count, sc.policy)
+    res = eng.run_stream(ticks, midx, 0.6)
+    assert autoscale_series(res, 0.025, 0.6) == golden["C5/autoscale_series@0.6"]
+    for lo, hi in ((0, 600_000_000), (60_000_000, 540_000_000), (1234567, 7654321)):
+        dev = eng.window_counts(lo, hi)
+        b = res.batches
+        host = window_counts_host(res.req_model, res.req_arrival, res.req_outcome, b["gpu"],
+                                  b["start"], b["finish"], len(sc.models), sc.gpu_count, lo, hi)
+        for k in host:
+            np.testing.assert_array_equal(dev[k], host[k], err_msg=k)
+    eng.close()
