@@ -85,13 +85,21 @@ def build_workload(duration_s: float, shard: int):
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms during the
     timed region (B200_PROFILING.md clocks line)."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.window = None  # (t0, t1) wall-clock bounds of the timed region
+
+    def start(self):
+        self.__enter__()
+        time.sleep(1.0)  # nvidia-smi start-up; sampling is running before timing
+
+    def stop(self):
+        self.__exit__(None, None, None)
 
     def __enter__(self):
         try:
@@ -115,18 +123,25 @@ class ClockSampler:
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
+        import datetime
         sm, mx, reasons = [], 0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for ln in getattr(self, "lines", []):
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 6:
+            if len(f) < 7:
                 continue
             try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
             except ValueError:
                 continue
-            for nm, v in zip(names, f[2:6]):
+            if self.window and not (self.window[0] - 0.25 <= ts <= self.window[1] + 0.25):
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
@@ -207,12 +222,15 @@ def run_b200(args, rank, world, local_rank):
     for _ in range(args.warmup):
         flush.fill_(1)
         eng.run_device(t_dev, m_dev, outs)
+    clk = ClockSampler(local_rank)
+    clk.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     dev_ms, batches, launches = 0.0, 0, 0
-    with ClockSampler(local_rank) as clk:
+    if True:
         t0 = time.perf_counter()
+        w0 = time.time()
         for _ in range(args.steps):
             flush.fill_(1)
             _, cnt = eng.run_device(t_dev, m_dev, outs)
@@ -221,6 +239,8 @@ def run_b200(args, rank, world, local_rank):
             launches += cnt["launches"] + 1  # + the L2 flush
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        clk.window = (w0, time.time())
+    clk.stop()
     if world > 1:
         dist.barrier()
     stats = dict(cnt)
@@ -333,7 +353,7 @@ def run_b200(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--duration", type=float, default=60.0)
