@@ -1,3 +1,5 @@
+"""Summarise an `ncu --metrics gpu__time_duration.sum,dram__bytes_* --csv` launch list
+per kernel (dev tool): python tools/ncu_launches.py launches.csv"""
 import csv, collections, sys
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = None; per = collections.defaultdict(dict); order = []
@@ -7,7 +9,7 @@ for r in rows:
         d = dict(zip(hdr, r))
         key = (d["ID"], d["Kernel Name"].split("(")[0].replace("<unnamed>::", "")[:40])
         v = float(d["Metric Value"].replace(",", "")); u = d.get("Metric Unit", "")
-        scale = {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "second": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        scale = {"ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "second": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         per[key][d["Metric Name"]] = v * scale
         if key not in order: order.append(key)
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])

@@ -1,3 +1,5 @@
+"""Map ncu SASS-level stall samples to CUDA source lines via nvdisasm line info
+(dev tool): python tools/ncu_source_lines.py <kernel> <sass.csv> [top]"""
 import csv, re, sys, collections
 sass = open("/tmp/dev/cubin/all.sass").read().splitlines()
 fn = sys.argv[1]
