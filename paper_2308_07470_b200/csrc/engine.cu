@@ -64,6 +64,7 @@ struct Ctx {
   Shard* d_shards = nullptr;
   std::vector<Shard> shards;        // host images
   size_t chain_smem = 0;            // dynamic smem of k_chain
+  int64_t max_slo = 0, max_lat = 0; // bounds for the sort-key width
   // per-run buffers (grown)
   int64_t cap = 0, W_cap = 0;
   int64_t *d_ticks = nullptr, *d_s_tick = nullptr, *d_sh_tick = nullptr;
@@ -153,18 +154,42 @@ __global__ void k_hist(const int32_t* __restrict__ model, int64_t n,
     for (int b = lane; b < B; b += 32) hist[w * B + b] = cnt[b];
 }
 
-// exclusive scan of each bin over chunks; totals to bins[b]
-__global__ void k_colscan(int32_t* __restrict__ hist, int64_t W, int32_t B,
-                          int32_t* __restrict__ bins) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  int32_t run = 0;
-  for (int64_t w = 0; w < W; w++) {
-    const int32_t v = hist[w * B + b];
-    hist[w * B + b] = run;
-    run += v;
+// Exclusive scan of each bin (column) over the chunks (rows) of hist[W][B];
+// totals to bins[b].  One block per bin, 256-row tiles scanned with warp
+// shuffles, a running carry between tiles.
+__global__ void __launch_bounds__(256)
+k_colscan(int32_t* __restrict__ hist, int64_t W, int32_t B, int32_t* __restrict__ bins) {
+  __shared__ int32_t wsum[8];
+  __shared__ int32_t carry_s;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < W; base += 256) {
+    const int64_t w = base + tid;
+    const int32_t v = w < W ? hist[w * B + b] : 0;
+    int32_t x = v;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    int32_t woff = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int32_t t = wsum[k];
+      if (k < wid) woff += t;
+      tot += t;
+    }
+    const int32_t carry = carry_s;
+    if (w < W) hist[w * B + b] = carry + woff + x - v;
+    __syncthreads();
+    if (tid == 0) carry_s = carry + tot;
+    __syncthreads();
   }
-  bins[b] = run;
+  if (tid == 0) bins[b] = carry_s;
 }
 
 // single block: slot offsets (exclusive scan over slots) and shard stream
@@ -481,9 +506,8 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 // --------------------------------------------------------- K3 fast path ---
 // (fastpath.cuh).  All sub-clusters are processed together: sort keys carry
-// the shard id in bits [kTickBits, 64).
+// the shard id above the tick bits (tb = bits needed by the run's ticks).
 
-constexpr int kTickBits = 40;  // event ticks < 2^40 ns (~18 minutes)
 
 __device__ __forceinline__ int shard_of_slot(const int32_t* slot_base, int32_t P,
                                              int32_t k) {
@@ -638,7 +662,7 @@ __global__ void k_batch_keys(const Shard* __restrict__ shards,
                              const int32_t* __restrict__ bbase,
                              const EvBatch* __restrict__ evb, int64_t n,
                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                             uint32_t* __restrict__ fail) {
+                             uint32_t* __restrict__ fail, int tb) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   int lo = 0, hi = slot_base[P];
@@ -651,52 +675,76 @@ __global__ void k_batch_keys(const Shard* __restrict__ shards,
   if (j >= nb[lo]) return;
   const int s = shard_of_slot(slot_base, P, lo);
   const int64_t t = evb[p].t;
-  if (t < 0 || t >= (int64_t(1) << kTickBits)) atomicOr(&fail[s], FP_CAPACITY);
+  if (t < 0 || t >= (int64_t(1) << tb)) atomicOr(&fail[s], FP_CAPACITY);
   const int64_t d = bbase[lo] + j;
-  keys[d] = ((uint64_t)s << kTickBits) | (uint64_t)(t & ((int64_t(1) << kTickBits) - 1));
+  keys[d] = ((uint64_t)s << tb) | (uint64_t)(t & ((int64_t(1) << tb) - 1));
   vals[d] = (uint32_t)p;
 }
 
 // --- LSD radix sort of (u64 key, u32 value) pairs, 8-bit digits, stable ---
 
-__global__ void k_rhist(const uint64_t* __restrict__ keys, int64_t n, int shift,
-                        int32_t* __restrict__ hist, int64_t W) {
-  __shared__ int32_t cnt[4][256];
+constexpr int kDigitBits = 12;
+constexpr int kDigits = 1 << kDigitBits;  // radix bins
+constexpr int kRadixWarps = 2;            // warps per block (16 KB smem each)
+
+__global__ void __launch_bounds__(32 * kRadixWarps)
+k_rhist(const uint64_t* __restrict__ keys, int64_t n, int shift,
+        int32_t* __restrict__ hist, int64_t W) {
+  __shared__ int32_t cnt[kRadixWarps][kDigits];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * 4 + wib;
-  for (int b = lane; b < 256; b += 32) cnt[wib][b] = 0;
+  const int64_t w = (int64_t)blockIdx.x * kRadixWarps + wib;
+  for (int b = lane; b < kDigits; b += 32) cnt[wib][b] = 0;
   __syncwarp();
   if (w < W) {
     const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
     for (int64_t i = lo + lane; i < hi; i += 32)
-      atomicAdd(&cnt[wib][(keys[i] >> shift) & 255], 1);
+      atomicAdd(&cnt[wib][(keys[i] >> shift) & (kDigits - 1)], 1);
   }
   __syncwarp();
   if (w < W)
-    for (int b = lane; b < 256; b += 32) hist[w * 256 + b] = cnt[wib][b];
+    for (int b = lane; b < kDigits; b += 32) hist[w * kDigits + b] = cnt[wib][b];
 }
 
-__global__ void k_binscan256(int32_t* __restrict__ bins) {
-  if (threadIdx.x != 0) return;
-  int32_t run = 0;
-  for (int b = 0; b < 256; b++) {
-    const int32_t c = bins[b];
-    bins[b] = run;
-    run += c;
+// exclusive scan of the kDigits bin totals (one block)
+__global__ void __launch_bounds__(1024) k_binscan(int32_t* __restrict__ bins) {
+  __shared__ int32_t part[1024];
+  const int t = threadIdx.x;
+  constexpr int per = kDigits / 1024;
+  int32_t loc[per];
+  int32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < per; k++) {
+    loc[k] = bins[t * per + k];
+    sum += loc[k];
+  }
+  part[t] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
+    const int32_t y = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += y;
+    __syncthreads();
+  }
+  int32_t run = part[t] - sum;
+#pragma unroll
+  for (int k = 0; k < per; k++) {
+    bins[t * per + k] = run;
+    run += loc[k];
   }
 }
 
-__global__ void k_rscatter(const uint64_t* __restrict__ kin,
+__global__ void __launch_bounds__(32 * kRadixWarps)
+k_rscatter(const uint64_t* __restrict__ kin,
                            const uint32_t* __restrict__ vin, int64_t n, int shift,
                            const int32_t* __restrict__ hist,
                            const int32_t* __restrict__ bins, int64_t W,
                            uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
-  __shared__ int32_t base_s[4][256];
+  __shared__ int32_t base_s[kRadixWarps][kDigits];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * 4 + wib;
+  const int64_t w = (int64_t)blockIdx.x * kRadixWarps + wib;
   if (w >= W) return;
   int32_t* base = base_s[wib];
-  for (int b = lane; b < 256; b += 32) base[b] = bins[b] + hist[w * 256 + b];
+  for (int b = lane; b < kDigits; b += 32) base[b] = bins[b] + hist[w * kDigits + b];
   __syncwarp();
   const unsigned lt = (1u << lane) - 1u;
   const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
@@ -710,7 +758,7 @@ __global__ void k_rscatter(const uint64_t* __restrict__ kin,
     if (act) {
       k = kin[i];
       v = vin[i];
-      dg = (int32_t)((k >> shift) & 255);
+      dg = (int32_t)((k >> shift) & (kDigits - 1));
     }
     const unsigned peers = __match_any_sync(0xffffffffu, dg) & amask;
     int32_t pos = 0;
@@ -728,7 +776,7 @@ __global__ void k_rscatter(const uint64_t* __restrict__ kin,
 // K3d: order runs of equal (shard, tick) by the full event key
 __global__ void k_runfix(const uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
                          int64_t nt, const EvBatch* __restrict__ evb,
-                         uint32_t* __restrict__ fail) {
+                         uint32_t* __restrict__ fail, int tb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   if (i > 0 && keys[i - 1] == keys[i]) return;        // not a run start
@@ -746,7 +794,7 @@ __global__ void k_runfix(const uint64_t* __restrict__ keys, uint32_t* __restrict
   }
   for (int64_t a = i + 1; a < e; a++)
     if (batch_cmp(evb[vals[a - 1]], evb[vals[a]]) == 0)
-      atomicOr(&fail[keys[i] >> kTickBits], FP_KEY_TIE);
+      atomicOr(&fail[keys[i] >> tb], FP_KEY_TIE);
 }
 
 // K3e: finish-time token of every sorted batch: key (shard|finish),
@@ -756,14 +804,14 @@ __global__ void k_token_keys(const uint32_t* __restrict__ bvals, int64_t nt,
                              const EvBatch* __restrict__ evb,
                              const int64_t* __restrict__ sbase,
                              uint64_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
-                             uint32_t* __restrict__ fail) {
+                             uint32_t* __restrict__ fail, int tb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
-  const int s = (int)(bkeys[i] >> kTickBits);
+  const int s = (int)(bkeys[i] >> tb);
   const EvBatch& e = evb[bvals[i]];
   const int64_t fin = e.exec + e.lat;
-  if (fin < 0 || fin >= (int64_t(1) << kTickBits)) atomicOr(&fail[s], FP_CAPACITY);
-  tkeys[i] = ((uint64_t)s << kTickBits) | (uint64_t)(fin & ((int64_t(1) << kTickBits) - 1));
+  if (fin < 0 || fin >= (int64_t(1) << tb)) atomicOr(&fail[s], FP_CAPACITY);
+  tkeys[i] = ((uint64_t)s << tb) | (uint64_t)(fin & ((int64_t(1) << tb) - 1));
   tvals[i] = (uint32_t)(i - sbase[s]);
 }
 
@@ -774,10 +822,10 @@ __global__ void k_match(const uint64_t* __restrict__ bkeys, const uint32_t* __re
                         const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
                         const uint64_t* __restrict__ tkeys,
                         const uint32_t* __restrict__ tvals, int32_t* __restrict__ ptr,
-                        uint32_t* __restrict__ fail) {
+                        uint32_t* __restrict__ fail, int tb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
-  const int s = (int)(bkeys[i] >> kTickBits);
+  const int s = (int)(bkeys[i] >> tb);
   const int64_t r = i - sbase[s];
   const int32_t G = shards[s].G;
   if (r < G) {
@@ -796,12 +844,12 @@ __global__ void k_match(const uint64_t* __restrict__ bkeys, const uint32_t* __re
 // tiefix reaches the fixed point the sequential index produces.
 __global__ void k_tiefix(const uint64_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
                          int64_t nt, const int64_t* __restrict__ sbase,
-                         const int32_t* __restrict__ gid, int32_t* __restrict__ changed) {
+                         const int32_t* __restrict__ gid, int32_t* __restrict__ changed, int tb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   if (i > 0 && tkeys[i - 1] == tkeys[i]) return;
   if (i + 1 >= nt || tkeys[i + 1] != tkeys[i]) return;
-  const int64_t base = sbase[tkeys[i] >> kTickBits];
+  const int64_t base = sbase[tkeys[i] >> tb];
   int64_t e = i + 1;
   while (e < nt && tkeys[e] == tkeys[i]) e++;
   bool moved = false;
@@ -823,11 +871,11 @@ __global__ void k_tiefix(const uint64_t* __restrict__ tkeys, uint32_t* __restric
 __global__ void k_jump(const int32_t* __restrict__ pin, int32_t* __restrict__ pout,
                        int64_t nt, const uint64_t* __restrict__ bkeys,
                        const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
-                       int32_t* __restrict__ changed) {
+                       int32_t* __restrict__ changed, int tb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const int32_t v = pin[i];
-  const int s = (int)(bkeys[i] >> kTickBits);
+  const int s = (int)(bkeys[i] >> tb);
   const int32_t G = shards[s].G;
   if (v < G) {
     pout[i] = v;
@@ -848,10 +896,10 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
                             const int32_t* __restrict__ gid,
                             const int64_t* __restrict__ rec_base,
                             const Shard* __restrict__ shards,
-                            BatchRec* __restrict__ recs, uint32_t* __restrict__ fail) {
+                            BatchRec* __restrict__ recs, uint32_t* __restrict__ fail, int tb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
-  const int s = (int)(bkeys[i] >> kTickBits);
+  const int s = (int)(bkeys[i] >> tb);
   const int64_t r = i - sbase[s];
   // token i (shard order) vs token i+1: equal finish => gid order
   if (i + 1 < nt && tkeys[i + 1] == tkeys[i]) {
@@ -863,7 +911,7 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
   const int32_t G = shards[s].G;
   if (r >= G) {  // popped token: free by exec_at, created before this batch
     const int64_t ti = sbase[s] + (r - G);
-    const int64_t fa = (int64_t)(tkeys[ti] & ((uint64_t(1) << kTickBits) - 1));
+    const int64_t fa = (int64_t)(tkeys[ti] & ((uint64_t(1) << tb) - 1));
     if (fa > e.exec) atomicOr(&fail[s], FP_NO_GPU);
     if ((int64_t)tvals[ti] >= r) atomicOr(&fail[s], FP_LATE_TOKEN);
   }
@@ -940,7 +988,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_bvA, c)) || (rc = grow(ctx, ctx->d_bvB, c)) ||
         (rc = grow(ctx, ctx->d_tvA, c)) || (rc = grow(ctx, ctx->d_tvB, c)) ||
         (rc = grow(ctx, ctx->d_ptrA, c)) || (rc = grow(ctx, ctx->d_ptrB, c)) ||
-        (rc = grow(ctx, ctx->d_rhist, ((c + kChunk - 1) / kChunk) * 256 + 256)) ||
+        (rc = grow(ctx, ctx->d_rhist, ((c + kChunk - 1) / kChunk + 1) * kDigits)) ||
         (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
         (rc = grow(ctx, ctx->d_jB, c)) ||
         (rc = grow(ctx, ctx->d_cp_pos, c / kJump + ctx->M + 2)) ||
@@ -1062,15 +1110,27 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_hist, nblk(W, wpb), 32 * wpb, smem, st>>>(
         d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_err));
-    KL(k_colscan, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, ctx->d_bins));
+    KL(k_colscan, B, 256, 0, st>>>(ctx->d_hist, W, B, ctx->d_bins));
   } else {
     CK(cudaMemsetAsync(ctx->d_bins, 0, sizeof(int32_t) * B, st));
   }
   KL(k_binoff, 1, 32, 0, st>>>(ctx->d_bins, M, P, ctx->d_mp,
                              ctx->d_bins + B + 1));
   int32_t herr = INT32_MAX;
+  int64_t last_tick = 0;
   CK(cudaMemcpyAsync(&herr, ctx->d_err, sizeof herr, cudaMemcpyDeviceToHost, st));
+  if (n > 0)
+    CK(cudaMemcpyAsync(&last_tick, d_ticks + (n - 1), sizeof last_tick,
+                       cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  // every event tick and finish time of a validated run is below the last
+  // arrival + SLO; the bound is generous and checked (FP_CAPACITY)
+  int tick_bits = 1;
+  {
+    const uint64_t bound = (uint64_t)(last_tick > 0 ? last_tick : 0) +
+                           2 * (uint64_t)ctx->max_slo + (uint64_t)ctx->max_lat + 1;
+    while (tick_bits < 62 && (uint64_t(1) << tick_bits) <= bound) tick_bits++;
+  }
   if (herr != INT32_MAX) {
     out->err_index = herr;
     ctx->err = "request for unknown model";
@@ -1162,18 +1222,20 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     if (nt > 0) {
       KL(k_batch_keys, nblk(n, 256), 256, 0, st>>>(
           ctx->d_shards, ctx->d_slot_base, P, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
-          ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail));
-      int bits = kTickBits;
-      while ((1 << (bits - kTickBits)) < P) bits++;
+          ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits));
+      // key = (shard << tick_bits) | tick; only the bits in use are sorted
+      int bits = tick_bits;
+      while ((1 << (bits - tick_bits)) < P) bits++;
       const int64_t Wr = (nt + kChunk - 1) / kChunk;
       auto radix = [&](uint64_t*& ka, uint32_t*& va, uint64_t*& kb, uint32_t*& vb) {
-        for (int shift = 0; shift < bits; shift += 8) {
-          KL(k_rhist, nblk(Wr, 4), 128, 0, st>>>(ka, nt, shift, ctx->d_rhist, Wr));
-          KL(k_colscan, nblk(256, 128), 128, 0, st>>>(ctx->d_rhist, Wr, 256,
-                                                                ctx->d_rhist + Wr * 256));
-          KL(k_binscan256, 1, 32, 0, st>>>(ctx->d_rhist + Wr * 256));
-          KL(k_rscatter, nblk(Wr, 4), 128, 0, st>>>(
-              ka, va, nt, shift, ctx->d_rhist, ctx->d_rhist + Wr * 256, Wr, kb, vb));
+        for (int shift = 0; shift < bits; shift += kDigitBits) {
+          KL(k_rhist, nblk(Wr, kRadixWarps), 32 * kRadixWarps, 0, st>>>(ka, nt, shift,
+                                                                          ctx->d_rhist, Wr));
+          KL(k_colscan, kDigits, 256, 0, st>>>(ctx->d_rhist, Wr, kDigits,
+                                                ctx->d_rhist + Wr * kDigits));
+          KL(k_binscan, 1, 1024, 0, st>>>(ctx->d_rhist + Wr * kDigits));
+          KL(k_rscatter, nblk(Wr, kRadixWarps), 32 * kRadixWarps, 0, st>>>(
+              ka, va, nt, shift, ctx->d_rhist, ctx->d_rhist + Wr * kDigits, Wr, kb, vb));
           std::swap(ka, kb);
           std::swap(va, vb);
         }
@@ -1182,25 +1244,25 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
       radix(ctx->d_bkA, ctx->d_bvA, ctx->d_bkB, ctx->d_bvB);
   pc.mark("sort_batches");
       KL(k_runfix, nblk(nt, 256), 256, 0, st>>>(ctx->d_bkA, ctx->d_bvA, nt,
-                                                          ctx->d_evb, ctx->d_fail));
+                                                          ctx->d_evb, ctx->d_fail, tick_bits));
       KL(k_token_keys, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_bvA, nt, ctx->d_bkA, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
-          ctx->d_fail));
+          ctx->d_fail, tick_bits));
   pc.mark("token_keys");
       radix(ctx->d_tkA, ctx->d_tvA, ctx->d_tkB, ctx->d_tvB);
   pc.mark("sort_tokens");
       for (int it = 0; it < 16; it++) {
         KL(k_match, nblk(nt, 256), 256, 0, st>>>(
             ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_shards, ctx->d_tkA,
-            ctx->d_tvA, ctx->d_ptrA, ctx->d_fail));
+            ctx->d_tvA, ctx->d_ptrA, ctx->d_fail, tick_bits));
         for (int round = 0; round < 64; round += 2) {
           CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
           KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
                                                             ctx->d_bkA, ctx->d_sbase,
-                                                            ctx->d_shards, ctx->d_changed));
+                                                            ctx->d_shards, ctx->d_changed, tick_bits));
           KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
                                                             ctx->d_bkA, ctx->d_sbase,
-                                                            ctx->d_shards, ctx->d_changed));
+                                                            ctx->d_shards, ctx->d_changed, tick_bits));
           int32_t changed = 0;
           CK(cudaMemcpyAsync(&changed, ctx->d_changed, sizeof changed,
                              cudaMemcpyDeviceToHost, st));
@@ -1210,7 +1272,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
         KL(k_tiefix, nblk(nt, 256), 256, 0, st>>>(ctx->d_tkA, ctx->d_tvA, nt,
                                                             ctx->d_sbase, ctx->d_ptrA,
-                                                            ctx->d_changed));
+                                                            ctx->d_changed, tick_bits));
         int32_t moved = 0;
         CK(cudaMemcpyAsync(&moved, ctx->d_changed, sizeof moved, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -1222,7 +1284,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                          cudaMemcpyHostToDevice, st));
       KL(k_fast_emit, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
-          ctx->d_ptrA, d_rb, ctx->d_shards, ctx->d_recs, ctx->d_fail));
+          ctx->d_ptrA, d_rb, ctx->d_shards, ctx->d_recs, ctx->d_fail, tick_bits));
     }
     CK(cudaMemcpyAsync(fail.data(), ctx->d_fail, sizeof(uint32_t) * P,
                        cudaMemcpyDeviceToHost, st));
@@ -1469,6 +1531,8 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     p.cnt = 0;
     p.max_batch = mb;
     p.target_batch = cfg->target_batch < mb ? cfg->target_batch : mb;
+    ctx->max_slo = std::max<int64_t>(ctx->max_slo, p.slo);
+    ctx->max_lat = std::max<int64_t>(ctx->max_lat, row[mb - 1]);
   }
   *status = SYM_ECUDA;
   auto fail = [&](const char* what, cudaError_t e) -> void* {

@@ -329,17 +329,61 @@ SYM_HD void arm_drop_timer(const Shard& S, ModelState& st, const ModelParam& P,
   st.dt_key = push_key(imax(fire, now), PR_DROP, who);
 }
 
-// scheduler.py:277-299.  The predicate is monotone in b, so the answer is
-// unique; this is a branch-light binary search over the l(b) row.
+// scheduler.py:277-299.  The predicate ok(b) is monotone in b (both the
+// start bound and l(b) are non-decreasing), so the largest feasible b is
+// unique and any search finds it.  The search is galloping from a hint (the
+// previous candidate's size): as arrivals stream in, the answer moves by a
+// step or two, so this costs ~2 probes of the l(b) row instead of ~log2(cap).
 SYM_HD int32_t max_feasible(const Shard& S, int32_t m, int64_t now,
-                            int64_t floor, int32_t cap, int64_t d) {
+                            int64_t floor, int32_t cap, int64_t d,
+                            int32_t hint = 0) {
   const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
   const int64_t dc = S.d_ctrl, dd = S.d_data;
-  if (imax(now + dc + dd, floor) + lat[0] > d) return 0;
-  int32_t lo = 1, hi = cap;
+  auto ok = [&](int32_t b) {
+    return imax(now + dc + dd * b, floor) + lat[b - 1] <= d;
+  };
+  int32_t lo, hi;  // invariant: ok(lo) (or lo == 0), !ok(hi + 1) (or hi == cap)
+  if (hint < 1 || hint > cap) hint = 1;
+  if (ok(hint)) {
+    lo = hint;
+    int32_t step = 1;
+    for (;;) {  // gallop up
+      const int32_t nb = lo + step;
+      if (nb > cap) {
+        hi = cap;
+        break;
+      }
+      if (!ok(nb)) {
+        hi = nb - 1;
+        break;
+      }
+      lo = nb;
+      step <<= 1;
+    }
+  } else {
+    hi = hint - 1;
+    int32_t step = 1;
+    for (;;) {  // gallop down
+      const int32_t nb = hint - step;
+      if (nb < 1) {
+        lo = 0;
+        break;
+      }
+      if (ok(nb)) {
+        lo = nb;
+        break;
+      }
+      hi = nb - 1;
+      step <<= 1;
+    }
+    if (lo == 0) {
+      if (hi < 1 || !ok(1)) return 0;
+      lo = 1;
+    }
+  }
   while (lo < hi) {
-    int32_t mid = (lo + hi + 1) >> 1;
-    if (imax(now + dc + dd * mid, floor) + lat[mid - 1] <= d)
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (ok(mid))
       lo = mid;
     else
       hi = mid - 1;
@@ -407,7 +451,7 @@ SYM_HD bool update_candidate(const Shard& S, int32_t m, ModelState& st,
     lb = st.c_lb;
     lnext = st.c_lb1;
   } else {
-    b = max_feasible(S, m, now, floor2, cap, d);
+    b = max_feasible(S, m, now, floor2, cap, d, st.has_cand ? st.c_size : 1);
     if (b == 0) {
       arm_drop_timer(S, st, P, m, now, who);
       if (st.has_cand) {
