@@ -310,6 +310,47 @@ SYM_HD int32_t chain_next(const FreshRec& r, const ModelParam& mp) {
   return r.qt == mp.cnt ? NX_LAST : mp.off + r.qt;
 }
 
+// K2' (fast path): the batch-chain pointer of every position, by the lean
+// loop; positions it cannot certify run the general fresh_scan.
+__global__ void __launch_bounds__(256)
+k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
+      const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
+      int32_t* __restrict__ nxt) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int lo = 0, hi = slot_base[P];
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+  }
+  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  int s = 0;
+  while (slot_base[s + 1] <= lo) s++;
+  const Shard& S = shards[s];
+  const int32_t m = lo - slot_base[s];
+  const int32_t q = (int32_t)(p - mp_all[lo].off);
+  nxt[p] = lean_chain_next(S, m, q);
+}
+
+// Positions the lean loop could not certify: the general fresh_scan.
+__global__ void __launch_bounds__(256)
+k_nxt_general(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
+              const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
+              int32_t* __restrict__ nxt) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n || nxt[p] != NX_UNSURE) return;
+  int lo = 0, hi = slot_base[P];
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+  }
+  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  int s = 0;
+  while (slot_base[s + 1] <= lo) s++;
+  const int32_t q = (int32_t)(p - mp_all[lo].off);
+  nxt[p] = chain_next(fresh_scan(shards[s], lo - slot_base[s], q, kFreshMaxSteps), mp_all[lo]);
+}
+
 __global__ void __launch_bounds__(256)
 k_fresh(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
         const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
@@ -603,7 +644,7 @@ __global__ void k_walk_expand(const int32_t* __restrict__ cp_pos,
                               const int32_t* __restrict__ slot_base, int32_t P,
                               const int32_t* __restrict__ nxt,
                               const int32_t* __restrict__ special,
-                              const FreshRec* __restrict__ fresh,
+                              const Shard* __restrict__ shards,
                               EvBatch* __restrict__ evb,
                               unsigned long long* __restrict__ mdrops) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -615,27 +656,56 @@ __global__ void k_walk_expand(const int32_t* __restrict__ cp_pos,
   const int s = shard_of_slot(slot_base, P, k);
   int32_t p = cp_pos[q];
   int64_t out = mp.off + c * kJump;
-  unsigned long long dr = 0;
   for (int j = 0; j < kJump && p >= 0; j++) {
-    const FreshRec& r = fresh[p];
     const int32_t v = nxt[p];
-    dr += (unsigned long long)r.drops;
-    if (v == NX_NONE || v == NX_SPECIAL) break;
+    if (v == NX_NONE) {  // trailing all-dropped scan: count its drops
+      const FreshRec r = fresh_scan(shards[s], k - slot_base[s], p - mp.off, kFreshMaxSteps);
+      atomicAdd(&mdrops[k], (unsigned long long)r.drops);
+      break;
+    }
+    if (v == NX_SPECIAL) break;
     EvBatch& e = evb[out++];
-    e.t = r.mt_t;
-    e.a = r.mt_a;
-    e.tp = r.mt_tp;
-    e.ap = r.mt_ap;
-    e.chain = 0;  // fresh scans only hold arrival-pushed timers
-    e.exec = r.c_exec;
-    e.lat = r.c_lb;
-    e.size = r.c_size;
-    e.first = mp.off + r.qh;
+    e.first = p;  // batch fields filled by k_chain_recs
     e.model = k - slot_base[s];
     if (v == NX_LAST) break;
     p = v;
   }
-  atomicAdd(&mdrops[k], dr);
+}
+
+// One thread per batch of the fast path: the full fresh-start record of its
+// chain position gives the batch (timer key, exec_at, l(b), size, members)
+// and the heads dropped before it.
+__global__ void __launch_bounds__(256)
+k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
+             int32_t P, int32_t M, const ModelParam* __restrict__ mp_all,
+             const int32_t* __restrict__ nb, const int32_t* __restrict__ bbase,
+             const int32_t* __restrict__ special, int64_t nt, EvBatch* __restrict__ evb,
+             unsigned long long* __restrict__ mdrops) {
+  const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= nt) return;
+  int lo = 0, hi = M;  // last model with bbase <= d
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (bbase[mid] <= d) lo = mid; else hi = mid;
+  }
+  while (nb[lo] == 0 || bbase[lo] + nb[lo] <= d) lo++;
+  if (special[lo]) return;  // filled by k_evolve
+  const int s = shard_of_slot(slot_base, P, lo);
+  const ModelParam& mp = mp_all[lo];
+  EvBatch& e = evb[mp.off + (d - bbase[lo])];
+  const int32_t m = lo - slot_base[s];
+  const FreshRec r = fresh_scan(shards[s], m, e.first - mp.off, kFreshMaxSteps);
+  e.t = r.mt_t;
+  e.a = r.mt_a;
+  e.tp = r.mt_tp;
+  e.ap = r.mt_ap;
+  e.chain = 0;  // fresh scans only hold arrival-pushed timers
+  e.exec = r.c_exec;
+  e.lat = r.c_lb;
+  e.size = r.c_size;
+  e.first = mp.off + r.qh;
+  e.model = m;
+  if (r.drops) atomicAdd(&mdrops[lo], (unsigned long long)r.drops);
 }
 
 // K3b: dense batch numbering: bbase[k] per model, sbase[s] per shard
@@ -1177,11 +1247,20 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                      cudaMemcpyHostToDevice, st));
   if (trace && n > 0)
     KL(k_fill64, nblk(n, 256), 256, 0, st>>>(ctx->d_drop_t, n, -1));
-  // ---- K2 fresh-start pre-scan
-  if (use_fresh && n > 0)
+  // ---- K2 fresh-start pre-scan: chain pointers for the fast path, full
+  // records (needed only by the sequential chain) otherwise
+  const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
+  bool have_fresh = false;
+  if (fast) {
+    KL(k_nxt, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, n,
+                                          ctx->d_nxt));
+    KL(k_nxt_general, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp,
+                                                  P, n, ctx->d_nxt));
+  } else if (use_fresh && n > 0) {
     KL(k_fresh, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
-                                          ctx->d_mp, P, n, ctx->d_fresh,
-                                          (flags & SYM_FLAG_NO_FAST) ? nullptr : ctx->d_nxt));
+                                          ctx->d_mp, P, n, ctx->d_fresh, nullptr));
+    have_fresh = true;
+  }
   CK(cudaGetLastError());
   pc.mark("fresh");
   CK(cudaEventRecord(ctx->ev[2], st));
@@ -1189,7 +1268,6 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   std::vector<uint32_t> fail(P, 0);
   std::vector<int64_t> sbase(P + 1, 0);
   std::vector<int64_t> mdrops(M, 0);
-  const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
   if (fast) {
     CK(cudaMemsetAsync(ctx->d_fail, 0, sizeof(uint32_t) * P, st));
     CK(cudaMemsetAsync(ctx->d_mdrops, 0, sizeof(int64_t) * M, st));
@@ -1206,10 +1284,10 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                                                    ctx->d_special));
     KL(k_walk_expand, nblk(ncp, 128), 128, 0, st>>>(
         ctx->d_cp_pos, ctx->d_cp_model, ncp, ctx->d_mp, ctx->d_slot_base, P, ctx->d_nxt,
-        ctx->d_special, ctx->d_fresh, ctx->d_evb, (unsigned long long*)ctx->d_mdrops));
+        ctx->d_special, ctx->d_shards, ctx->d_evb, (unsigned long long*)ctx->d_mdrops));
     // models whose chain needs the general (non-draining) evolution
     KL(k_evolve, nblk(M, 64), 64, 0, st>>>(ctx->d_shards, ctx->d_slot_base, P, M,
-                                                     ctx->d_fresh, ctx->d_evb, ctx->d_nb,
+                                                     nullptr, ctx->d_evb, ctx->d_nb,
                                                      ctx->d_mdrops, ctx->d_fail,
                                                      ctx->d_special));
   pc.mark("evolve");
@@ -1220,6 +1298,9 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     CK(cudaStreamSynchronize(st));
     const int64_t nt = sbase[P];
     if (nt > 0) {
+      KL(k_chain_recs, nblk(nt, 256), 256, 0, st>>>(
+          ctx->d_shards, ctx->d_slot_base, P, M, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
+          ctx->d_special, nt, ctx->d_evb, (unsigned long long*)ctx->d_mdrops));
       KL(k_batch_keys, nblk(n, 256), 256, 0, st>>>(
           ctx->d_shards, ctx->d_slot_base, P, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
           ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits));
@@ -1314,6 +1395,11 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   }
   ctx->last_fast_fail = fail;
   if (n_chain > 0) {
+    if (use_fresh && !have_fresh && n > 0) {  // adoption records for the chain
+      KL(k_fresh, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P,
+                                              n, ctx->d_fresh, nullptr));
+      have_fresh = true;
+    }
     CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
                        cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(ctx->d_skip, skip.data(), sizeof(int32_t) * P,

@@ -140,3 +140,62 @@ SYM_HD int32_t evolve_model(const Shard& S, int32_t m, const FreshRec* fresh,
 }
 
 }  // namespace sym
+
+namespace sym {
+
+// Chain-pointer codes (see chain_next in engine.cu); NX_UNSURE asks for the
+// general fresh_scan.
+constexpr int32_t NX_UNSURE = -4;
+constexpr int32_t NX_LAST_LEAN = -1;  // == NX_LAST in engine.cu
+
+// Lean restatement of a fresh start at model position q for the deferred
+// policy with prefix gathering, valid while no head is dropped and the
+// candidate holds the whole queue (the underload regime).  Returns the
+// batch-chain pointer (absolute next fresh position or NX_LAST), or
+// NX_UNSURE as soon as the run leaves that regime.  Exact by construction:
+//  * drops: none while now + d_ctrl + d_data + l(1) <= head deadline
+//    (scheduler.py:223-225); later entries have later deadlines (FIFO, one
+//    SLO per model);
+//  * candidate: b = max_feasible with cap = min(len, max_batch)
+//    (scheduler.py:246-252), exec_at/latest as scheduler.py:262-270; the
+//    model timer is re-pushed only when (size, exec_at, latest) changes (the
+//    head is fixed, scheduler.py:272-273), at max(exec_at - delay(b), now)
+//    (scheduler.py:361-363);
+//  * the model timer precedes the drop timer (it fires no later than
+//    latest - delay < deadline - l(1) - delay(1) + 1), and precedes an
+//    arrival at the same tick, so the batch closes at the
+//    first arrival k with fire <= a_{k+1}.
+SYM_HD int32_t lean_chain_next(const Shard& S, int32_t m, int32_t q) {
+  const ModelParam& P = S.mp[m];
+  if (S.kind != K_DEFERRED || S.gather != G_PREFIX) return NX_UNSURE;
+  const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
+  const int64_t* tick = S.s_tick + P.off;
+  const int64_t dc = S.d_ctrl, dd = S.d_data;
+  const int64_t d = tick[q] + P.slo;
+  int32_t b = 0;
+  int64_t c_exec = 0, c_latest = 0, fire = 0;
+  for (int32_t k = q; k < P.cnt; k++) {
+    const int64_t now = tick[k];
+    if (now + P.base1 > d) return NX_UNSURE;  // the head would be dropped
+    const int32_t len = k - q + 1;
+    const int32_t cap = len < P.max_batch ? len : P.max_batch;
+    const int32_t nb = max_feasible(S, m, now, NEG_INF, cap, d, b > 0 ? b : 1);
+    if (nb != len) return NX_UNSURE;  // would not drain the queue
+    const int64_t l_next = nb < P.max_batch ? lat[nb] : lat[P.max_batch - 1];
+    int64_t exec = now + dc + dd * nb;
+    if (d - l_next > exec) exec = d - l_next;
+    const int64_t latest = d - lat[nb - 1];
+    if (nb != b || exec != c_exec || latest != c_latest) {
+      b = nb;
+      c_exec = exec;
+      c_latest = latest;
+      const int64_t f = exec - (dc + dd * nb);
+      fire = f < now ? now : f;
+    }
+    if (k + 1 >= P.cnt) return NX_LAST_LEAN;
+    if (fire <= tick[k + 1]) return P.off + k + 1;
+  }
+  return NX_UNSURE;
+}
+
+}  // namespace sym
