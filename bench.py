@@ -51,6 +51,19 @@ def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
         # fresh-start pre-scan: read each sorted arrival once (tick, A', g),
         # write one FreshRec and one chain pointer per position
         "k_fresh": n * (8 + 4 + 4 + FRESH_REC_BYTES + 4),
+        # lean chain pointer: each sorted tick read once (neighbours share
+        # the line), one 4-byte pointer written per position
+        "k_nxt": n * (8 + 4),
+        "k_nxt_general": n * 4,
+        # batch records from the chain positions' fresh scans: the members'
+        # ticks/ids once, one EvBatch written per batch
+        "k_chain_recs": n * (8 + 4 + 4) + nb * (4 + EV_BATCH_BYTES),
+        "k_walk": 0,
+        "k_jump": nb * (4 + 4 + 8 + 4),
+        "k_match": nb * (8 + 8 + 4 + 4),
+        "k_tiefix": nb * (8 + 4),
+        "k_token_keys": nb * (4 + 8 + EV_BATCH_BYTES + 8 + 4),
+        "k_runfix": nb * 8,
         "k_double": n * (4 + 4),
         "k_walk_expand": nb * (FRESH_REC_BYTES + 4 + EV_BATCH_BYTES),
         "k_batch_keys": nb * (8 + 8 + 4),

@@ -291,25 +291,6 @@ __global__ void k_aself(const int64_t* __restrict__ s_tick,
 
 // --------------------------------------------------------------- K2 -------
 
-// Batch-chain pointer of a fresh start at position p (fastpath.cuh):
-//   >= 0  a batch starts at p and drains the queue; the model is fresh again
-//         at that absolute position
-//   NX_LAST  a batch starts at p, drains the queue, no arrivals remain
-//   NX_NONE  no batch: every queued request was dropped, none remain
-//   NX_SPECIAL  anything else (non-draining grant, drop timer first, scan cap)
-constexpr int32_t NX_LAST = -1, NX_NONE = -2, NX_SPECIAL = -3;
-
-SYM_HD int32_t chain_next(const FreshRec& r, const ModelParam& mp) {
-  if (r.steps < 0) return NX_SPECIAL;
-  if (r.c_size == 0) return r.qh == r.qt && r.qt == mp.cnt ? NX_NONE : NX_SPECIAL;
-  if (r.c_size != r.qt - r.qh) return NX_SPECIAL;  // grant would leave a remainder
-  // the model timer must be the next event (it precedes the drop timer in a
-  // fresh scan, fastpath.cuh FP_DROP_TIMER)
-  const bool mt_first = r.mt_t < r.dt_t || (r.mt_t == r.dt_t && r.mt_a <= r.dt_a);
-  if (!mt_first) return NX_SPECIAL;
-  return r.qt == mp.cnt ? NX_LAST : mp.off + r.qt;
-}
-
 // K2' (fast path): the batch-chain pointer of every position, by the lean
 // loop; positions it cannot certify run the general fresh_scan.
 __global__ void __launch_bounds__(256)

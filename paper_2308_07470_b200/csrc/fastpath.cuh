@@ -143,10 +143,27 @@ SYM_HD int32_t evolve_model(const Shard& S, int32_t m, const FreshRec* fresh,
 
 namespace sym {
 
-// Chain-pointer codes (see chain_next in engine.cu); NX_UNSURE asks for the
-// general fresh_scan.
-constexpr int32_t NX_UNSURE = -4;
-constexpr int32_t NX_LAST_LEAN = -1;  // == NX_LAST in engine.cu
+// Batch-chain pointer of a fresh start at position p (fastpath.cuh):
+//   >= 0  a batch starts at p and drains the queue; the model is fresh again
+//         at that absolute position
+//   NX_LAST  a batch starts at p, drains the queue, no arrivals remain
+//   NX_NONE  no batch: every queued request was dropped, none remain
+//   NX_SPECIAL  anything else (non-draining grant, drop timer first, scan cap)
+constexpr int32_t NX_LAST = -1, NX_NONE = -2, NX_SPECIAL = -3;
+constexpr int32_t NX_UNSURE = -4;  // ask the general fresh_scan
+constexpr int32_t NX_LAST_LEAN = NX_LAST;
+
+SYM_HD int32_t chain_next(const FreshRec& r, const ModelParam& mp) {
+  if (r.steps < 0) return NX_SPECIAL;
+  if (r.c_size == 0) return r.qh == r.qt && r.qt == mp.cnt ? NX_NONE : NX_SPECIAL;
+  if (r.c_size != r.qt - r.qh) return NX_SPECIAL;  // grant would leave a remainder
+  // the model timer must be the next event (it precedes the drop timer in a
+  // fresh scan, fastpath.cuh FP_DROP_TIMER)
+  const bool mt_first = r.mt_t < r.dt_t || (r.mt_t == r.dt_t && r.mt_a <= r.dt_a);
+  if (!mt_first) return NX_SPECIAL;
+  return r.qt == mp.cnt ? NX_LAST : mp.off + r.qt;
+}
+
 
 // Lean restatement of a fresh start at model position q for the deferred
 // policy with prefix gathering, valid while no head is dropped and the
@@ -172,28 +189,26 @@ SYM_HD int32_t lean_chain_next(const Shard& S, int32_t m, int32_t q) {
   const int64_t* tick = S.s_tick + P.off;
   const int64_t dc = S.d_ctrl, dd = S.d_data;
   const int64_t d = tick[q] + P.slo;
-  int32_t b = 0;
-  int64_t c_exec = 0, c_latest = 0, fire = 0;
-  for (int32_t k = q; k < P.cnt; k++) {
-    const int64_t now = tick[k];
-    if (now + P.base1 > d) return NX_UNSURE;  // the head would be dropped
+  const int32_t mb = P.max_batch, cnt = P.cnt;
+  // While the candidate drains the queue its size is the queue length, so
+  // it changes at every arrival and the timer is re-pushed each time: the
+  // test at arrival k depends only on (q, k).
+  int64_t now = tick[q];
+  for (int32_t k = q; k < cnt; k++) {
     const int32_t len = k - q + 1;
-    const int32_t cap = len < P.max_batch ? len : P.max_batch;
-    const int32_t nb = max_feasible(S, m, now, NEG_INF, cap, d, b > 0 ? b : 1);
-    if (nb != len) return NX_UNSURE;  // would not drain the queue
-    const int64_t l_next = nb < P.max_batch ? lat[nb] : lat[P.max_batch - 1];
-    int64_t exec = now + dc + dd * nb;
-    if (d - l_next > exec) exec = d - l_next;
-    const int64_t latest = d - lat[nb - 1];
-    if (nb != b || exec != c_exec || latest != c_latest) {
-      b = nb;
-      c_exec = exec;
-      c_latest = latest;
-      const int64_t f = exec - (dc + dd * nb);
-      fire = f < now ? now : f;
-    }
-    if (k + 1 >= P.cnt) return NX_LAST_LEAN;
-    if (fire <= tick[k + 1]) return P.off + k + 1;
+    if (len > mb) return NX_UNSURE;  // capped: would not drain
+    const int64_t delay = dc + dd * len;
+    const int64_t lb = lat[len - 1];
+    // b == len  <=>  ok(len) (monotone); also excludes head drops
+    if (now + delay + lb > d) return NX_UNSURE;
+    const int64_t l_next = len < mb ? lat[len] : lat[mb - 1];
+    const int64_t exec = now + delay > d - l_next ? now + delay : d - l_next;
+    const int64_t f = exec - delay;
+    const int64_t fire = f < now ? now : f;
+    if (k + 1 >= cnt) return NX_LAST_LEAN;
+    const int64_t next = tick[k + 1];
+    if (fire <= next) return P.off + k + 1;
+    now = next;
   }
   return NX_UNSURE;
 }

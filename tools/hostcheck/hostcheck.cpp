@@ -7,6 +7,7 @@
 #include <vector>
 #include <algorithm>
 #include "../../paper_2308_07470_b200/csrc/engine_core.cuh"
+#include "../../paper_2308_07470_b200/csrc/fastpath.cuh"
 #include "../../oracle/symoracle.h"
 
 using namespace sym;
@@ -72,5 +73,15 @@ extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64
   *n_ord = S.n_recs;
   counters[0] = total_drops(S); counters[1] = S.ops; counters[2] = S.evictions; counters[3] = S.registrations;
   counters[4] = S.handler_ops_max; counters[5] = S.chain_events; counters[6] = S.absorbed; counters[7] = S.fresh_adoptions;
+  // lean chain pointer vs the general scan, every position
+  int64_t certified = 0, mismatch = 0;
+  for (int m = 0; m < M; m++)
+    for (int q = 0; q < cnt[m]; q++) {
+      int32_t v = lean_chain_next(S, m, q);
+      if (v == NX_UNSURE) continue;
+      certified++;
+      if (v != chain_next(fresh_scan(S, m, q, 1 << 16), mp[m])) mismatch++;
+    }
+  counters[8] = certified; counters[9] = mismatch;
   return 0;
 }
