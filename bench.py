@@ -71,8 +71,11 @@ def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
         "k_rhist": nb * 8,
         "k_fast_emit": nb * (EV_BATCH_BYTES + 12 + 4 + 8 + BATCH_REC_BYTES),
         # per-request RunResult arrays from batch records
-        "k_init_out": n * 5 * 8,
-        "k_expand": nb * BATCH_REC_BYTES + n * (4 + 8 + 5 * 8),
+        "k_fill32": n * 4,
+        "k_bid": nb * BATCH_REC_BYTES + n * 4,
+        # one thread per request: inverse map, batch id, tick, model read,
+        # five int64 written coalesced; batch records read once
+        "k_out": n * (4 + 4 + 8 + 4 + 5 * 8) + nb * BATCH_REC_BYTES,
         "k_copy_batches": nb * (BATCH_REC_BYTES + 4 + 64),
     }
     return table.get(kernel)

@@ -10,7 +10,8 @@
 //   K1e k_aself     canonical A' of every arrival (same-tick cascades)
 //   K2  k_fresh     fresh-start pre-scan: thread per sorted position
 //   K4  k_chain     one CTA per sub-cluster runs the live-event chain
-//   K5  k_init_out / k_expand  per-request RunResult arrays from batch records
+//   K3  k_nxt ... k_fast_emit  the parallel validated path (fastpath.cuh)
+//   K5  k_bid / k_out  per-request RunResult arrays from batch records
 // The chain (engine_core.cuh) is the only sequential part; everything else is
 // a bandwidth-bound pass over the request stream.
 #include <cuda_runtime.h>
@@ -35,6 +36,7 @@ using namespace sym;
 namespace {
 
 constexpr int kChunk = 4096;      // stream elements per warp in K1
+constexpr int kChunkR = 1024;     // keys per warp in the radix passes
 constexpr int kFreshMaxSteps = 1 << 16;
 constexpr int kVersion = 1;
 
@@ -56,6 +58,7 @@ struct Ctx {
   int32_t* d_slot_of_model = nullptr;
   int32_t* d_shard_of_model = nullptr;
   int32_t* d_slot_base = nullptr;   // [P+1]
+  int64_t* d_slo_model = nullptr;   // [M] SLO by global model id
   // chain state (independent of n)
   ModelState* d_ms = nullptr;
   int32_t *d_pq = nullptr, *d_gt = nullptr, *d_mlt = nullptr,
@@ -68,6 +71,7 @@ struct Ctx {
   // per-run buffers (grown)
   int64_t cap = 0, W_cap = 0;
   int64_t *d_ticks = nullptr, *d_s_tick = nullptr, *d_sh_tick = nullptr;
+  int32_t *d_inv = nullptr, *d_bid = nullptr;  // stream -> sorted position, position -> record
   int32_t *d_model = nullptr, *d_s_g = nullptr, *d_s_i = nullptr,
           *d_s_aself = nullptr;
   int32_t* d_hist = nullptr;        // [W][B]
@@ -227,7 +231,8 @@ __global__ void k_scatter(const int64_t* __restrict__ ticks,
                           int64_t* __restrict__ s_tick,
                           int32_t* __restrict__ s_g,
                           int32_t* __restrict__ s_i,
-                          int64_t* __restrict__ sh_tick) {
+                          int64_t* __restrict__ sh_tick,
+                          int32_t* __restrict__ inv) {
   extern __shared__ int32_t sh[];
   const int B = M + P;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -266,6 +271,7 @@ __global__ void k_scatter(const int64_t* __restrict__ ticks,
       s_g[pos] = j;
       s_i[pos] = (int32_t)i;
       sh_tick[j] = t;
+      inv[i] = pos;  // coalesced: i is the lane's stream index
     }
     __syncwarp();
   }
@@ -424,52 +430,55 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
 
 // --------------------------------------------------------------- K5 -------
 
-__global__ void k_init_out(int64_t n, int64_t* __restrict__ disp,
-                           int64_t* __restrict__ start,
-                           int64_t* __restrict__ fin, int64_t* __restrict__ bat,
-                           int64_t* __restrict__ outc) {
+__global__ void k_fill32(int32_t* p, int64_t n, int32_t v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  disp[i] = -1;
-  start[i] = -1;
-  fin[i] = -1;
-  bat[i] = -1;
-  outc[i] = 2;  // OUTCOME_DROPPED: every request resolves
+  if (i < n) p[i] = v;
 }
 
-// one warp per batch record
-__global__ void k_expand(const BatchRec* __restrict__ recs,
-                         const int64_t* __restrict__ rec_base,
-                         const int64_t* __restrict__ rec_count, int32_t P,
-                         const int32_t* __restrict__ s_i,
-                         const int64_t* __restrict__ s_tick,
-                         const ModelParam* __restrict__ mp_all,
-                         const int32_t* __restrict__ slot_base,
-                         int64_t total, int64_t* __restrict__ disp,
-                         int64_t* __restrict__ start,
-                         int64_t* __restrict__ fin, int64_t* __restrict__ bat,
-                         int64_t* __restrict__ outc) {
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+// every batch stamps its record index on its member positions
+__global__ void k_bid(const BatchRec* __restrict__ recs, const int64_t* __restrict__ rec_base,
+                      const int64_t* __restrict__ rec_count, int32_t P, int64_t total,
+                      int32_t* __restrict__ bid) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= total) return;
-  // map the dense index to (shard, record)
   int s = 0;
   int64_t k = w;
   while (s < P && k >= rec_count[s]) {
     k -= rec_count[s];
     s++;
   }
-  const BatchRec& r = recs[rec_base[s] + k];
-  const int64_t slo = mp_all[slot_base[s] + r.model].slo;
-  for (int j = lane; j < r.size; j += 32) {
-    const int64_t p = r.first + j;
-    const int64_t i = s_i[p];
-    disp[i] = r.emitted;
-    start[i] = r.start;
-    fin[i] = r.finish;
-    bat[i] = r.size;
-    outc[i] = r.finish <= s_tick[p] + slo ? 0 : 1;
+  const int64_t ri = rec_base[s] + k;
+  const BatchRec& r = recs[ri];
+  for (int32_t j = 0; j < r.size; j++) bid[r.first + j] = (int32_t)ri;
+}
+
+// RunResult arrays (simulator.py:74-78, 159-173, 249-258) in stream order:
+// one thread per request, reads scattered, writes coalesced.  A request no
+// batch covers was dropped (every request resolves).
+__global__ void k_out(int64_t n, const int32_t* __restrict__ inv,
+                      const int32_t* __restrict__ bid, const BatchRec* __restrict__ recs,
+                      const int64_t* __restrict__ ticks, const int32_t* __restrict__ model,
+                      const int64_t* __restrict__ slo_by_model,
+                      int64_t* __restrict__ disp, int64_t* __restrict__ start,
+                      int64_t* __restrict__ fin, int64_t* __restrict__ bat,
+                      int64_t* __restrict__ outc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t r = bid[inv[i]];
+  if (r < 0) {
+    disp[i] = -1;
+    start[i] = -1;
+    fin[i] = -1;
+    bat[i] = -1;
+    outc[i] = 2;  // OUTCOME_DROPPED
+    return;
   }
+  const BatchRec& b = recs[r];
+  disp[i] = b.emitted;
+  start[i] = b.start;
+  fin[i] = b.finish;
+  bat[i] = b.size;
+  outc[i] = b.finish <= ticks[i] + slo_by_model[model[i]] ? 0 : 1;
 }
 
 __global__ void k_drop_out(int64_t n, const int32_t* __restrict__ s_i,
@@ -747,7 +756,7 @@ k_rhist(const uint64_t* __restrict__ keys, int64_t n, int shift,
   for (int b = lane; b < kDigits; b += 32) cnt[wib][b] = 0;
   __syncwarp();
   if (w < W) {
-    const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
+    const int64_t lo = w * kChunkR, hi = (lo + kChunkR < n ? lo + kChunkR : n);
     for (int64_t i = lo + lane; i < hi; i += 32)
       atomicAdd(&cnt[wib][(keys[i] >> shift) & (kDigits - 1)], 1);
   }
@@ -798,7 +807,7 @@ k_rscatter(const uint64_t* __restrict__ kin,
   for (int b = lane; b < kDigits; b += 32) base[b] = bins[b] + hist[w * kDigits + b];
   __syncwarp();
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
+  const int64_t lo = w * kChunkR, hi = (lo + kChunkR < n ? lo + kChunkR : n);
   for (int64_t i0 = lo; i0 < hi; i0 += 32) {
     const int64_t i = i0 + lane;
     const bool act = i < hi;
@@ -1030,6 +1039,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
     if ((rc = grow(ctx, ctx->d_ticks, c)) || (rc = grow(ctx, ctx->d_model, c)) ||
         (rc = grow(ctx, ctx->d_s_tick, c)) || (rc = grow(ctx, ctx->d_sh_tick, c)) ||
         (rc = grow(ctx, ctx->d_s_g, c)) || (rc = grow(ctx, ctx->d_s_i, c)) ||
+        (rc = grow(ctx, ctx->d_inv, c)) || (rc = grow(ctx, ctx->d_bid, c)) ||
         (rc = grow(ctx, ctx->d_s_aself, c)) || (rc = grow(ctx, ctx->d_fresh, c)) ||
         (rc = grow(ctx, ctx->d_recs, c + ctx->P)) ||
         (rc = grow(ctx, ctx->d_drop_t, c)) || (rc = grow(ctx, ctx->d_drop_ks, c)) ||
@@ -1039,7 +1049,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_bvA, c)) || (rc = grow(ctx, ctx->d_bvB, c)) ||
         (rc = grow(ctx, ctx->d_tvA, c)) || (rc = grow(ctx, ctx->d_tvB, c)) ||
         (rc = grow(ctx, ctx->d_ptrA, c)) || (rc = grow(ctx, ctx->d_ptrB, c)) ||
-        (rc = grow(ctx, ctx->d_rhist, ((c + kChunk - 1) / kChunk + 1) * kDigits)) ||
+        (rc = grow(ctx, ctx->d_rhist, ((c + kChunkR - 1) / kChunkR + 1) * kDigits)) ||
         (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
         (rc = grow(ctx, ctx->d_jB, c)) ||
         (rc = grow(ctx, ctx->d_cp_pos, c / kJump + ctx->M + 2)) ||
@@ -1191,7 +1201,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_scatter, nblk(W, wpb), 32 * wpb, smem, st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, ctx->d_bins, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
-        ctx->d_sh_tick));
+        ctx->d_sh_tick, ctx->d_inv));
   if (n > 0)
     KL(k_aself, nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
                                           ctx->d_sh_tick, ctx->d_bins + B + 1,
@@ -1288,7 +1298,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
       // key = (shard << tick_bits) | tick; only the bits in use are sorted
       int bits = tick_bits;
       while ((1 << (bits - tick_bits)) < P) bits++;
-      const int64_t Wr = (nt + kChunk - 1) / kChunk;
+      const int64_t Wr = (nt + kChunkR - 1) / kChunkR;
       auto radix = [&](uint64_t*& ka, uint32_t*& va, uint64_t*& kb, uint32_t*& vb) {
         for (int shift = 0; shift < bits; shift += kDigitBits) {
           KL(k_rhist, nblk(Wr, kRadixWarps), 32 * kRadixWarps, 0, st>>>(ka, nt, shift,
@@ -1317,14 +1327,28 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         KL(k_match, nblk(nt, 256), 256, 0, st>>>(
             ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_shards, ctx->d_tkA,
             ctx->d_tvA, ctx->d_ptrA, ctx->d_fail, tick_bits));
+        // chains are the per-GPU batch sequences: ~nt/G long.  Run enough
+        // rounds for that before the first convergence check.
+        int warm = 0;
+        for (int64_t len = nt / std::max(1, ctx->G / P) + 1; len > 1; len = (len + 1) / 2) warm++;
+        warm = (warm + 1) & ~1;
         for (int round = 0; round < 64; round += 2) {
+          if (round + 2 <= warm) {
+            KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
+                                                    ctx->d_bkA, ctx->d_sbase, ctx->d_shards,
+                                                    ctx->d_changed, tick_bits));
+            KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
+                                                    ctx->d_bkA, ctx->d_sbase, ctx->d_shards,
+                                                    ctx->d_changed, tick_bits));
+            continue;
+          }
           CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
           KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
-                                                            ctx->d_bkA, ctx->d_sbase,
-                                                            ctx->d_shards, ctx->d_changed, tick_bits));
+                                                  ctx->d_bkA, ctx->d_sbase, ctx->d_shards,
+                                                  ctx->d_changed, tick_bits));
           KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
-                                                            ctx->d_bkA, ctx->d_sbase,
-                                                            ctx->d_shards, ctx->d_changed, tick_bits));
+                                                  ctx->d_bkA, ctx->d_sbase, ctx->d_shards,
+                                                  ctx->d_changed, tick_bits));
           int32_t changed = 0;
           CK(cudaMemcpyAsync(&changed, ctx->d_changed, sizeof changed,
                              cudaMemcpyDeviceToHost, st));
@@ -1421,14 +1445,14 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                      cudaMemcpyHostToDevice, st));
   const bool expand = !(flags & SYM_FLAG_NO_EXPAND) && out->req_dispatch;
   if (expand && n > 0) {
-    KL(k_init_out, nblk(n, 256), 256, 0, st>>>(n, out->req_dispatch,
-                                             out->req_start, out->req_finish,
-                                             out->req_batch, out->req_outcome));
+    KL(k_fill32, nblk(n, 256), 256, 0, st>>>(ctx->d_bid, n, -1));
     if (total > 0)
-      KL(k_expand, nblk(total * 32, 256), 256, 0, st>>>(
-          ctx->d_recs, d_meta, d_meta + P + 1, P, ctx->d_s_i, ctx->d_s_tick,
-          ctx->d_mp, ctx->d_slot_base, total, out->req_dispatch,
-          out->req_start, out->req_finish, out->req_batch, out->req_outcome));
+      KL(k_bid, nblk(total, 256), 256, 0, st>>>(ctx->d_recs, d_meta, d_meta + P + 1, P, total,
+                                                ctx->d_bid));
+    KL(k_out, nblk(n, 256), 256, 0, st>>>(n, ctx->d_inv, ctx->d_bid, ctx->d_recs, d_ticks,
+                                          d_model, ctx->d_slo_model, out->req_dispatch,
+                                          out->req_start, out->req_finish, out->req_batch,
+                                          out->req_outcome));
   }
   if (trace && out->drop_t && n > 0)
     KL(k_drop_out, nblk(n, 256), 256, 0, st>>>(
@@ -1658,6 +1682,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_skip, P);
   ALLOC(ctx->d_changed, 1);
   ALLOC(ctx->d_special, M);
+  ALLOC(ctx->d_slo_model, M);
   ALLOC(ctx->d_meta, 3 * (P + 1));
 #undef ALLOC
   {  // keep pool memory mapped across synchronisations (no remap stalls)
@@ -1673,6 +1698,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   cudaMemcpy(ctx->d_slot_of_model, ctx->slot_of_model.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
   cudaMemcpy(ctx->d_shard_of_model, ctx->shard_of_model.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
   cudaMemcpy(ctx->d_slot_base, ctx->slot_base.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->d_slo_model, cfg->slo_ns, sizeof(int64_t) * M, cudaMemcpyHostToDevice);
   cudaMemcpy(ctx->d_bins + B + P + 2, ctx->model_of_slot.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
   cudaMemcpy(ctx->d_bins + B + P + 2 + M, ctx->gpu_base.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice);
   int64_t om = 0, og = 0;
@@ -1731,6 +1757,7 @@ void sym_destroy(void* engine) {
                   ctx->d_mcs,  ctx->d_dirty,  ctx->d_free,  ctx->d_mcl,
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,   ctx->d_s_aself,
+                  ctx->d_inv, ctx->d_bid,
                   ctx->d_hist, ctx->d_bins,   ctx->d_err,   ctx->d_fresh,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
@@ -1739,7 +1766,7 @@ void sym_destroy(void* engine) {
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
                   ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_cp_pos,
                   ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
-                  ctx->d_drop, ctx->d_dka, ctx->d_bat};
+                  ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& ev : ctx->ev)
