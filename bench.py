@@ -69,6 +69,7 @@ def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
         "k_batch_keys": nb * (8 + 8 + 4),
         "k_rscatter": nb * (12 + 12),
         "k_rhist": nb * 8,
+        "k_scan_up": None, "k_scan_mid": None, "k_scan_down": None,
         "k_fast_emit": nb * (EV_BATCH_BYTES + 12 + 4 + 8 + BATCH_REC_BYTES),
         # per-request RunResult arrays from batch records
         "k_fill32": n * 4,

@@ -2,8 +2,8 @@
 //
 // Pipeline of one run (all on the engine's stream, inputs resident in HBM):
 //   K1a k_hist      per-warp-chunk histograms of (slot, shard) of the stream
-//   K1b k_colscan   per-bin exclusive scan over chunks  -> stable bases
-//   K1c k_binoff    bin offsets, per-model ModelParam.off/cnt
+//   K1b k_scan_*    flat exclusive scan of the bin-major histogram -> stable bases
+//   K1c k_binoff    per-model ModelParam.off/cnt, shard offsets
 //   K1d k_scatter   stable scatter to the (shard, model)-sorted layout with
 //                   warp __match_any_sync ranking (one warp per chunk keeps
 //                   stream order without any global atomics)
@@ -89,6 +89,7 @@ struct Ctx {
   uint32_t* d_fail = nullptr;
   int32_t* d_skip = nullptr;
   int64_t* d_meta = nullptr;       // [3*(P+1)]: rec_base | rec_count | spare
+  int32_t* d_scan_part = nullptr;   // block sums of flat_scan
   // staging for the host-buffer entry point (grown, never freed per call)
   int64_t *d_req = nullptr, *d_drop = nullptr;
   int32_t* d_dka = nullptr;
@@ -155,69 +156,109 @@ __global__ void k_hist(const int32_t* __restrict__ model, int64_t n,
   }
   __syncwarp();
   if (w < W)
-    for (int b = lane; b < B; b += 32) hist[w * B + b] = cnt[b];
+    for (int b = lane; b < B; b += 32) hist[(int64_t)b * W + w] = cnt[b];
 }
 
-// Exclusive scan of each bin (column) over the chunks (rows) of hist[W][B];
-// totals to bins[b].  One block per bin, 256-row tiles scanned with warp
-// shuffles, a running carry between tiles.
-__global__ void __launch_bounds__(256)
-k_colscan(int32_t* __restrict__ hist, int64_t W, int32_t B, int32_t* __restrict__ bins) {
-  __shared__ int32_t wsum[8];
-  __shared__ int32_t carry_s;
-  const int b = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) carry_s = 0;
+// ---- device-wide exclusive scan of an int32 array (reduce, scan the block
+// sums, rescan with offsets).  Histograms are stored bin-major (hist[b][w]),
+// so this one scan yields every stable scatter base: base(w, b) =
+// sum over bins < b + sum over chunks < w of bin b.
+constexpr int kScanItems = 4096;  // elements per block (1024 threads x 4)
+
+__device__ __forceinline__ int32_t block_exclusive_scan(int32_t v, int32_t* total) {
+  __shared__ int32_t wsum[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
   __syncthreads();
-  for (int64_t base = 0; base < W; base += 256) {
-    const int64_t w = base + tid;
-    const int32_t v = w < W ? hist[w * B + b] : 0;
-    int32_t x = v;  // inclusive warp scan
+  if (wid == 0) {
+    int32_t w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
     }
-    if (lane == 31) wsum[wid] = x;
-    __syncthreads();
-    int32_t woff = 0, tot = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int32_t t = wsum[k];
-      if (k < wid) woff += t;
-      tot += t;
-    }
-    const int32_t carry = carry_s;
-    if (w < W) hist[w * B + b] = carry + woff + x - v;
-    __syncthreads();
-    if (tid == 0) carry_s = carry + tot;
-    __syncthreads();
+    wsum[lane] = w;  // inclusive warp prefix
   }
-  if (tid == 0) bins[b] = carry_s;
+  __syncthreads();
+  const int32_t before = wid > 0 ? wsum[wid - 1] : 0;
+  *total = wsum[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before + x - v;
 }
 
-// single block: slot offsets (exclusive scan over slots) and shard stream
-// offsets (exclusive scan over shards); fills ModelParam.off/cnt.
-__global__ void k_binoff(int32_t* __restrict__ bins, int32_t M, int32_t P,
-                         ModelParam* __restrict__ mp,
+__global__ void __launch_bounds__(1024)
+k_scan_up(const int32_t* __restrict__ a, int64_t len, int32_t* __restrict__ part) {
+  const int64_t base = (int64_t)blockIdx.x * kScanItems + threadIdx.x * 4;
+  int32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+    if (base + k < len) v += a[base + k];
+  int32_t tot;
+  block_exclusive_scan(v, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024)
+k_scan_mid(int32_t* __restrict__ part, int64_t nparts) {
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < nparts; b0 += 1024) {
+    const int64_t i = b0 + threadIdx.x;
+    const int32_t v = i < nparts ? part[i] : 0;
+    int32_t tot;
+    const int32_t ex = block_exclusive_scan(v, &tot);
+    const int32_t c = carry;
+    if (i < nparts) part[i] = c + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c + tot;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+k_scan_down(int32_t* __restrict__ a, int64_t len, const int32_t* __restrict__ part) {
+  const int64_t base = (int64_t)blockIdx.x * kScanItems + threadIdx.x * 4;
+  int32_t loc[4];
+  int32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    loc[k] = base + k < len ? a[base + k] : 0;
+    v += loc[k];
+  }
+  int32_t tot;
+  int32_t run = block_exclusive_scan(v, &tot) + part[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    if (base + k < len) a[base + k] = run;
+    run += loc[k];
+  }
+}
+
+// ModelParam.off/cnt per slot and the shard stream offsets, read off the
+// scanned bin-major histogram (first column of every bin).
+__global__ void k_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t M, int32_t P,
+                         int64_t n, ModelParam* __restrict__ mp,
                          int32_t* __restrict__ shard_off) {
-  if (threadIdx.x == 0) {
-    int32_t run = 0;
-    for (int s = 0; s < M; s++) {
-      const int32_t c = bins[s];
-      mp[s].off = run;
-      mp[s].cnt = c;
-      bins[s] = run;
-      run += c;
-    }
-    run = 0;
-    for (int s = 0; s < P; s++) {
-      const int32_t c = bins[M + s];
-      bins[M + s] = run;
-      shard_off[s] = run;
-      run += c;
-    }
-    shard_off[P] = run;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  auto first = [&](int bin) -> int32_t {
+    return W > 0 ? hist[(int64_t)bin * W] : 0;
+  };
+  if (b < M) {
+    const int32_t o = first(b);
+    const int32_t e = b + 1 < M ? first(b + 1) : (int32_t)n;
+    mp[b].off = o;
+    mp[b].cnt = e - o;
+  } else if (b < M + P) {
+    const int s = b - M;
+    shard_off[s] = first(b) - (int32_t)n;
+    if (s == P - 1) shard_off[P] = (int32_t)n;
   }
 }
 
@@ -226,8 +267,7 @@ __global__ void k_scatter(const int64_t* __restrict__ ticks,
                           const int32_t* __restrict__ slot_of_model,
                           const int32_t* __restrict__ shard_of_model,
                           int32_t M, int32_t P,
-                          const int32_t* __restrict__ hist,
-                          const int32_t* __restrict__ bins, int64_t W,
+                          const int32_t* __restrict__ hist, int64_t W,
                           int64_t* __restrict__ s_tick,
                           int32_t* __restrict__ s_g,
                           int32_t* __restrict__ s_i,
@@ -239,7 +279,10 @@ __global__ void k_scatter(const int64_t* __restrict__ ticks,
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (w >= W) return;
   int32_t* base = sh + wib * B;
-  for (int b = lane; b < B; b += 32) base[b] = bins[b] + hist[w * B + b];
+  // bin-major flat exclusive scan: slot bins give sorted positions; shard
+  // bins follow all n slot entries, so subtract n for shard-stream indices
+  for (int b = lane; b < B; b += 32)
+    base[b] = hist[(int64_t)b * W + w] - (b >= M ? (int32_t)n : 0);
   __syncwarp();
   const unsigned lt = (1u << lane) - 1u;
   const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
@@ -762,49 +805,20 @@ k_rhist(const uint64_t* __restrict__ keys, int64_t n, int shift,
   }
   __syncwarp();
   if (w < W)
-    for (int b = lane; b < kDigits; b += 32) hist[w * kDigits + b] = cnt[wib][b];
-}
-
-// exclusive scan of the kDigits bin totals (one block)
-__global__ void __launch_bounds__(1024) k_binscan(int32_t* __restrict__ bins) {
-  __shared__ int32_t part[1024];
-  const int t = threadIdx.x;
-  constexpr int per = kDigits / 1024;
-  int32_t loc[per];
-  int32_t sum = 0;
-#pragma unroll
-  for (int k = 0; k < per; k++) {
-    loc[k] = bins[t * per + k];
-    sum += loc[k];
-  }
-  part[t] = sum;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
-    const int32_t y = t >= o ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += y;
-    __syncthreads();
-  }
-  int32_t run = part[t] - sum;
-#pragma unroll
-  for (int k = 0; k < per; k++) {
-    bins[t * per + k] = run;
-    run += loc[k];
-  }
+    for (int b = lane; b < kDigits; b += 32) hist[(int64_t)b * W + w] = cnt[wib][b];
 }
 
 __global__ void __launch_bounds__(32 * kRadixWarps)
 k_rscatter(const uint64_t* __restrict__ kin,
                            const uint32_t* __restrict__ vin, int64_t n, int shift,
-                           const int32_t* __restrict__ hist,
-                           const int32_t* __restrict__ bins, int64_t W,
+                           const int32_t* __restrict__ hist, int64_t W,
                            uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
   __shared__ int32_t base_s[kRadixWarps][kDigits];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = (int64_t)blockIdx.x * kRadixWarps + wib;
   if (w >= W) return;
   int32_t* base = base_s[wib];
-  for (int b = lane; b < kDigits; b += 32) base[b] = bins[b] + hist[w * kDigits + b];
+  for (int b = lane; b < kDigits; b += 32) base[b] = hist[(int64_t)b * W + w];
   __syncwarp();
   const unsigned lt = (1u << lane) - 1u;
   const int64_t lo = w * kChunkR, hi = (lo + kChunkR < n ? lo + kChunkR : n);
@@ -1040,6 +1054,10 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_s_tick, c)) || (rc = grow(ctx, ctx->d_sh_tick, c)) ||
         (rc = grow(ctx, ctx->d_s_g, c)) || (rc = grow(ctx, ctx->d_s_i, c)) ||
         (rc = grow(ctx, ctx->d_inv, c)) || (rc = grow(ctx, ctx->d_bid, c)) ||
+        (rc = grow(ctx, ctx->d_scan_part,
+                   std::max<int64_t>(((c + kChunkR - 1) / kChunkR + 1) * kDigits,
+                                     ((c + kChunk - 1) / kChunk + 1) * (ctx->M + ctx->P)) /
+                           kScanItems + 2)) ||
         (rc = grow(ctx, ctx->d_s_aself, c)) || (rc = grow(ctx, ctx->d_fresh, c)) ||
         (rc = grow(ctx, ctx->d_recs, c + ctx->P)) ||
         (rc = grow(ctx, ctx->d_drop_t, c)) || (rc = grow(ctx, ctx->d_drop_ks, c)) ||
@@ -1154,6 +1172,12 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   int64_t launches = 0;
   PhaseClock pc(st);
   KernelTimer kt{ctx, st, (flags & SYM_FLAG_KERNEL_TIMES) != 0, {}};
+  auto flat_scan = [&](int32_t* a, int64_t len) {
+    const int64_t nparts = (len + kScanItems - 1) / kScanItems;
+    KL(k_scan_up, nparts, 1024, 0, st>>>(a, len, ctx->d_scan_part));
+    KL(k_scan_mid, 1, 1024, 0, st>>>(ctx->d_scan_part, nparts));
+    KL(k_scan_down, nparts, 1024, 0, st>>>(a, len, ctx->d_scan_part));
+  };
   const int32_t M = ctx->M, P = ctx->P;
   const int B = M + P;
   const bool trace = flags & SYM_FLAG_TRACE;
@@ -1171,12 +1195,10 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_hist, nblk(W, wpb), 32 * wpb, smem, st>>>(
         d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_err));
-    KL(k_colscan, B, 256, 0, st>>>(ctx->d_hist, W, B, ctx->d_bins));
-  } else {
-    CK(cudaMemsetAsync(ctx->d_bins, 0, sizeof(int32_t) * B, st));
+    flat_scan(ctx->d_hist, W * B);
   }
-  KL(k_binoff, 1, 32, 0, st>>>(ctx->d_bins, M, P, ctx->d_mp,
-                             ctx->d_bins + B + 1));
+  KL(k_binoff, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, M, P, n, ctx->d_mp,
+                                           ctx->d_bins + B + 1));
   int32_t herr = INT32_MAX;
   int64_t last_tick = 0;
   CK(cudaMemcpyAsync(&herr, ctx->d_err, sizeof herr, cudaMemcpyDeviceToHost, st));
@@ -1200,7 +1222,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   if (W > 0)
     KL(k_scatter, nblk(W, wpb), 32 * wpb, smem, st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
-        ctx->d_hist, ctx->d_bins, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
+        ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
         ctx->d_sh_tick, ctx->d_inv));
   if (n > 0)
     KL(k_aself, nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
@@ -1303,11 +1325,9 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         for (int shift = 0; shift < bits; shift += kDigitBits) {
           KL(k_rhist, nblk(Wr, kRadixWarps), 32 * kRadixWarps, 0, st>>>(ka, nt, shift,
                                                                           ctx->d_rhist, Wr));
-          KL(k_colscan, kDigits, 256, 0, st>>>(ctx->d_rhist, Wr, kDigits,
-                                                ctx->d_rhist + Wr * kDigits));
-          KL(k_binscan, 1, 1024, 0, st>>>(ctx->d_rhist + Wr * kDigits));
+          flat_scan(ctx->d_rhist, Wr * kDigits);
           KL(k_rscatter, nblk(Wr, kRadixWarps), 32 * kRadixWarps, 0, st>>>(
-              ka, va, nt, shift, ctx->d_rhist, ctx->d_rhist + Wr * kDigits, Wr, kb, vb));
+              ka, va, nt, shift, ctx->d_rhist, Wr, kb, vb));
           std::swap(ka, kb);
           std::swap(va, vb);
         }
@@ -1757,7 +1777,7 @@ void sym_destroy(void* engine) {
                   ctx->d_mcs,  ctx->d_dirty,  ctx->d_free,  ctx->d_mcl,
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,   ctx->d_s_aself,
-                  ctx->d_inv, ctx->d_bid,
+                  ctx->d_inv, ctx->d_bid, ctx->d_scan_part,
                   ctx->d_hist, ctx->d_bins,   ctx->d_err,   ctx->d_fresh,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
