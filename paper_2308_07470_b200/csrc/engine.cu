@@ -35,8 +35,8 @@ using namespace sym;
 
 namespace {
 
-constexpr int kChunk = 4096;      // stream elements per warp in K1
 constexpr int kChunkR = 1024;     // keys per warp in the radix passes
+constexpr int kChunkI = 1024;     // stream elements per warp in the ingest
 constexpr int kFreshMaxSteps = 1 << 16;
 constexpr int kVersion = 1;
 
@@ -143,7 +143,7 @@ __global__ void k_hist(const int32_t* __restrict__ model, int64_t n,
   for (int b = lane; b < B; b += 32) cnt[b] = 0;
   __syncwarp();
   if (w < W) {
-    const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
+    const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
     for (int64_t i = lo + lane; i < hi; i += 32) {
       const int32_t m = model[i];
       if (m < 0 || m >= M) {
@@ -262,30 +262,74 @@ __global__ void k_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t M,
   }
 }
 
-__global__ void k_scatter(const int64_t* __restrict__ ticks,
-                          const int32_t* __restrict__ model, int64_t n,
-                          const int32_t* __restrict__ slot_of_model,
-                          const int32_t* __restrict__ shard_of_model,
-                          int32_t M, int32_t P,
-                          const int32_t* __restrict__ hist, int64_t W,
-                          int64_t* __restrict__ s_tick,
-                          int32_t* __restrict__ s_g,
-                          int32_t* __restrict__ s_i,
-                          int64_t* __restrict__ sh_tick,
-                          int32_t* __restrict__ inv) {
-  extern __shared__ int32_t sh[];
+// Stable scatter of the stream into the (shard, model)-sorted layout.  One
+// warp per kChunkI-element chunk: ranks come from __match_any_sync against
+// running per-bin offsets (stream order within a bin is preserved), the
+// chunk is first staged in shared memory in bin order, then written out so
+// consecutive lanes write consecutive positions of a bin run (coalesced).
+constexpr int kScatterWarps = 2;
+
+__host__ __device__ inline size_t scatter_smem_per_warp(int B) {
+  return sizeof(int32_t) * 3 * (size_t)B +
+         (size_t)kChunkI * (sizeof(int64_t) + 3 * sizeof(int32_t));
+}
+
+__global__ void __launch_bounds__(32 * kScatterWarps)
+k_scatter(const int64_t* __restrict__ ticks,
+          const int32_t* __restrict__ model, int64_t n,
+          const int32_t* __restrict__ slot_of_model,
+          const int32_t* __restrict__ shard_of_model,
+          int32_t M, int32_t P,
+          const int32_t* __restrict__ hist, int64_t W,
+          int64_t* __restrict__ s_tick,
+          int32_t* __restrict__ s_g,
+          int32_t* __restrict__ s_i,
+          int64_t* __restrict__ sh_tick,
+          int32_t* __restrict__ inv) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int B = M + P;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const int64_t w = (int64_t)blockIdx.x * kScatterWarps + wib;
   if (w >= W) return;
-  int32_t* base = sh + wib * B;
+  unsigned char* mine = smem_raw + wib * scatter_smem_per_warp(B);
+  int64_t* st_t = reinterpret_cast<int64_t*>(mine);
+  int32_t* st_g = reinterpret_cast<int32_t*>(st_t + kChunkI);
+  int32_t* st_i = st_g + kChunkI;
+  int32_t* st_b = st_i + kChunkI;
+  int32_t* gbase = st_b + kChunkI;  // global base of (bin, chunk)
+  int32_t* lstart = gbase + B;      // local start of the bin in the chunk
+  int32_t* lcur = lstart + B;       // running local offset (slot bins) /
+                                    // running global shard index (shard bins)
   // bin-major flat exclusive scan: slot bins give sorted positions; shard
-  // bins follow all n slot entries, so subtract n for shard-stream indices
-  for (int b = lane; b < B; b += 32)
-    base[b] = hist[(int64_t)b * W + w] - (b >= M ? (int32_t)n : 0);
+  // bins follow all n slot entries (subtract n for shard-stream indices).
+  // The chunk's count of a bin is the next flat entry minus this one.
+  const int64_t total = 2 * n;
+  int32_t run = 0;
+  for (int b0 = 0; b0 < B; b0 += 32) {
+    const int b = b0 + lane;
+    int32_t cnt = 0, g = 0;
+    if (b < B) {
+      const int64_t f = (int64_t)b * W + w;
+      g = hist[f];
+      const int64_t nx = f + 1 < (int64_t)B * W ? hist[f + 1] : total;
+      cnt = b < M ? (int32_t)(nx - g) : 0;
+    }
+    int32_t x = cnt;  // local exclusive scan over slot bins
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (b < B) {
+      gbase[b] = b < M ? g : g - (int32_t)n;
+      lstart[b] = run + x - cnt;
+      lcur[b] = b < M ? run + x - cnt : g - (int32_t)n;
+    }
+    run += __shfl_sync(0xffffffffu, x, 31);
+  }
   __syncwarp();
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t lo = w * kChunk, hi = (lo + kChunk < n ? lo + kChunk : n);
+  const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
   for (int64_t i0 = lo; i0 < hi; i0 += 32) {
     const int64_t i = i0 + lane;
     const bool act = i < hi;
@@ -300,23 +344,33 @@ __global__ void k_scatter(const int64_t* __restrict__ ticks,
     }
     const unsigned ps = __match_any_sync(0xffffffffu, sl) & amask;
     const unsigned pd = __match_any_sync(0xffffffffu, sd) & amask;
-    int32_t pos = 0, j = 0;
+    int32_t e = 0, j = 0;
     if (act) {
-      pos = base[sl] + __popc(ps & lt);
-      j = base[sd] + __popc(pd & lt);
+      e = lcur[sl] + __popc(ps & lt);
+      j = lcur[sd] + __popc(pd & lt);
     }
     __syncwarp();
     if (act) {
-      // the highest peer advances the running bases
-      if ((ps >> lane) == 1u) base[sl] += __popc(ps);
-      if ((pd >> lane) == 1u) base[sd] += __popc(pd);
-      s_tick[pos] = t;
-      s_g[pos] = j;
-      s_i[pos] = (int32_t)i;
+      // the highest peer advances the running offsets
+      if ((ps >> lane) == 1u) lcur[sl] += __popc(ps);
+      if ((pd >> lane) == 1u) lcur[sd] += __popc(pd);
+      st_t[e] = t;
+      st_g[e] = j;
+      st_i[e] = (int32_t)i;
+      st_b[e] = sl;
       sh_tick[j] = t;
-      inv[i] = pos;  // coalesced: i is the lane's stream index
+      inv[i] = gbase[sl] + (e - lstart[sl]);  // coalesced in i
     }
     __syncwarp();
+  }
+  __syncwarp();
+  const int32_t len = (int32_t)(hi - lo);
+  for (int32_t e = lane; e < len; e += 32) {  // bin runs, coalesced
+    const int32_t b = st_b[e];
+    const int32_t pos = gbase[b] + (e - lstart[b]);
+    s_tick[pos] = st_t[e];
+    s_g[pos] = st_g[e];
+    s_i[pos] = st_i[e];
   }
 }
 
@@ -1045,7 +1099,7 @@ __global__ void k_window_busy(const BatchRec* __restrict__ recs,
 // ------------------------------------------------------------ driver ------
 
 int ensure_capacity(Ctx* ctx, int64_t n) {
-  const int64_t W = (n + kChunk - 1) / kChunk;
+  const int64_t W = (n + kChunkI - 1) / kChunkI;
   const int B = ctx->M + ctx->P;
   if (n > ctx->cap) {
     int64_t c = n + n / 8 + 1024;
@@ -1056,7 +1110,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_inv, c)) || (rc = grow(ctx, ctx->d_bid, c)) ||
         (rc = grow(ctx, ctx->d_scan_part,
                    std::max<int64_t>(((c + kChunkR - 1) / kChunkR + 1) * kDigits,
-                                     ((c + kChunk - 1) / kChunk + 1) * (ctx->M + ctx->P)) /
+                                     ((c + kChunkI - 1) / kChunkI + 1) * (ctx->M + ctx->P)) /
                            kScanItems + 2)) ||
         (rc = grow(ctx, ctx->d_s_aself, c)) || (rc = grow(ctx, ctx->d_fresh, c)) ||
         (rc = grow(ctx, ctx->d_recs, c + ctx->P)) ||
@@ -1184,7 +1238,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const bool use_fresh = !trace && !(flags & SYM_FLAG_NO_FRESH);
   int rc;
   if ((rc = ensure_capacity(ctx, n))) return rc;
-  const int64_t W = (n + kChunk - 1) / kChunk;
+  const int64_t W = (n + kChunkI - 1) / kChunkI;
   CK(cudaEventRecord(ctx->ev[0], st));
   // ---- K1 ingest
   int32_t big = INT32_MAX;
@@ -1220,7 +1274,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     return SYM_EPROTO;
   }
   if (W > 0)
-    KL(k_scatter, nblk(W, wpb), 32 * wpb, smem, st>>>(
+    KL(k_scatter, nblk(W, kScatterWarps), 32 * kScatterWarps,
+       kScatterWarps * scatter_smem_per_warp(B), st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
         ctx->d_sh_tick, ctx->d_inv));
@@ -1761,6 +1816,11 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     if ((e = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ctx->chain_smem)) != cudaSuccess)
       return fail("smem attribute", e);
+    const size_t sc = kScatterWarps * scatter_smem_per_warp(ctx->M + ctx->P);
+    if (sc > (size_t)dev_max) return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
+    if ((e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sc)) != cudaSuccess)
+      return fail("scatter smem attribute", e);
   }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail("init", e);
   *status = SYM_OK;
