@@ -270,8 +270,9 @@ __global__ void k_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t M,
 constexpr int kScatterWarps = 2;
 
 __host__ __device__ inline size_t scatter_smem_per_warp(int B) {
-  return sizeof(int32_t) * 3 * (size_t)B +
-         (size_t)kChunkI * (sizeof(int64_t) + 3 * sizeof(int32_t));
+  const size_t bytes = sizeof(int32_t) * 3 * (size_t)B +
+                       (size_t)kChunkI * (sizeof(int64_t) + 3 * sizeof(int32_t));
+  return (bytes + 15) & ~size_t(15);  // keep every warp's int64 staging aligned
 }
 
 __global__ void __launch_bounds__(32 * kScatterWarps)
