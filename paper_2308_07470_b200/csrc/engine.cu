@@ -95,6 +95,7 @@ struct Ctx {
   int32_t* d_dka = nullptr;
   sym_batch* d_bat = nullptr;
   int64_t stage_cap = 0, bat_cap = 0;
+  int32_t* d_closek = nullptr;      // closing arrival of lean-certified starts
   int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
           *d_cp_model = nullptr, *d_special = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
@@ -395,33 +396,46 @@ __global__ void k_aself(const int64_t* __restrict__ s_tick,
 
 // --------------------------------------------------------------- K2 -------
 
-// K2' (fast path): the batch-chain pointer of every position, by the lean
-// loop; positions it cannot certify run the general fresh_scan.
+// K2' (fast path): the batch-chain pointer of every position by the lean
+// monotone sweep (fastpath.cuh), one thread per 32 consecutive positions;
+// close_k[p] keeps the closing arrival of certified starts for k_chain_recs.
+constexpr int kSweep = 32;
+
 __global__ void __launch_bounds__(256)
 k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
       const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
-      int32_t* __restrict__ nxt) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
+      int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
+  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kSweep;
+  if (p0 >= n) return;
+  const int64_t p1 = p0 + kSweep < n ? p0 + kSweep : n;
   int lo = 0, hi = slot_base[P];
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+    if (mp_all[mid].off <= p0) lo = mid; else hi = mid;
   }
-  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p0) lo++;
   int s = 0;
   while (slot_base[s + 1] <= lo) s++;
-  const Shard& S = shards[s];
-  const int32_t m = lo - slot_base[s];
-  const int32_t q = (int32_t)(p - mp_all[lo].off);
-  nxt[p] = lean_chain_next(S, m, q);
+  int64_t p = p0;
+  while (p < p1) {  // the range may cross model (and shard) boundaries
+    while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+    while (slot_base[s + 1] <= lo) s++;
+    const ModelParam& mp = mp_all[lo];
+    const int64_t end = mp.off + mp.cnt < p1 ? mp.off + mp.cnt : p1;
+    lean_chain_sweep(shards[s], lo - slot_base[s], (int32_t)(p - mp.off),
+                     (int32_t)(end - mp.off), [&](int32_t q, int32_t v, int32_t k) {
+                       nxt[mp.off + q] = v;
+                       close_k[mp.off + q] = k;
+                     });
+    p = end;
+  }
 }
 
 // Positions the lean loop could not certify: the general fresh_scan.
 __global__ void __launch_bounds__(256)
 k_nxt_general(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
               const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
-              int32_t* __restrict__ nxt) {
+              int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n || nxt[p] != NX_UNSURE) return;
   int lo = 0, hi = slot_base[P];
@@ -434,6 +448,7 @@ k_nxt_general(const Shard* __restrict__ shards, const int32_t* __restrict__ slot
   while (slot_base[s + 1] <= lo) s++;
   const int32_t q = (int32_t)(p - mp_all[lo].off);
   nxt[p] = chain_next(fresh_scan(shards[s], lo - slot_base[s], q, kFreshMaxSteps), mp_all[lo]);
+  close_k[p] = -1;  // not certified by the lean sweep: k_chain_recs rescans
 }
 
 __global__ void __launch_bounds__(256)
@@ -768,7 +783,7 @@ k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_
              int32_t P, int32_t M, const ModelParam* __restrict__ mp_all,
              const int32_t* __restrict__ nb, const int32_t* __restrict__ bbase,
              const int32_t* __restrict__ special, int64_t nt, EvBatch* __restrict__ evb,
-             unsigned long long* __restrict__ mdrops) {
+             unsigned long long* __restrict__ mdrops, const int32_t* __restrict__ close_k) {
   const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nt) return;
   int lo = 0, hi = M;  // last model with bbase <= d
@@ -782,6 +797,11 @@ k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_
   const ModelParam& mp = mp_all[lo];
   EvBatch& e = evb[mp.off + (d - bbase[lo])];
   const int32_t m = lo - slot_base[s];
+  const int32_t ck = close_k[e.first];
+  if (ck >= 0) {  // certified by the lean sweep: O(1) from (q, k)
+    lean_batch(shards[s], m, e.first - mp.off, ck, e);
+    return;
+  }
   const FreshRec r = fresh_scan(shards[s], m, e.first - mp.off, kFreshMaxSteps);
   e.t = r.mt_t;
   e.a = r.mt_a;
@@ -1124,6 +1144,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_ptrA, c)) || (rc = grow(ctx, ctx->d_ptrB, c)) ||
         (rc = grow(ctx, ctx->d_rhist, ((c + kChunkR - 1) / kChunkR + 1) * kDigits)) ||
         (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
+        (rc = grow(ctx, ctx->d_closek, c)) ||
         (rc = grow(ctx, ctx->d_jB, c)) ||
         (rc = grow(ctx, ctx->d_cp_pos, c / kJump + ctx->M + 2)) ||
         (rc = grow(ctx, ctx->d_cp_model, c / kJump + ctx->M + 2)))
@@ -1321,10 +1342,10 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
   bool have_fresh = false;
   if (fast) {
-    KL(k_nxt, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, n,
-                                          ctx->d_nxt));
+    KL(k_nxt, nblk((n + kSweep - 1) / kSweep, 256), 256, 0, st>>>(
+        ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, n, ctx->d_nxt, ctx->d_closek));
     KL(k_nxt_general, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp,
-                                                  P, n, ctx->d_nxt));
+                                                  P, n, ctx->d_nxt, ctx->d_closek));
   } else if (use_fresh && n > 0) {
     KL(k_fresh, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
                                           ctx->d_mp, P, n, ctx->d_fresh, nullptr));
@@ -1369,7 +1390,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     if (nt > 0) {
       KL(k_chain_recs, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_shards, ctx->d_slot_base, P, M, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
-          ctx->d_special, nt, ctx->d_evb, (unsigned long long*)ctx->d_mdrops));
+          ctx->d_special, nt, ctx->d_evb, (unsigned long long*)ctx->d_mdrops, ctx->d_closek));
       KL(k_batch_keys, nblk(n, 256), 256, 0, st>>>(
           ctx->d_shards, ctx->d_slot_base, P, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
           ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits));
@@ -1838,7 +1859,7 @@ void sym_destroy(void* engine) {
                   ctx->d_mcs,  ctx->d_dirty,  ctx->d_free,  ctx->d_mcl,
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,   ctx->d_s_aself,
-                  ctx->d_inv, ctx->d_bid, ctx->d_scan_part,
+                  ctx->d_inv, ctx->d_bid, ctx->d_scan_part, ctx->d_closek,
                   ctx->d_hist, ctx->d_bins,   ctx->d_err,   ctx->d_fresh,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,

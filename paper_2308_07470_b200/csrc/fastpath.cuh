@@ -213,4 +213,80 @@ SYM_HD int32_t lean_chain_next(const Shard& S, int32_t m, int32_t q) {
   return NX_UNSURE;
 }
 
+
+// Monotone sweep of lean_chain_next over consecutive positions [q0, q1) of
+// model m.  For a start q the batch closes at the first k with
+//   fire(q, k) = max(a_k, d_q - l(len+1) - delay(len)) <= a_{k+1},
+// len = k - q + 1.  Moving the start to q+1 raises d and lowers len, so
+// fire(q+1, k) >= fire(q, k): close(q+1, k) implies close(q, k), and the
+// regime tests ok(len) / len <= max_batch only get weaker.  Hence the
+// closing index never moves backwards and one forward pointer serves the
+// whole range (two-pointer sweep, O(q1 - q0 + b) instead of O((q1 - q0) b)).
+// The result for each q equals lean_chain_next(S, m, q) (host-verified).
+template <class Emit>
+SYM_HD void lean_chain_sweep(const Shard& S, int32_t m, int32_t q0, int32_t q1, Emit emit) {
+  const ModelParam& P = S.mp[m];
+  if (S.kind != K_DEFERRED || S.gather != G_PREFIX) {
+    for (int32_t q = q0; q < q1; q++) emit(q, NX_UNSURE, 0);
+    return;
+  }
+  const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
+  const int64_t* tick = S.s_tick + P.off;
+  const int64_t dc = S.d_ctrl, dd = S.d_data;
+  const int32_t mb = P.max_batch, cnt = P.cnt;
+  int32_t k = q0;
+  for (int32_t q = q0; q < q1; q++) {
+    if (k < q) k = q;
+    const int64_t d = tick[q] + P.slo;
+    int32_t v = NX_UNSURE;
+    for (;; k++) {
+      const int32_t len = k - q + 1;
+      if (len > mb) break;  // capped: would not drain (UNSURE)
+      const int64_t now = tick[k];
+      const int64_t delay = dc + dd * len;
+      if (now + delay + lat[len - 1] > d) break;  // b < len (UNSURE)
+      const int64_t l_next = len < mb ? lat[len] : lat[mb - 1];
+      const int64_t exec = now + delay > d - l_next ? now + delay : d - l_next;
+      const int64_t f = exec - delay;
+      const int64_t fire = f < now ? now : f;
+      if (k + 1 >= cnt) {
+        v = NX_LAST;
+        break;
+      }
+      if (fire <= tick[k + 1]) {
+        v = P.off + k + 1;
+        break;
+      }
+    }
+    emit(q, v, k);
+  }
+}
+
+// The batch a certified fresh start q produces, from (q, k) alone: the
+// candidate (len, exec_at) at the closing arrival k and its model timer,
+// pushed by arrival k (the size changes at every arrival in this regime).
+SYM_HD void lean_batch(const Shard& S, int32_t m, int32_t q, int32_t k, EvBatch& e) {
+  const ModelParam& P = S.mp[m];
+  const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
+  const int64_t* tick = S.s_tick + P.off;
+  const int32_t len = k - q + 1, mb = P.max_batch;
+  const int64_t d = tick[q] + P.slo, now = tick[k];
+  const int64_t delay = S.d_ctrl + S.d_data * len;
+  const int64_t l_next = len < mb ? lat[len] : lat[mb - 1];
+  const int64_t exec = now + delay > d - l_next ? now + delay : d - l_next;
+  const int64_t f = exec - delay;
+  const int64_t fire = f < now ? now : f;
+  const int32_t pos = P.off + k;
+  e.t = fire;
+  e.a = fire == now ? S.s_g[pos] + 1 : A_BASE;  // push_key with pusher = arrival k
+  e.tp = now;
+  e.ap = S.s_aself[pos];
+  e.chain = 0;
+  e.exec = exec;
+  e.lat = lat[len - 1];
+  e.size = len;
+  e.first = P.off + q;
+  e.model = m;
+}
+
 }  // namespace sym

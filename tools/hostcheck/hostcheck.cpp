@@ -82,6 +82,21 @@ extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64
       certified++;
       if (v != chain_next(fresh_scan(S, m, q, 1 << 16), mp[m])) mismatch++;
     }
+  // monotone sweep == per-position lean result; lean_batch == general record
+  for (int m = 0; m < M; m++) {
+    for (int q0 = 0; q0 < cnt[m]; q0 += 7) {
+      int q1 = std::min(cnt[m], q0 + 7);
+      lean_chain_sweep(S, m, q0, q1, [&](int32_t q, int32_t v, int32_t k) {
+        if (v != lean_chain_next(S, m, q)) mismatch += 1000;
+        if (v == NX_UNSURE) return;
+        FreshRec r = fresh_scan(S, m, q, 1 << 16);
+        EvBatch e; lean_batch(S, m, q, k, e);
+        if (e.t != r.mt_t || e.a != r.mt_a || e.tp != r.mt_tp || e.ap != r.mt_ap ||
+            e.exec != r.c_exec || e.lat != r.c_lb || e.size != r.c_size ||
+            e.first != off[m] + r.qh || r.drops != 0) mismatch += 1000000;
+      });
+    }
+  }
   counters[8] = certified; counters[9] = mismatch;
   return 0;
 }
