@@ -861,9 +861,9 @@ __global__ void k_batch_keys(const Shard* __restrict__ shards,
 
 // --- LSD radix sort of (u64 key, u32 value) pairs, 8-bit digits, stable ---
 
-constexpr int kDigitBits = 12;
+constexpr int kDigitBits = 8;
 constexpr int kDigits = 1 << kDigitBits;  // radix bins
-constexpr int kRadixWarps = 2;            // warps per block (16 KB smem each)
+constexpr int kRadixWarps = 4;            // warps per block (1 KB smem each)
 
 __global__ void __launch_bounds__(32 * kRadixWarps)
 k_rhist(const uint64_t* __restrict__ keys, int64_t n, int shift,
@@ -978,13 +978,14 @@ __global__ void k_match(const uint64_t* __restrict__ bkeys, const uint32_t* __re
   const int64_t r = i - sbase[s];
   const int32_t G = shards[s].G;
   if (r < G) {
-    ptr[i] = (int32_t)r;  // terminal: gid r
+    ptr[i] = -(int32_t)r - 1;  // terminal: gid r
     return;
   }
   const int64_t ti = sbase[s] + (r - G);
   const int64_t c = tvals[ti];
-  // a token created at or after its consumer would loop; validated in emit
-  ptr[i] = c < r ? (int32_t)(G + c) : 0;  // >= G: "same gid as rank c"
+  // >= 0: "same gid as the batch at absolute index sbase + c"; a token
+  // created at or after its consumer would loop (validated in emit)
+  ptr[i] = c < r ? (int32_t)(sbase[s] + c) : -1;
 }
 
 // Equal-finish tokens pop in gid order (scheduler.py:338: min (free_at,
@@ -1004,9 +1005,9 @@ __global__ void k_tiefix(const uint64_t* __restrict__ tkeys, uint32_t* __restric
   bool moved = false;
   for (int64_t a = i + 1; a < e; a++) {
     const uint32_t v = tvals[a];
-    const int32_t gv = gid[base + v];
+    const int32_t gv = -gid[base + v] - 1;
     int64_t b = a;
-    while (b > i && gid[base + tvals[b - 1]] > gv) {
+    while (b > i && -gid[base + tvals[b - 1]] - 1 > gv) {
       tvals[b] = tvals[b - 1];
       b--;
       moved = true;
@@ -1016,23 +1017,20 @@ __global__ void k_tiefix(const uint64_t* __restrict__ tkeys, uint32_t* __restric
   if (moved) *changed = 1;
 }
 
-// pointer jumping: ptr >= G refers to rank ptr-G of the same shard
+// pointer jumping over absolute indices: ptr >= 0 follows the creator,
+// ptr < 0 is resolved (gid = -ptr - 1)
 __global__ void k_jump(const int32_t* __restrict__ pin, int32_t* __restrict__ pout,
-                       int64_t nt, const uint64_t* __restrict__ bkeys,
-                       const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
-                       int32_t* __restrict__ changed, int tb) {
+                       int64_t nt, int32_t* __restrict__ changed) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const int32_t v = pin[i];
-  const int s = (int)(bkeys[i] >> tb);
-  const int32_t G = shards[s].G;
-  if (v < G) {
+  if (v < 0) {
     pout[i] = v;
     return;
   }
-  const int32_t w = pin[sbase[s] + (v - G)];
+  const int32_t w = pin[v];
   pout[i] = w;
-  if (w >= G) *changed = 1;
+  if (w >= 0) *changed = 1;
 }
 
 // K3g: token ties must pop in gid order; emit the BatchRec of every batch
@@ -1052,8 +1050,8 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
   const int64_t r = i - sbase[s];
   // token i (shard order) vs token i+1: equal finish => gid order
   if (i + 1 < nt && tkeys[i + 1] == tkeys[i]) {
-    const int32_t g0 = gid[sbase[s] + tvals[i]];
-    const int32_t g1 = gid[sbase[s] + tvals[i + 1]];
+    const int32_t g0 = -gid[sbase[s] + tvals[i]] - 1;
+    const int32_t g1 = -gid[sbase[s] + tvals[i + 1]] - 1;
     if (g0 > g1) atomicOr(&fail[s], FP_TOKEN_TIE);
   }
   const EvBatch& e = evb[bvals[i]];
@@ -1072,7 +1070,7 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
   o.ka = e.a;
   o.ksub = r;  // processing order = rank (the chain counter of the chain)
   o.model = e.model;
-  o.gpu = gid[i];
+  o.gpu = -gid[i] - 1;
   o.size = e.size;
   o.first = e.first;
   o.shrunk_from = 0;
@@ -1431,21 +1429,13 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         warm = (warm + 1) & ~1;
         for (int round = 0; round < 64; round += 2) {
           if (round + 2 <= warm) {
-            KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
-                                                    ctx->d_bkA, ctx->d_sbase, ctx->d_shards,
-                                                    ctx->d_changed, tick_bits));
-            KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
-                                                    ctx->d_bkA, ctx->d_sbase, ctx->d_shards,
-                                                    ctx->d_changed, tick_bits));
+            KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt, ctx->d_changed));
+            KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt, ctx->d_changed));
             continue;
           }
           CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
-          KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt,
-                                                  ctx->d_bkA, ctx->d_sbase, ctx->d_shards,
-                                                  ctx->d_changed, tick_bits));
-          KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt,
-                                                  ctx->d_bkA, ctx->d_sbase, ctx->d_shards,
-                                                  ctx->d_changed, tick_bits));
+          KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt, ctx->d_changed));
+          KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt, ctx->d_changed));
           int32_t changed = 0;
           CK(cudaMemcpyAsync(&changed, ctx->d_changed, sizeof changed,
                              cudaMemcpyDeviceToHost, st));
