@@ -59,9 +59,8 @@ def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
         # ticks/ids once, one EvBatch written per batch
         "k_chain_recs": n * (8 + 4 + 4) + nb * (4 + EV_BATCH_BYTES),
         "k_walk": 0,
-        "k_jump": nb * (4 + 4 + 8 + 4),
-        "k_match": nb * (8 + 8 + 4 + 4),
-        "k_tiefix": nb * (8 + 4),
+        # match + pointer jumping (~log2(nb/G) rounds) + tie repair, one launch
+        "k_match_coop": nb * (8 + 4 + 4 + 4) + nb * 12 * 12,
         "k_token_keys": nb * (4 + 8 + EV_BATCH_BYTES + 8 + 4),
         "k_runfix": nb * 8,
         "k_double": n * (4 + 4),

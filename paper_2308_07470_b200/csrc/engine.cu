@@ -14,6 +14,7 @@
 //   K5  k_bid / k_out  per-request RunResult arrays from batch records
 // The chain (engine_core.cuh) is the only sequential part; everything else is
 // a bandwidth-bound pass over the request stream.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -964,73 +965,89 @@ __global__ void k_token_keys(const uint32_t* __restrict__ bvals, int64_t nt,
   tvals[i] = (uint32_t)(i - sbase[s]);
 }
 
-// K3f: batch of shard-rank r pops token rank r: initial (0, r) for r < G,
-// else the (r-G)-th finish token; ptr = creator rank (or r itself if initial)
-__global__ void k_match(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bvals,
-                        int64_t nt, const EvBatch* __restrict__ evb,
-                        const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
-                        const uint64_t* __restrict__ tkeys,
-                        const uint32_t* __restrict__ tvals, int32_t* __restrict__ ptr,
-                        uint32_t* __restrict__ fail, int tb) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nt) return;
-  const int s = (int)(bkeys[i] >> tb);
-  const int64_t r = i - sbase[s];
-  const int32_t G = shards[s].G;
-  if (r < G) {
-    ptr[i] = -(int32_t)r - 1;  // terminal: gid r
-    return;
-  }
-  const int64_t ti = sbase[s] + (r - G);
-  const int64_t c = tvals[ti];
-  // >= 0: "same gid as the batch at absolute index sbase + c"; a token
-  // created at or after its consumer would loop (validated in emit)
-  ptr[i] = c < r ? (int32_t)(sbase[s] + c) : -1;
-}
 
-// Equal-finish tokens pop in gid order (scheduler.py:338: min (free_at,
-// gid)).  Re-sort each tie group by the gids just resolved; a token's gid
-// only depends on strictly earlier tokens, so iterating match -> jump ->
-// tiefix reaches the fixed point the sequential index produces.
-__global__ void k_tiefix(const uint64_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
-                         int64_t nt, const int64_t* __restrict__ sbase,
-                         const int32_t* __restrict__ gid, int32_t* __restrict__ changed, int tb) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nt) return;
-  if (i > 0 && tkeys[i - 1] == tkeys[i]) return;
-  if (i + 1 >= nt || tkeys[i + 1] != tkeys[i]) return;
-  const int64_t base = sbase[tkeys[i] >> tb];
-  int64_t e = i + 1;
-  while (e < nt && tkeys[e] == tkeys[i]) e++;
-  bool moved = false;
-  for (int64_t a = i + 1; a < e; a++) {
-    const uint32_t v = tvals[a];
-    const int32_t gv = -gid[base + v] - 1;
-    int64_t b = a;
-    while (b > i && -gid[base + tvals[b - 1]] - 1 > gv) {
-      tvals[b] = tvals[b - 1];
-      b--;
-      moved = true;
+
+
+
+// The whole matching phase in one cooperative launch: match (batch r pops
+// token r) -> pointer jumping to convergence -> re-sort equal-finish token
+// groups by the resolved gid, repeated until no group moves.  Grid-wide
+// syncs replace the host round trips; convergence flags alternate by parity
+// so a flag is reset one phase before it is written.
+__global__ void __launch_bounds__(256)
+k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bvals,
+             int64_t nt, const int64_t* __restrict__ sbase,
+             const Shard* __restrict__ shards, const uint64_t* __restrict__ tkeys,
+             uint32_t* __restrict__ tvals, int32_t* __restrict__ ptrA,
+             int32_t* __restrict__ ptrB, int32_t* __restrict__ flags, int tb) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid0 == 0) flags[0] = flags[1] = flags[2] = flags[3] = 0;
+  grid.sync();
+  for (int it = 0; it < 16; it++) {
+    for (int64_t i = tid0; i < nt; i += stride) {  // match
+      const int s = (int)(bkeys[i] >> tb);
+      const int64_t r = i - sbase[s];
+      const int32_t G = shards[s].G;
+      if (r < G) {
+        ptrA[i] = -(int32_t)r - 1;
+      } else {
+        const int64_t c = tvals[sbase[s] + (r - G)];
+        ptrA[i] = c < r ? (int32_t)(sbase[s] + c) : -1;
+      }
     }
-    tvals[b] = v;
+    grid.sync();
+    int32_t* pin = ptrA;
+    int32_t* pout = ptrB;
+    for (int round = 0; round < 64; round++) {  // pointer jumping
+      if (tid0 == 0) flags[(round + 1) & 1] = 0;
+      bool open = false;
+      for (int64_t i = tid0; i < nt; i += stride) {
+        const int32_t v = pin[i];
+        const int32_t w = v < 0 ? v : pin[v];
+        pout[i] = w;
+        open |= w >= 0;
+      }
+      if (open) flags[round & 1] = 1;
+      grid.sync();
+      const bool more = flags[round & 1] != 0;
+      int32_t* t = pin;
+      pin = pout;
+      pout = t;
+      if (!more) break;
+      grid.sync();  // everyone read the flag before it is reset again
+    }
+    if (pin != ptrA) {
+      for (int64_t i = tid0; i < nt; i += stride) ptrA[i] = pin[i];
+      grid.sync();
+    }
+    if (tid0 == 0) flags[2 + ((it + 1) & 1)] = 0;
+    bool moved = false;
+    for (int64_t i = tid0; i < nt; i += stride) {  // equal-finish groups by gid
+      if (i > 0 && tkeys[i - 1] == tkeys[i]) continue;
+      if (i + 1 >= nt || tkeys[i + 1] != tkeys[i]) continue;
+      const int64_t base = sbase[tkeys[i] >> tb];
+      int64_t e = i + 1;
+      while (e < nt && tkeys[e] == tkeys[i]) e++;
+      for (int64_t a = i + 1; a < e; a++) {
+        const uint32_t v = tvals[a];
+        const int32_t gv = -ptrA[base + v] - 1;
+        int64_t b = a;
+        while (b > i && -ptrA[base + tvals[b - 1]] - 1 > gv) {
+          tvals[b] = tvals[b - 1];
+          b--;
+          moved = true;
+        }
+        tvals[b] = v;
+      }
+    }
+    if (moved) flags[2 + (it & 1)] = 1;
+    grid.sync();
+    if (flags[2 + (it & 1)] == 0) break;
+    grid.sync();
   }
-  if (moved) *changed = 1;
-}
-
-// pointer jumping over absolute indices: ptr >= 0 follows the creator,
-// ptr < 0 is resolved (gid = -ptr - 1)
-__global__ void k_jump(const int32_t* __restrict__ pin, int32_t* __restrict__ pout,
-                       int64_t nt, int32_t* __restrict__ changed) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nt) return;
-  const int32_t v = pin[i];
-  if (v < 0) {
-    pout[i] = v;
-    return;
-  }
-  const int32_t w = pin[v];
-  pout[i] = w;
-  if (w >= 0) *changed = 1;
 }
 
 // K3g: token ties must pop in gid order; emit the BatchRec of every batch
@@ -1418,38 +1435,22 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   pc.mark("token_keys");
       radix(ctx->d_tkA, ctx->d_tvA, ctx->d_tkB, ctx->d_tvB);
   pc.mark("sort_tokens");
-      for (int it = 0; it < 16; it++) {
-        KL(k_match, nblk(nt, 256), 256, 0, st>>>(
-            ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_shards, ctx->d_tkA,
-            ctx->d_tvA, ctx->d_ptrA, ctx->d_fail, tick_bits));
-        // chains are the per-GPU batch sequences: ~nt/G long.  Run enough
-        // rounds for that before the first convergence check.
-        int warm = 0;
-        for (int64_t len = nt / std::max(1, ctx->G / P) + 1; len > 1; len = (len + 1) / 2) warm++;
-        warm = (warm + 1) & ~1;
-        for (int round = 0; round < 64; round += 2) {
-          if (round + 2 <= warm) {
-            KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt, ctx->d_changed));
-            KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt, ctx->d_changed));
-            continue;
-          }
-          CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
-          KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrA, ctx->d_ptrB, nt, ctx->d_changed));
-          KL(k_jump, nblk(nt, 256), 256, 0, st>>>(ctx->d_ptrB, ctx->d_ptrA, nt, ctx->d_changed));
-          int32_t changed = 0;
-          CK(cudaMemcpyAsync(&changed, ctx->d_changed, sizeof changed,
-                             cudaMemcpyDeviceToHost, st));
-          CK(cudaStreamSynchronize(st));
-          if (!changed) break;
-        }
-        CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t), st));
-        KL(k_tiefix, nblk(nt, 256), 256, 0, st>>>(ctx->d_tkA, ctx->d_tvA, nt,
-                                                            ctx->d_sbase, ctx->d_ptrA,
-                                                            ctx->d_changed, tick_bits));
-        int32_t moved = 0;
-        CK(cudaMemcpyAsync(&moved, ctx->d_changed, sizeof moved, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        if (!moved) break;
+      {
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_match_coop, 256, 0);
+        int nsm = 0;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+        const int64_t want = (nt + 255) / 256;
+        dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * nsm)));
+        int64_t a_nt = nt;
+        int a_tb = tick_bits;
+        void* args[] = {&ctx->d_bkA, &ctx->d_bvA, &a_nt, &ctx->d_sbase, &ctx->d_shards,
+                        &ctx->d_tkA, &ctx->d_tvA, &ctx->d_ptrA, &ctx->d_ptrB,
+                        &ctx->d_changed, &a_tb};
+        kt.begin("k_match_coop");
+        ++launches;
+        CK(cudaLaunchCooperativeKernel((void*)k_match_coop, grid, dim3(256), args, 0, st));
+        kt.end();
       }
   pc.mark("match_loop");
       int64_t* d_rb = ctx->d_meta + 2 * (P + 1);
@@ -1767,7 +1768,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_sbase, P + 1);
   ALLOC(ctx->d_fail, P);
   ALLOC(ctx->d_skip, P);
-  ALLOC(ctx->d_changed, 1);
+  ALLOC(ctx->d_changed, 4);
   ALLOC(ctx->d_special, M);
   ALLOC(ctx->d_slo_model, M);
   ALLOC(ctx->d_meta, 3 * (P + 1));
