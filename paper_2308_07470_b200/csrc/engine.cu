@@ -36,8 +36,8 @@ using namespace sym;
 
 namespace {
 
-constexpr int kChunkR = 1024;     // keys per warp in the radix passes
-constexpr int kChunkI = 1024;     // stream elements per warp in the ingest
+constexpr int kChunkR = 256;      // keys per warp in the radix passes
+constexpr int kChunkI = 512;      // stream elements per warp in the ingest
 constexpr int kFreshMaxSteps = 1 << 16;
 constexpr int kVersion = 1;
 
@@ -269,7 +269,7 @@ __global__ void k_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t M,
 // running per-bin offsets (stream order within a bin is preserved), the
 // chunk is first staged in shared memory in bin order, then written out so
 // consecutive lanes write consecutive positions of a bin run (coalesced).
-constexpr int kScatterWarps = 2;
+constexpr int kScatterWarps = 4;
 
 __host__ __device__ inline size_t scatter_smem_per_warp(int B) {
   const size_t bytes = sizeof(int32_t) * 3 * (size_t)B +
