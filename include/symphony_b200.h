@@ -72,6 +72,16 @@ typedef struct {
   int32_t device;             /* CUDA device ordinal */
   const int32_t *shard_of_model; /* [n_models], NULL = all in shard 0 */
   const int32_t *gpus_per_shard; /* [n_shards], NULL = n_gpus in shard 0 */
+  /* Jittered network (network.py:69-77, scheduler.py:197-200): per dispatch,
+   * ctrl() + data() * b where a histogram delay is one numpy
+   * Generator(Philox(net_key)).choice(vals, p) draw (vals[searchsorted(cdf,
+   * u, 'right')]) and n == 0 means the constant (no draw).  Both n == 0:
+   * jitterless.  Every sub-cluster starts its own stream (one Engine each). */
+  int32_t net_ctrl_n, net_data_n;
+  const int64_t *net_ctrl_vals, *net_data_vals;
+  const double *net_ctrl_cdf, *net_data_cdf;
+  int64_t net_ctrl_const, net_data_const;
+  uint64_t net_key[2];
 } sym_config;
 
 /* Batch record = one ExecutionOrder (scheduler.py:123-135) / one gpu_logs

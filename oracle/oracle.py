@@ -36,6 +36,11 @@ class _Config(C.Structure):
         ("_pad", C.c_int32), ("d_ctrl_ns", C.c_int64), ("d_data_ns", C.c_int64),
         ("lat_ns", _i64p), ("lat_stride", C.c_int32), ("_pad2", C.c_int32),
         ("max_batch", _i32p), ("slo_ns", _i64p), ("timeout_ns", _i64p),
+        ("net_ctrl_n", C.c_int32), ("net_data_n", C.c_int32),
+        ("net_ctrl_vals", _i64p), ("net_data_vals", _i64p),
+        ("net_ctrl_cdf", C.POINTER(C.c_double)), ("net_data_cdf", C.POINTER(C.c_double)),
+        ("net_ctrl_const", C.c_int64), ("net_data_const", C.c_int64),
+        ("net_key", C.c_uint64 * 2),
     ]
 
 
@@ -96,7 +101,7 @@ def _arr(p, n, dtype):
 
 def run(lat_ns, max_batch, slo_ns, timeout_ns, n_gpus, arr_ticks, arr_midx,
         kind="deferred", gather="prefix", target_batch=0, d_ctrl_ns=0,
-        d_data_ns=0, record_trace=False, check_invariants=False) -> dict:
+        d_data_ns=0, record_trace=False, check_invariants=False, net=None) -> dict:
     """Run the restated reference loop on one engine (one sub-cluster).
 
     lat_ns: int64 [M, stride] with lat_ns[m, b-1] = l_m(b).
@@ -117,6 +122,20 @@ def run(lat_ns, max_batch, slo_ns, timeout_ns, n_gpus, arr_ticks, arr_midx,
                   lat.ctypes.data_as(_i64p), lat.shape[1], 0,
                   mb.ctypes.data_as(_i32p), slo.ctypes.data_as(_i64p),
                   tmo.ctypes.data_as(_i64p))
+    keep = []
+    if net is not None:  # JitterTables (paper_2308_07470_b200.network)
+        cv = np.ascontiguousarray(net.ctrl_vals, np.int64)
+        cc = np.ascontiguousarray(net.ctrl_cdf, np.float64)
+        dv = np.ascontiguousarray(net.data_vals, np.int64)
+        dc = np.ascontiguousarray(net.data_cdf, np.float64)
+        keep += [cv, cc, dv, dc]
+        cfg.net_ctrl_n, cfg.net_data_n = len(cv), len(dv)
+        cfg.net_ctrl_vals = cv.ctypes.data_as(_i64p)
+        cfg.net_data_vals = dv.ctypes.data_as(_i64p)
+        cfg.net_ctrl_cdf = cc.ctypes.data_as(C.POINTER(C.c_double))
+        cfg.net_data_cdf = dc.ctypes.data_as(C.POINTER(C.c_double))
+        cfg.net_ctrl_const, cfg.net_data_const = int(net.ctrl_const), int(net.data_const)
+        cfg.net_key[0], cfg.net_key[1] = int(net.key[0]), int(net.key[1])
     outs = {k: np.empty(n, np.int64) for k in
             ("dispatch", "start", "finish", "batch", "outcome")}
     res = _Result()

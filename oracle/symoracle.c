@@ -42,6 +42,66 @@ enum { DROP_DEADLINE = 0, DROP_POLICY = 1 };                /* scheduler.py:46-4
 
 static inline int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
+/* ------------------------------------------ numpy Philox4x64-10 stream -- */
+/* numpy.random.Philox with an explicit key: counter starts at 0 and is
+ * incremented before each block of 4 words; random() is (u64 >> 11) * 2^-53
+ * and choice(vals, p) is vals[searchsorted(cumsum(p)/sum, u, 'right')]
+ * (numpy _generator.pyx choice / philox.h; verified against numpy by
+ * tests/test_oracle_golden.py::test_philox_stream_matches_numpy). */
+
+typedef struct {
+  uint64_t key[2];
+  uint64_t ctr;
+  uint64_t buf[4];
+  int pos;
+} philox_t;
+
+static void philox_block(uint64_t ctr, const uint64_t key[2], uint64_t out[4]) {
+  uint64_t c0 = ctr, c1 = 0, c2 = 0, c3 = 0, k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; r++) {
+    if (r) {
+      k0 += UINT64_C(0x9E3779B97F4A7C15);
+      k1 += UINT64_C(0xBB67AE8584CAA73B);
+    }
+    __uint128_t p0 = (__uint128_t)UINT64_C(0xD2E7470EE14C6C93) * c0;
+    __uint128_t p1 = (__uint128_t)UINT64_C(0xCA5A826395121157) * c2;
+    uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0;
+    uint64_t hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+    uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+static double philox_random(philox_t *g) {
+  if (g->pos >= 4) {
+    g->ctr += 1;
+    philox_block(g->ctr, g->key, g->buf);
+    g->pos = 0;
+  }
+  return (double)(g->buf[g->pos++] >> 11) * (1.0 / 9007199254740992.0);
+}
+
+static int64_t choice_draw(philox_t *g, int32_t n, const int64_t *vals,
+                           const double *cdf) {
+  double u = philox_random(g);
+  int32_t lo = 0, hi = n; /* number of cdf entries <= u */
+  while (lo < hi) {
+    int32_t mid = (lo + hi) / 2;
+    if (cdf[mid] <= u)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return vals[lo < n ? lo : n - 1];
+}
+
 /* ------------------------------------------------------ event heap (L3) */
 
 typedef struct {
@@ -226,6 +286,8 @@ typedef struct {
   int64_t *ord_mem_off, *ord_mem; /* member rids per order */
   int64_t tr_cap, tr_rid_cap;
   int err;
+  int jitter;
+  philox_t net;
 } sim_t;
 
 /* ------------------------------------------------- host callbacks ------ */
@@ -657,6 +719,17 @@ static int model_granted_gpu(sim_t *s, int32_t mid, int32_t gid,
   p->qh += b;
   int64_t start = p->c_exec;
   int64_t lat_b = p->lat[b - 1];
+  if (s->jitter) { /* sample_dispatch_delay: ctrl() + data() * b */
+    const symo_config *c = s->cfg;
+    int64_t dctrl = c->net_ctrl_n ? choice_draw(&s->net, c->net_ctrl_n, c->net_ctrl_vals,
+                                                c->net_ctrl_cdf)
+                                  : c->net_ctrl_const;
+    int64_t ddata = c->net_data_n ? choice_draw(&s->net, c->net_data_n, c->net_data_vals,
+                                                c->net_data_cdf)
+                                  : c->net_data_const;
+    int64_t actual = dctrl + ddata * b;
+    if (now + actual > start) start = now + actual;
+  }
   if ((rc = emit_order(s, gid, mid, b, start, start + lat_b, now, members)))
     return rc;
   int64_t believed_free = p->c_exec + lat_b;
@@ -780,6 +853,11 @@ int32_t symo_run(const symo_config *cfg, const int64_t *arr_ticks,
   out->err_index = -1;
   if (out->n != n) return SYMO_EINVAL;
   s->cfg = cfg;
+  s->jitter = cfg->net_ctrl_n > 0 || cfg->net_data_n > 0;
+  s->net.key[0] = cfg->net_key[0];
+  s->net.key[1] = cfg->net_key[1];
+  s->net.ctr = 0;
+  s->net.pos = 4;
   s->arr_ticks = arr_ticks;
   s->arr_midx = arr_midx;
   s->n = n;

@@ -43,6 +43,14 @@ typedef struct {
   const int32_t *max_batch;   /* [n_models] */
   const int64_t *slo_ns;      /* [n_models] */
   const int64_t *timeout_ns;  /* [n_models], resolved per model */
+  /* jittered network (network.py:69-77): a histogram delay is one
+   * Generator(Philox(key)).choice(vals, p) draw; n == 0 means the constant
+   * value (no draw).  Both constant => no sampling (simulator.py:116-117). */
+  int32_t net_ctrl_n, net_data_n;
+  const int64_t *net_ctrl_vals, *net_data_vals;
+  const double *net_ctrl_cdf, *net_data_cdf;
+  int64_t net_ctrl_const, net_data_const;
+  uint64_t net_key[2];
 } symo_config;
 
 typedef struct {

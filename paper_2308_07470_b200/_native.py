@@ -30,6 +30,11 @@ class SymConfig(C.Structure):
         ("lat_ns", i64p), ("max_batch", i32p), ("slo_ns", i64p), ("timeout_ns", i64p),
         ("n_shards", C.c_int32), ("device", C.c_int32),
         ("shard_of_model", i32p), ("gpus_per_shard", i32p),
+        ("net_ctrl_n", C.c_int32), ("net_data_n", C.c_int32),
+        ("net_ctrl_vals", i64p), ("net_data_vals", i64p),
+        ("net_ctrl_cdf", C.POINTER(C.c_double)), ("net_data_cdf", C.POINTER(C.c_double)),
+        ("net_ctrl_const", C.c_int64), ("net_data_const", C.c_int64),
+        ("net_key", C.c_uint64 * 2),
     ]
 
 

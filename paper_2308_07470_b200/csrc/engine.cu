@@ -60,6 +60,13 @@ struct Ctx {
   int32_t* d_shard_of_model = nullptr;
   int32_t* d_slot_base = nullptr;   // [P+1]
   int64_t* d_slo_model = nullptr;   // [M] SLO by global model id
+  // jittered network
+  bool jitter = false;
+  int32_t net_ctrl_n = 0, net_data_n = 0;
+  int64_t net_ctrl_const = 0, net_data_const = 0;
+  uint64_t net_key[2] = {0, 0};
+  int64_t* d_net_vals = nullptr;   // ctrl vals | data vals
+  double* d_net_cdf = nullptr;     // ctrl cdf | data cdf
   // chain state (independent of n)
   ModelState* d_ms = nullptr;
   int32_t *d_pq = nullptr, *d_gt = nullptr, *d_mlt = nullptr,
@@ -1132,6 +1139,94 @@ __global__ void k_window_busy(const BatchRec* __restrict__ recs,
   if (b > a) atomicAdd(&busy[gpu_base[s] + r.gpu], (unsigned long long)(b - a));
 }
 
+
+// ------------------------------------------- jittered network (K5') ------
+// numpy's Philox4x64-10 (philox.h) is counter based: word j of the engine's
+// network stream is word j % 4 of the block for counter j / 4 + 1, and
+// Generator.random() is (word >> 11) * 2^-53.  The k-th dispatch of a
+// sub-cluster draws ctrl then data (each only if it is a histogram), so its
+// delay is computable in parallel from k alone (scheduler.py:197-200).
+
+__device__ __forceinline__ uint64_t philox_word(uint64_t j, uint64_t k0, uint64_t k1) {
+  uint64_t c0 = j / 4 + 1, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    const uint64_t a = 0xD2E7470EE14C6C93ull * c0, ah = __umul64hi(0xD2E7470EE14C6C93ull, c0);
+    const uint64_t b = 0xCA5A826395121157ull * c2, bh = __umul64hi(0xCA5A826395121157ull, c2);
+    const uint64_t n0 = bh ^ c1 ^ k0, n2 = ah ^ c3 ^ k1;
+    c0 = n0;
+    c1 = b;
+    c2 = n2;
+    c3 = a;
+  }
+  const int w = (int)(j & 3);
+  return w == 0 ? c0 : w == 1 ? c1 : w == 2 ? c2 : c3;
+}
+
+__device__ __forceinline__ int64_t choice_draw(uint64_t j, uint64_t k0, uint64_t k1,
+                                               const int64_t* vals, const double* cdf,
+                                               int32_t n) {
+  const double u = (double)(philox_word(j, k0, k1) >> 11) * (1.0 / 9007199254740992.0);
+  int32_t lo = 0, hi = n;  // searchsorted(cdf, u, 'right')
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (cdf[mid] <= u) lo = mid + 1; else hi = mid;
+  }
+  return vals[lo < n ? lo : n - 1];
+}
+
+// start = max(exec_at, emitted + ctrl() + data() * b); sort key (gpu, record)
+__global__ void k_jitter_start(BatchRec* __restrict__ recs, const int64_t* __restrict__ rec_base,
+                               const int64_t* __restrict__ rec_count, int32_t P, int64_t total,
+                               const int32_t* __restrict__ gpu_base, int32_t nc, int32_t nd,
+                               const int64_t* __restrict__ vals, const double* __restrict__ cdf,
+                               int64_t cconst, int64_t dconst, uint64_t k0, uint64_t k1,
+                               uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= total) return;
+  int s = 0;
+  int64_t k = w;
+  while (s < P && k >= rec_count[s]) {
+    k -= rec_count[s];
+    s++;
+  }
+  const int64_t ri = rec_base[s] + k;
+  BatchRec& r = recs[ri];
+  const int per = (nc > 0) + (nd > 0);
+  const uint64_t j0 = (uint64_t)k * per;  // k-th dispatch of this sub-cluster
+  const int64_t dc = nc > 0 ? choice_draw(j0, k0, k1, vals, cdf, nc) : cconst;
+  const int64_t dd = nd > 0 ? choice_draw(j0 + (nc > 0), k0, k1, vals + nc, cdf + nc, nd) : dconst;
+  const int64_t actual = dc + dd * r.size;
+  const int64_t lat = r.finish - r.start;
+  if (r.emitted + actual > r.start) r.start = r.emitted + actual;
+  r.finish = r.start + lat;
+  keys[w] = ((uint64_t)(gpu_base[s] + r.gpu) << 32) | (uint64_t)ri;
+  idx[w] = (uint32_t)ri;
+}
+
+// EmulatedGpu.execute (simulator.py:54-62): per GPU, in emission order, a
+// start before the previous finish is shifted to it
+__global__ void k_serialize(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                            int64_t total, BatchRec* __restrict__ recs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  if (i > 0 && (keys[i - 1] >> 32) == (keys[i] >> 32)) return;  // not a GPU's first
+  int64_t busy = 0;
+  for (int64_t e = i; e < total && (keys[e] >> 32) == (keys[i] >> 32); e++) {
+    BatchRec& r = recs[idx[e]];
+    if (r.start < busy) {
+      const int64_t sh = busy - r.start;
+      r.start += sh;
+      r.finish += sh;
+    }
+    busy = r.finish;
+  }
+}
+
 // ------------------------------------------------------------ driver ------
 
 int ensure_capacity(Ctx* ctx, int64_t n) {
@@ -1531,6 +1626,32 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                      cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_meta + P + 1, rec_count.data(), sizeof(int64_t) * P,
                      cudaMemcpyHostToDevice, st));
+  if (ctx->jitter && total > 0) {
+    if (total > ctx->cap) {
+      ctx->err = "jitter scratch too small";
+      return SYM_EINVAL;
+    }
+    const int32_t* d_gpu_base = ctx->d_bins + B + P + 2 + M;
+    KL(k_jitter_start, nblk(total, 256), 256, 0, st>>>(
+        ctx->d_recs, d_meta, d_meta + P + 1, P, total, d_gpu_base, ctx->net_ctrl_n,
+        ctx->net_data_n, ctx->d_net_vals, ctx->d_net_cdf, ctx->net_ctrl_const,
+        ctx->net_data_const, ctx->net_key[0], ctx->net_key[1], ctx->d_tkA, ctx->d_tvA));
+    int bits = 32;
+    while ((int64_t(1) << (bits - 32)) < ctx->G) bits++;
+    const int64_t Wj = (total + kChunkR - 1) / kChunkR;
+    uint64_t* ka = ctx->d_tkA; uint64_t* kb = ctx->d_tkB;
+    uint32_t* va = ctx->d_tvA; uint32_t* vb = ctx->d_tvB;
+    for (int shift = 32; shift < bits; shift += kDigitBits) {  // records already in order
+      KL(k_rhist, nblk(Wj, kRadixWarps), 32 * kRadixWarps, 0, st>>>(ka, total, shift,
+                                                                      ctx->d_rhist, Wj));
+      flat_scan(ctx->d_rhist, Wj * kDigits);
+      KL(k_rscatter, nblk(Wj, kRadixWarps), 32 * kRadixWarps, 0, st>>>(
+          ka, va, total, shift, ctx->d_rhist, Wj, kb, vb));
+      std::swap(ka, kb);
+      std::swap(va, vb);
+    }
+    KL(k_serialize, nblk(total, 256), 256, 0, st>>>(ka, va, total, ctx->d_recs));
+  }
   const bool expand = !(flags & SYM_FLAG_NO_EXPAND) && out->req_dispatch;
   if (expand && n > 0) {
     KL(k_fill32, nblk(n, 256), 256, 0, st>>>(ctx->d_bid, n, -1));
@@ -1771,6 +1892,23 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_changed, 4);
   ALLOC(ctx->d_special, M);
   ALLOC(ctx->d_slo_model, M);
+  ctx->net_ctrl_n = cfg->net_ctrl_n > 0 ? cfg->net_ctrl_n : 0;
+  ctx->net_data_n = cfg->net_data_n > 0 ? cfg->net_data_n : 0;
+  ctx->jitter = ctx->net_ctrl_n + ctx->net_data_n > 0;
+  ctx->net_ctrl_const = cfg->net_ctrl_const;
+  ctx->net_data_const = cfg->net_data_const;
+  ctx->net_key[0] = cfg->net_key[0];
+  ctx->net_key[1] = cfg->net_key[1];
+  ALLOC(ctx->d_net_vals, ctx->net_ctrl_n + ctx->net_data_n + 1);
+  ALLOC(ctx->d_net_cdf, ctx->net_ctrl_n + ctx->net_data_n + 1);
+  if (ctx->net_ctrl_n) {
+    cudaMemcpy(ctx->d_net_vals, cfg->net_ctrl_vals, sizeof(int64_t) * ctx->net_ctrl_n, cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->d_net_cdf, cfg->net_ctrl_cdf, sizeof(double) * ctx->net_ctrl_n, cudaMemcpyHostToDevice);
+  }
+  if (ctx->net_data_n) {
+    cudaMemcpy(ctx->d_net_vals + ctx->net_ctrl_n, cfg->net_data_vals, sizeof(int64_t) * ctx->net_data_n, cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->d_net_cdf + ctx->net_ctrl_n, cfg->net_data_cdf, sizeof(double) * ctx->net_data_n, cudaMemcpyHostToDevice);
+  }
   ALLOC(ctx->d_meta, 3 * (P + 1));
 #undef ALLOC
   {  // keep pool memory mapped across synchronisations (no remap stalls)
@@ -1859,7 +1997,8 @@ void sym_destroy(void* engine) {
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
                   ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_cp_pos,
                   ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
-                  ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model};
+                  ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
+                  ctx->d_net_vals, ctx->d_net_cdf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& ev : ctx->ev)

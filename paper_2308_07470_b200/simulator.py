@@ -22,7 +22,7 @@ from types import SimpleNamespace
 import numpy as np
 
 from . import _native
-from .network import NetworkModel
+from .network import NetworkModel, jitter_tables
 from .profile import ModelSpec
 from .scheduler import PolicyConfig, ProtocolError
 from .units import s_to_ns
@@ -125,10 +125,9 @@ class Engine:
         self.models = list(models)
         self.policy = policy
         self.network = network or NetworkModel.zero()
-        if not self.network.jitterless:
-            raise NotImplementedError(
-                "jittered (histogram) network delays are not supported by the "
-                "B200 engine yet (SURVEY.md §8f row 3)")
+        # jittered delays: per-dispatch draws from the engine's numpy Philox
+        # substream, reproduced on the device (simulator.py:116-122)
+        self._jitter = jitter_tables(self.network, seed)
         self.seed = seed
         self.record_trace = record_trace
         self.check_invariants = check_invariants
@@ -175,6 +174,18 @@ class Engine:
         cfg.device = self.device
         cfg.shard_of_model = self.shard_of_model.ctypes.data_as(_native.i32p)
         cfg.gpus_per_shard = self.gpus_per_shard.ctypes.data_as(_native.i32p)
+        j = self._jitter
+        if j is not None:
+            self._jit_keep = [np.ascontiguousarray(a) for a in (j.ctrl_vals, j.ctrl_cdf,
+                                                                j.data_vals, j.data_cdf)]
+            cv, cc, dv, dc = self._jit_keep
+            cfg.net_ctrl_n, cfg.net_data_n = len(cv), len(dv)
+            cfg.net_ctrl_vals = cv.ctypes.data_as(_native.i64p)
+            cfg.net_data_vals = dv.ctypes.data_as(_native.i64p)
+            cfg.net_ctrl_cdf = cc.ctypes.data_as(C.POINTER(C.c_double))
+            cfg.net_data_cdf = dc.ctypes.data_as(C.POINTER(C.c_double))
+            cfg.net_ctrl_const, cfg.net_data_const = int(j.ctrl_const), int(j.data_const)
+            cfg.net_key[0], cfg.net_key[1] = int(j.key[0]), int(j.key[1])
         status = C.c_int32(0)
         h = lib.sym_create(C.byref(cfg), C.byref(status))
         if not h:

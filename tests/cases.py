@@ -34,6 +34,42 @@ def bundled():
                    ticks, midx, (sc.duration_s, sc.warmup_s, sc.cooldown_s))
 
 
+JITTER_NETS = {
+    "J1": {"d_ctrl": {"kind": "histogram", "values_us": [5, 30, 120, 900],
+                      "weights": [0.6, 0.3, 0.09, 0.01], "plan_percentile": 0.5},
+           "d_data": {"kind": "histogram", "values_us": [1, 3, 10], "weights": [0.8, 0.15, 0.05]}},
+    "J2": {"d_ctrl": {"kind": "histogram", "values_us": [0, 400, 1500],
+                      "weights": [0.8, 0.15, 0.05], "plan_percentile": 0.7},
+           "d_data": {"kind": "constant", "value_us": 0}},
+    "J3": {"d_ctrl": {"kind": "constant", "value_us": 30},
+           "d_data": {"kind": "histogram", "values_us": [0, 2, 50], "weights": [0.5, 0.4, 0.1],
+                      "plan_percentile": 0.6}},
+}
+JITTER_CASES = [("table2_resnet50", "J1", None), ("fig6_stagger", "J2", None),
+                ("fig4b_timeout_zoo", "J3", None), ("table2_resnet50", "J1", "eager"),
+                ("fig2_flattop", "J2", None), ("table2_inceptionresnet", "J3", "timeout")]
+
+
+def jitter():
+    """(key, models, gpus, policy, ticks, midx, (dur, warm, cool), network, seed)"""
+    import copy
+    from paper_2308_07470_b200._bundled import BUNDLED
+    from paper_2308_07470_b200.scenario import _bundled_trace_dir, scenario_from_dict
+    for name, net, kind in JITTER_CASES:
+        doc = copy.deepcopy(BUNDLED[name])
+        doc["network"] = JITTER_NETS[net]
+        if kind:
+            doc.setdefault("policy", {})["kind"] = kind
+            if kind == "timeout":
+                doc["policy"]["timeout_slo_frac"] = 0.3
+        sc = scenario_from_dict(doc, name=name, base_dir=_bundled_trace_dir())
+        ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models],
+                                        sc.duration_s, sc.seed)
+        yield (f"jitter/{name}/{net}/{kind or 'base'}", list(sc.models), sc.gpu_count,
+               sc.policy, ticks, midx, (sc.duration_s, sc.warmup_s, sc.cooldown_s),
+               sc.network, sc.seed)
+
+
 def stress(n=60):
     for seed in range(n):
         c = make_case(seed)

@@ -49,9 +49,9 @@ def policy_for(base, variant):
     return PolicyConfig(**POLICIES[variant])
 
 
-def run_case(models, gpus, policy, ticks, midx, duration_s, warm, cool):
-    eng = Engine(list(models), gpus, policy,
-                 NetworkModel.constant(policy.d_ctrl_ns, policy.d_data_ns), record_trace=True)
+def run_case(models, gpus, policy, ticks, midx, duration_s, warm, cool, network=None, seed=0):
+    network = network or NetworkModel.constant(policy.d_ctrl_ns, policy.d_data_ns)
+    eng = Engine(list(models), gpus, policy, network, seed=seed, record_trace=True)
     t0 = time.time()
     res = eng.run_stream(ticks, midx, duration_s)
     el = time.time() - t0
@@ -188,6 +188,47 @@ def autoscale_cases(out):
     print("autoscale", series, flush=True)
 
 
+JITTER_NETS = {
+    "J1": {"d_ctrl": {"kind": "histogram", "values_us": [5, 30, 120, 900],
+                      "weights": [0.6, 0.3, 0.09, 0.01], "plan_percentile": 0.5},
+           "d_data": {"kind": "histogram", "values_us": [1, 3, 10], "weights": [0.8, 0.15, 0.05]}},
+    "J2": {"d_ctrl": {"kind": "histogram", "values_us": [0, 400, 1500],
+                      "weights": [0.8, 0.15, 0.05], "plan_percentile": 0.7},
+           "d_data": {"kind": "constant", "value_us": 0}},
+    "J3": {"d_ctrl": {"kind": "constant", "value_us": 30},
+           "d_data": {"kind": "histogram", "values_us": [0, 2, 50], "weights": [0.5, 0.4, 0.1],
+                      "plan_percentile": 0.6}},
+}
+JITTER_CASES = [("table2_resnet50", "J1", None), ("fig6_stagger", "J2", None),
+                ("fig4b_timeout_zoo", "J3", None), ("table2_resnet50", "J1", "eager"),
+                ("fig2_flattop", "J2", None), ("table2_inceptionresnet", "J3", "timeout")]
+
+
+def jitter_cases(out):
+    """Jittered network (network.py:69-77): histogram delays sampled per
+    dispatch from the engine's Philox substream; LATE outcomes appear."""
+    import copy
+    import os as _os
+    from batchsym.scenario import scenario_from_dict
+    import yaml
+    root = "/root/reference/pkg/src/batchsym/scenarios"
+    for name, net, kind in JITTER_CASES:
+        doc = yaml.safe_load(open(_os.path.join(root, name + ".yaml")))
+        doc = copy.deepcopy(doc)
+        doc["network"] = JITTER_NETS[net]
+        if kind:
+            doc.setdefault("policy", {})["kind"] = kind
+            if kind == "timeout":
+                doc["policy"]["timeout_slo_frac"] = 0.3
+        sc = scenario_from_dict(doc, name=name, base_dir=root)
+        ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models],
+                                        sc.duration_s, sc.seed)
+        key = f"jitter/{name}/{net}/{kind or 'base'}"
+        out[key] = run_case(sc.models, sc.gpu_count, sc.policy, ticks, midx, sc.duration_s,
+                            sc.warmup_s, sc.cooldown_s, network=sc.network, seed=sc.seed)
+        print(key, out[key]["late"], out[key]["drops"], flush=True)
+
+
 def stress_cases(out, n_cases=60):
     sys.path.insert(0, os.path.join(REPO, "tests"))
     from stress_cases import make_case
@@ -205,6 +246,7 @@ if __name__ == "__main__":
     out = {"generator": "tests/golden/make_golden.py", "reference": "batchsym 0.1.0",
            "numpy": np.__version__}
     known_answers(out)
+    jitter_cases(out)
     autoscale_cases(out)
     bundled_cases(out)
     stress_cases(out)

@@ -149,8 +149,7 @@ def test_engine_api_validates_before_device(monkeypatch):
     with pytest.raises(ValueError):
         Engine(m, 0, PolicyConfig("deferred"))
     jitter = NetworkModel(DelayDist.histogram([0, 10], [1, 1]), DelayDist.constant(0))
-    with pytest.raises(NotImplementedError):
-        Engine(m, 1, PolicyConfig("deferred"), jitter)
+    assert Engine(m, 1, PolicyConfig("deferred"), jitter)._jitter is not None
     with pytest.raises(ValueError):
         Engine(m * 1, 2, PolicyConfig("deferred"), shards=([0], [1, 1]))
 

@@ -173,3 +173,29 @@ def test_window_counts_and_autoscale_on_device(golden):
         for k in host:
             np.testing.assert_array_equal(dev[k], host[k], err_msg=k)
     eng.close()
+
+
+JIT = list(cases.jitter())
+
+
+@pytest.mark.parametrize("use_fast", [True, False], ids=["fast", "chain"])
+@pytest.mark.parametrize("case", JIT, ids=[c[0] for c in JIT])
+def test_engine_jitter_parity(case, use_fast, golden):
+    """Jittered network on the device: per-dispatch Philox draws and the
+    per-GPU serialisation reproduce the reference (starts, finishes, LATE
+    outcomes, gpu_logs, trace) exactly."""
+    from paper_2308_07470_b200.network import jitter_tables
+    key, models, gpus, policy, ticks, midx, (dur, warm, cool), net, seed = case
+    eng = _engine(models, gpus, policy, network=net, seed=seed, use_fast=use_fast,
+                  record_trace=not use_fast)
+    res = eng.run_stream(ticks, midx, dur)
+    g = golden[key]
+    check_against_golden(g, res.req_dispatch, res.req_start, res.req_finish, res.req_batch,
+                         res.req_outcome, res.gpu_logs, _counters(eng, res),
+                         trace=None if use_fast else res.trace)
+    o = oracle.run(arr_ticks=ticks, arr_midx=midx, net=jitter_tables(net, seed),
+                   **oracle_args(models, gpus, policy))
+    for k in ("req_dispatch", "req_start", "req_finish", "req_batch", "req_outcome"):
+        np.testing.assert_array_equal(getattr(res, k), o[k], err_msg=k)
+    check_stats(res, g, dur, warm, cool)
+    eng.close()
