@@ -286,7 +286,9 @@ class Engine:
             req_arrival=ticks.copy(), req_deadline=ticks + self._slo[midx64],
             req_dispatch=disp, req_start=start, req_finish=fin, req_batch=bsz,
             req_outcome=outc, gpu_logs=_GpuLogs(batches, self.gpu_count),
-            drops=int(res.drops), completions=int(np.count_nonzero(outc == OUTCOME_COMPLETED)),
+            # n_completed counts every completion event, LATE ones included
+            # (simulator.py:251-252)
+            drops=int(res.drops), completions=int(np.count_nonzero(outc != OUTCOME_DROPPED)),
             late=int(np.count_nonzero(outc == OUTCOME_LATE)), batches=batches)
         if self.record_trace:
             result.trace = self._build_trace(ticks, midx64, batches, drop_t, drop_ks, drop_ka)
