@@ -277,8 +277,8 @@ def run_b200(args, rank, world, local_rank):
         res = eng.run_stream(pin_t, pin_m, args.duration)
         e2e_s.append(time.perf_counter() - t0)
     e2e_time = sum(e2e_s) / len(e2e_s)
-    h2d = n * (8 + 4)
-    d2h = n * 5 * 8 + len(res.batches) * BATCH_REC_BYTES
+    h2d = n * (8 + 8)                      # ticks + int64 model ids
+    d2h = n * 8 * 8 + len(res.batches) * BATCH_REC_BYTES  # 8 RunResult arrays + records
 
     # parity spot check of the timed outputs against the API result
     for k, ref in (("batch", res.req_batch), ("outcome", res.req_outcome)):

@@ -45,7 +45,8 @@ enum {
   SYM_FLAG_NO_FRESH = 2u,   /* disable the parallel fresh-start pre-scan */
   SYM_FLAG_NO_EXPAND = 4u,  /* leave per-request arrays untouched (bench) */
   SYM_FLAG_NO_FAST = 8u,    /* always run the sequential live-event chain */
-  SYM_FLAG_KERNEL_TIMES = 16u /* CUDA-event time every kernel (profiling) */
+  SYM_FLAG_KERNEL_TIMES = 16u, /* CUDA-event time every kernel (profiling) */
+  SYM_FLAG_MODEL_I64 = 32u    /* arr_model holds int64 ids (numpy default) */
 };
 
 /* Engine configuration.  Models are numbered 0..n_models-1 in the order of
@@ -102,6 +103,9 @@ typedef struct {
    * (= rid - 1 for a single shard); RunResult fields simulator.py:74-78.
    * May be NULL with SYM_FLAG_NO_EXPAND. */
   int64_t *req_dispatch, *req_start, *req_finish, *req_batch, *req_outcome;
+  /* optional (may be NULL): arrival, deadline = arrival + SLO, model id as
+   * int64 -- the remaining RunResult arrays (simulator.py:71-73) */
+  int64_t *req_arrival, *req_deadline, *req_model;
   /* Trace support (SYM_FLAG_TRACE): per request, tick and processing
    * position of its drop, -1 if not dropped. */
   int64_t *drop_t, *drop_key_sub;
@@ -128,10 +132,12 @@ void *sym_create(const sym_config *cfg, int32_t *status);
 void sym_destroy(void *engine);
 
 /* Host buffers in, host buffers out (end-to-end API: the H2D and D2H copies
- * are part of the call).  arr_ticks must be non-decreasing
- * (generate_arrivals / load_replay_trace guarantee it). */
+ * are part of the call).  arr_model is int32, or int64 with
+ * SYM_FLAG_MODEL_I64.  arr_ticks must be non-decreasing (generate_arrivals /
+ * load_replay_trace guarantee it); a violation returns SYM_EINVAL with
+ * err_index set. */
 int32_t sym_run(void *engine, const int64_t *arr_ticks,
-                const int32_t *arr_model, int64_t n, uint32_t flags,
+                const void *arr_model, int64_t n, uint32_t flags,
                 sym_result *out);
 
 /* Same, but every pointer in the call (arrivals, per-request outputs,
@@ -139,8 +145,12 @@ int32_t sym_run(void *engine, const int64_t *arr_ticks,
  * nothing crosses PCIe except the counters.  Used with inputs already
  * resident in HBM. */
 int32_t sym_run_device(void *engine, const int64_t *d_arr_ticks,
-                       const int32_t *d_arr_model, int64_t n, uint32_t flags,
+                       const void *d_arr_model, int64_t n, uint32_t flags,
                        sym_result *out);
+
+/* Copy the last run's batch records (emission order per GPU) to a host
+ * buffer of capacity cap; returns the count (or -status on failure). */
+int64_t sym_last_batches(void *engine, sym_batch *host, int64_t cap);
 
 /* Integer reductions of a finished run for compute_stats
  * (metrics.py:71-132): per model counts of completed/late/dropped among

@@ -9,12 +9,15 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import numpy as np
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libsymphony_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 
 SYM_OK, SYM_EPROTO, SYM_EINVAL, SYM_EINVARIANT, SYM_ECUDA, SYM_ENOMEM = range(6)
 FLAG_TRACE, FLAG_NO_FRESH, FLAG_NO_EXPAND, FLAG_NO_FAST, FLAG_KERNEL_TIMES = 1, 2, 4, 8, 16
+FLAG_MODEL_I64 = 32
 KIND = {"deferred": 0, "eager": 1, "timeout": 2}
 GATHER = {"prefix": 0, "drop_head": 1}
 
@@ -58,6 +61,7 @@ class SymResult(C.Structure):
         ("n", C.c_int64),
         ("req_dispatch", i64p), ("req_start", i64p), ("req_finish", i64p),
         ("req_batch", i64p), ("req_outcome", i64p),
+        ("req_arrival", i64p), ("req_deadline", i64p), ("req_model", i64p),
         ("drop_t", i64p), ("drop_key_sub", i64p), ("drop_key_a", i32p),
         ("batches", C.c_void_p), ("batch_cap", C.c_int64), ("n_batches", C.c_int64),
         ("drops", C.c_int64), ("completions", C.c_int64), ("late", C.c_int64),
@@ -74,7 +78,8 @@ class SymResult(C.Structure):
 
 
 EXPORTS = ("sym_create", "sym_destroy", "sym_run", "sym_run_device",
-           "sym_window_counts", "sym_last_error", "sym_version", "sym_kernel_times")
+           "sym_window_counts", "sym_last_error", "sym_version", "sym_kernel_times",
+           "sym_last_batches")
 
 _lib = None
 
@@ -106,7 +111,22 @@ def load(path: str | None = None):
     lib.sym_last_error.argtypes = [C.c_void_p]
     lib.sym_last_error.restype = C.c_char_p
     lib.sym_version.restype = C.c_int32
+    lib.sym_last_batches.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    lib.sym_last_batches.restype = C.c_int64
     lib.sym_kernel_times.argtypes = [C.c_void_p, C.c_int32]
     lib.sym_kernel_times.restype = C.c_char_p
     _lib = lib
     return lib
+
+
+def pinned_empty(n: int, dtype=np.int64):
+    """A host array in page-locked memory from torch's caching host allocator
+    (recycled across calls once the array is freed), so device->host copies
+    run at full PCIe speed; plain numpy memory if torch is unavailable."""
+    dtype = np.dtype(dtype)
+    try:
+        import torch
+        t = torch.empty(max(int(n), 1) * dtype.itemsize, dtype=torch.uint8, pin_memory=True)
+        return t.numpy().view(dtype)[:n]
+    except Exception:  # noqa: BLE001 -- no torch / no driver: pageable memory
+        return np.empty(n, dtype)

@@ -139,7 +139,8 @@ int grow(Ctx* ctx, T*& p, int64_t count) {
 
 // --------------------------------------------------------------- K1 -------
 
-__global__ void k_hist(const int32_t* __restrict__ model, int64_t n,
+__global__ void k_hist(const int32_t* __restrict__ model, const int64_t* __restrict__ ticks,
+                       int64_t n,
                        const int32_t* __restrict__ slot_of_model,
                        const int32_t* __restrict__ shard_of_model, int32_t M,
                        int32_t P, int32_t* __restrict__ hist, int64_t W,
@@ -154,6 +155,8 @@ __global__ void k_hist(const int32_t* __restrict__ model, int64_t n,
   if (w < W) {
     const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
     for (int64_t i = lo + lane; i < hi; i += 32) {
+      if (i > 0 && ticks[i] < ticks[i - 1])  // arrivals must be time-ordered
+        atomicMin(err + 1, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
       const int32_t m = model[i];
       if (m < 0 || m >= M) {
         atomicMin(err, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
@@ -551,6 +554,13 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
 
 // --------------------------------------------------------------- K5 -------
 
+__global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t v = in[i];
+  out[i] = (v < 0 || v > INT32_MAX) ? -1 : (int32_t)v;  // out of range -> EPROTO
+}
+
 __global__ void k_fill32(int32_t* p, int64_t n, int32_t v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -582,9 +592,16 @@ __global__ void k_out(int64_t n, const int32_t* __restrict__ inv,
                       const int64_t* __restrict__ slo_by_model,
                       int64_t* __restrict__ disp, int64_t* __restrict__ start,
                       int64_t* __restrict__ fin, int64_t* __restrict__ bat,
-                      int64_t* __restrict__ outc) {
+                      int64_t* __restrict__ outc, int64_t* __restrict__ o_arr,
+                      int64_t* __restrict__ o_dl, int64_t* __restrict__ o_model) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int64_t tick = ticks[i];
+  const int32_t mi = model[i];
+  const int64_t dl = tick + slo_by_model[mi];
+  if (o_arr) o_arr[i] = tick;
+  if (o_dl) o_dl[i] = dl;
+  if (o_model) o_model[i] = mi;
   const int32_t r = bid[inv[i]];
   if (r < 0) {
     disp[i] = -1;
@@ -599,7 +616,7 @@ __global__ void k_out(int64_t n, const int32_t* __restrict__ inv,
   start[i] = b.start;
   fin[i] = b.finish;
   bat[i] = b.size;
-  outc[i] = b.finish <= ticks[i] + slo_by_model[model[i]] ? 0 : 1;
+  outc[i] = b.finish <= dl ? 0 : 1;
 }
 
 __global__ void k_drop_out(int64_t n, const int32_t* __restrict__ s_i,
@@ -1373,21 +1390,21 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const int64_t W = (n + kChunkI - 1) / kChunkI;
   CK(cudaEventRecord(ctx->ev[0], st));
   // ---- K1 ingest
-  int32_t big = INT32_MAX;
-  CK(cudaMemcpyAsync(ctx->d_err, &big, sizeof big, cudaMemcpyHostToDevice, st));
+  const int32_t big[2] = {INT32_MAX, INT32_MAX};
+  CK(cudaMemcpyAsync(ctx->d_err, big, sizeof big, cudaMemcpyHostToDevice, st));
   const int wpb = 4;
   const size_t smem = sizeof(int32_t) * (size_t)B * wpb;
   if (W > 0) {
     KL(k_hist, nblk(W, wpb), 32 * wpb, smem, st>>>(
-        d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
+        d_model, d_ticks, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_err));
     flat_scan(ctx->d_hist, W * B);
   }
   KL(k_binoff, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, M, P, n, ctx->d_mp,
                                            ctx->d_bins + B + 1));
-  int32_t herr = INT32_MAX;
+  int32_t herr2[2] = {INT32_MAX, INT32_MAX};
   int64_t last_tick = 0;
-  CK(cudaMemcpyAsync(&herr, ctx->d_err, sizeof herr, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(herr2, ctx->d_err, sizeof herr2, cudaMemcpyDeviceToHost, st));
   if (n > 0)
     CK(cudaMemcpyAsync(&last_tick, d_ticks + (n - 1), sizeof last_tick,
                        cudaMemcpyDeviceToHost, st));
@@ -1400,10 +1417,16 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                            2 * (uint64_t)ctx->max_slo + (uint64_t)ctx->max_lat + 1;
     while (tick_bits < 62 && (uint64_t(1) << tick_bits) <= bound) tick_bits++;
   }
+  const int32_t herr = herr2[0];
   if (herr != INT32_MAX) {
     out->err_index = herr;
     ctx->err = "request for unknown model";
     return SYM_EPROTO;
+  }
+  if (herr2[1] != INT32_MAX) {
+    out->err_index = herr2[1];
+    ctx->err = "arrival ticks must be non-decreasing";
+    return SYM_EINVAL;
   }
   if (W > 0)
     KL(k_scatter, nblk(W, kScatterWarps), 32 * kScatterWarps,
@@ -1661,7 +1684,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_out, nblk(n, 256), 256, 0, st>>>(n, ctx->d_inv, ctx->d_bid, ctx->d_recs, d_ticks,
                                           d_model, ctx->d_slo_model, out->req_dispatch,
                                           out->req_start, out->req_finish, out->req_batch,
-                                          out->req_outcome));
+                                          out->req_outcome, out->req_arrival, out->req_deadline,
+                                          out->req_model));
   }
   if (trace && out->drop_t && n > 0)
     KL(k_drop_out, nblk(n, 256), 256, 0, st>>>(
@@ -1882,7 +1906,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_shards, P);
   // bins: [B+1] totals, then shard_off [P+1], model_of_slot [M], gpu_base [P+1]
   ALLOC(ctx->d_bins, (M + P + 1) + (P + 1) + M + (P + 1));
-  ALLOC(ctx->d_err, 1);
+  ALLOC(ctx->d_err, 2);
   ALLOC(ctx->d_nb, M);
   ALLOC(ctx->d_bbase, M);
   ALLOC(ctx->d_mdrops, M);
@@ -2008,17 +2032,26 @@ void sym_destroy(void* engine) {
 }
 
 int32_t sym_run_device(void* engine, const int64_t* d_arr_ticks,
-                       const int32_t* d_arr_model, int64_t n, uint32_t flags,
+                       const void* d_arr_model, int64_t n, uint32_t flags,
                        sym_result* out) {
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return SYM_ECUDA;
   out->n = n;
   out->err_index = -1;
-  return run_device(ctx, d_arr_ticks, d_arr_model, n, flags, out, true);
+  const int32_t* model = static_cast<const int32_t*>(d_arr_model);
+  if (flags & SYM_FLAG_MODEL_I64) {
+    int rc;
+    if ((rc = ensure_capacity(ctx, n))) return rc;
+    if (n > 0)
+      k_narrow<<<nblk(n, 256), 256, 0, ctx->stream>>>(static_cast<const int64_t*>(d_arr_model),
+                                                        n, ctx->d_model);
+    model = ctx->d_model;
+  }
+  return run_device(ctx, d_arr_ticks, model, n, flags, out, true);
 }
 
-int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model,
+int32_t sym_run(void* engine, const int64_t* arr_ticks, const void* arr_model,
                 int64_t n, uint32_t flags, sym_result* out) {
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
@@ -2029,15 +2062,21 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model
   if (n > 0) {
     CK(cudaMemcpyAsync(ctx->d_ticks, arr_ticks, sizeof(int64_t) * n,
                        cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ctx->d_model, arr_model, sizeof(int32_t) * n,
-                       cudaMemcpyHostToDevice, st));
+    if (flags & SYM_FLAG_MODEL_I64) {  // widen on the device, not the host
+      CK(cudaMemcpyAsync(ctx->d_s_tick, arr_model, sizeof(int64_t) * n,
+                         cudaMemcpyHostToDevice, st));  // s_tick is free until ingest
+      k_narrow<<<nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, n, ctx->d_model);
+    } else {
+      CK(cudaMemcpyAsync(ctx->d_model, arr_model, sizeof(int32_t) * n,
+                         cudaMemcpyHostToDevice, st));
+    }
   }
   // device-side output staging (persistent, grown on demand)
   sym_result dev = *out;
   const bool want_req = out->req_dispatch && !(flags & SYM_FLAG_NO_EXPAND);
   const bool want_drop = (flags & SYM_FLAG_TRACE) && out->drop_t;
   if (n + 1 > ctx->stage_cap) {
-    if ((rc = grow(ctx, ctx->d_req, 5 * (n + 1))) || (rc = grow(ctx, ctx->d_drop, 2 * (n + 1))) ||
+    if ((rc = grow(ctx, ctx->d_req, 8 * (n + 1))) || (rc = grow(ctx, ctx->d_drop, 2 * (n + 1))) ||
         (rc = grow(ctx, ctx->d_dka, n + 1)))
       return rc;
     ctx->stage_cap = n + 1;
@@ -2056,6 +2095,9 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model
   dev.req_finish = want_req ? d_req + 2 * sc : nullptr;
   dev.req_batch = want_req ? d_req + 3 * sc : nullptr;
   dev.req_outcome = want_req ? d_req + 4 * sc : nullptr;
+  dev.req_arrival = want_req && out->req_arrival ? d_req + 5 * sc : nullptr;
+  dev.req_deadline = want_req && out->req_deadline ? d_req + 6 * sc : nullptr;
+  dev.req_model = want_req && out->req_model ? d_req + 7 * sc : nullptr;
   dev.drop_t = want_drop ? d_drop : nullptr;
   dev.drop_key_sub = want_drop ? d_drop + sc : nullptr;
   dev.drop_key_a = want_drop ? d_dka : nullptr;
@@ -2065,11 +2107,13 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model
   rc = run_device(ctx, ctx->d_ticks, ctx->d_model, n, flags, &dev, true);
   if (rc == SYM_OK) {
     if (want_req && n > 0) {
-      int64_t* dsts[5] = {out->req_dispatch, out->req_start, out->req_finish,
-                          out->req_batch, out->req_outcome};
-      for (int k = 0; k < 5; k++)
-        CK(cudaMemcpyAsync(dsts[k], d_req + k * sc, sizeof(int64_t) * n,
-                           cudaMemcpyDeviceToHost, st));
+      int64_t* dsts[8] = {out->req_dispatch, out->req_start, out->req_finish,
+                          out->req_batch, out->req_outcome, out->req_arrival,
+                          out->req_deadline, out->req_model};
+      for (int k = 0; k < 8; k++)
+        if (dsts[k])
+          CK(cudaMemcpyAsync(dsts[k], d_req + k * sc, sizeof(int64_t) * n,
+                             cudaMemcpyDeviceToHost, st));
     }
     if (want_drop && n > 0) {
       CK(cudaMemcpyAsync(out->drop_t, d_drop, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
@@ -2086,7 +2130,8 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model
   int64_t keep_cap = out->batch_cap;
   int64_t *k0 = out->req_dispatch, *k1 = out->req_start, *k2 = out->req_finish,
           *k3 = out->req_batch, *k4 = out->req_outcome, *k5 = out->drop_t,
-          *k6 = out->drop_key_sub;
+          *k6 = out->drop_key_sub, *k8 = out->req_arrival, *k9 = out->req_deadline,
+          *k10 = out->req_model;
   int32_t* k7 = out->drop_key_a;
   *out = dev;
   out->batches = keep_b;
@@ -2096,10 +2141,43 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const int32_t* arr_model
   out->req_finish = k2;
   out->req_batch = k3;
   out->req_outcome = k4;
+  out->req_arrival = k8;
+  out->req_deadline = k9;
+  out->req_model = k10;
   out->drop_t = k5;
   out->drop_key_sub = k6;
   out->drop_key_a = k7;
   return rc;
+}
+
+int64_t sym_last_batches(void* engine, sym_batch* host, int64_t cap) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx || !ctx->has_run) return -SYM_EINVAL;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return -SYM_ECUDA;
+  int64_t total = 0;
+  for (int64_t c : ctx->last_nrecs) total += c;
+  if (total > cap) return -SYM_EINVAL;
+  if (total == 0) return 0;
+  cudaStream_t st = ctx->stream;
+  const int32_t M = ctx->M, P = ctx->P, B = M + P;
+  if (total + 1 > ctx->bat_cap) {
+    if (grow(ctx, ctx->d_bat, total + 1)) return -SYM_ECUDA;
+    ctx->bat_cap = total + 1;
+  }
+  int64_t* meta = ctx->d_meta;
+  if (cudaMemcpyAsync(meta, ctx->last_rec_base.data(), sizeof(int64_t) * P,
+                      cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(meta + P + 1, ctx->last_nrecs.data(), sizeof(int64_t) * P,
+                      cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return -SYM_ECUDA;
+  k_copy_batches<<<nblk(total, 256), 256, 0, st>>>(
+      ctx->d_recs, meta, meta + P + 1, P, ctx->d_s_i, ctx->d_bins + B + P + 2,
+      ctx->d_slot_base, ctx->d_bins + B + P + 2 + M, total, ctx->d_bat);
+  if (cudaMemcpyAsync(host, ctx->d_bat, sizeof(sym_batch) * total, cudaMemcpyDeviceToHost,
+                      st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return -SYM_ECUDA;
+  return total;
 }
 
 int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,

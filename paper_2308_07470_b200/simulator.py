@@ -244,26 +244,22 @@ class Engine:
         return self.run_stream(ticks, midx, duration_s)
 
     def run_stream(self, arr_ticks, arr_midx, duration_s: float) -> RunResult:
+        """simulator.py:201-226 on the B200.  Validation (model ids in range,
+        time-ordered arrivals) happens on the device; results are written by
+        the device straight into page-locked arrays."""
         ticks = np.ascontiguousarray(arr_ticks, dtype=np.int64)
-        midx64 = np.asarray(arr_midx, dtype=np.int64)
+        midx = np.ascontiguousarray(arr_midx, dtype=np.int64)
         n = len(ticks)
-        if len(midx64) != n:
+        if len(midx) != n:
             raise ValueError("arr_ticks and arr_midx differ in length")
-        M = len(self.models)
-        if n:
-            bad = np.nonzero((midx64 < 0) | (midx64 >= M))[0]
-            if len(bad):
-                raise ProtocolError(f"request for unknown model {int(midx64[bad[0]])}")
-            if np.any(np.diff(ticks) < 0):
-                raise ValueError("arrival ticks must be non-decreasing")
-        midx = np.ascontiguousarray(midx64, dtype=np.int32)
         self._ensure()
-        outs = [np.empty(n, np.int64) for _ in range(5)]
-        batches = np.empty(max(n, 1), dtype=_native.BATCH_DTYPE)
+        names = ("dispatch", "start", "finish", "batch", "outcome", "arrival", "deadline",
+                 "model")
+        outs = {k: _native.pinned_empty(n) for k in names}
         res = _native.SymResult()
         res.n = n
-        (res.req_dispatch, res.req_start, res.req_finish, res.req_batch,
-         res.req_outcome) = (a.ctypes.data_as(_native.i64p) for a in outs)
+        for k in names:
+            setattr(res, "req_" + k, outs[k].ctypes.data_as(_native.i64p))
         if self.record_trace:
             drop_t = np.empty(n, np.int64)
             drop_ks = np.empty(n, np.int64)
@@ -271,27 +267,32 @@ class Engine:
             res.drop_t = drop_t.ctypes.data_as(_native.i64p)
             res.drop_key_sub = drop_ks.ctypes.data_as(_native.i64p)
             res.drop_key_a = drop_ka.ctypes.data_as(_native.i32p)
-        res.batches = batches.ctypes.data
-        res.batch_cap = len(batches)
         rc = self._lib.sym_run(self._handle, ticks.ctypes.data, midx.ctypes.data, n,
-                               self._flags(), C.byref(res))
+                               self._flags() | _native.FLAG_MODEL_I64, C.byref(res))
         if rc != _native.SYM_OK:
+            if rc == _native.SYM_EPROTO and 0 <= res.err_index < n:
+                raise ProtocolError(f"request for unknown model {int(midx[res.err_index])}")
             self._raise(rc, res)
         self._absorb_counters(res)
-        batches = batches[: res.n_batches].copy()
-        disp, start, fin, bsz, outc = outs
+        batches = _native.pinned_empty(res.n_batches, _native.BATCH_DTYPE)
+        got = self._lib.sym_last_batches(self._handle, batches.ctypes.data, len(batches))
+        if got != res.n_batches:
+            raise RuntimeError(f"sym_last_batches returned {got}")
+        outc = outs["outcome"]
         result = RunResult(
             model_names=[m.name for m in self.models], gpu_count=self.gpu_count,
-            duration_ns=s_to_ns(duration_s), req_model=midx64.copy(),
-            req_arrival=ticks.copy(), req_deadline=ticks + self._slo[midx64],
-            req_dispatch=disp, req_start=start, req_finish=fin, req_batch=bsz,
-            req_outcome=outc, gpu_logs=_GpuLogs(batches, self.gpu_count),
+            duration_ns=s_to_ns(duration_s), req_model=outs["model"],
+            req_arrival=outs["arrival"], req_deadline=outs["deadline"],
+            req_dispatch=outs["dispatch"], req_start=outs["start"], req_finish=outs["finish"],
+            req_batch=outs["batch"], req_outcome=outc,
+            gpu_logs=_GpuLogs(batches, self.gpu_count), drops=int(res.drops),
             # n_completed counts every completion event, LATE ones included
             # (simulator.py:251-252)
-            drops=int(res.drops), completions=int(np.count_nonzero(outc != OUTCOME_DROPPED)),
-            late=int(np.count_nonzero(outc == OUTCOME_LATE)), batches=batches)
+            completions=n - int(res.drops),
+            late=int(np.count_nonzero(outc == OUTCOME_LATE)) if self._jitter is not None else 0,
+            batches=batches)
         if self.record_trace:
-            result.trace = self._build_trace(ticks, midx64, batches, drop_t, drop_ks, drop_ka)
+            result.trace = self._build_trace(ticks, midx, batches, drop_t, drop_ks, drop_ka)
         if self.check_invariants:
             self._verify(result)
         return result
