@@ -269,10 +269,16 @@ def run_b200(args, rank, world, local_rank):
     ktimes = eng.kernel_times(reset=True)
 
     # end to end through the public API: pinned host arrays in, RunResult out
+    # (steady state: two untimed calls warm the pinned-memory pool, and each
+    # result is released before the next call, as a streaming caller would)
     pin_t = torch.from_numpy(ticks).pin_memory().numpy()
     pin_m = torch.from_numpy(midx).pin_memory().numpy()
+    for _ in range(2):
+        eng.run_stream(pin_t, pin_m, args.duration)
     e2e_s = []
-    for _ in range(max(1, min(args.steps, 3))):
+    res = None
+    for _ in range(max(3, min(args.steps, 10))):
+        res = None
         t0 = time.perf_counter()
         res = eng.run_stream(pin_t, pin_m, args.duration)
         e2e_s.append(time.perf_counter() - t0)
