@@ -410,35 +410,70 @@ __global__ void k_aself(const int64_t* __restrict__ s_tick,
 // K2' (fast path): the batch-chain pointer of every position by the lean
 // monotone sweep (fastpath.cuh), one thread per 32 consecutive positions;
 // close_k[p] keeps the closing arrival of certified starts for k_chain_recs.
-constexpr int kSweep = 32;
+constexpr int kSweep = 32;          // positions per lane
+constexpr int kSweepWarps = 4;      // warps per block
+constexpr int kSweepMargin = 512;   // ticks staged past a warp's range
+constexpr int kSweepSpan = 32 * kSweep;  // positions per warp
+constexpr int kSweepWin = kSweepSpan + kSweepMargin;
 
-__global__ void __launch_bounds__(256)
+__host__ __device__ constexpr size_t nxt_smem_per_warp() {
+  return sizeof(int64_t) * kSweepWin + 2 * sizeof(int32_t) * kSweepSpan;
+}
+
+// A warp covers kSweepSpan consecutive sorted positions (lane l the l-th run
+// of kSweep).  Its tick window is staged once with coalesced loads, every
+// lane sweeps out of shared memory (global only beyond the margin), and the
+// pointers are staged and written back coalesced.
+__global__ void __launch_bounds__(32 * kSweepWarps)
 k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
       const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
-      int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
-  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kSweep;
-  if (p0 >= n) return;
-  const int64_t p1 = p0 + kSweep < n ? p0 + kSweep : n;
-  int lo = 0, hi = slot_base[P];
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (mp_all[mid].off <= p0) lo = mid; else hi = mid;
+      const int64_t* __restrict__ s_tick, int32_t* __restrict__ nxt,
+      int32_t* __restrict__ close_k) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wbase = ((int64_t)blockIdx.x * kSweepWarps + wib) * kSweepSpan;
+  if (wbase >= n) return;
+  unsigned char* mine = smem_raw + wib * nxt_smem_per_warp();
+  int64_t* win = reinterpret_cast<int64_t*>(mine);
+  int32_t* o_nx = reinterpret_cast<int32_t*>(win + kSweepWin);
+  int32_t* o_ck = o_nx + kSweepSpan;
+  const int64_t wend = wbase + kSweepWin < n ? wbase + kSweepWin : n;
+  for (int64_t g = wbase + lane; g < wend; g += 32) win[g - wbase] = s_tick[g];
+  __syncwarp();
+  const int64_t p0 = wbase + (int64_t)lane * kSweep;
+  if (p0 < n) {
+    const int64_t p1 = p0 + kSweep < n ? p0 + kSweep : n;
+    int lo = 0, hi = slot_base[P];
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (mp_all[mid].off <= p0) lo = mid; else hi = mid;
+    }
+    int s = 0;
+    int64_t p = p0;
+    while (p < p1) {  // the range may cross model (and shard) boundaries
+      while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+      while (slot_base[s + 1] <= lo) s++;
+      const ModelParam& mp = mp_all[lo];
+      const int64_t off = mp.off;
+      const int64_t end = off + mp.cnt < p1 ? off + mp.cnt : p1;
+      lean_chain_sweep(
+          shards[s], lo - slot_base[s], (int32_t)(p - off), (int32_t)(end - off),
+          [&](int32_t q, int32_t v, int32_t k) {
+            o_nx[off + q - wbase] = v;
+            o_ck[off + q - wbase] = k;
+          },
+          [&](int32_t k) {
+            const int64_t gpos = off + k;
+            return gpos < wend ? win[gpos - wbase] : s_tick[gpos];
+          });
+      p = end;
+    }
   }
-  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p0) lo++;
-  int s = 0;
-  while (slot_base[s + 1] <= lo) s++;
-  int64_t p = p0;
-  while (p < p1) {  // the range may cross model (and shard) boundaries
-    while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
-    while (slot_base[s + 1] <= lo) s++;
-    const ModelParam& mp = mp_all[lo];
-    const int64_t end = mp.off + mp.cnt < p1 ? mp.off + mp.cnt : p1;
-    lean_chain_sweep(shards[s], lo - slot_base[s], (int32_t)(p - mp.off),
-                     (int32_t)(end - mp.off), [&](int32_t q, int32_t v, int32_t k) {
-                       nxt[mp.off + q] = v;
-                       close_k[mp.off + q] = k;
-                     });
-    p = end;
+  __syncwarp();
+  const int64_t oend = wbase + kSweepSpan < n ? wbase + kSweepSpan : n;
+  for (int64_t g = wbase + lane; g < oend; g += 32) {
+    nxt[g] = o_nx[g - wbase];
+    close_k[g] = o_ck[g - wbase];
   }
 }
 
@@ -1475,8 +1510,9 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
   bool have_fresh = false;
   if (fast) {
-    KL(k_nxt, nblk((n + kSweep - 1) / kSweep, 256), 256, 0, st>>>(
-        ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, n, ctx->d_nxt, ctx->d_closek));
+    KL(k_nxt, nblk((n + kSweepSpan - 1) / kSweepSpan, kSweepWarps), 32 * kSweepWarps,
+       kSweepWarps * nxt_smem_per_warp(), st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P,
+                                                n, ctx->d_s_tick, ctx->d_nxt, ctx->d_closek));
     KL(k_nxt_general, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp,
                                                   P, n, ctx->d_nxt, ctx->d_closek));
   } else if (use_fresh && n > 0) {
@@ -1991,6 +2027,9 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     if ((e = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ctx->chain_smem)) != cudaSuccess)
       return fail("smem attribute", e);
+    if ((e = cudaFuncSetAttribute(k_nxt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kSweepWarps * nxt_smem_per_warp()))) != cudaSuccess)
+      return fail("sweep smem attribute", e);
     const size_t sc = kScatterWarps * scatter_smem_per_warp(ctx->M + ctx->P);
     if (sc > (size_t)dev_max) return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
     if ((e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -223,26 +223,28 @@ SYM_HD int32_t lean_chain_next(const Shard& S, int32_t m, int32_t q) {
 // closing index never moves backwards and one forward pointer serves the
 // whole range (two-pointer sweep, O(q1 - q0 + b) instead of O((q1 - q0) b)).
 // The result for each q equals lean_chain_next(S, m, q) (host-verified).
-template <class Emit>
-SYM_HD void lean_chain_sweep(const Shard& S, int32_t m, int32_t q0, int32_t q1, Emit emit) {
+// `tick(k)` returns the k-th (model-relative) arrival tick; the CUDA kernel
+// serves it from a shared-memory window.
+template <class Emit, class Tick>
+SYM_HD void lean_chain_sweep(const Shard& S, int32_t m, int32_t q0, int32_t q1, Emit emit,
+                             Tick tick) {
   const ModelParam& P = S.mp[m];
   if (S.kind != K_DEFERRED || S.gather != G_PREFIX) {
     for (int32_t q = q0; q < q1; q++) emit(q, NX_UNSURE, 0);
     return;
   }
   const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
-  const int64_t* tick = S.s_tick + P.off;
   const int64_t dc = S.d_ctrl, dd = S.d_data;
   const int32_t mb = P.max_batch, cnt = P.cnt;
   int32_t k = q0;
   for (int32_t q = q0; q < q1; q++) {
     if (k < q) k = q;
-    const int64_t d = tick[q] + P.slo;
+    const int64_t d = tick(q) + P.slo;
     int32_t v = NX_UNSURE;
     for (;; k++) {
       const int32_t len = k - q + 1;
       if (len > mb) break;  // capped: would not drain (UNSURE)
-      const int64_t now = tick[k];
+      const int64_t now = tick(k);
       const int64_t delay = dc + dd * len;
       if (now + delay + lat[len - 1] > d) break;  // b < len (UNSURE)
       const int64_t l_next = len < mb ? lat[len] : lat[mb - 1];
@@ -253,13 +255,19 @@ SYM_HD void lean_chain_sweep(const Shard& S, int32_t m, int32_t q0, int32_t q1, 
         v = NX_LAST;
         break;
       }
-      if (fire <= tick[k + 1]) {
+      if (fire <= tick(k + 1)) {
         v = P.off + k + 1;
         break;
       }
     }
     emit(q, v, k);
   }
+}
+
+template <class Emit>
+SYM_HD void lean_chain_sweep(const Shard& S, int32_t m, int32_t q0, int32_t q1, Emit emit) {
+  const int64_t* t = S.s_tick + S.mp[m].off;
+  lean_chain_sweep(S, m, q0, q1, emit, [t](int32_t k) { return t[k]; });
 }
 
 // The batch a certified fresh start q produces, from (q, k) alone: the
