@@ -1891,6 +1891,13 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     p.cnt = 0;
     p.max_batch = mb;
     p.target_batch = cfg->target_batch < mb ? cfg->target_batch : mb;
+    // exact affine detection: l(b) = a*b + c for every b in [1, max_batch]
+    p.aff_a = mb > 1 ? row[1] - row[0] : 0;
+    p.aff_b = row[0] - p.aff_a;
+    p.affine = 1;
+    for (int b = 0; b < mb; b++)
+      if (row[b] != p.aff_a * (b + 1) + p.aff_b) p.affine = 0;
+    p._pad = 0;
     ctx->max_slo = std::max<int64_t>(ctx->max_slo, p.slo);
     ctx->max_lat = std::max<int64_t>(ctx->max_lat, row[mb - 1]);
   }

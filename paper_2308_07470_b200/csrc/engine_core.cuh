@@ -99,6 +99,9 @@ struct ModelParam {
   int64_t slo;
   int64_t timeout_ns;   // resolved (PolicyConfig.resolve_timeout_ns)
   int64_t base1;        // d_ctrl + d_data + l(1)
+  int64_t aff_a, aff_b; // l(b) = aff_a * b + aff_b exactly, when affine != 0
+  int32_t affine;       // the lat row is exactly affine in b (linear profiles)
+  int32_t _pad;
   int32_t off;          // first position of this model in the sorted stream
   int32_t cnt;          // arrivals of this model
   int32_t max_batch;

@@ -233,7 +233,11 @@ SYM_HD void lean_chain_sweep(const Shard& S, int32_t m, int32_t q0, int32_t q1, 
     for (int32_t q = q0; q < q1; q++) emit(q, NX_UNSURE, 0);
     return;
   }
-  const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
+  const int64_t* lat_row = S.lat + (int64_t)m * S.lat_stride;
+  const bool aff = P.affine != 0;
+  const int64_t la = P.aff_a, lb0 = P.aff_b;
+  // l(b): exact affine form for linear profiles (no table loads), else the row
+  auto lat = [&](int32_t i) { return aff ? la * (i + 1) + lb0 : lat_row[i]; };
   const int64_t dc = S.d_ctrl, dd = S.d_data;
   const int32_t mb = P.max_batch, cnt = P.cnt;
   int32_t k = q0;
@@ -246,8 +250,8 @@ SYM_HD void lean_chain_sweep(const Shard& S, int32_t m, int32_t q0, int32_t q1, 
       if (len > mb) break;  // capped: would not drain (UNSURE)
       const int64_t now = tick(k);
       const int64_t delay = dc + dd * len;
-      if (now + delay + lat[len - 1] > d) break;  // b < len (UNSURE)
-      const int64_t l_next = len < mb ? lat[len] : lat[mb - 1];
+      if (now + delay + lat(len - 1) > d) break;  // b < len (UNSURE)
+      const int64_t l_next = len < mb ? lat(len) : lat(mb - 1);
       const int64_t exec = now + delay > d - l_next ? now + delay : d - l_next;
       const int64_t f = exec - delay;
       const int64_t fire = f < now ? now : f;

@@ -32,6 +32,9 @@ extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64
     mp[m].base1 = cfg->d_ctrl_ns + cfg->d_data_ns + cfg->lat_ns[(int64_t)m * cfg->lat_stride];
     mp[m].off = off[m]; mp[m].cnt = cnt[m]; mp[m].max_batch = cfg->max_batch[m];
     mp[m].target_batch = std::min(cfg->target_batch, cfg->max_batch[m]);
+    { const int64_t* row = cfg->lat_ns + (int64_t)m * cfg->lat_stride; int mb = cfg->max_batch[m];
+      mp[m].aff_a = mb > 1 ? row[1] - row[0] : 0; mp[m].aff_b = row[0] - mp[m].aff_a; mp[m].affine = 1;
+      for (int b = 0; b < mb; b++) if (row[b] != mp[m].aff_a * (b + 1) + mp[m].aff_b) mp[m].affine = 0; }
   }
   int32_t Mp = 1; while (Mp < M) Mp <<= 1;
   int32_t Gp = 1; while (Gp < G) Gp <<= 1;

@@ -4,7 +4,8 @@ import csv, re, sys, collections
 sass = open("/tmp/dev/cubin/all.sass").read().splitlines()
 fn = sys.argv[1]
 # collect line info for the function section
-start = next(i for i, l in enumerate(sass) if l.startswith("//---") and fn in l)
+mangled = f"{len(fn)}{fn}E"  # exact Itanium-mangled function name component
+start = next(i for i, l in enumerate(sass) if l.startswith("//---") and mangled in l)
 end = next((i for i in range(start + 1, len(sass)) if sass[i].startswith("//---")), len(sass))
 cur = None; off2line = {}
 for l in sass[start:end]:
