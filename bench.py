@@ -54,6 +54,7 @@ def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
         # lean chain pointer: each sorted tick read once (neighbours share
         # the line), one 4-byte pointer written per position
         "k_nxt": n * (8 + 4),
+        "k_nxt_pp": n * (8 + 4 + 4),
         "k_nxt_general": n * 4,
         # batch records from the chain positions' fresh scans: the members'
         # ticks/ids once, one EvBatch written per batch

@@ -477,6 +477,27 @@ k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
   }
 }
 
+// One lane per sorted position (lanes in lock step on neighbouring ticks);
+// close_k = the closing arrival for k_chain_recs.
+__global__ void __launch_bounds__(256)
+k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
+         const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
+         int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int lo = 0, hi = slot_base[P];
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+  }
+  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  int s = 0;
+  while (slot_base[s + 1] <= lo) s++;
+  const int32_t v = lean_chain_next(shards[s], lo - slot_base[s], (int32_t)(p - mp_all[lo].off));
+  nxt[p] = v;
+  close_k[p] = v >= 0 ? v - 1 - mp_all[lo].off : (v == NX_LAST ? mp_all[lo].cnt - 1 : -1);
+}
+
 // Positions the lean loop could not certify: the general fresh_scan.
 __global__ void __launch_bounds__(256)
 k_nxt_general(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
@@ -1510,9 +1531,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
   bool have_fresh = false;
   if (fast) {
-    KL(k_nxt, nblk((n + kSweepSpan - 1) / kSweepSpan, kSweepWarps), 32 * kSweepWarps,
-       kSweepWarps * nxt_smem_per_warp(), st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P,
-                                                n, ctx->d_s_tick, ctx->d_nxt, ctx->d_closek));
+    KL(k_nxt_pp, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, n,
+                                             ctx->d_nxt, ctx->d_closek));
     KL(k_nxt_general, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp,
                                                   P, n, ctx->d_nxt, ctx->d_closek));
   } else if (use_fresh && n > 0) {

@@ -185,7 +185,10 @@ SYM_HD int32_t chain_next(const FreshRec& r, const ModelParam& mp) {
 SYM_HD int32_t lean_chain_next(const Shard& S, int32_t m, int32_t q) {
   const ModelParam& P = S.mp[m];
   if (S.kind != K_DEFERRED || S.gather != G_PREFIX) return NX_UNSURE;
-  const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
+  const int64_t* lat_row = S.lat + (int64_t)m * S.lat_stride;
+  const bool aff = P.affine != 0;
+  const int64_t la = P.aff_a, lb0 = P.aff_b;
+  auto lat = [&](int32_t i) { return aff ? la * (i + 1) + lb0 : lat_row[i]; };
   const int64_t* tick = S.s_tick + P.off;
   const int64_t dc = S.d_ctrl, dd = S.d_data;
   const int64_t d = tick[q] + P.slo;
@@ -198,10 +201,9 @@ SYM_HD int32_t lean_chain_next(const Shard& S, int32_t m, int32_t q) {
     const int32_t len = k - q + 1;
     if (len > mb) return NX_UNSURE;  // capped: would not drain
     const int64_t delay = dc + dd * len;
-    const int64_t lb = lat[len - 1];
     // b == len  <=>  ok(len) (monotone); also excludes head drops
-    if (now + delay + lb > d) return NX_UNSURE;
-    const int64_t l_next = len < mb ? lat[len] : lat[mb - 1];
+    if (now + delay + lat(len - 1) > d) return NX_UNSURE;
+    const int64_t l_next = len < mb ? lat(len) : lat(mb - 1);
     const int64_t exec = now + delay > d - l_next ? now + delay : d - l_next;
     const int64_t f = exec - delay;
     const int64_t fire = f < now ? now : f;
@@ -212,7 +214,6 @@ SYM_HD int32_t lean_chain_next(const Shard& S, int32_t m, int32_t q) {
   }
   return NX_UNSURE;
 }
-
 
 // Monotone sweep of lean_chain_next over consecutive positions [q0, q1) of
 // model m.  For a start q the batch closes at the first k with
