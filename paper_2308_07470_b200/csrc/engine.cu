@@ -484,18 +484,30 @@ k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base
          const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
          int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  int lo = 0, hi = slot_base[P];
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+  const int lane = threadIdx.x & 31;
+  // one model lookup per warp (its lanes are consecutive positions), then
+  // each lane steps forward to its own model
+  const int64_t p_lead = p - lane < n ? p - lane : n - 1;
+  int lo = 0;
+  if (lane == 0) {
+    int hi = slot_base[P];
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (mp_all[mid].off <= p_lead) lo = mid; else hi = mid;
+    }
   }
+  lo = __shfl_sync(0xffffffffu, lo, 0);
+  if (p >= n) return;
   while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
   int s = 0;
   while (slot_base[s + 1] <= lo) s++;
-  const int32_t v = lean_chain_next(shards[s], lo - slot_base[s], (int32_t)(p - mp_all[lo].off));
+  const Shard& S = shards[s];
+  const int32_t m = lo - slot_base[s];
+  const ModelParam& mp = mp_all[lo];
+  const int32_t q = (int32_t)(p - mp.off);
+  const int32_t v = rel32_ok(S, mp) ? lean_chain_next32(S, m, q) : lean_chain_next(S, m, q);
   nxt[p] = v;
-  close_k[p] = v >= 0 ? v - 1 - mp_all[lo].off : (v == NX_LAST ? mp_all[lo].cnt - 1 : -1);
+  close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
 }
 
 // Positions the lean loop could not certify: the general fresh_scan.

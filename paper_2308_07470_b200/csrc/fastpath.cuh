@@ -215,6 +215,47 @@ SYM_HD int32_t lean_chain_next(const Shard& S, int32_t m, int32_t q) {
   return NX_UNSURE;
 }
 
+// lean_chain_next in 32-bit arithmetic relative to the head's tick, for an
+// affine l(b).  Every quantity compared is within [0, slo + l(max_batch) +
+// delay(max_batch)] of the head tick as long as the batch is still open
+// (now <= deadline - l(1) - delay(1)), so int32 is exact when that bound is
+// below 2^31 -- the caller checks it (rel32_ok) and otherwise uses the
+// 64-bit form.  The next tick is compared after clamping at the bound.
+SYM_HD bool rel32_ok(const Shard& S, const ModelParam& P) {
+  const int64_t top = P.slo + P.aff_a * (int64_t)P.max_batch + P.aff_b +
+                      S.d_ctrl + S.d_data * (int64_t)P.max_batch;
+  return P.affine && S.kind == K_DEFERRED && S.gather == G_PREFIX && top < (int64_t(1) << 30) &&
+         P.aff_a >= 0 && P.aff_b >= 0;
+}
+
+SYM_HD int32_t lean_chain_next32(const Shard& S, int32_t m, int32_t q) {
+  const ModelParam& P = S.mp[m];
+  const int64_t* tick = S.s_tick + P.off;
+  const int64_t t0 = tick[q];
+  const int32_t la = (int32_t)P.aff_a, lb0 = (int32_t)P.aff_b;
+  const int32_t dc = (int32_t)S.d_ctrl, dd = (int32_t)S.d_data;
+  const int32_t d = (int32_t)P.slo;  // deadline relative to the head
+  const int32_t mb = P.max_batch, cnt = P.cnt;
+  const int64_t cap = int64_t(1) << 30;
+  int32_t now = 0;
+  for (int32_t k = q; k < cnt; k++) {
+    const int32_t len = k - q + 1;
+    if (len > mb) return NX_UNSURE;
+    const int32_t delay = dc + dd * len;
+    if (now + delay + la * len + lb0 > d) return NX_UNSURE;  // b < len
+    const int32_t l_next = la * (len < mb ? len + 1 : mb) + lb0;
+    const int32_t exec = now + delay > d - l_next ? now + delay : d - l_next;
+    const int32_t f = exec - delay;
+    const int32_t fire = f < now ? now : f;
+    if (k + 1 >= cnt) return NX_LAST;
+    const int64_t nx = tick[k + 1] - t0;
+    const int32_t next = (int32_t)(nx < cap ? nx : cap);
+    if (fire <= next) return P.off + k + 1;
+    now = next;
+  }
+  return NX_UNSURE;
+}
+
 // Monotone sweep of lean_chain_next over consecutive positions [q0, q1) of
 // model m.  For a start q the batch closes at the first k with
 //   fire(q, k) = max(a_k, d_q - l(len+1) - delay(len)) <= a_{k+1},
