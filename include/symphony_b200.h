@@ -169,6 +169,35 @@ const char *sym_last_error(void *engine);
 const char *sym_kernel_times(void *engine, int32_t reset);
 int32_t sym_version(void);
 
+/* ---- result-file text (reference outputs.py:72-121) ----------------------
+ * The per-request CSV bodies are formatted on the GPU: one thread per row
+ * renders the decimal fields, a block scan places rows, the text stays in
+ * HBM until fetched.  Rows only; the caller prepends the header line.
+ *   SYM_TEXT_REQUESTS: requests.csv rows (outputs.py:72-88)
+ *   SYM_TEXT_LATENCY:  latency.csv rows, served requests only
+ *                      (outputs.py:112-121) */
+enum { SYM_TEXT_REQUESTS = 0, SYM_TEXT_LATENCY = 1 };
+
+typedef struct {
+  int64_t n;                  /* requests; row i is request id i+1 */
+  /* per-request int64 columns, host or device pointers (UVA); model ids
+   * index `names` */
+  const int64_t *req_model, *req_arrival, *req_dispatch, *req_start,
+      *req_finish, *req_batch, *req_outcome;
+  int32_t n_names, _pad;
+  const char *names;          /* concatenated UTF-8 model names */
+  const int64_t *name_off;    /* [n_names + 1] byte offsets into names */
+} sym_text_columns;
+
+/* Format on `device`; returns a text handle (NULL + *status on failure:
+ * SYM_EINVAL for a model id outside names or an outcome outside -1..2) and
+ * sets *out_len to the byte length. */
+void *sym_text_format(int32_t kind, const sym_text_columns *cols, int32_t device,
+                      int64_t *out_len, int32_t *status);
+/* Copy the text to a host buffer of len bytes (len == *out_len). */
+int32_t sym_text_fetch(void *text, char *dst, int64_t len);
+void sym_text_free(void *text);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,7 +79,16 @@ class SymResult(C.Structure):
 
 EXPORTS = ("sym_create", "sym_destroy", "sym_run", "sym_run_device",
            "sym_window_counts", "sym_last_error", "sym_version", "sym_kernel_times",
-           "sym_last_batches")
+           "sym_last_batches", "sym_text_format", "sym_text_fetch", "sym_text_free")
+
+TEXT_REQUESTS, TEXT_LATENCY = 0, 1
+
+
+class SymTextColumns(C.Structure):
+    _fields_ = [("n", C.c_int64)] + [(k, i64p) for k in (
+        "req_model", "req_arrival", "req_dispatch", "req_start", "req_finish", "req_batch",
+        "req_outcome")] + [("n_names", C.c_int32), ("_pad", C.c_int32),
+                           ("names", C.c_char_p), ("name_off", i64p)]
 
 _lib = None
 
@@ -115,6 +124,12 @@ def load(path: str | None = None):
     lib.sym_last_batches.restype = C.c_int64
     lib.sym_kernel_times.argtypes = [C.c_void_p, C.c_int32]
     lib.sym_kernel_times.restype = C.c_char_p
+    lib.sym_text_format.argtypes = [C.c_int32, C.POINTER(SymTextColumns), C.c_int32, i64p, i32p]
+    lib.sym_text_format.restype = C.c_void_p
+    lib.sym_text_fetch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    lib.sym_text_fetch.restype = C.c_int32
+    lib.sym_text_free.argtypes = [C.c_void_p]
+    lib.sym_text_free.restype = None
     _lib = lib
     return lib
 

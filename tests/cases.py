@@ -98,3 +98,30 @@ def config_cases(names=("C1", "C2", "C3", "C4", "C5")):
             else:
                 yield (f"{name}/{v}@{dur}", list(sc.models), sc.gpu_count, sc.policy, ticks,
                        midx, (dur, 0.1 * dur, 0.1 * dur))
+
+
+OUTPUT_CASES = ["fig6_stagger", "fig7_skip", "table2_inceptionresnet", "fig4b_timeout_zoo",
+                "jitter/fig6_stagger/J2/base", "jitter/table2_inceptionresnet/J3/timeout"]
+
+
+def outputs():
+    """(key, scenario, ticks, midx) for the output-file golden cases
+    (make_golden.output_cases)."""
+    import copy
+    from paper_2308_07470_b200._bundled import BUNDLED
+    from paper_2308_07470_b200.scenario import _bundled_trace_dir, scenario_from_dict
+    for case in OUTPUT_CASES:
+        if case.startswith("jitter/"):
+            _, name, net, kind = case.split("/")
+            doc = copy.deepcopy(BUNDLED[name])
+            doc["network"] = JITTER_NETS[net]
+            if kind != "base":
+                doc.setdefault("policy", {})["kind"] = kind
+                if kind == "timeout":
+                    doc["policy"]["timeout_slo_frac"] = 0.3
+            sc = scenario_from_dict(doc, name=name, base_dir=_bundled_trace_dir())
+        else:
+            sc = load_scenario(case)
+        ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models],
+                                        sc.duration_s, sc.seed)
+        yield f"outputs/{case}", sc, ticks, midx

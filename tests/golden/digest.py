@@ -40,3 +40,8 @@ def event_trace_digest(trace) -> str:
         flat.extend((t, TRACE_KIND[kind], mid, gid, size, start, finish, len(rids)))
         flat.extend(rids)
     return _h(flat)
+
+
+def text_digest(text: str) -> str:
+    """Digest of one output file's exact bytes (outputs.py writers)."""
+    return hashlib.sha256(text.encode("utf-8")).hexdigest()[:32]

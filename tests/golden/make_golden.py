@@ -229,6 +229,58 @@ def jitter_cases(out):
         print(key, out[key]["late"], out[key]["drops"], flush=True)
 
 
+OUTPUT_FILES = ("summary.json", "requests.csv", "trace.csv", "batch_hist.csv",
+                "latency.csv", "utilization.csv")
+OUTPUT_CASES = ["fig6_stagger", "fig7_skip", "table2_inceptionresnet", "fig4b_timeout_zoo",
+                "jitter/fig6_stagger/J2/base", "jitter/table2_inceptionresnet/J3/timeout"]
+
+
+def output_cases(out):
+    """Exact bytes of the reference's six result files (outputs.py) for a
+    few bundled and jittered runs, as digests of the file text."""
+    import copy
+    import yaml
+    from batchsym import outputs as RO
+    from batchsym.scenario import scenario_from_dict
+    root = "/root/reference/pkg/src/batchsym/scenarios"
+    for case in OUTPUT_CASES:
+        if case.startswith("jitter/"):
+            _, name, net, kind = case.split("/")
+            doc = copy.deepcopy(yaml.safe_load(open(os.path.join(root, name + ".yaml"))))
+            doc["network"] = JITTER_NETS[net]
+            if kind != "base":
+                doc.setdefault("policy", {})["kind"] = kind
+                if kind == "timeout":
+                    doc["policy"]["timeout_slo_frac"] = 0.3
+            sc = scenario_from_dict(doc, name=name, base_dir=root)
+        else:
+            sc = load_scenario(case)
+        ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models],
+                                        sc.duration_s, sc.seed)
+        eng = Engine(list(sc.models), sc.gpu_count, sc.policy, sc.network, seed=sc.seed,
+                     record_trace=True)
+        res = eng.run_stream(ticks, midx, sc.duration_s)
+        st = RM.compute_stats(res, sc.warmup_s, sc.cooldown_s, sc.duration_s)
+        extra = {"gpu_count": sc.gpu_count, "policy": sc.policy.kind}
+        t0 = time.time()
+        files = {
+            "summary.json": RO.summary_json(st, sc.name, sc.seed, extra),
+            "requests.csv": RO.requests_csv(res),
+            "trace.csv": RO.trace_csv(res),
+            "batch_hist.csv": RO.batch_hist_csv(st),
+            "latency.csv": RO.latency_csv(res),
+            "utilization.csv": RO.utilization_csv(res, st),
+        }
+        el = time.time() - t0
+        out[f"outputs/{case}"] = {
+            "scenario": sc.name, "seed": sc.seed, "extra": extra,
+            "digests": {k: D.text_digest(v) for k, v in files.items()},
+            "bytes": {k: len(v) for k, v in files.items()},
+            "ref_seconds": round(el, 3),
+        }
+        print("outputs", case, round(el, 3), flush=True)
+
+
 def stress_cases(out, n_cases=60):
     sys.path.insert(0, os.path.join(REPO, "tests"))
     from stress_cases import make_case
@@ -243,6 +295,13 @@ def stress_cases(out, n_cases=60):
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["outputs"]:  # refresh only the output-file digests
+        path = os.path.join(HERE, "golden.json")
+        out = json.load(open(path))
+        output_cases(out)
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1, sort_keys=True)
+        sys.exit(0)
     out = {"generator": "tests/golden/make_golden.py", "reference": "batchsym 0.1.0",
            "numpy": np.__version__}
     known_answers(out)
@@ -251,6 +310,7 @@ if __name__ == "__main__":
     bundled_cases(out)
     stress_cases(out)
     config_cases(out)
+    output_cases(out)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
     print("wrote golden.json")
