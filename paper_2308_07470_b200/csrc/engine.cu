@@ -129,11 +129,14 @@ struct Ctx {
     }                                                                   \
   } while (0)
 
+// Device memory is stream-ordered (the device's default pool, release
+// threshold at max): no allocation or free synchronises the device, so
+// several engines (threads, streams) run their kernels concurrently.
 template <class T>
 int grow(Ctx* ctx, T*& p, int64_t count) {
-  if (p) cudaFree(p);
+  if (p) cudaFreeAsync(p, ctx->stream);
   p = nullptr;
-  CK(cudaMalloc((void**)&p, sizeof(T) * (size_t)(count > 0 ? count : 1)));
+  CK(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)(count > 0 ? count : 1), ctx->stream));
   return SYM_OK;
 }
 
@@ -572,9 +575,8 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
         int32_t* __restrict__ dirty_all, const int32_t* __restrict__ slot_base,
         size_t smem_bytes, const int32_t* __restrict__ skip) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ Shard S;  // hot scalars of the sub-cluster live in smem
   if (threadIdx.x != 0 || skip[blockIdx.x]) return;
-  S = shards[blockIdx.x];
+  Shard S = shards[blockIdx.x];  // hot scalars of the sub-cluster in registers
   const Shard orig = S;  // global pointers, restored before the write-back
   ModelState* const ms_global = S.ms;
   size_t used = 0;
@@ -1945,6 +1947,13 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     return fail("stream", e);
   for (auto& ev : ctx->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail("event", e);
+  {  // keep pool memory mapped across synchronisations (no remap stalls)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   // chain state
   ctx->shards.resize(P);
   std::vector<int32_t> mp2(P), gp2(P);
@@ -1960,9 +1969,9 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     tot_m2 += 2 * a;
     tot_g2 += 2 * b;
   }
-#define ALLOC(p, cnt)                                                      \
-  if ((e = cudaMalloc((void**)&(p), sizeof(*(p)) * (size_t)(cnt))) !=      \
-      cudaSuccess)                                                          \
+#define ALLOC(p, cnt)                                                        \
+  if ((e = cudaMallocAsync((void**)&(p), sizeof(*(p)) * (size_t)(cnt),       \
+                           ctx->stream)) != cudaSuccess)                      \
     return fail(#p, e);
   ALLOC(ctx->d_lat, (int64_t)M * ctx->lat_stride);
   ALLOC(ctx->d_mp, M);
@@ -2001,31 +2010,24 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_net_vals, ctx->net_ctrl_n + ctx->net_data_n + 1);
   ALLOC(ctx->d_net_cdf, ctx->net_ctrl_n + ctx->net_data_n + 1);
   if (ctx->net_ctrl_n) {
-    cudaMemcpy(ctx->d_net_vals, cfg->net_ctrl_vals, sizeof(int64_t) * ctx->net_ctrl_n, cudaMemcpyHostToDevice);
-    cudaMemcpy(ctx->d_net_cdf, cfg->net_ctrl_cdf, sizeof(double) * ctx->net_ctrl_n, cudaMemcpyHostToDevice);
+    cudaMemcpyAsync(ctx->d_net_vals, cfg->net_ctrl_vals, sizeof(int64_t) * ctx->net_ctrl_n, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(ctx->d_net_cdf, cfg->net_ctrl_cdf, sizeof(double) * ctx->net_ctrl_n, cudaMemcpyHostToDevice, ctx->stream);
   }
   if (ctx->net_data_n) {
-    cudaMemcpy(ctx->d_net_vals + ctx->net_ctrl_n, cfg->net_data_vals, sizeof(int64_t) * ctx->net_data_n, cudaMemcpyHostToDevice);
-    cudaMemcpy(ctx->d_net_cdf + ctx->net_ctrl_n, cfg->net_data_cdf, sizeof(double) * ctx->net_data_n, cudaMemcpyHostToDevice);
+    cudaMemcpyAsync(ctx->d_net_vals + ctx->net_ctrl_n, cfg->net_data_vals, sizeof(int64_t) * ctx->net_data_n, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(ctx->d_net_cdf + ctx->net_ctrl_n, cfg->net_data_cdf, sizeof(double) * ctx->net_data_n, cudaMemcpyHostToDevice, ctx->stream);
   }
   ALLOC(ctx->d_meta, 3 * (P + 1));
 #undef ALLOC
-  {  // keep pool memory mapped across synchronisations (no remap stalls)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
   const int B = M + P;
-  cudaMemcpy(ctx->d_lat, lat.data(), sizeof(int64_t) * lat.size(), cudaMemcpyHostToDevice);
-  cudaMemcpy(ctx->d_mp, ctx->mp_host.data(), sizeof(ModelParam) * M, cudaMemcpyHostToDevice);
-  cudaMemcpy(ctx->d_slot_of_model, ctx->slot_of_model.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
-  cudaMemcpy(ctx->d_shard_of_model, ctx->shard_of_model.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
-  cudaMemcpy(ctx->d_slot_base, ctx->slot_base.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice);
-  cudaMemcpy(ctx->d_slo_model, cfg->slo_ns, sizeof(int64_t) * M, cudaMemcpyHostToDevice);
-  cudaMemcpy(ctx->d_bins + B + P + 2, ctx->model_of_slot.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice);
-  cudaMemcpy(ctx->d_bins + B + P + 2 + M, ctx->gpu_base.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice);
+  cudaMemcpyAsync(ctx->d_lat, lat.data(), sizeof(int64_t) * lat.size(), cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(ctx->d_mp, ctx->mp_host.data(), sizeof(ModelParam) * M, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(ctx->d_slot_of_model, ctx->slot_of_model.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(ctx->d_shard_of_model, ctx->shard_of_model.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(ctx->d_slot_base, ctx->slot_base.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(ctx->d_slo_model, cfg->slo_ns, sizeof(int64_t) * M, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(ctx->d_bins + B + P + 2, ctx->model_of_slot.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(ctx->d_bins + B + P + 2 + M, ctx->gpu_base.data(), sizeof(int32_t) * (P + 1), cudaMemcpyHostToDevice, ctx->stream);
   int64_t om = 0, og = 0;
   for (int s = 0; s < P; s++) {
     Shard& S = ctx->shards[s];
@@ -2075,7 +2077,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
                                   (int)sc)) != cudaSuccess)
       return fail("scatter smem attribute", e);
   }
-  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail("init", e);
+  if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return fail("init", e);
   *status = SYM_OK;
   return ctx;
 }
@@ -2102,7 +2104,8 @@ void sym_destroy(void* engine) {
                   ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
                   ctx->d_net_vals, ctx->d_net_cdf};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, ctx->stream);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -2273,7 +2276,7 @@ int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,
   const int32_t M = ctx->M, P = ctx->P, G = ctx->G;
   const int64_t n = ctx->last_n;
   unsigned long long* d = nullptr;
-  CK(cudaMalloc((void**)&d, sizeof(unsigned long long) * (4 * (size_t)M + G)));
+  CK(cudaMallocAsync((void**)&d, sizeof(unsigned long long) * (4 * (size_t)M + G), st));
   CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * (4 * (size_t)M + G), st));
   if (n > 0)
     k_window_req<<<nblk(n, 256), 256, 0, st>>>(ctx->last_ticks, ctx->last_model,
@@ -2294,8 +2297,8 @@ int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,
   std::vector<unsigned long long> h(4 * (size_t)M + G);
   CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(),
                      cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(d, st);
   CK(cudaStreamSynchronize(st));
-  cudaFree(d);
   for (int32_t m = 0; m < M; m++) {
     model_arrivals[m] = (int64_t)h[m];
     model_completed[m] = (int64_t)h[M + m];

@@ -190,6 +190,7 @@ struct Text {
   int device;
   char* d;
   int64_t len;
+  cudaStream_t st;  // stream-ordered memory: nothing here syncs the device
 };
 
 #define CK(x)                              \
@@ -204,13 +205,15 @@ int32_t format(const Cols& c, int64_t nb, size_t smem, cudaStream_t st, int64_t*
   if (nb) {
     k_text_len<KIND><<<(unsigned)nb, kRows, 0, st>>>(c, d_chunk, d_err);
     k_text_scan<<<1, 1024, 0, st>>>(d_chunk, nb);
+  } else if (cudaMemsetAsync(d_chunk, 0, 8, st) != cudaSuccess) {
+    return SYM_ECUDA;
   }
   if (cudaMemcpyAsync(&t->len, d_chunk + nb, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     return SYM_ECUDA;
   if (h_err) return SYM_EINVAL;
-  if (cudaMalloc(&t->d, t->len ? t->len : 1) != cudaSuccess) return SYM_ENOMEM;
+  if (cudaMallocAsync((void**)&t->d, t->len ? t->len : 1, st) != cudaSuccess) return SYM_ENOMEM;
   if (nb) {
     if (cudaFuncSetAttribute(k_text_write<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
@@ -247,7 +250,7 @@ void* sym_text_format(int32_t kind, const sym_text_columns* cols, int32_t device
   int prev = 0;
   cudaGetDevice(&prev);
   if (cudaSetDevice(device) != cudaSuccess) return nullptr;
-  Text* t = new (std::nothrow) Text{device, nullptr, 0};
+  Text* t = new (std::nothrow) Text{device, nullptr, 0, nullptr};
   cudaStream_t st = nullptr;
   char* blob = nullptr;  // columns | chunk sizes | names | offsets | err
   int32_t rc = SYM_ECUDA;
@@ -267,7 +270,7 @@ void* sym_text_format(int32_t kind, const sym_text_columns* cols, int32_t device
     size_t o_err = o_noff + size_t(N + 1) * 8, bytes = o_err + 16;
     Cols c{};
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    if (cudaMalloc(&blob, bytes) != cudaSuccess) {
+    if (cudaMallocAsync((void**)&blob, bytes, st) != cudaSuccess) {
       rc = SYM_ENOMEM;
       goto done;
     }
@@ -298,15 +301,21 @@ void* sym_text_format(int32_t kind, const sym_text_columns* cols, int32_t device
 cuda_fail:
   rc = SYM_ECUDA;
 done:
-  if (blob) cudaFree(blob);
-  if (st) cudaStreamDestroy(st);
-  cudaSetDevice(prev);
-  *status = rc;
+  if (blob) cudaFreeAsync(blob, st);
   if (rc != SYM_OK) {
-    if (t->d) cudaFree(t->d);
+    if (t->d) cudaFreeAsync(t->d, st);
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+    cudaSetDevice(prev);
+    *status = rc;
     delete t;
     return nullptr;
   }
+  t->st = st;
+  cudaSetDevice(prev);
+  *status = rc;
   *out_len = t->len;
   return t;
 }
@@ -318,7 +327,8 @@ int32_t sym_text_fetch(void* text, char* dst, int64_t len) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(t->device);
-  cudaError_t e = cudaMemcpy(dst, t->d, size_t(len), cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaMemcpyAsync(dst, t->d, size_t(len), cudaMemcpyDeviceToHost, t->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(t->st);
   cudaSetDevice(prev);
   return e == cudaSuccess ? SYM_OK : SYM_ECUDA;
 }
@@ -329,7 +339,9 @@ void sym_text_free(void* text) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(t->device);
-  if (t->d) cudaFree(t->d);
+  if (t->d) cudaFreeAsync(t->d, t->st);
+  cudaStreamSynchronize(t->st);
+  cudaStreamDestroy(t->st);
   cudaSetDevice(prev);
   delete t;
 }

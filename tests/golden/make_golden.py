@@ -281,6 +281,66 @@ def output_cases(out):
         print("outputs", case, round(el, 3), flush=True)
 
 
+SWEEP_CASES = [
+    ("beta_ratio", "table2_resnet50", [1.0, 6.0], ["deferred", "eager"], None),
+    ("timeout", "fig4b_timeout_sweep", [10.0, 60.0], None, None),
+    ("offered_load", "table2_resnet50", [0.5, 1.25], None, 5000.0),
+    ("slo", "table2_inceptionresnet", [40.0, 90.0], ["deferred", "timeout:30"], None),
+]
+
+
+def sweep_cases(out):
+    """Rows of the reference's grid sweeps (sweeps.py:67-142), each point a
+    goodput search or fixed-rate run through run_scenario."""
+    from batchsym import sweeps as RS
+    rows = {}
+    for dim, name, grid, pols, peak in SWEEP_CASES:
+        t0 = time.time()
+        rows[f"{dim}/{name}"] = RS.run_sweep(dim, load_scenario(name), grid, pols, peak)
+        print("sweep", dim, name, round(time.time() - t0, 2), flush=True)
+    out["sweeps"] = rows
+
+
+SCALEBENCH_SHARDS = [(8, 16), (32, 4), (1, 1), (64, 128)]
+SCALEBENCH_KEEP = 5000
+
+
+def scalebench_cases(out):
+    """The reference's wall-clock shard loop (scalebench.py:49-85), run for a
+    short interval with its Engine captured: the digest of its arrival
+    stream and of the first SCALEBENCH_KEEP requests' outcomes pin the
+    package's restated stream and the equivalence of the step loop with
+    run_stream on that stream."""
+    from batchsym import scalebench as RSB
+    keep = SCALEBENCH_KEEP
+    cases = {}
+    for n_models, n_gpus in SCALEBENCH_SHARDS:
+        captured = []
+
+        class Capture(RSB.Engine):
+            def __init__(self, *a, **k):
+                super().__init__(*a, **k)
+                captured.append(self)
+        orig = RSB.Engine
+        RSB.Engine = Capture
+        try:
+            n = RSB._shard_loop(n_models, n_gpus, 0.5)
+        finally:
+            RSB.Engine = orig
+        eng = captured[0]
+        assert n >= 2 * keep, n
+        cases[f"{n_models}x{n_gpus}"] = {
+            "n_models": n_models, "n_gpus": n_gpus, "keep": keep,
+            "stream": D.trace_digest(eng._arrival[:keep], eng._model_idx[:keep]),
+            "requests": D.requests_digest(eng._dispatch[:keep], eng._start[:keep],
+                                          eng._finish[:keep], eng._batch[:keep],
+                                          eng._outcome[:keep]),
+            "resolved": int(sum(1 for o in eng._outcome[:keep] if o >= 0)),
+        }
+        print("scalebench", n_models, n_gpus, n, flush=True)
+    out["scalebench"] = cases
+
+
 def stress_cases(out, n_cases=60):
     sys.path.insert(0, os.path.join(REPO, "tests"))
     from stress_cases import make_case
@@ -295,10 +355,11 @@ def stress_cases(out, n_cases=60):
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] == ["outputs"]:  # refresh only the output-file digests
+    if sys.argv[1:] in (["outputs"], ["sweeps"], ["scalebench"]):  # refresh one section only
         path = os.path.join(HERE, "golden.json")
         out = json.load(open(path))
-        output_cases(out)
+        {"outputs": output_cases, "sweeps": sweep_cases,
+         "scalebench": scalebench_cases}[sys.argv[1]](out)
         with open(path, "w") as fh:
             json.dump(out, fh, indent=1, sort_keys=True)
         sys.exit(0)
@@ -311,6 +372,8 @@ if __name__ == "__main__":
     stress_cases(out)
     config_cases(out)
     output_cases(out)
+    sweep_cases(out)
+    scalebench_cases(out)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
     print("wrote golden.json")

@@ -72,3 +72,24 @@ def check_against_golden(g: dict, dispatch, start, finish, batch, outcome, gpu_l
         assert v == g[k], f"{k}: {v} != golden {g[k]}"
     if trace is not None:
         assert D.event_trace_digest(trace) == g["events"]
+
+
+def oracle_run_scenario(scenario, record_trace=False, check_invariants=False):
+    """run_scenario on the CPU oracle (test infrastructure: lets the CPU
+    suite exercise the host callers -- goodput_search, sweeps -- whose GPU
+    runs go through the engine)."""
+    from conftest import oracle_args
+    from oracle import oracle
+    from paper_2308_07470_b200.network import jitter_tables
+    from paper_2308_07470_b200.workload import generate_arrivals
+    assert scenario.shards is None
+    models = list(scenario.models)
+    ticks, midx = generate_arrivals(scenario.workload, [m.name for m in models],
+                                    scenario.duration_s, scenario.seed)
+    o = oracle.run(arr_ticks=ticks, arr_midx=midx, record_trace=record_trace,
+                   net=jitter_tables(scenario.network, scenario.seed),
+                   **oracle_args(models, scenario.gpu_count, scenario.policy))
+    res = oracle_result(o, models, scenario.gpu_count, ticks, midx, scenario.duration_s)
+    if record_trace:
+        res.trace = oracle_trace(o)
+    return res

@@ -5,7 +5,7 @@ sass = open("/tmp/dev/cubin/all.sass").read().splitlines()
 fn = sys.argv[1]
 # collect line info for the function section
 mangled = f"{len(fn)}{fn}E"  # exact Itanium-mangled function name component
-start = next(i for i, l in enumerate(sass) if l.startswith("//---") and mangled in l)
+start = next(i for i, l in enumerate(sass) if l.startswith("//---") and ".text." in l and mangled in l)
 end = next((i for i in range(start + 1, len(sass)) if sass[i].startswith("//---")), len(sass))
 cur = None; off2line = {}
 for l in sass[start:end]:
