@@ -198,6 +198,41 @@ void *sym_text_format(int32_t kind, const sym_text_columns *cols, int32_t device
 int32_t sym_text_fetch(void *text, char *dst, int64_t len);
 void sym_text_free(void *text);
 
+/* ---- sub-cluster partitioning (reference partitioner.py) ----------------
+ * Scores follow evaluate (partitioner.py:114-145) operation for operation in
+ * IEEE double, so objectives and tie-breaks match the reference exactly. */
+typedef struct {
+  int32_t m, l;                 /* models, sub-clusters (l <= 64) */
+  const double *rates, *static_mem, *dynamic_mem;  /* [m] */
+  double rate_cap, mem_cap;     /* +inf when absent */
+  double weight;                /* effective_weight() */
+  double mean_rate, mean_mem;   /* sum(x) / l, as the reference computes them */
+  const int32_t *current;       /* [m] or NULL */
+  const double *change_cost;    /* [m * l] or NULL (every entry 1.0) */
+  double change_budget;
+} sym_part_problem;
+
+/* brute_force (partitioner.py:422-435): the first (itertools.product order)
+ * minimum of (infeasible, objective) over all l^m <= 4e6 assignments. */
+int32_t sym_part_brute_force(const sym_part_problem *p, int32_t device, int32_t *best_x,
+                             double *best_obj, int32_t *best_feasible);
+/* Score `count` assignments (row-major [count][m]); best_index is the first
+ * minimum of (infeasible, objective) -- the random baseline's selection
+ * (partitioner.py:392-419). */
+int32_t sym_part_evaluate(const sym_part_problem *p, int32_t device, const int32_t *xs,
+                          int64_t count, double *obj, int32_t *feasible,
+                          int64_t *best_index);
+/* `restarts` independent greedy + first-improvement local searches
+ * (partitioner.py:247-389), restart ids first_restart.. (restart 0 starts
+ * from `current` when given); order = models heaviest first.  One warp per
+ * restart; a restart stops at its local optimum or after budget_s seconds
+ * (<= 0: no limit).  Writes every restart's final assignment
+ * [restarts][m], score (violation, objective) and improving steps. */
+int32_t sym_part_solve(const sym_part_problem *p, int32_t device, const int32_t *order,
+                       uint64_t seed, int64_t first_restart, int32_t restarts,
+                       double budget_s, int32_t *xs, double *viol, double *obj,
+                       int64_t *steps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,9 +79,20 @@ class SymResult(C.Structure):
 
 EXPORTS = ("sym_create", "sym_destroy", "sym_run", "sym_run_device",
            "sym_window_counts", "sym_last_error", "sym_version", "sym_kernel_times",
-           "sym_last_batches", "sym_text_format", "sym_text_fetch", "sym_text_free")
+           "sym_last_batches", "sym_text_format", "sym_text_fetch", "sym_text_free",
+           "sym_part_brute_force", "sym_part_evaluate", "sym_part_solve")
 
 TEXT_REQUESTS, TEXT_LATENCY = 0, 1
+
+
+class SymPartProblem(C.Structure):
+    _fields_ = [("m", C.c_int32), ("l", C.c_int32),
+                ("rates", C.POINTER(C.c_double)), ("static_mem", C.POINTER(C.c_double)),
+                ("dynamic_mem", C.POINTER(C.c_double)),
+                ("rate_cap", C.c_double), ("mem_cap", C.c_double), ("weight", C.c_double),
+                ("mean_rate", C.c_double), ("mean_mem", C.c_double),
+                ("current", C.POINTER(C.c_int32)), ("change_cost", C.POINTER(C.c_double)),
+                ("change_budget", C.c_double)]
 
 
 class SymTextColumns(C.Structure):
@@ -130,6 +141,15 @@ def load(path: str | None = None):
     lib.sym_text_fetch.restype = C.c_int32
     lib.sym_text_free.argtypes = [C.c_void_p]
     lib.sym_text_free.restype = None
+    pp = C.POINTER(SymPartProblem)
+    lib.sym_part_brute_force.argtypes = [pp, C.c_int32, i32p, C.POINTER(C.c_double), i32p]
+    lib.sym_part_evaluate.argtypes = [pp, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
+                                      C.c_void_p, C.POINTER(C.c_int64)]
+    lib.sym_part_solve.argtypes = [pp, C.c_int32, C.c_void_p, C.c_uint64, C.c_int64,
+                                   C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p]
+    for fn in (lib.sym_part_brute_force, lib.sym_part_evaluate, lib.sym_part_solve):
+        fn.restype = C.c_int32
     _lib = lib
     return lib
 

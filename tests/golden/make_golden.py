@@ -341,6 +341,84 @@ def scalebench_cases(out):
     out["scalebench"] = cases
 
 
+PART_BRUTE = [(8, 3, 0), (10, 2, 1), (12, 3, 2), (9, 4, 3), (13, 3, 4), (6, 10, 5), (20, 2, 6)]
+PART_TEXT = """# l=3
+# R_max=400
+# S_max=
+# w=0.05
+# C_max=7.5
+model,rate_rps,static_mem_mb,dynamic_mem_mb
+resnet50,120.5,98,40
+bert,80,420.25,120
+gpt2,35.125,510,200
+vgg16,60,530,90
+mobilenet,220,17,8
+"""
+
+
+def _part_variants(P, seed):
+    """The random instance plus capped / weighted / change-budget variants."""
+    from dataclasses import replace as dreplace
+    base = P.random_instance(*seed)
+    m, l = base.n_models, base.subclusters
+    rng = np.random.default_rng(seed[2] + 100)
+    cur = tuple(int(v) for v in rng.integers(0, l, m))
+    cost = tuple(tuple(round(float(c), 3) for c in row) for row in rng.uniform(0.5, 3.0, (m, l)))
+    return {
+        "plain": base,
+        "tight": dreplace(base, rate_cap=base.rate_cap / 1.5 * 1.02, mem_cap=base.mem_cap / 1.4),
+        "infeasible": dreplace(base, rate_cap=1.0),
+        "weighted": dreplace(base, weight=0.125),
+        "budget": dreplace(base, current=cur, change_cost=cost, change_budget=6.0 + seed[2]),
+        "unit_budget": dreplace(base, current=cur, change_budget=4.0),
+    }
+
+
+def partition_cases(out):
+    """Reference partitioner (partitioner.py): brute-force optima, the first
+    minimum over the random baseline's first draws, the solver's objective at
+    a 1 s budget (a quality bar), and a parsed problem file."""
+    from batchsym import partitioner as P
+    from batchsym.workload import substream
+    brute, rnd = {}, {}
+    for inst in PART_BRUTE:
+        for name, prob in _part_variants(P, inst).items():
+            t0 = time.time()
+            r = P.brute_force(prob)
+            ev = r.evaluation
+            brute[f"{inst}/{name}"] = {"assignment": list(r.assignment), "objective": ev.objective,
+                                       "feasible": ev.feasible, "change_cost": ev.change_cost,
+                                       "seconds": round(time.time() - t0, 2)}
+            rng = substream(inst[2], 1)
+            best_key, best_k, rows = None, None, []
+            for _ in range(4):
+                rows += [[int(v) for v in row] for row in rng.integers(0, prob.subclusters,
+                                                                       size=(256, prob.n_models))]
+            for k, x in enumerate(rows):
+                e = P.evaluate(prob, x)
+                key = (0.0 if e.feasible else 1.0, e.objective)
+                if best_key is None or key < best_key:
+                    best_key, best_k = key, k
+            rnd[f"{inst}/{name}"] = {"index": best_k, "assignment": rows[best_k],
+                                     "objective": best_key[1], "feasible": best_key[0] == 0.0}
+            print("partition", inst, name, brute[f"{inst}/{name}"]["seconds"], flush=True)
+    solve = {}
+    for inst in [(60, 8, 11), (200, 16, 12), (40, 4, 13)]:
+        prob = P.random_instance(*inst)
+        r = P.solve(prob, 1.0, inst[2])
+        solve[str(inst)] = {"objective": r.evaluation.objective, "feasible": r.feasible,
+                            "restarts": r.restarts}
+        print("partition solve", inst, r.evaluation.objective, r.restarts, flush=True)
+    pp = P.parse_problem(PART_TEXT)
+    out["partition"] = {"brute": brute, "random_first": rnd, "solve_1s": solve,
+                        "parsed": {"names": list(pp.names), "rates": list(pp.rates),
+                                   "static": list(pp.static_mem), "dynamic": list(pp.dynamic_mem),
+                                   "l": pp.subclusters, "rate_cap": pp.rate_cap,
+                                   "mem_cap": str(pp.mem_cap), "weight": pp.weight,
+                                   "change_budget": pp.change_budget,
+                                   "csv": P.assignment_csv(pp, [0, 1, 2, 0, 1])}}
+
+
 def stress_cases(out, n_cases=60):
     sys.path.insert(0, os.path.join(REPO, "tests"))
     from stress_cases import make_case
@@ -355,11 +433,11 @@ def stress_cases(out, n_cases=60):
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] in (["outputs"], ["sweeps"], ["scalebench"]):  # refresh one section only
+    if sys.argv[1:] in (["outputs"], ["sweeps"], ["scalebench"], ["partition"]):  # refresh one section only
         path = os.path.join(HERE, "golden.json")
         out = json.load(open(path))
         {"outputs": output_cases, "sweeps": sweep_cases,
-         "scalebench": scalebench_cases}[sys.argv[1]](out)
+         "scalebench": scalebench_cases, "partition": partition_cases}[sys.argv[1]](out)
         with open(path, "w") as fh:
             json.dump(out, fh, indent=1, sort_keys=True)
         sys.exit(0)
@@ -374,6 +452,7 @@ if __name__ == "__main__":
     output_cases(out)
     sweep_cases(out)
     scalebench_cases(out)
+    partition_cases(out)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
     print("wrote golden.json")
