@@ -1093,30 +1093,24 @@ k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bv
       }
     }
     grid.sync();
-    int32_t* pin = ptrA;
-    int32_t* pout = ptrB;
-    for (int round = 0; round < 64; round++) {  // pointer jumping
-      if (tid0 == 0) flags[(round + 1) & 1] = 0;
-      bool open = false;
+    // Resolve gids by pointer jumping IN PLACE and without barriers: every
+    // entry always holds an ancestor on its creator chain (or the resolved
+    // -gid-1), so reading a neighbour's stale or freshly jumped value is
+    // equally valid, and each jump strictly shortens the remaining chain.
+    // Loads bypass L1 (other SMs write these entries).  Each thread sweeps
+    // its entries until all are resolved: ~log2(depth) sweeps, one grid
+    // barrier in total instead of two per doubling round.
+    for (bool open = true; open;) {
+      open = false;
       for (int64_t i = tid0; i < nt; i += stride) {
-        const int32_t v = pin[i];
-        const int32_t w = v < 0 ? v : pin[v];
-        pout[i] = w;
+        const int32_t v = __ldcg(ptrA + i);
+        if (v < 0) continue;
+        const int32_t w = __ldcg(ptrA + v);
+        __stcg(ptrA + i, w);
         open |= w >= 0;
       }
-      if (open) flags[round & 1] = 1;
-      grid.sync();
-      const bool more = flags[round & 1] != 0;
-      int32_t* t = pin;
-      pin = pout;
-      pout = t;
-      if (!more) break;
-      grid.sync();  // everyone read the flag before it is reset again
     }
-    if (pin != ptrA) {
-      for (int64_t i = tid0; i < nt; i += stride) ptrA[i] = pin[i];
-      grid.sync();
-    }
+    grid.sync();
     if (tid0 == 0) flags[2 + ((it + 1) & 1)] = 0;
     bool moved = false;
     for (int64_t i = tid0; i < nt; i += stride) {  // equal-finish groups by gid
