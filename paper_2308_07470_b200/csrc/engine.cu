@@ -508,7 +508,10 @@ k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base
   const int32_t m = lo - slot_base[s];
   const ModelParam& mp = mp_all[lo];
   const int32_t q = (int32_t)(p - mp.off);
-  const int32_t v = rel32_ok(S, mp) ? lean_chain_next32(S, m, q) : lean_chain_next(S, m, q);
+  const bool affine = mp.affine && S.kind == K_DEFERRED && S.gather == G_PREFIX;
+  const int32_t v = affine ? lean_chain_next_affine(S, mp, q)
+                           : rel32_ok(S, mp) ? lean_chain_next32(S, m, q)
+                                             : lean_chain_next(S, m, q);
   nxt[p] = v;
   close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
 }

@@ -256,6 +256,46 @@ SYM_HD int32_t lean_chain_next32(const Shard& S, int32_t m, int32_t q) {
   return NX_UNSURE;
 }
 
+// lean_chain_next for an exactly affine l(b) = a*b + b0, restated on
+// u_j = tick_j + c1*j with c1 = a + d_data.  With len = k - q + 1 and
+// len < max_batch the closing test  d_q - l(len+1) - delay(len) <= tick_{k+1}
+// is  u_{k+1} >= u_q + (slo - a - b0 - d_ctrl),  and ok(len) is
+// u_k <= u_q + (slo - d_ctrl - b0 - c1); both sides are exact int64, so the
+// scan is one load, one multiply-add and one compare per step instead of the
+// full candidate arithmetic.  ok is monotone in k, so it is checked once at
+// the closing index.  The len == max_batch step (l_next = l(max_batch)) and
+// the last arrival keep the scalar form.  Equals lean_chain_next at every
+// position (tools/hostcheck).
+SYM_HD int32_t lean_chain_next_affine(const Shard& S, const ModelParam& P, int32_t q) {
+  const int64_t* tick = S.s_tick + P.off;
+  const int64_t a = P.aff_a, b0 = P.aff_b, dc = S.d_ctrl, dd = S.d_data;
+  const int64_t c1 = a + dd;
+  const int32_t mb = P.max_batch, cnt = P.cnt;
+  const int64_t uq = tick[q] + c1 * q;
+  const int64_t T = uq + (P.slo - a - b0 - dc);
+  const int64_t OK = uq + (P.slo - dc - b0 - c1);
+  const int32_t kmax = cnt - 2 < q + mb - 2 ? cnt - 2 : q + mb - 2;  // len < mb, k+1 < cnt
+  int32_t k = q;
+  while (k <= kmax && tick[k + 1] + c1 * (k + 1) < T) k++;
+  if (k <= kmax)  // closes at k
+    return tick[k] + c1 * k <= OK ? P.off + k + 1 : NX_UNSURE;
+  // not closed below len = max_batch: every k up to kmax must be ok, then
+  // the step at k1 = min(cnt - 1, q + mb - 1) in the scalar form
+  const int32_t k1 = kmax + 1;
+  if (k1 - q + 1 > mb) return NX_UNSURE;
+  const int64_t now = tick[k1];
+  if (now + c1 * k1 > OK) return NX_UNSURE;  // ok(len) fails at k1 (or earlier)
+  if (k1 + 1 >= cnt) return NX_LAST;
+  const int32_t len = k1 - q + 1;  // == mb here
+  const int64_t d = tick[q] + P.slo;
+  const int64_t delay = dc + dd * len;
+  const int64_t l_next = a * mb + b0;
+  const int64_t exec = now + delay > d - l_next ? now + delay : d - l_next;
+  const int64_t f = exec - delay;
+  const int64_t fire = f < now ? now : f;
+  return fire <= tick[k1 + 1] ? P.off + k1 + 1 : NX_UNSURE;
+}
+
 // Monotone sweep of lean_chain_next over consecutive positions [q0, q1) of
 // model m.  For a start q the batch closes at the first k with
 //   fire(q, k) = max(a_k, d_q - l(len+1) - delay(len)) <= a_{k+1},

@@ -82,6 +82,8 @@ extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64
     for (int q = 0; q < cnt[m]; q++) {
       int32_t v = lean_chain_next(S, m, q);
       if (rel32_ok(S, mp[m]) && lean_chain_next32(S, m, q) != v) mismatch += 1000000000;
+      if (mp[m].affine && S.kind == K_DEFERRED && S.gather == G_PREFIX &&
+          lean_chain_next_affine(S, mp[m], q) != v) mismatch += 100000000;
       if (v == NX_UNSURE) continue;
       certified++;
       if (v != chain_next(fresh_scan(S, m, q, 1 << 16), mp[m])) mismatch++;
