@@ -37,7 +37,9 @@ using namespace sym;
 namespace {
 
 constexpr int kChunkR = 256;      // keys per warp in the radix passes
-constexpr int kChunkI = 512;      // stream elements per warp in the ingest
+constexpr int kIngestWarps = 8;                    // warps per ingest block
+constexpr int kPerLane = 8;                        // stream elements per lane
+constexpr int kChunkI = kIngestWarps * 32 * kPerLane;  // stream elements per block
 constexpr int kFreshMaxSteps = 1 << 16;
 constexpr int kVersion = 1;
 
@@ -142,36 +144,42 @@ int grow(Ctx* ctx, T*& p, int64_t count) {
 
 // --------------------------------------------------------------- K1 -------
 
-__global__ void k_hist(const int32_t* __restrict__ model, const int64_t* __restrict__ ticks,
-                       int64_t n,
-                       const int32_t* __restrict__ slot_of_model,
-                       const int32_t* __restrict__ shard_of_model, int32_t M,
-                       int32_t P, int32_t* __restrict__ hist, int64_t W,
-                       int32_t* __restrict__ err) {
-  extern __shared__ int32_t sh[];
-  const int B = M + P;
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
-  int32_t* cnt = sh + wib * B;
-  for (int b = lane; b < B; b += 32) cnt[b] = 0;
-  __syncwarp();
-  if (w < W) {
-    const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
-    for (int64_t i = lo + lane; i < hi; i += 32) {
+// Per-block-chunk histogram of (slot, shard) bins, bin-major (hist[b][w]);
+// also checks model ids and the time order of the stream.  Equal bins of a
+// warp round are aggregated with __match_any_sync before the shared atomic.
+__global__ void __launch_bounds__(32 * kIngestWarps)
+k_hist(const int32_t* __restrict__ model, const int64_t* __restrict__ ticks, int64_t n,
+       const int32_t* __restrict__ slot_of_model, const int32_t* __restrict__ shard_of_model,
+       int32_t M, int32_t P, int32_t* __restrict__ hist, int64_t W,
+       int32_t* __restrict__ err) {
+  extern __shared__ int32_t cnt[];
+  const int B = M + P, lane = threadIdx.x & 31;
+  const int64_t w = blockIdx.x;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
+  for (int64_t i0 = lo + (threadIdx.x & ~31); i0 < hi; i0 += blockDim.x) {
+    const int64_t i = i0 + lane;
+    int32_t sl = -1 - lane, sd = -2 - lane - 32;  // unique dummies when inactive
+    if (i < hi) {
       if (i > 0 && ticks[i] < ticks[i - 1])  // arrivals must be time-ordered
         atomicMin(err + 1, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
       const int32_t m = model[i];
       if (m < 0 || m >= M) {
         atomicMin(err, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
-        continue;
+      } else {
+        sl = slot_of_model[m];
+        sd = M + shard_of_model[m];
       }
-      atomicAdd(&cnt[slot_of_model[m]], 1);
-      atomicAdd(&cnt[M + shard_of_model[m]], 1);
     }
+    const unsigned ps = __match_any_sync(0xffffffffu, sl);
+    const unsigned pd = __match_any_sync(0xffffffffu, sd);
+    if (sl >= 0 && (ps >> lane) == 1u) atomicAdd(&cnt[sl], __popc(ps));
+    if (sl >= 0 && (pd >> lane) == 1u) atomicAdd(&cnt[sd], __popc(pd));
   }
-  __syncwarp();
+  __syncthreads();
   if (w < W)
-    for (int b = lane; b < B; b += 32) hist[(int64_t)b * W + w] = cnt[b];
+    for (int b = threadIdx.x; b < B; b += blockDim.x) hist[(int64_t)b * W + w] = cnt[b];
 }
 
 // ---- device-wide exclusive scan of an int32 array (reduce, scan the block
@@ -277,20 +285,18 @@ __global__ void k_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t M,
   }
 }
 
-// Stable scatter of the stream into the (shard, model)-sorted layout.  One
-// warp per kChunkI-element chunk: ranks come from __match_any_sync against
-// running per-bin offsets (stream order within a bin is preserved), the
-// chunk is first staged in shared memory in bin order, then written out so
-// consecutive lanes write consecutive positions of a bin run (coalesced).
-constexpr int kScatterWarps = 4;
-
-__host__ __device__ inline size_t scatter_smem_per_warp(int B) {
-  const size_t bytes = sizeof(int32_t) * 3 * (size_t)B +
-                       (size_t)kChunkI * (sizeof(int64_t) + 3 * sizeof(int32_t));
-  return (bytes + 15) & ~size_t(15);  // keep every warp's int64 staging aligned
+// Stable scatter of the stream into the (shard, model)-sorted layout, one
+// block per kChunkI-element chunk.  Each warp owns a contiguous sub-chunk,
+// counts its bins (__match_any_sync), the counts are turned into per-warp
+// offsets (warp order = stream order), and a second pass over the values
+// kept in registers ranks every element.  The chunk is staged in shared
+// memory in bin order and written out as bin runs of ~kChunkI/M elements.
+__host__ __device__ inline size_t scatter_smem(int B) {
+  return (size_t)kChunkI * (sizeof(int64_t) + 3 * sizeof(int32_t)) +
+         sizeof(int32_t) * ((size_t)kIngestWarps * B + 2 * (size_t)B + 32);
 }
 
-__global__ void __launch_bounds__(32 * kScatterWarps)
+__global__ void __launch_bounds__(32 * kIngestWarps)
 k_scatter(const int64_t* __restrict__ ticks,
           const int32_t* __restrict__ model, int64_t n,
           const int32_t* __restrict__ slot_of_model,
@@ -305,83 +311,120 @@ k_scatter(const int64_t* __restrict__ ticks,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int B = M + P;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * kScatterWarps + wib;
-  if (w >= W) return;
-  unsigned char* mine = smem_raw + wib * scatter_smem_per_warp(B);
-  int64_t* st_t = reinterpret_cast<int64_t*>(mine);
+  const int64_t w = blockIdx.x;
+  int64_t* st_t = reinterpret_cast<int64_t*>(smem_raw);
   int32_t* st_g = reinterpret_cast<int32_t*>(st_t + kChunkI);
   int32_t* st_i = st_g + kChunkI;
   int32_t* st_b = st_i + kChunkI;
-  int32_t* gbase = st_b + kChunkI;  // global base of (bin, chunk)
-  int32_t* lstart = gbase + B;      // local start of the bin in the chunk
-  int32_t* lcur = lstart + B;       // running local offset (slot bins) /
-                                    // running global shard index (shard bins)
-  // bin-major flat exclusive scan: slot bins give sorted positions; shard
-  // bins follow all n slot entries (subtract n for shard-stream indices).
-  // The chunk's count of a bin is the next flat entry minus this one.
-  const int64_t total = 2 * n;
-  int32_t run = 0;
-  for (int b0 = 0; b0 < B; b0 += 32) {
-    const int b = b0 + lane;
-    int32_t cnt = 0, g = 0;
-    if (b < B) {
-      const int64_t f = (int64_t)b * W + w;
-      g = hist[f];
-      const int64_t nx = f + 1 < (int64_t)B * W ? hist[f + 1] : total;
-      cnt = b < M ? (int32_t)(nx - g) : 0;
+  int32_t* wcnt = st_b + kChunkI;          // [warp][bin] counts -> offsets
+  int32_t* gbase = wcnt + kIngestWarps * B;  // global base of (bin, chunk)
+  int32_t* lstart = gbase + B;             // local start of a slot bin
+  int32_t* scratch = lstart + B;           // [32] block scan of bin counts
+  int32_t* mine = wcnt + wib * B;
+  for (int b = lane; b < B; b += 32) mine[b] = 0;
+  // pass 1: load this lane's elements once, count the warp's bins
+  const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
+  const int64_t wlo = lo + (int64_t)wib * 32 * kPerLane;
+  int64_t t[kPerLane];
+  int32_t sl[kPerLane], sd[kPerLane];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < kPerLane; r++) {
+    const int64_t i = wlo + r * 32 + lane;
+    sl[r] = -1 - lane;
+    sd[r] = -2 - lane - 32;
+    t[r] = 0;
+    if (i < hi) {
+      const int32_t m = model[i];
+      sl[r] = slot_of_model[m];
+      sd[r] = M + shard_of_model[m];
+      t[r] = ticks[i];
     }
-    int32_t x = cnt;  // local exclusive scan over slot bins
+    const unsigned ps = __match_any_sync(0xffffffffu, sl[r]);
+    const unsigned pd = __match_any_sync(0xffffffffu, sd[r]);
+    if (sl[r] >= 0 && (ps >> lane) == 1u) mine[sl[r]] += __popc(ps);
+    if (sl[r] >= 0 && (pd >> lane) == 1u) mine[sd[r]] += __popc(pd);
+    __syncwarp();
+  }
+  // bases from the scanned histogram; per-warp offsets; local bin starts
+  __syncthreads();
+  const int64_t total = 2 * n;
+  const int per = (B + blockDim.x - 1) / blockDim.x;  // bins per thread
+  int32_t run = 0;
+  for (int k = 0; k < per; k++) {
+    const int b = threadIdx.x * per + k;
+    if (b >= B) break;
+    const int64_t f = (int64_t)b * W + w;
+    const int32_t g = hist[f];
+    const int64_t nx = f + 1 < (int64_t)B * W ? hist[f + 1] : total;
+    gbase[b] = b < M ? g : g - (int32_t)n;
+    int32_t acc = 0;
+    for (int q = 0; q < kIngestWarps; q++) {
+      const int32_t c = wcnt[q * B + b];
+      wcnt[q * B + b] = acc;
+      acc += c;
+    }
+    lstart[b] = run;  // provisional: thread-local prefix
+    run += b < M ? (int32_t)(nx - g) : 0;
+  }
+  // block exclusive scan of the per-thread bin totals
+  {
+    int32_t x = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    if (b < B) {
-      gbase[b] = b < M ? g : g - (int32_t)n;
-      lstart[b] = run + x - cnt;
-      lcur[b] = b < M ? run + x - cnt : g - (int32_t)n;
+    if (lane == 31) scratch[wib] = x;
+    __syncthreads();
+    if (wib == 0) {
+      int32_t v = lane < kIngestWarps ? scratch[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (lane < kIngestWarps) scratch[lane] = v;
     }
-    run += __shfl_sync(0xffffffffu, x, 31);
+    __syncthreads();
+    const int32_t before = (wib ? scratch[wib - 1] : 0) + x - run;
+    for (int k = 0; k < per; k++) {
+      const int b = threadIdx.x * per + k;
+      if (b >= B) break;
+      lstart[b] += before;
+    }
   }
-  __syncwarp();
+  __syncthreads();
+  // pass 2: rank, stage in bin order, shard-stream index, inverse map
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
-  for (int64_t i0 = lo; i0 < hi; i0 += 32) {
-    const int64_t i = i0 + lane;
+#pragma unroll
+  for (int r = 0; r < kPerLane; r++) {
+    const int64_t i = wlo + r * 32 + lane;
     const bool act = i < hi;
-    const unsigned amask = __ballot_sync(0xffffffffu, act);
-    int32_t sl = -1 - lane, sd = -1 - lane;  // unique dummies when inactive
-    int64_t t = 0;
-    if (act) {
-      const int32_t m = model[i];
-      sl = slot_of_model[m];
-      sd = M + shard_of_model[m];
-      t = ticks[i];
-    }
-    const unsigned ps = __match_any_sync(0xffffffffu, sl) & amask;
-    const unsigned pd = __match_any_sync(0xffffffffu, sd) & amask;
+    const unsigned ps = __match_any_sync(0xffffffffu, sl[r]);
+    const unsigned pd = __match_any_sync(0xffffffffu, sd[r]);
     int32_t e = 0, j = 0;
     if (act) {
-      e = lcur[sl] + __popc(ps & lt);
-      j = lcur[sd] + __popc(pd & lt);
+      e = mine[sl[r]] + __popc(ps & lt);
+      j = gbase[sd[r]] + mine[sd[r]] + __popc(pd & lt);
     }
     __syncwarp();
     if (act) {
-      // the highest peer advances the running offsets
-      if ((ps >> lane) == 1u) lcur[sl] += __popc(ps);
-      if ((pd >> lane) == 1u) lcur[sd] += __popc(pd);
-      st_t[e] = t;
-      st_g[e] = j;
-      st_i[e] = (int32_t)i;
-      st_b[e] = sl;
-      sh_tick[j] = t;
-      inv[i] = gbase[sl] + (e - lstart[sl]);  // coalesced in i
+      if ((ps >> lane) == 1u) mine[sl[r]] += __popc(ps);  // highest peer advances
+      if ((pd >> lane) == 1u) mine[sd[r]] += __popc(pd);
+      const int32_t le = lstart[sl[r]] + e;
+      st_t[le] = t[r];
+      st_g[le] = j;
+      st_i[le] = (int32_t)i;
+      st_b[le] = sl[r];
+      sh_tick[j] = t[r];
+      inv[i] = gbase[sl[r]] + e;  // coalesced in i
     }
     __syncwarp();
   }
-  __syncwarp();
+  __syncthreads();
   const int32_t len = (int32_t)(hi - lo);
-  for (int32_t e = lane; e < len; e += 32) {  // bin runs, coalesced
+  for (int32_t e = threadIdx.x; e < len; e += blockDim.x) {  // bin runs
     const int32_t b = st_b[e];
     const int32_t pos = gbase[b] + (e - lstart[b]);
     s_tick[pos] = st_t[e];
@@ -1459,10 +1502,9 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   // ---- K1 ingest
   const int32_t big[2] = {INT32_MAX, INT32_MAX};
   CK(cudaMemcpyAsync(ctx->d_err, big, sizeof big, cudaMemcpyHostToDevice, st));
-  const int wpb = 4;
-  const size_t smem = sizeof(int32_t) * (size_t)B * wpb;
+  const size_t smem = sizeof(int32_t) * (size_t)B;
   if (W > 0) {
-    KL(k_hist, nblk(W, wpb), 32 * wpb, smem, st>>>(
+    KL(k_hist, W, 32 * kIngestWarps, smem, st>>>(
         d_model, d_ticks, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_err));
     flat_scan(ctx->d_hist, W * B);
@@ -1496,8 +1538,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     return SYM_EINVAL;
   }
   if (W > 0)
-    KL(k_scatter, nblk(W, kScatterWarps), 32 * kScatterWarps,
-       kScatterWarps * scatter_smem_per_warp(B), st>>>(
+    KL(k_scatter, W, 32 * kIngestWarps, scatter_smem(B), st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
         ctx->d_sh_tick, ctx->d_inv));
@@ -2068,7 +2109,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     if ((e = cudaFuncSetAttribute(k_nxt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kSweepWarps * nxt_smem_per_warp()))) != cudaSuccess)
       return fail("sweep smem attribute", e);
-    const size_t sc = kScatterWarps * scatter_smem_per_warp(ctx->M + ctx->P);
+    const size_t sc = scatter_smem(ctx->M + ctx->P);
     if (sc > (size_t)dev_max) return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
     if ((e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sc)) != cudaSuccess)
