@@ -28,6 +28,8 @@ def summarize(path):
     out = {}
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("<unnamed>::", "")
+        if name in out:  # first launch of each kernel
+            continue
         d = {}
         for w in WANT:
             if w in hdr:
@@ -53,7 +55,6 @@ def summarize(path):
                      "stall_lg_throttle": d.get("smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio"),
                      "registers": d.get("launch__registers_per_thread"),
                      "grid": d.get("launch__grid_size"), "block": d.get("launch__block_size")}
-        break
     return out
 
 
