@@ -525,15 +525,25 @@ k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
 
 // One lane per sorted position (lanes in lock step on neighbouring ticks);
 // close_k = the closing arrival for k_chain_recs.
+//
+// Affine profiles (the common case) use lean_chain_next_affine's test on
+// u_j = tick_j + c1*j, but instead of every lane scanning forward to its own
+// closing arrival (a loop as long as the warp's longest batch), the warp
+// stages the ticks of its 64-position window in registers (two coalesced
+// loads) and each lane binary-searches its first u_j >= T through shuffles:
+// six uniform steps.  A closing index beyond the window (batches longer
+// than ~32) continues with the scalar scan.
 __global__ void __launch_bounds__(256)
 k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
          const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
          int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  const int64_t p0 = p - lane;  // window base (warp-uniform)
+  if (p0 >= n) return;          // whole warp out of range
   // one model lookup per warp (its lanes are consecutive positions), then
   // each lane steps forward to its own model
-  const int64_t p_lead = p - lane < n ? p - lane : n - 1;
+  const int64_t p_lead = p0;
   int lo = 0;
   if (lane == 0) {
     int hi = slot_base[P];
@@ -543,18 +553,59 @@ k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base
     }
   }
   lo = __shfl_sync(0xffffffffu, lo, 0);
-  if (p >= n) return;
-  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  const bool valid = p < n;
+  const int64_t pc = valid ? p : n - 1;
+  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= pc) lo++;
   int s = 0;
   while (slot_base[s + 1] <= lo) s++;
   const Shard& S = shards[s];
   const int32_t m = lo - slot_base[s];
   const ModelParam& mp = mp_all[lo];
-  const int32_t q = (int32_t)(p - mp.off);
+  const int64_t* tick_g = S.s_tick;
+  const int64_t w0 = p0 + lane < n ? tick_g[p0 + lane] : INT64_MAX;
+  const int64_t w1 = p0 + 32 + lane < n ? tick_g[p0 + 32 + lane] : INT64_MAX;
+  const int32_t q = (int32_t)(pc - mp.off);
   const bool affine = mp.affine && S.kind == K_DEFERRED && S.gather == G_PREFIX;
-  const int32_t v = affine ? lean_chain_next_affine(S, mp, q)
-                           : rel32_ok(S, mp) ? lean_chain_next32(S, m, q)
-                                             : lean_chain_next(S, m, q);
+  // affine search state (absolute positions)
+  const int64_t a = mp.aff_a, b0 = mp.aff_b, dc = S.d_ctrl, dd = S.d_data, c1 = a + dd;
+  const int32_t mb = mp.max_batch, cnt = mp.cnt;
+  const int64_t off = mp.off;
+  const int64_t uq = valid ? w0 + c1 * q : 0;  // tick_p is this lane's w0
+  const int64_t T = uq + (mp.slo - a - b0 - dc);
+  const int32_t kmax = cnt - 2 < q + mb - 2 ? cnt - 2 : q + mb - 2;
+  const int64_t jend = off + (int64_t)kmax + 1;     // last candidate j (absolute)
+  const int64_t jw = jend < p0 + 63 ? jend : p0 + 63;  // last candidate in the window
+  int32_t jlo = (int32_t)(pc + 1 - p0), jhi = (int32_t)(jw - p0) + 1;  // [jlo, jhi)
+  if (!affine || !valid) jhi = jlo;
+#pragma unroll
+  for (int it = 0; it < 6; it++) {
+    const bool act = jlo < jhi;
+    const int mid = act ? (jlo + jhi) >> 1 : 0;
+    const int64_t v0 = __shfl_sync(0xffffffffu, w0, mid & 31);
+    const int64_t v1 = __shfl_sync(0xffffffffu, w1, mid & 31);
+    const int64_t t = mid < 32 ? v0 : v1;
+    if (act) {
+      if (t + c1 * (p0 + mid - off) >= T) jhi = mid;
+      else jlo = mid + 1;
+    }
+  }
+  if (!valid) return;
+  int32_t v;
+  if (affine) {
+    int64_t j = p0 + jlo;  // first j in the window with u_j >= T, or jw + 1
+    if (j > jw && jw < jend) {  // continue past the window
+      while (j <= jend && tick_g[j] + c1 * (j - off) < T) j++;
+    }
+    if (j <= jend) {  // closes at k = j - 1
+      const int64_t k = j - 1;
+      const int64_t OK = uq + (mp.slo - dc - b0 - c1);
+      v = tick_g[k] + c1 * (k - off) <= OK ? (int32_t)j : NX_UNSURE;
+    } else {
+      v = lean_chain_next_affine_tail(S, mp, q);
+    }
+  } else {
+    v = rel32_ok(S, mp) ? lean_chain_next32(S, m, q) : lean_chain_next(S, m, q);
+  }
   nxt[p] = v;
   close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
 }

@@ -266,6 +266,8 @@ SYM_HD int32_t lean_chain_next32(const Shard& S, int32_t m, int32_t q) {
 // the closing index.  The len == max_batch step (l_next = l(max_batch)) and
 // the last arrival keep the scalar form.  Equals lean_chain_next at every
 // position (tools/hostcheck).
+SYM_HD int32_t lean_chain_next_affine_tail(const Shard& S, const ModelParam& P, int32_t q);
+
 SYM_HD int32_t lean_chain_next_affine(const Shard& S, const ModelParam& P, int32_t q) {
   const int64_t* tick = S.s_tick + P.off;
   const int64_t a = P.aff_a, b0 = P.aff_b, dc = S.d_ctrl, dd = S.d_data;
@@ -279,8 +281,19 @@ SYM_HD int32_t lean_chain_next_affine(const Shard& S, const ModelParam& P, int32
   while (k <= kmax && tick[k + 1] + c1 * (k + 1) < T) k++;
   if (k <= kmax)  // closes at k
     return tick[k] + c1 * k <= OK ? P.off + k + 1 : NX_UNSURE;
-  // not closed below len = max_batch: every k up to kmax must be ok, then
-  // the step at k1 = min(cnt - 1, q + mb - 1) in the scalar form
+  return lean_chain_next_affine_tail(S, P, q);
+}
+
+// The not-closed-below-max_batch tail of lean_chain_next_affine: every k up
+// to kmax must be ok, then the step at k1 = min(cnt - 1, q + mb - 1) in the
+// scalar form (l_next = l(max_batch) at the cap).
+SYM_HD int32_t lean_chain_next_affine_tail(const Shard& S, const ModelParam& P, int32_t q) {
+  const int64_t* tick = S.s_tick + P.off;
+  const int64_t a = P.aff_a, b0 = P.aff_b, dc = S.d_ctrl, dd = S.d_data;
+  const int64_t c1 = a + dd;
+  const int32_t mb = P.max_batch, cnt = P.cnt;
+  const int64_t OK = tick[q] + c1 * q + (P.slo - dc - b0 - c1);
+  const int32_t kmax = cnt - 2 < q + mb - 2 ? cnt - 2 : q + mb - 2;
   const int32_t k1 = kmax + 1;
   if (k1 - q + 1 > mb) return NX_UNSURE;
   const int64_t now = tick[k1];
