@@ -19,3 +19,17 @@ for _ in range(steps):
     out, cnt = eng.run_device(t, m)
 torch.cuda.synchronize()
 print(len(ticks), cnt["ms_total"])
+if len(sys.argv) > 2 and sys.argv[2] == "ktimes":
+    eng.kernel_times(reset=True)
+    reps = 20
+    tot = 0.0
+    for _ in range(reps):
+        out, cnt = eng.run_device(t, m, kernel_times=True)
+        tot += cnt["ms_total"]
+    kt = eng.kernel_times()
+    ksum = sum(v[1] for v in kt.values()) / reps
+    print(f"ms_total {tot / reps:.3f}  kernel sum {ksum:.3f}  launches/step "
+          f"{sum(v[0] for v in kt.values()) / reps:.0f}")
+    for _ in range(3):
+        out, cnt = eng.run_device(t, m)
+        print("plain ms_total", round(cnt["ms_total"], 3), {k: round(v, 3) for k, v in cnt.items() if k.startswith("ms_")})
