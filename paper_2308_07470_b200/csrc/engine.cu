@@ -1,16 +1,16 @@
 // engine.cu -- B200 (sm_100a) kernels and the C ABI of include/symphony_b200.h.
 //
 // Pipeline of one run (all on the engine's stream, inputs resident in HBM):
-//   K1a k_hist      per-warp-chunk histograms of (slot, shard) of the stream
+//   K1a k_hist      per-block-chunk histograms of (slot, shard) of the stream
 //   K1b k_scan_*    flat exclusive scan of the bin-major histogram -> stable bases
 //   K1c k_binoff    per-model ModelParam.off/cnt, shard offsets
 //   K1d k_scatter   stable scatter to the (shard, model)-sorted layout with
-//                   warp __match_any_sync ranking (one warp per chunk keeps
+//                   warp __match_any_sync ranking (per-warp offsets keep
 //                   stream order without any global atomics)
 //   K1e k_aself     canonical A' of every arrival (same-tick cascades)
-//   K2  k_fresh     fresh-start pre-scan: thread per sorted position
+//   K2  k_fresh     fresh-start pre-scan (chain fallback only)
+//   K3  k_nxt_pp ... k_fast_emit  the parallel validated path (fastpath.cuh)
 //   K4  k_chain     one CTA per sub-cluster runs the live-event chain
-//   K3  k_nxt ... k_fast_emit  the parallel validated path (fastpath.cuh)
 //   K5  k_bid / k_out  per-request RunResult arrays from batch records
 // The chain (engine_core.cuh) is the only sequential part; everything else is
 // a bandwidth-bound pass over the request stream.
@@ -93,7 +93,7 @@ struct Ctx {
   EvBatch* d_evb = nullptr;
   uint64_t *d_bkA = nullptr, *d_bkB = nullptr, *d_tkA = nullptr, *d_tkB = nullptr;
   uint32_t *d_bvA = nullptr, *d_bvB = nullptr, *d_tvA = nullptr, *d_tvB = nullptr;
-  int32_t *d_ptrA = nullptr, *d_ptrB = nullptr, *d_rhist = nullptr;
+  int32_t *d_ptrA = nullptr, *d_rhist = nullptr;
   int32_t *d_nb = nullptr, *d_bbase = nullptr, *d_changed = nullptr;
   int64_t *d_mdrops = nullptr, *d_sbase = nullptr;
   uint32_t* d_fail = nullptr;
@@ -456,73 +456,6 @@ __global__ void k_aself(const int64_t* __restrict__ s_tick,
 // K2' (fast path): the batch-chain pointer of every position by the lean
 // monotone sweep (fastpath.cuh), one thread per 32 consecutive positions;
 // close_k[p] keeps the closing arrival of certified starts for k_chain_recs.
-constexpr int kSweep = 32;          // positions per lane
-constexpr int kSweepWarps = 4;      // warps per block
-constexpr int kSweepMargin = 512;   // ticks staged past a warp's range
-constexpr int kSweepSpan = 32 * kSweep;  // positions per warp
-constexpr int kSweepWin = kSweepSpan + kSweepMargin;
-
-__host__ __device__ constexpr size_t nxt_smem_per_warp() {
-  return sizeof(int64_t) * kSweepWin + 2 * sizeof(int32_t) * kSweepSpan;
-}
-
-// A warp covers kSweepSpan consecutive sorted positions (lane l the l-th run
-// of kSweep).  Its tick window is staged once with coalesced loads, every
-// lane sweeps out of shared memory (global only beyond the margin), and the
-// pointers are staged and written back coalesced.
-__global__ void __launch_bounds__(32 * kSweepWarps)
-k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
-      const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
-      const int64_t* __restrict__ s_tick, int32_t* __restrict__ nxt,
-      int32_t* __restrict__ close_k) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t wbase = ((int64_t)blockIdx.x * kSweepWarps + wib) * kSweepSpan;
-  if (wbase >= n) return;
-  unsigned char* mine = smem_raw + wib * nxt_smem_per_warp();
-  int64_t* win = reinterpret_cast<int64_t*>(mine);
-  int32_t* o_nx = reinterpret_cast<int32_t*>(win + kSweepWin);
-  int32_t* o_ck = o_nx + kSweepSpan;
-  const int64_t wend = wbase + kSweepWin < n ? wbase + kSweepWin : n;
-  for (int64_t g = wbase + lane; g < wend; g += 32) win[g - wbase] = s_tick[g];
-  __syncwarp();
-  const int64_t p0 = wbase + (int64_t)lane * kSweep;
-  if (p0 < n) {
-    const int64_t p1 = p0 + kSweep < n ? p0 + kSweep : n;
-    int lo = 0, hi = slot_base[P];
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (mp_all[mid].off <= p0) lo = mid; else hi = mid;
-    }
-    int s = 0;
-    int64_t p = p0;
-    while (p < p1) {  // the range may cross model (and shard) boundaries
-      while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
-      while (slot_base[s + 1] <= lo) s++;
-      const ModelParam& mp = mp_all[lo];
-      const int64_t off = mp.off;
-      const int64_t end = off + mp.cnt < p1 ? off + mp.cnt : p1;
-      lean_chain_sweep(
-          shards[s], lo - slot_base[s], (int32_t)(p - off), (int32_t)(end - off),
-          [&](int32_t q, int32_t v, int32_t k) {
-            o_nx[off + q - wbase] = v;
-            o_ck[off + q - wbase] = k;
-          },
-          [&](int32_t k) {
-            const int64_t gpos = off + k;
-            return gpos < wend ? win[gpos - wbase] : s_tick[gpos];
-          });
-      p = end;
-    }
-  }
-  __syncwarp();
-  const int64_t oend = wbase + kSweepSpan < n ? wbase + kSweepSpan : n;
-  for (int64_t g = wbase + lane; g < oend; g += 32) {
-    nxt[g] = o_nx[g - wbase];
-    close_k[g] = o_ck[g - wbase];
-  }
-}
-
 // One lane per sorted position (lanes in lock step on neighbouring ticks);
 // close_k = the closing arrival for k_chain_recs.
 //
@@ -1170,7 +1103,7 @@ k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bv
              int64_t nt, const int64_t* __restrict__ sbase,
              const Shard* __restrict__ shards, const uint64_t* __restrict__ tkeys,
              uint32_t* __restrict__ tvals, int32_t* __restrict__ ptrA,
-             int32_t* __restrict__ ptrB, int32_t* __restrict__ flags, int tb) {
+             int32_t* __restrict__ flags, int tb) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1429,7 +1362,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_tkA, c)) || (rc = grow(ctx, ctx->d_tkB, c)) ||
         (rc = grow(ctx, ctx->d_bvA, c)) || (rc = grow(ctx, ctx->d_bvB, c)) ||
         (rc = grow(ctx, ctx->d_tvA, c)) || (rc = grow(ctx, ctx->d_tvB, c)) ||
-        (rc = grow(ctx, ctx->d_ptrA, c)) || (rc = grow(ctx, ctx->d_ptrB, c)) ||
+        (rc = grow(ctx, ctx->d_ptrA, c)) ||
         (rc = grow(ctx, ctx->d_rhist, ((c + kChunkR - 1) / kChunkR + 1) * kDigits)) ||
         (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
         (rc = grow(ctx, ctx->d_closek, c)) ||
@@ -1722,8 +1655,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         int64_t a_nt = nt;
         int a_tb = tick_bits;
         void* args[] = {&ctx->d_bkA, &ctx->d_bvA, &a_nt, &ctx->d_sbase, &ctx->d_shards,
-                        &ctx->d_tkA, &ctx->d_tvA, &ctx->d_ptrA, &ctx->d_ptrB,
-                        &ctx->d_changed, &a_tb};
+                        &ctx->d_tkA, &ctx->d_tvA, &ctx->d_ptrA, &ctx->d_changed, &a_tb};
         kt.begin("k_match_coop");
         ++launches;
         CK(cudaLaunchCooperativeKernel((void*)k_match_coop, grid, dim3(256), args, 0, st));
@@ -2157,9 +2089,6 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     if ((e = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ctx->chain_smem)) != cudaSuccess)
       return fail("smem attribute", e);
-    if ((e = cudaFuncSetAttribute(k_nxt, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kSweepWarps * nxt_smem_per_warp()))) != cudaSuccess)
-      return fail("sweep smem attribute", e);
     const size_t sc = scatter_smem(ctx->M + ctx->P);
     if (sc > (size_t)dev_max) return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
     if ((e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2186,7 +2115,7 @@ void sym_destroy(void* engine) {
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
                   ctx->d_bvA, ctx->d_bvB, ctx->d_tvA, ctx->d_tvB, ctx->d_ptrA,
-                  ctx->d_ptrB, ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
+                  ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
                   ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_cp_pos,
                   ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
