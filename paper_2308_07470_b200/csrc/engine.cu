@@ -998,10 +998,18 @@ k_rhist(const uint64_t* __restrict__ keys, int64_t n, int shift,
   const int64_t w = (int64_t)blockIdx.x * kRadixWarps + wib;
   for (int b = lane; b < kDigits; b += 32) cnt[wib][b] = 0;
   __syncwarp();
-  if (w < W) {
+  if (w < W) {  // all of the lane's keys in flight at once, then count
+    constexpr int R = kChunkR / 32;
     const int64_t lo = w * kChunkR, hi = (lo + kChunkR < n ? lo + kChunkR : n);
-    for (int64_t i = lo + lane; i < hi; i += 32)
-      atomicAdd(&cnt[wib][(keys[i] >> shift) & (kDigits - 1)], 1);
+    uint64_t k[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t i = lo + r * 32 + lane;
+      k[r] = i < hi ? keys[i] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++)
+      if (lo + r * 32 + lane < hi) atomicAdd(&cnt[wib][(k[r] >> shift) & (kDigits - 1)], 1);
   }
   __syncwarp();
   if (w < W)
@@ -1022,26 +1030,29 @@ k_rscatter(const uint64_t* __restrict__ kin,
   __syncwarp();
   const unsigned lt = (1u << lane) - 1u;
   const int64_t lo = w * kChunkR, hi = (lo + kChunkR < n ? lo + kChunkR : n);
-  for (int64_t i0 = lo; i0 < hi; i0 += 32) {
-    const int64_t i = i0 + lane;
-    const bool act = i < hi;
-    const unsigned amask = __ballot_sync(0xffffffffu, act);
-    uint64_t k = 0;
-    uint32_t v = 0;
-    int32_t dg = -1 - lane;
-    if (act) {
-      k = kin[i];
-      v = vin[i];
-      dg = (int32_t)((k >> shift) & (kDigits - 1));
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, dg) & amask;
+  // all of the lane's keys and values in flight at once (the pass is
+  // latency-bound: few warps per SM for ~10^6 keys), then rank round by round
+  constexpr int R = kChunkR / 32;
+  uint64_t k[R];
+  uint32_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const int64_t i = lo + r * 32 + lane;
+    k[r] = i < hi ? kin[i] : 0;
+    v[r] = i < hi ? vin[i] : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const bool act = lo + r * 32 + lane < hi;
+    const int32_t dg = act ? (int32_t)((k[r] >> shift) & (kDigits - 1)) : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
     int32_t pos = 0;
     if (act) pos = base[dg] + __popc(peers & lt);
     __syncwarp();
     if (act) {
       if ((peers >> lane) == 1u) base[dg] += __popc(peers);
-      kout[pos] = k;
-      vout[pos] = v;
+      kout[pos] = k[r];
+      vout[pos] = v[r];
     }
     __syncwarp();
   }
