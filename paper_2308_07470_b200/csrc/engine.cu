@@ -1059,6 +1059,100 @@ k_rscatter(const uint64_t* __restrict__ kin,
 }
 
 // K3d: order runs of equal (shard, tick) by the full event key
+// Batch order by merging instead of radix sorting.  k_batch_keys lays the
+// batches out as one run per model, each already in event order (a model's
+// chain), so the global order is a merge of M sorted runs: ceil(log2 M)
+// rounds of stable pairwise merge path.  Round r merges the runs of models
+// [2^(r+1) p, 2^(r+1) p + 2^r) and [.. + 2^r, 2^(r+1) (p+1)).  The key is
+// (shard << tb | tick); equal keys fall back to the full batch_cmp order
+// (A', pusher position, chain before arrival), so no fix-up pass is needed.
+constexpr int kMergeItems = 8;  // outputs per thread
+
+__device__ __forceinline__ int64_t run_bound(const int32_t* __restrict__ bbase, int32_t M,
+                                             int64_t nt, int64_t m) {
+  return m < M ? bbase[m] : nt;
+}
+
+// x strictly before y in batch order
+__device__ __forceinline__ bool batch_less(uint64_t kx, uint32_t vx, uint64_t ky, uint32_t vy,
+                                           const EvBatch* __restrict__ evb) {
+  if (kx != ky) return kx < ky;
+  return batch_cmp(evb[vx], evb[vy]) < 0;
+}
+
+__global__ void __launch_bounds__(256)
+k_merge_round(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+              uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t nt,
+              const int32_t* __restrict__ bbase, int32_t M, int round,
+              const EvBatch* __restrict__ evb) {
+  const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergeItems;
+  if (k0 >= nt) return;
+  const int64_t span = int64_t(1) << (round + 1), half = span >> 1;
+  // the pair containing output k0: last p with bound(p * span) <= k0
+  int64_t lo = 0, hi = (M + span - 1) / span;  // pairs [lo, hi)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (run_bound(bbase, M, nt, mid * span) <= k0) lo = mid; else hi = mid;
+  }
+  const int64_t a0 = run_bound(bbase, M, nt, lo * span);
+  const int64_t a1 = run_bound(bbase, M, nt, lo * span + half);
+  const int64_t b1 = run_bound(bbase, M, nt, (lo + 1) * span);
+  const int64_t la = a1 - a0, lb = b1 - a1;
+  const int64_t diag = k0 - a0;
+  // merge path: i = elements of A among the first diag outputs (A first on ties)
+  int64_t i_lo = diag > lb ? diag - lb : 0, i_hi = diag < la ? diag : la;
+  while (i_lo < i_hi) {
+    const int64_t mid = (i_lo + i_hi) >> 1;
+    const int64_t j = diag - 1 - mid;
+    if (batch_less(kin[a1 + j], vin[a1 + j], kin[a0 + mid], vin[a0 + mid], evb))
+      i_hi = mid;
+    else
+      i_lo = mid + 1;
+  }
+  int64_t ia = a0 + i_lo, ib = a1 + (diag - i_lo);
+  const int64_t kend = k0 + kMergeItems < b1 ? k0 + kMergeItems : b1;
+  for (int64_t k = k0; k < kend; k++) {
+    bool take_a;
+    if (ia >= a1) take_a = false;
+    else if (ib >= b1) take_a = true;
+    else take_a = !batch_less(kin[ib], vin[ib], kin[ia], vin[ia], evb);
+    const int64_t src = take_a ? ia++ : ib++;
+    kout[k] = kin[src];
+    vout[k] = vin[src];
+  }
+  // outputs beyond this pair in the same thread chunk belong to the next
+  // pair(s): handled by walking on with fresh searches
+  for (int64_t k = kend; k < k0 + kMergeItems && k < nt;) {
+    int64_t p2 = lo + 1;
+    while (run_bound(bbase, M, nt, (p2 + 1) * span) <= k) p2++;
+    const int64_t c0 = run_bound(bbase, M, nt, p2 * span);
+    const int64_t c1 = run_bound(bbase, M, nt, p2 * span + half);
+    const int64_t d1 = run_bound(bbase, M, nt, (p2 + 1) * span);
+    const int64_t lc = c1 - c0, ld = d1 - c1, dg = k - c0;
+    int64_t x_lo = dg > ld ? dg - ld : 0, x_hi = dg < lc ? dg : lc;
+    while (x_lo < x_hi) {
+      const int64_t mid = (x_lo + x_hi) >> 1;
+      const int64_t j = dg - 1 - mid;
+      if (batch_less(kin[c1 + j], vin[c1 + j], kin[c0 + mid], vin[c0 + mid], evb))
+        x_hi = mid;
+      else
+        x_lo = mid + 1;
+    }
+    int64_t xa = c0 + x_lo, xb = c1 + (dg - x_lo);
+    const int64_t e2 = k0 + kMergeItems < d1 ? k0 + kMergeItems : d1;
+    for (; k < e2 && k < nt; k++) {
+      bool take_a;
+      if (xa >= c1) take_a = false;
+      else if (xb >= d1) take_a = true;
+      else take_a = !batch_less(kin[xb], vin[xb], kin[xa], vin[xa], evb);
+      const int64_t src = take_a ? xa++ : xb++;
+      kout[k] = kin[src];
+      vout[k] = vin[src];
+    }
+    lo = p2;
+  }
+}
+
 __global__ void k_runfix(const uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
                          int64_t nt, const EvBatch* __restrict__ evb,
                          uint32_t* __restrict__ fail, int tb) {
@@ -1094,6 +1188,9 @@ __global__ void k_token_keys(const uint32_t* __restrict__ bvals, int64_t nt,
   if (i >= nt) return;
   const int s = (int)(bkeys[i] >> tb);
   const EvBatch& e = evb[bvals[i]];
+  // two batches whose keys tie up to the chain counter: order undecidable
+  if (i + 1 < nt && bkeys[i + 1] == bkeys[i] && batch_cmp(e, evb[bvals[i + 1]]) == 0)
+    atomicOr(&fail[s], FP_KEY_TIE);
   const int64_t fin = e.exec + e.lat;
   if (fin < 0 || fin >= (int64_t(1) << tb)) atomicOr(&fail[s], FP_CAPACITY);
   tkeys[i] = ((uint64_t)s << tb) | (uint64_t)(fin & ((int64_t(1) << tb) - 1));
@@ -1646,10 +1743,14 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         }
       };
   pc.mark("batch_keys");
-      radix(ctx->d_bkA, ctx->d_bvA, ctx->d_bkB, ctx->d_bvB);
+      for (int round = 0; (int64_t(1) << round) < M; round++) {
+        KL(k_merge_round, nblk((nt + kMergeItems - 1) / kMergeItems, 256), 256, 0, st>>>(
+            ctx->d_bkA, ctx->d_bvA, ctx->d_bkB, ctx->d_bvB, nt, ctx->d_bbase, M, round,
+            ctx->d_evb));
+        std::swap(ctx->d_bkA, ctx->d_bkB);
+        std::swap(ctx->d_bvA, ctx->d_bvB);
+      }
   pc.mark("sort_batches");
-      KL(k_runfix, nblk(nt, 256), 256, 0, st>>>(ctx->d_bkA, ctx->d_bvA, nt,
-                                                          ctx->d_evb, ctx->d_fail, tick_bits));
       KL(k_token_keys, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_bvA, nt, ctx->d_bkA, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
           ctx->d_fail, tick_bits));
