@@ -106,6 +106,7 @@ struct Ctx {
   sym_batch* d_bat = nullptr;
   int64_t stage_cap = 0, bat_cap = 0;
   int32_t* d_closek = nullptr;      // closing arrival of lean-certified starts
+  int32_t *d_jC = nullptr;          // J_64 kept while J_256 is built
   int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
           *d_cp_model = nullptr, *d_special = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
@@ -810,16 +811,18 @@ k_evolve(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base
 // K3a' (parallel unconstrained evolution).  J1 = the chain pointer where it
 // continues; J_{2k}[p] = J_k[J_k[p]]: the position 2k batches after p, or -1
 // if the chain ends (or needs the sequential path) within 2k batches.
-__global__ void k_double(const int32_t* __restrict__ jin, int32_t* __restrict__ jout,
-                         int64_t n, int first) {
+// J_{4k} = (J_k)^4 in one pass: three gathers that stay near p (chains move
+// forward by ~a batch per hop), so four doublings' worth of pointer chasing
+// costs one read, three L2-local gathers and one write per position.
+// first: jin is the raw chain pointer (NX_* sentinels -> -1).
+__global__ void k_jump4(const int32_t* __restrict__ jin, int32_t* __restrict__ jout,
+                        int64_t n) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   int32_t v = jin[p];
-  if (first) {
-    jout[p] = v >= 0 ? v : -1;
-    return;
-  }
-  jout[p] = v >= 0 ? jin[v] : -1;
+#pragma unroll
+  for (int h = 0; h < 3; h++) v = v >= 0 ? jin[v] : -1;
+  jout[p] = v >= 0 ? v : -1;
 }
 
 constexpr int kJump = 64;  // batches per checkpoint (J_64)
@@ -828,8 +831,17 @@ constexpr int kJump = 64;  // batches per checkpoint (J_64)
 // recording a checkpoint every 64 batches; then count the tail with the
 // single-step pointers.  Models whose chain meets NX_SPECIAL are left to
 // the sequential k_evolve (special[k] = 1).
+// One thread per model walks its batch chain: J_256 hops (coarse
+// checkpoints, every 4th checkpoint slot), then J_64 hops, then the < 64
+// remaining batches one by one (counting them and spotting a special
+// model).  The three checkpoints between two coarse ones are filled in
+// parallel by k_walk_fill.  A coarse slot that has a successor is marked by
+// cp_model = -2 - k until filled.
+constexpr int kCoarse = 4;  // checkpoints per J_256 hop
+
 __global__ void k_walk(const ModelParam* __restrict__ mp_all, int32_t M,
                        const int32_t* __restrict__ nxt, const int32_t* __restrict__ j64,
+                       const int32_t* __restrict__ j256,
                        int32_t* __restrict__ cp_pos, int32_t* __restrict__ cp_model,
                        int32_t* __restrict__ nb, int32_t* __restrict__ special) {
   const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -839,6 +851,12 @@ __global__ void k_walk(const ModelParam* __restrict__ mp_all, int32_t M,
   if (mp.cnt > 0) {
     const int64_t cbase = mp.off / kJump + k;  // disjoint per-model slots
     int32_t p = mp.off, c = 0;
+    for (int32_t q = j256[p]; q >= 0; q = j256[p]) {
+      cp_pos[cbase + c] = p;
+      cp_model[cbase + c] = -2 - k;  // k_walk_fill completes slots c+1..c+3
+      c += kCoarse;
+      p = q;
+    }
     while (j64[p] >= 0) {
       cp_pos[cbase + c] = p;
       cp_model[cbase + c] = k;
@@ -862,6 +880,22 @@ __global__ void k_walk(const ModelParam* __restrict__ mp_all, int32_t M,
   }
   nb[k] = sp ? 0 : count;
   special[k] = sp;
+}
+
+__global__ void k_walk_fill(int32_t* __restrict__ cp_pos, int32_t* __restrict__ cp_model,
+                            int64_t ncp, const int32_t* __restrict__ j64) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= ncp) return;
+  const int32_t tag = cp_model[q];
+  if (tag > -2) return;  // not a coarse slot with a successor
+  const int32_t k = -2 - tag;
+  int32_t p = cp_pos[q];
+  cp_model[q] = k;
+  for (int h = 1; h < kCoarse; h++) {
+    p = j64[p];
+    cp_pos[q + h] = p;
+    cp_model[q + h] = k;
+  }
 }
 
 // One thread per checkpoint: materialise up to 64 batches (EvBatch) from
@@ -1474,7 +1508,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_rhist, ((c + kChunkR - 1) / kChunkR + 1) * kDigits)) ||
         (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
         (rc = grow(ctx, ctx->d_closek, c)) ||
-        (rc = grow(ctx, ctx->d_jB, c)) ||
+        (rc = grow(ctx, ctx->d_jB, c)) || (rc = grow(ctx, ctx->d_jC, c)) ||
         (rc = grow(ctx, ctx->d_cp_pos, c / kJump + ctx->M + 2)) ||
         (rc = grow(ctx, ctx->d_cp_model, c / kJump + ctx->M + 2)))
       return rc;
@@ -1696,15 +1730,16 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     CK(cudaMemsetAsync(ctx->d_mdrops, 0, sizeof(int64_t) * M, st));
     const int64_t ncp = n / kJump + M + 2;
     CK(cudaMemsetAsync(ctx->d_cp_model, 0xff, sizeof(int32_t) * ncp, st));
-    // J_64 by six doublings of the chain pointer
-    KL(k_double, nblk(n, 256), 256, 0, st>>>(ctx->d_nxt, ctx->d_jA, n, 1));
-    for (int d = 0; d < 6; d++) {
-      KL(k_double, nblk(n, 256), 256, 0, st>>>(ctx->d_jA, ctx->d_jB, n, 0));
-      std::swap(ctx->d_jA, ctx->d_jB);
-    }
-    KL(k_walk, nblk(M, 64), 64, 0, st>>>(ctx->d_mp, M, ctx->d_nxt, ctx->d_jA,
-                                                   ctx->d_cp_pos, ctx->d_cp_model, ctx->d_nb,
-                                                   ctx->d_special));
+    // J_4, J_16, J_64 (kept in jC), J_256 by quadrupling the chain pointer
+    KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_nxt, ctx->d_jA, n));
+    KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jA, ctx->d_jB, n));
+    KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jB, ctx->d_jC, n));
+    KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jC, ctx->d_jA, n));
+    KL(k_walk, nblk(M, 64), 64, 0, st>>>(ctx->d_mp, M, ctx->d_nxt, ctx->d_jC, ctx->d_jA,
+                                         ctx->d_cp_pos, ctx->d_cp_model, ctx->d_nb,
+                                         ctx->d_special));
+    KL(k_walk_fill, nblk(ncp, 256), 256, 0, st>>>(ctx->d_cp_pos, ctx->d_cp_model, ncp,
+                                                 ctx->d_jC));
     KL(k_walk_expand, nblk(ncp, 128), 128, 0, st>>>(
         ctx->d_cp_pos, ctx->d_cp_model, ncp, ctx->d_mp, ctx->d_slot_base, P, ctx->d_nxt,
         ctx->d_special, ctx->d_shards, ctx->d_evb, (unsigned long long*)ctx->d_mdrops));
@@ -2229,7 +2264,7 @@ void sym_destroy(void* engine) {
                   ctx->d_bvA, ctx->d_bvB, ctx->d_tvA, ctx->d_tvB, ctx->d_ptrA,
                   ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
-                  ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_cp_pos,
+                  ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_jC, ctx->d_cp_pos,
                   ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
                   ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
                   ctx->d_net_vals, ctx->d_net_cdf};
