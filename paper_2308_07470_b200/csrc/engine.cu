@@ -1187,28 +1187,6 @@ k_merge_round(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin
   }
 }
 
-__global__ void k_runfix(const uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                         int64_t nt, const EvBatch* __restrict__ evb,
-                         uint32_t* __restrict__ fail, int tb) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nt) return;
-  if (i > 0 && keys[i - 1] == keys[i]) return;        // not a run start
-  if (i + 1 >= nt || keys[i + 1] != keys[i]) return;  // singleton
-  int64_t e = i + 1;
-  while (e < nt && keys[e] == keys[i]) e++;
-  for (int64_t a = i + 1; a < e; a++) {  // insertion sort, runs are tiny
-    const uint32_t v = vals[a];
-    int64_t b = a;
-    while (b > i && batch_cmp(evb[v], evb[vals[b - 1]]) < 0) {
-      vals[b] = vals[b - 1];
-      b--;
-    }
-    vals[b] = v;
-  }
-  for (int64_t a = i + 1; a < e; a++)
-    if (batch_cmp(evb[vals[a - 1]], evb[vals[a]]) == 0)
-      atomicOr(&fail[keys[i] >> tb], FP_KEY_TIE);
-}
 
 // K3e: finish-time token of every sorted batch: key (shard|finish),
 // value = the batch's rank within its shard
