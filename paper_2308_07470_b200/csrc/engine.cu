@@ -838,10 +838,11 @@ constexpr int kJump = 64;  // batches per checkpoint (J_64)
 // parallel by k_walk_fill.  A coarse slot that has a successor is marked by
 // cp_model = -2 - k until filled.
 constexpr int kCoarse = 4;  // checkpoints per J_256 hop
+constexpr int kSub = 16;    // batches per k_walk_expand thread (J_16)
 
 __global__ void k_walk(const ModelParam* __restrict__ mp_all, int32_t M,
-                       const int32_t* __restrict__ nxt, const int32_t* __restrict__ j64,
-                       const int32_t* __restrict__ j256,
+                       const int32_t* __restrict__ nxt, const int32_t* __restrict__ j16,
+                       const int32_t* __restrict__ j64, const int32_t* __restrict__ j256,
                        int32_t* __restrict__ cp_pos, int32_t* __restrict__ cp_model,
                        int32_t* __restrict__ nb, int32_t* __restrict__ special) {
   const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -866,7 +867,11 @@ __global__ void k_walk(const ModelParam* __restrict__ mp_all, int32_t M,
     cp_pos[cbase + c] = p;
     cp_model[cbase + c] = k;
     count = c * kJump;
-    for (;;) {  // tail: < 64 batches
+    for (int32_t q = j16[p]; q >= 0; q = j16[p]) {  // < 64 left: J_16 hops
+      count += kSub;
+      p = q;
+    }
+    for (;;) {  // tail: < 16 batches
       const int32_t v = nxt[p];
       if (v == NX_SPECIAL) {
         sp = 1;
@@ -900,16 +905,22 @@ __global__ void k_walk_fill(int32_t* __restrict__ cp_pos, int32_t* __restrict__ 
 
 // One thread per checkpoint: materialise up to 64 batches (EvBatch) from
 // the fresh-start records along the chain, and add their drops.
+// One thread per kSub batches of a checkpoint (4 threads per J_64
+// checkpoint, started by J_16 hops): lists the batch starts in chain order.
 __global__ void k_walk_expand(const int32_t* __restrict__ cp_pos,
                               const int32_t* __restrict__ cp_model, int64_t ncp,
                               const ModelParam* __restrict__ mp_all,
                               const int32_t* __restrict__ slot_base, int32_t P,
                               const int32_t* __restrict__ nxt,
+                              const int32_t* __restrict__ j16,
                               const int32_t* __restrict__ special,
                               const Shard* __restrict__ shards,
                               EvBatch* __restrict__ evb,
                               unsigned long long* __restrict__ mdrops) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int kPer = kJump / kSub;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t q = t / kPer;
+  const int sub = (int)(t % kPer);
   if (q >= ncp) return;
   const int32_t k = cp_model[q];
   if (k < 0 || special[k]) return;
@@ -917,8 +928,10 @@ __global__ void k_walk_expand(const int32_t* __restrict__ cp_pos,
   const int64_t c = q - (mp.off / kJump + k);  // checkpoint ordinal
   const int s = shard_of_slot(slot_base, P, k);
   int32_t p = cp_pos[q];
-  int64_t out = mp.off + c * kJump;
-  for (int j = 0; j < kJump && p >= 0; j++) {
+  for (int h = 0; h < sub && p >= 0; h++) p = j16[p];
+  if (p < 0) return;  // the chain ends before this thread's batches
+  int64_t out = mp.off + c * kJump + sub * kSub;
+  for (int j = 0; j < kSub && p >= 0; j++) {
     const int32_t v = nxt[p];
     if (v == NX_NONE) {  // trailing all-dropped scan: count its drops
       const FreshRec r = fresh_scan(shards[s], k - slot_base[s], p - mp.off, kFreshMaxSteps);
@@ -1713,14 +1726,16 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jA, ctx->d_jB, n));
     KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jB, ctx->d_jC, n));
     KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jC, ctx->d_jA, n));
-    KL(k_walk, nblk(M, 64), 64, 0, st>>>(ctx->d_mp, M, ctx->d_nxt, ctx->d_jC, ctx->d_jA,
+    KL(k_walk, nblk(M, 64), 64, 0, st>>>(ctx->d_mp, M, ctx->d_nxt, ctx->d_jB, ctx->d_jC,
+                                         ctx->d_jA,
                                          ctx->d_cp_pos, ctx->d_cp_model, ctx->d_nb,
                                          ctx->d_special));
     KL(k_walk_fill, nblk(ncp, 256), 256, 0, st>>>(ctx->d_cp_pos, ctx->d_cp_model, ncp,
                                                  ctx->d_jC));
-    KL(k_walk_expand, nblk(ncp, 128), 128, 0, st>>>(
+    KL(k_walk_expand, nblk(ncp * (kJump / kSub), 128), 128, 0, st>>>(
         ctx->d_cp_pos, ctx->d_cp_model, ncp, ctx->d_mp, ctx->d_slot_base, P, ctx->d_nxt,
-        ctx->d_special, ctx->d_shards, ctx->d_evb, (unsigned long long*)ctx->d_mdrops));
+        ctx->d_jB, ctx->d_special, ctx->d_shards, ctx->d_evb,
+        (unsigned long long*)ctx->d_mdrops));
     // models whose chain needs the general (non-draining) evolution
     KL(k_evolve, nblk(M, 64), 64, 0, st>>>(ctx->d_shards, ctx->d_slot_base, P, M,
                                                      nullptr, ctx->d_evb, ctx->d_nb,
