@@ -107,6 +107,7 @@ struct Ctx {
   int64_t stage_cap = 0, bat_cap = 0;
   int32_t* d_closek = nullptr;      // closing arrival of lean-certified starts
   int32_t *d_jC = nullptr;          // J_64 kept while J_256 is built
+  int32_t *d_s_slot = nullptr;      // [n] model slot of each sorted position
   int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
           *d_cp_model = nullptr, *d_special = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
@@ -308,7 +309,7 @@ k_scatter(const int64_t* __restrict__ ticks,
           int32_t* __restrict__ s_g,
           int32_t* __restrict__ s_i,
           int64_t* __restrict__ sh_tick,
-          int32_t* __restrict__ inv) {
+          int32_t* __restrict__ inv, int32_t* __restrict__ s_slot) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int B = M + P;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -431,6 +432,7 @@ k_scatter(const int64_t* __restrict__ ticks,
     s_tick[pos] = st_t[e];
     s_g[pos] = st_g[e];
     s_i[pos] = st_i[e];
+    s_slot[pos] = b;
   }
 }
 
@@ -470,26 +472,15 @@ __global__ void k_aself(const int64_t* __restrict__ s_tick,
 __global__ void __launch_bounds__(256)
 k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
          const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
+         const int32_t* __restrict__ s_slot,
          int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int64_t p0 = p - lane;  // window base (warp-uniform)
   if (p0 >= n) return;          // whole warp out of range
-  // one model lookup per warp (its lanes are consecutive positions), then
-  // each lane steps forward to its own model
-  const int64_t p_lead = p0;
-  int lo = 0;
-  if (lane == 0) {
-    int hi = slot_base[P];
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (mp_all[mid].off <= p_lead) lo = mid; else hi = mid;
-    }
-  }
-  lo = __shfl_sync(0xffffffffu, lo, 0);
   const bool valid = p < n;
   const int64_t pc = valid ? p : n - 1;
-  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= pc) lo++;
+  const int lo = s_slot[pc];  // model slot of the position (k_scatter)
   int s = 0;
   while (slot_base[s + 1] <= lo) s++;
   const Shard& S = shards[s];
@@ -1012,15 +1003,11 @@ __global__ void k_batch_keys(const Shard* __restrict__ shards,
                              const int32_t* __restrict__ bbase,
                              const EvBatch* __restrict__ evb, int64_t n,
                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                             uint32_t* __restrict__ fail, int tb) {
+                             uint32_t* __restrict__ fail, int tb,
+                             const int32_t* __restrict__ s_slot) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  int lo = 0, hi = slot_base[P];
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
-  }
-  while (mp_all[lo].cnt == 0 || mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  const int lo = s_slot[p];
   const int32_t j = (int32_t)(p - mp_all[lo].off);
   if (j >= nb[lo]) return;
   const int s = shard_of_slot(slot_base, P, lo);
@@ -1500,6 +1487,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
         (rc = grow(ctx, ctx->d_closek, c)) ||
         (rc = grow(ctx, ctx->d_jB, c)) || (rc = grow(ctx, ctx->d_jC, c)) ||
+        (rc = grow(ctx, ctx->d_s_slot, c)) ||
         (rc = grow(ctx, ctx->d_cp_pos, c / kJump + ctx->M + 2)) ||
         (rc = grow(ctx, ctx->d_cp_model, c / kJump + ctx->M + 2)))
       return rc;
@@ -1658,7 +1646,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_scatter, W, 32 * kIngestWarps, scatter_smem(B), st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
-        ctx->d_sh_tick, ctx->d_inv));
+        ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot));
   if (n > 0)
     KL(k_aself, nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
                                           ctx->d_sh_tick, ctx->d_bins + B + 1,
@@ -1701,7 +1689,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   bool have_fresh = false;
   if (fast) {
     KL(k_nxt_pp, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, n,
-                                             ctx->d_nxt, ctx->d_closek));
+                                             ctx->d_s_slot, ctx->d_nxt, ctx->d_closek));
     KL(k_nxt_general, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp,
                                                   P, n, ctx->d_nxt, ctx->d_closek));
   } else if (use_fresh && n > 0) {
@@ -1754,7 +1742,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
           ctx->d_special, nt, ctx->d_evb, (unsigned long long*)ctx->d_mdrops, ctx->d_closek));
       KL(k_batch_keys, nblk(n, 256), 256, 0, st>>>(
           ctx->d_shards, ctx->d_slot_base, P, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
-          ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits));
+          ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits, ctx->d_s_slot));
       // key = (shard << tick_bits) | tick; only the bits in use are sorted
       int bits = tick_bits;
       while ((1 << (bits - tick_bits)) < P) bits++;
@@ -2257,7 +2245,8 @@ void sym_destroy(void* engine) {
                   ctx->d_bvA, ctx->d_bvB, ctx->d_tvA, ctx->d_tvB, ctx->d_ptrA,
                   ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
-                  ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_jC, ctx->d_cp_pos,
+                  ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_jC, ctx->d_s_slot,
+                  ctx->d_cp_pos,
                   ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
                   ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
                   ctx->d_net_vals, ctx->d_net_cdf};
