@@ -174,9 +174,10 @@ k_hist(const int32_t* __restrict__ model, const int64_t* __restrict__ ticks, int
         sd = M + shard_of_model[m];
       }
     }
-    const unsigned ps = __match_any_sync(0xffffffffu, sl);
+    // slot bins: ~M distinct addresses per round, plain shared atomics;
+    // shard bins: few addresses, aggregated per warp first
+    if (sl >= 0) atomicAdd(&cnt[sl], 1);
     const unsigned pd = __match_any_sync(0xffffffffu, sd);
-    if (sl >= 0 && (ps >> lane) == 1u) atomicAdd(&cnt[sl], __popc(ps));
     if (sl >= 0 && (pd >> lane) == 1u) atomicAdd(&cnt[sd], __popc(pd));
   }
   __syncthreads();
@@ -342,10 +343,9 @@ k_scatter(const int64_t* __restrict__ ticks,
       sd[r] = M + shard_of_model[m];
       t[r] = ticks[i];
     }
-    const unsigned ps = __match_any_sync(0xffffffffu, sl[r]);
+    if (sl[r] >= 0) atomicAdd_block(&mine[sl[r]], 1);  // counting only
     const unsigned pd = __match_any_sync(0xffffffffu, sd[r]);
-    if (sl[r] >= 0 && (ps >> lane) == 1u) mine[sl[r]] += __popc(ps);
-    if (sl[r] >= 0 && (pd >> lane) == 1u) mine[sd[r]] += __popc(pd);
+    if (sl[r] >= 0 && (pd >> lane) == 1u) atomicAdd_block(&mine[sd[r]], __popc(pd));
     __syncwarp();
   }
   // bases from the scanned histogram; per-warp offsets; local bin starts
