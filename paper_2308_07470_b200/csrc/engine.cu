@@ -441,9 +441,11 @@ __global__ void k_aself(const int64_t* __restrict__ s_tick,
                         const int32_t* __restrict__ s_g,
                         const int64_t* __restrict__ sh_tick,
                         const int32_t* __restrict__ shard_off, int32_t P,
-                        int64_t n, int32_t* __restrict__ s_aself) {
+                        int64_t n, int32_t* __restrict__ s_aself,
+                        int32_t* __restrict__ bid) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
+  bid[p] = -1;  // "no batch" until k_bid (saves a fill pass over n)
   const int32_t j = s_g[p];
   int lo = 0, hi = P;  // last s with shard_off[s] <= j
   while (hi - lo > 1) {
@@ -653,10 +655,6 @@ __global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __r
   out[i] = (v < 0 || v > INT32_MAX) ? -1 : (int32_t)v;  // out of range -> EPROTO
 }
 
-__global__ void k_fill32(int32_t* p, int64_t n, int32_t v) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
-}
 
 // every batch stamps its record index on its member positions
 __global__ void k_bid(const BatchRec* __restrict__ recs, const int64_t* __restrict__ rec_base,
@@ -1650,7 +1648,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   if (n > 0)
     KL(k_aself, nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
                                           ctx->d_sh_tick, ctx->d_bins + B + 1,
-                                          P, n, ctx->d_s_aself));
+                                          P, n, ctx->d_s_aself, ctx->d_bid));
   CK(cudaGetLastError());
   pc.mark("ingest");
   CK(cudaEventRecord(ctx->ev[1], st));
@@ -1896,7 +1894,6 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   }
   const bool expand = !(flags & SYM_FLAG_NO_EXPAND) && out->req_dispatch;
   if (expand && n > 0) {
-    KL(k_fill32, nblk(n, 256), 256, 0, st>>>(ctx->d_bid, n, -1));
     if (total > 0)
       KL(k_bid, nblk(total, 256), 256, 0, st>>>(ctx->d_recs, d_meta, d_meta + P + 1, P, total,
                                                 ctx->d_bid));
