@@ -45,3 +45,44 @@ def test_random_cases_engine_equals_oracle(chunk):
                     eng.handler_ops_max) == (ref["ops"], ref["evictions"],
                                              ref["registrations"], ref["handler_ops_max"]), seed
             eng.close()
+
+
+JSEEDS = list(range(3000, 3200))
+
+
+@pytest.mark.parametrize("chunk", range(8))
+def test_random_jittered_cases_engine_equals_oracle(chunk):
+    """The same generator with a random histogram network: per-dispatch
+    Philox draws, GPU serialisation and LATE outcomes (network.py:69-77,
+    simulator.py:54-62); planning bounds from the histograms' percentiles."""
+    import random
+    from dataclasses import replace
+    from oracle import oracle
+    from paper_2308_07470_b200.network import DelayDist, NetworkModel, jitter_tables
+    from paper_2308_07470_b200.simulator import Engine
+    for seed in JSEEDS[chunk::8]:
+        models, gpus, policy, ticks, midx = _case(seed)
+        rng = random.Random(seed)
+
+        def dist():
+            if rng.random() < 0.3:
+                return DelayDist.constant(rng.choice([0, 5_000, 300_000]))
+            k = rng.randint(1, 4)
+            return DelayDist.histogram([rng.randint(0, 3_000_000) for _ in range(k)],
+                                       [rng.uniform(0.01, 1.0) for _ in range(k)],
+                                       rng.choice([0.5, 0.7, 0.9]))
+        net = NetworkModel(dist(), dist())
+        if net.jitterless:
+            net = NetworkModel(DelayDist.histogram([0, 50_000, 2_000_000], [0.7, 0.2, 0.1]),
+                               net.d_data)
+        policy = replace(policy, d_ctrl_ns=net.plan_ctrl_ns, d_data_ns=net.plan_data_ns)
+        ref = oracle.run(arr_ticks=ticks, arr_midx=midx, net=jitter_tables(net, seed),
+                         **oracle_args(models, gpus, policy))
+        for use_fast in (True, False):
+            eng = Engine(models, gpus, policy, net, seed=seed, use_fast=use_fast)
+            res = eng.run_stream(ticks, midx, 1.0)
+            for k in OUT:
+                np.testing.assert_array_equal(getattr(res, k), ref[k],
+                                              err_msg=f"seed {seed} fast={use_fast} {k}")
+            assert res.late == ref["late"] and res.drops == ref["drops"], seed
+            eng.close()
