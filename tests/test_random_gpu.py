@@ -86,3 +86,40 @@ def test_random_jittered_cases_engine_equals_oracle(chunk):
                                               err_msg=f"seed {seed} fast={use_fast} {k}")
             assert res.late == ref["late"] and res.drops == ref["drops"], seed
             eng.close()
+
+
+@pytest.mark.parametrize("combo", range(40))
+def test_random_subclusters_in_one_call(combo):
+    """2-5 random cases as independent sub-clusters of ONE engine call (one
+    policy): each sub-cluster's results equal its own oracle run, whatever
+    the interleaving of the merged stream."""
+    import random
+    from oracle import oracle
+    from paper_2308_07470_b200.profile import ModelSpec
+    from paper_2308_07470_b200.simulator import Engine
+    rng = random.Random(combo)
+    parts = [_case(5000 + 10 * combo + k) for k in range(rng.randint(2, 5))]
+    policy = parts[0][2]
+    models, som, gps, ticks, midx = [], [], [], [], []
+    for s, (ms, g, _, t, m) in enumerate(parts):
+        base = len(models)
+        models += [ModelSpec(base + x.model_id, f"s{s}_{x.name}", x.profile, x.slo_ns) for x in ms]
+        som += [s] * len(ms)
+        gps.append(g)
+        ticks.append(np.asarray(t, np.int64))
+        midx.append(np.asarray(m, np.int64) + base)
+    t_all, m_all = np.concatenate(ticks), np.concatenate(midx)
+    order = np.argsort(t_all, kind="stable")
+    t_all, m_all = t_all[order], m_all[order]
+    eng = Engine(models, sum(gps), policy, shards=(som, gps))
+    res = eng.run_stream(t_all, m_all, 1.0)
+    lo = 0
+    for s, (ms, g, _, _, _) in enumerate(parts):
+        sel = np.nonzero((m_all >= lo) & (m_all < lo + len(ms)))[0]
+        ref = oracle.run(arr_ticks=t_all[sel], arr_midx=m_all[sel] - lo,
+                         **oracle_args(list(ms), g, policy))
+        for k in OUT:
+            np.testing.assert_array_equal(getattr(res, k)[sel], ref[k],
+                                          err_msg=f"combo {combo} shard {s} {k}")
+        lo += len(ms)
+    eng.close()
