@@ -1977,6 +1977,18 @@ extern "C" {
 
 int32_t sym_version(void) { return kVersion; }
 
+#ifdef SYM_CHAIN_PROF
+// dev build only (tools/chain_prof.py): read and clear the chain counters
+int32_t sym_chain_prof(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, sym::g_chain_prof, sizeof(unsigned long long) * 16) !=
+      cudaSuccess)
+    return SYM_ECUDA;
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(sym::g_chain_prof, z, sizeof z);
+  return SYM_OK;
+}
+#endif
+
 const char* sym_kernel_times(void* engine, int32_t reset) {
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx) return "{}";

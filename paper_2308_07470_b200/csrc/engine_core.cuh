@@ -194,38 +194,30 @@ SYM_HD bool gpu_before(const Shard& S, int32_t x, int32_t y) {
   return x < y;
 }
 
-// Leaf-to-root update of a tournament tree along one path.  The siblings of
-// the path are not modified by the update, so all of them (and their keys)
-// are loaded up front -- two waves of independent loads instead of
-// log2(width) dependent round trips -- and the winners are then resolved in
-// registers.  kMaxLevels bounds the width at 2^14 leaves.
+// Leaf-to-root update of a tournament tree along one path: at each level the
+// path's winner meets the winner of the sibling subtree (siblings are not
+// modified by the climb).  A plain loop over the tree's actual height: the
+// trees live in shared memory, and unrolling to a fixed 14 levels with
+// runtime guards cost the single chain thread more than the loads
+// (tools/chain_prof.py).
 constexpr int kMaxLevels = 14;
 
 SYM_HD void gpu_tree_update(Shard& S, int32_t gid) {
-  const int32_t L = S.Glog;
-  const int32_t node = S.Gp + gid;
-  int32_t sib[kMaxLevels];
-  int64_t sk[kMaxLevels];
-#pragma unroll
-  for (int l = 0; l < kMaxLevels; l++)
-    if (l < L) sib[l] = S.gt[(node >> l) ^ 1];
-#pragma unroll
-  for (int l = 0; l < kMaxLevels; l++)
-    if (l < L) sk[l] = sib[l] >= 0 ? S.free_at[sib[l]] : 0;
+  int32_t node = S.Gp + gid;
   const int64_t f = S.free_at[gid];
   int32_t cur = f == OUTSTANDING ? -1 : gid;
   int64_t ck = f;
   S.gt[node] = cur;
-#pragma unroll
-  for (int l = 0; l < kMaxLevels; l++) {
-    if (l < L) {
-      const int32_t o = sib[l];
-      if (o >= 0 && (cur < 0 || sk[l] < ck || (sk[l] == ck && o < cur))) {
+  for (; node > 1; node >>= 1) {
+    const int32_t o = S.gt[node ^ 1];
+    if (o >= 0) {
+      const int64_t ok = S.free_at[o];
+      if (cur < 0 || ok < ck || (ok == ck && o < cur)) {
         cur = o;
-        ck = sk[l];
+        ck = ok;
       }
-      S.gt[node >> (l + 1)] = cur;
     }
+    S.gt[node >> 1] = cur;
   }
 }
 
@@ -269,31 +261,21 @@ SYM_HD bool model_before(const Shard& S, int32_t x, int32_t y) {
 }
 
 SYM_HD void pq_update(Shard& S, int32_t mid) {
-  const int32_t L = S.Mlog;
-  const int32_t node = S.Mp + mid;
-  int32_t sib[kMaxLevels];
-  int64_t st[kMaxLevels];
-#pragma unroll
-  for (int l = 0; l < kMaxLevels; l++)
-    if (l < L) sib[l] = S.pq[(node >> l) ^ 1];
-#pragma unroll
-  for (int l = 0; l < kMaxLevels; l++)
-    if (l < L) st[l] = sib[l] >= 0 ? S.ms[sib[l]].nx_key.t : 0;
+  int32_t node = S.Mp + mid;
   int32_t cur = S.ms[mid].nx_type != EV_NONE ? mid : -1;
   int64_t ck = S.ms[mid].nx_key.t;
   S.pq[node] = cur;
-#pragma unroll
-  for (int l = 0; l < kMaxLevels; l++) {
-    if (l < L) {
-      const int32_t o = sib[l];
-      // leaves of models without a next event are -1, so o >= 0 has one
-      if (o >= 0 && (cur < 0 || st[l] < ck ||
-                     (st[l] == ck && key_less(S.ms[o].nx_key, S.ms[cur].nx_key)))) {
+  for (; node > 1; node >>= 1) {
+    const int32_t o = S.pq[node ^ 1];
+    // leaves of models without a next event are -1, so o >= 0 has one
+    if (o >= 0) {
+      const int64_t ot = S.ms[o].nx_key.t;
+      if (cur < 0 || ot < ck || (ot == ck && key_less(S.ms[o].nx_key, S.ms[cur].nx_key))) {
         cur = o;
-        ck = st[l];
+        ck = ot;
       }
-      S.pq[node >> (l + 1)] = cur;
     }
+    S.pq[node >> 1] = cur;
   }
 }
 
@@ -878,15 +860,34 @@ SYM_HD void refresh_model(Shard& S, int32_t m, const FreshRec* fresh) {
   prefetch_fresh(fresh, P, st);
 }
 
+// Dev-only cycle attribution of the chain (tools/chain_prof.py builds a
+// separate library with -DSYM_CHAIN_PROF): [0..3] handler cycles by event
+// type (MT, DT, ARR, GPU), [4..7] their counts, [8] dispatch, [9] refresh,
+// [10] pq_update, [11] refreshed models.
+#if defined(SYM_CHAIN_PROF) && defined(__CUDACC__)
+__device__ unsigned long long g_chain_prof[16];
+#endif
+#if defined(SYM_CHAIN_PROF) && defined(__CUDA_ARCH__)
+#define SYM_PROF_T(v) const long long v = clock64()
+#define SYM_PROF_ADD(i, x) atomicAdd(&g_chain_prof[i], (unsigned long long)(x))
+#else
+#define SYM_PROF_T(v)
+#define SYM_PROF_ADD(i, x)
+#endif
+
 // Process one chain event; returns false when the sub-cluster is drained.
 // dirty must hold M+1 entries.
 SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
+  SYM_PROF_T(t0);
   const int32_t m = S.pq[1];
   const bool have_m = m >= 0;
   if (!have_m && !S.gt_armed) return false;
   int32_t nd = 0;
   const int64_t ops0 = S.ops, ev0 = S.evictions;
   bool timer_event = true;
+  int prof_type = 3;
+  (void)prof_type;
+  SYM_PROF_T(t1);
   if (S.gt_armed && (!have_m || key_less(S.gt_key, S.ms[m].nx_key))) {
     Pusher who;
     who.t = S.gt_key.t;
@@ -899,6 +900,7 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
     who.t = st.nx_key.t;
     who.a_self = who.a_after = st.nx_key.a;
     who.sub = S.chain_events;
+    prof_type = st.nx_type - 1;
     switch (st.nx_type) {
       case EV_MT: on_model_timer(S, m, who.t, who); break;
       case EV_DT: on_drop_timer(S, m, who.t, who); break;
@@ -910,15 +912,25 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
     }
     dirty[nd++] = m;
   }
+  SYM_PROF_T(t2);
   S.chain_events += 1;
   if (timer_event) {
     const int64_t ops = (S.ops - ops0) - 2 * (S.evictions - ev0);
     if (ops > S.handler_ops_max) S.handler_ops_max = ops;
   }
   for (int32_t i = 0; i < nd; i++) {
+    SYM_PROF_T(r0);
     refresh_model(S, dirty[i], fresh);
+    SYM_PROF_T(r1);
     pq_update(S, dirty[i]);
+    SYM_PROF_T(r2);
+    SYM_PROF_ADD(9, r1 - r0);
+    SYM_PROF_ADD(10, r2 - r1);
   }
+  SYM_PROF_ADD(prof_type, t2 - t1);
+  SYM_PROF_ADD(4 + prof_type, 1);
+  SYM_PROF_ADD(8, t1 - t0);
+  SYM_PROF_ADD(11, nd);
   return true;
 }
 
