@@ -590,7 +590,8 @@ struct SmemPlan {
     return al(sizeof(int32_t) * 2 * S.Gp) + al(sizeof(int64_t) * S.G) +
            al(sizeof(int32_t) * 2 * S.Mp) + al(sizeof(ModelState) * S.M) +
            al(sizeof(ModelParam) * S.M) + 2 * al(sizeof(int32_t) * 2 * S.Mp) +
-           al(sizeof(int32_t) * S.M) + al(sizeof(int64_t) * S.M);
+           al(sizeof(int32_t) * S.M) + al(sizeof(int64_t) * S.M) +
+           al(sizeof(int64_t) * S.M * S.lat_stride);
   }
 };
 
@@ -628,14 +629,26 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
   place(S.mc_bs_tree, sizeof(int32_t) * 2 * S.Mp, false);
   place(S.mc_size, sizeof(int32_t) * S.M, false);
   place(S.mc_latest, sizeof(int64_t) * S.M, false);
+  {  // latency rows last: small model sets keep every l(b) probe on chip
+    const int64_t* lat_g = S.lat;
+    int64_t* lat_s = const_cast<int64_t*>(lat_g);
+    if (place(lat_s, sizeof(int64_t) * S.M * S.lat_stride, true)) S.lat = lat_s;
+  }
   int32_t* dirty = dirty_all + slot_base[blockIdx.x] + blockIdx.x;
+#ifdef SYM_CHAIN_PROF
+  sym::g_chain_prof_on = 1;
+#endif
   chain_init(S, fresh);
   while (chain_step(S, dirty, fresh)) {
   }
+#ifdef SYM_CHAIN_PROF
+  sym::g_chain_prof_on = 0;
+#endif
   if (ms_in_smem)
     for (int32_t k = 0; k < S.M; k++) ms_global[k] = S.ms[k];
   S.ms = orig.ms;
   S.mp = orig.mp;
+  S.lat = orig.lat;
   S.gt = orig.gt;
   S.free_at = orig.free_at;
   S.pq = orig.pq;

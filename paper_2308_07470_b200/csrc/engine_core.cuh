@@ -43,6 +43,24 @@
 
 namespace sym {
 
+// Dev-only cycle attribution of the chain (tools/chain_prof.py builds a
+// separate library with -DSYM_CHAIN_PROF): [0..3] handler cycles by event
+// type (MT, DT, ARR, GPU), [4..7] their counts, [8] dispatch, [9] refresh,
+// [10] pq_update, [11] refreshed models, [12] update_candidate,
+// [13] update_candidate calls, [14] scan_model, [15] set_gpu_timer.
+#if defined(SYM_CHAIN_PROF) && defined(__CUDACC__)
+__device__ unsigned long long g_chain_prof[16];
+__device__ int g_chain_prof_on;  // set by k_chain only (other kernels share helpers)
+#endif
+#if defined(SYM_CHAIN_PROF) && defined(__CUDA_ARCH__)
+#define SYM_PROF_T(v) const long long v = clock64()
+#define SYM_PROF_ADD(i, x) \
+  (g_chain_prof_on ? atomicAdd(&g_chain_prof[i], (unsigned long long)(x)) : 0ull)
+#else
+#define SYM_PROF_T(v)
+#define SYM_PROF_ADD(i, x)
+#endif
+
 constexpr int64_t NEG_INF = -(int64_t(1) << 62);  // units.py:17
 constexpr int64_t OUTSTANDING = -1;               // scheduler.py:41
 constexpr int64_t FREE_SENTINEL = INT64_MAX;      // leaf absent from an index
@@ -381,9 +399,9 @@ SYM_HD int32_t max_feasible(const Shard& S, int32_t m, int64_t now,
 // unchanged, the reference's bisection is replaced by the two probes that
 // certify the same answer (the predicate is monotone in b, so b is the
 // unique maximum iff ok(b) and not ok(b+1) or b == cap).
-SYM_HD bool update_candidate(const Shard& S, int32_t m, ModelState& st,
-                             int64_t now, int64_t gpu_floor,
-                             const Pusher& who) {
+SYM_HD bool update_candidate_impl(const Shard& S, int32_t m, ModelState& st,
+                                  int64_t now, int64_t gpu_floor,
+                                  const Pusher& who) {
   const ModelParam& P = S.mp[m];
   bool hc = st.has_cand && st.c_head == st.qh;  // cache valid for the head
   int64_t dh = 0;
@@ -467,6 +485,16 @@ SYM_HD bool update_candidate(const Shard& S, int32_t m, ModelState& st,
   return true;
 }
 
+SYM_HD bool update_candidate(const Shard& S, int32_t m, ModelState& st, int64_t now,
+                             int64_t gpu_floor, const Pusher& who) {
+  SYM_PROF_T(u0);
+  const bool r = update_candidate_impl(S, m, st, now, gpu_floor, who);
+  SYM_PROF_T(u1);
+  SYM_PROF_ADD(12, u1 - u0);
+  SYM_PROF_ADD(13, 1);
+  return r;
+}
+
 // ------------------------------------------------------- RankPlane --------
 
 SYM_HD void unregister(Shard& S, int32_t m) {  // scheduler.py:430-436
@@ -478,7 +506,7 @@ SYM_HD void unregister(Shard& S, int32_t m) {  // scheduler.py:430-436
 }
 
 // scheduler.py:438-457
-SYM_HD void set_gpu_timer(Shard& S, int64_t now, const Pusher& who) {
+SYM_HD void set_gpu_timer_impl(Shard& S, int64_t now, const Pusher& who) {
   const int32_t gid = S.gt[1];
   const int32_t bm = S.mc_bs_tree[1];
   if (bm < 0 || gid < 0) {
@@ -493,6 +521,13 @@ SYM_HD void set_gpu_timer(Shard& S, int64_t now, const Pusher& who) {
   S.gt_fire = fire;
   S.gt_gid = gid;
   S.gt_key = push_key(fire, PR_GPU, who);
+}
+
+SYM_HD void set_gpu_timer(Shard& S, int64_t now, const Pusher& who) {
+  SYM_PROF_T(g0);
+  set_gpu_timer_impl(S, now, who);
+  SYM_PROF_T(g1);
+  SYM_PROF_ADD(15, g1 - g0);
 }
 
 // Model-local half of inform_candidate: model_gen[m] += 1 supersedes the
@@ -833,7 +868,7 @@ SYM_HD void prefetch_fresh(const FreshRec* fresh, const ModelParam& P,
                            const ModelState& st) {
 #ifdef __CUDA_ARCH__
   if (fresh && st.qt < P.cnt)
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(fresh + P.off + st.qt));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(fresh + P.off + st.qt));
 #else
   (void)fresh;
   (void)P;
@@ -856,24 +891,12 @@ SYM_HD void refresh_model(Shard& S, int32_t m, const FreshRec* fresh) {
       return;
     }
   }
+  SYM_PROF_T(s0);
   S.absorbed += scan_model(S, m, st, -1);
+  SYM_PROF_T(s1);
+  SYM_PROF_ADD(14, s1 - s0);
   prefetch_fresh(fresh, P, st);
 }
-
-// Dev-only cycle attribution of the chain (tools/chain_prof.py builds a
-// separate library with -DSYM_CHAIN_PROF): [0..3] handler cycles by event
-// type (MT, DT, ARR, GPU), [4..7] their counts, [8] dispatch, [9] refresh,
-// [10] pq_update, [11] refreshed models.
-#if defined(SYM_CHAIN_PROF) && defined(__CUDACC__)
-__device__ unsigned long long g_chain_prof[16];
-#endif
-#if defined(SYM_CHAIN_PROF) && defined(__CUDA_ARCH__)
-#define SYM_PROF_T(v) const long long v = clock64()
-#define SYM_PROF_ADD(i, x) atomicAdd(&g_chain_prof[i], (unsigned long long)(x))
-#else
-#define SYM_PROF_T(v)
-#define SYM_PROF_ADD(i, x)
-#endif
 
 // Process one chain event; returns false when the sub-cluster is drained.
 // dirty must hold M+1 entries.
