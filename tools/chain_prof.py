@@ -39,6 +39,9 @@ def report(label):
     print(f"{label}: events {n}, cycles/event {tot / n:.0f} | handler {sum(v[0:4]) / n:.0f} "
           f"dispatch {v[8] / n:.0f} refresh {v[9] / n:.0f} pq {v[10] / n:.0f} "
           f"(refreshed/event {v[11] / n:.2f}) | {parts}", flush=True)
+    print(f"    update_candidate {v[13] / n:.2f} calls/event x {v[12] / max(v[13], 1):.0f} cycles; "
+          f"scan_model {v[14] / n:.0f} cycles/event; set_gpu_timer {v[15] / n:.0f} cycles/event",
+          flush=True)
 
 
 sc = SCN.load_scenario("table2_resnet50").with_rate(11678.8)
