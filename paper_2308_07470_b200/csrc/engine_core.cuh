@@ -219,8 +219,6 @@ SYM_HD bool gpu_before(const Shard& S, int32_t x, int32_t y) {
 // trees live in shared memory, and unrolling to a fixed 14 levels with
 // runtime guards cost the single chain thread more than the loads
 // (tools/chain_prof.py).
-constexpr int kMaxLevels = 14;
-
 SYM_HD void gpu_tree_update(Shard& S, int32_t gid) {
   int32_t node = S.Gp + gid;
   const int64_t f = S.free_at[gid];
@@ -922,8 +920,9 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
   int32_t nd = 0;
   const int64_t ops0 = S.ops, ev0 = S.evictions;
   bool timer_event = true;
+#ifdef SYM_CHAIN_PROF
   int prof_type = 3;
-  (void)prof_type;
+#endif
   SYM_PROF_T(t1);
   if (S.gt_armed && (!have_m || key_less(S.gt_key, S.ms[m].nx_key))) {
     Pusher who;
@@ -937,7 +936,9 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
     who.t = st.nx_key.t;
     who.a_self = who.a_after = st.nx_key.a;
     who.sub = S.chain_events;
+#ifdef SYM_CHAIN_PROF
     prof_type = st.nx_type - 1;
+#endif
     switch (st.nx_type) {
       case EV_MT: on_model_timer(S, m, who.t, who); break;
       case EV_DT: on_drop_timer(S, m, who.t, who); break;
