@@ -108,6 +108,8 @@ struct Ctx {
   int32_t* d_closek = nullptr;      // closing arrival of lean-certified starts
   int32_t *d_jC = nullptr;          // J_64 kept while J_256 is built
   int32_t *d_s_slot = nullptr;      // [n] model slot of each sorted position
+  int32_t *d_unsure = nullptr;      // [n] positions the lean pointer could not certify
+  int32_t *d_unsure_n = nullptr;    // [1] their count
   int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
           *d_cp_model = nullptr, *d_special = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
@@ -475,7 +477,8 @@ __global__ void __launch_bounds__(256)
 k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
          const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
          const int32_t* __restrict__ s_slot,
-         int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
+         int32_t* __restrict__ nxt, int32_t* __restrict__ close_k,
+         int32_t* __restrict__ unsure, int32_t* __restrict__ unsure_n) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int64_t p0 = p - lane;  // window base (warp-uniform)
@@ -535,15 +538,15 @@ k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base
   }
   nxt[p] = v;
   close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
+  if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = (int32_t)p;  // for k_nxt_general
 }
 
 // Positions the lean loop could not certify: the general fresh_scan.
-__global__ void __launch_bounds__(256)
-k_nxt_general(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
-              const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
-              int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n || nxt[p] != NX_UNSURE) return;
+__device__ __forceinline__ void nxt_general_one(const Shard* __restrict__ shards,
+                                                const int32_t* __restrict__ slot_base,
+                                                const ModelParam* __restrict__ mp_all, int32_t P,
+                                                int64_t p, int32_t* __restrict__ nxt,
+                                                int32_t* __restrict__ close_k) {
   int lo = 0, hi = slot_base[P];
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -556,6 +559,17 @@ k_nxt_general(const Shard* __restrict__ shards, const int32_t* __restrict__ slot
   nxt[p] = chain_next(fresh_scan(shards[s], lo - slot_base[s], q, kFreshMaxSteps), mp_all[lo]);
   close_k[p] = -1;  // not certified by the lean sweep: k_chain_recs rescans
 }
+
+__global__ void __launch_bounds__(256)
+k_nxt_general(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
+              const ModelParam* __restrict__ mp_all, int32_t P,
+              const int32_t* __restrict__ unsure, const int32_t* __restrict__ unsure_n,
+              int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
+  const int32_t cnt = *unsure_n;  // listed by k_nxt_pp; usually none
+  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < cnt; u += gridDim.x * blockDim.x)
+    nxt_general_one(shards, slot_base, mp_all, P, unsure[u], nxt, close_k);
+}
+
 
 __global__ void __launch_bounds__(256)
 k_fresh(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
@@ -1498,7 +1512,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
         (rc = grow(ctx, ctx->d_closek, c)) ||
         (rc = grow(ctx, ctx->d_jB, c)) || (rc = grow(ctx, ctx->d_jC, c)) ||
-        (rc = grow(ctx, ctx->d_s_slot, c)) ||
+        (rc = grow(ctx, ctx->d_s_slot, c)) || (rc = grow(ctx, ctx->d_unsure, c)) ||
         (rc = grow(ctx, ctx->d_cp_pos, c / kJump + ctx->M + 2)) ||
         (rc = grow(ctx, ctx->d_cp_model, c / kJump + ctx->M + 2)))
       return rc;
@@ -1699,10 +1713,13 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
   bool have_fresh = false;
   if (fast) {
+    CK(cudaMemsetAsync(ctx->d_unsure_n, 0, sizeof(int32_t), st));
     KL(k_nxt_pp, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, n,
-                                             ctx->d_s_slot, ctx->d_nxt, ctx->d_closek));
-    KL(k_nxt_general, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp,
-                                                  P, n, ctx->d_nxt, ctx->d_closek));
+                                             ctx->d_s_slot, ctx->d_nxt, ctx->d_closek,
+                                             ctx->d_unsure, ctx->d_unsure_n));
+    KL(k_nxt_general, 148 * 4, 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P,
+                                             ctx->d_unsure, ctx->d_unsure_n, ctx->d_nxt,
+                                             ctx->d_closek));
   } else if (use_fresh && n > 0) {
     KL(k_fresh, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base,
                                           ctx->d_mp, P, n, ctx->d_fresh, nullptr));
@@ -2169,6 +2186,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_fail, P);
   ALLOC(ctx->d_skip, P);
   ALLOC(ctx->d_changed, 4);
+  ALLOC(ctx->d_unsure_n, 1);
   ALLOC(ctx->d_special, M);
   ALLOC(ctx->d_slo_model, M);
   ctx->net_ctrl_n = cfg->net_ctrl_n > 0 ? cfg->net_ctrl_n : 0;
@@ -2268,6 +2286,7 @@ void sym_destroy(void* engine) {
                   ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
                   ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_jC, ctx->d_s_slot,
+                  ctx->d_unsure, ctx->d_unsure_n,
                   ctx->d_cp_pos,
                   ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
                   ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
