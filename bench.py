@@ -58,7 +58,7 @@ def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
         "k_nxt_general": n * 4,
         # batch records from the chain positions' fresh scans: the members'
         # ticks/ids once, one EvBatch written per batch
-        "k_chain_recs": n * (8 + 4 + 4) + nb * (4 + EV_BATCH_BYTES),
+        "k_chain_recs": n * (8 + 4 + 4) + nb * (4 + EV_BATCH_BYTES + 8 + 4),
         "k_walk": 0,
         # match + pointer jumping (~log2(nb/G) rounds) + tie repair, one launch
         "k_match_coop": nb * (8 + 4 + 4 + 4) + nb * 12 * 12,
@@ -68,7 +68,6 @@ def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
         # stable merge-path round over the batch runs: read and write key+value
         "k_merge_round": nb * (12 + 12),
         "k_walk_expand": nb * (FRESH_REC_BYTES + 4 + EV_BATCH_BYTES),
-        "k_batch_keys": nb * (8 + 8 + 4),
         "k_rscatter": nb * (12 + 12),
         "k_rhist": nb * 8,
         "k_scan_up": None, "k_scan_mid": None, "k_scan_down": None,

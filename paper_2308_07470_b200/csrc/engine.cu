@@ -971,7 +971,9 @@ k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_
              int32_t P, int32_t M, const ModelParam* __restrict__ mp_all,
              const int32_t* __restrict__ nb, const int32_t* __restrict__ bbase,
              const int32_t* __restrict__ special, int64_t nt, EvBatch* __restrict__ evb,
-             unsigned long long* __restrict__ mdrops, const int32_t* __restrict__ close_k) {
+             unsigned long long* __restrict__ mdrops, const int32_t* __restrict__ close_k,
+             uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+             uint32_t* __restrict__ fail, int tb) {
   const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nt) return;
   int lo = 0, hi = M;  // last model with bbase <= d
@@ -980,28 +982,35 @@ k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_
     if (bbase[mid] <= d) lo = mid; else hi = mid;
   }
   while (nb[lo] == 0 || bbase[lo] + nb[lo] <= d) lo++;
-  if (special[lo]) return;  // filled by k_evolve
   const int s = shard_of_slot(slot_base, P, lo);
   const ModelParam& mp = mp_all[lo];
-  EvBatch& e = evb[mp.off + (d - bbase[lo])];
-  const int32_t m = lo - slot_base[s];
-  const int32_t ck = close_k[e.first];
-  if (ck >= 0) {  // certified by the lean sweep: O(1) from (q, k)
-    lean_batch(shards[s], m, e.first - mp.off, ck, e);
-    return;
+  const int64_t p = mp.off + (d - bbase[lo]);
+  EvBatch& e = evb[p];
+  if (!special[lo]) {  // special models' records come from k_evolve
+    const int32_t m = lo - slot_base[s];
+    const int32_t ck = close_k[e.first];
+    if (ck >= 0) {  // certified by the lean sweep: O(1) from (q, k)
+      lean_batch(shards[s], m, e.first - mp.off, ck, e);
+    } else {
+      const FreshRec r = fresh_scan(shards[s], m, e.first - mp.off, kFreshMaxSteps);
+      e.t = r.mt_t;
+      e.a = r.mt_a;
+      e.tp = r.mt_tp;
+      e.ap = r.mt_ap;
+      e.chain = 0;  // fresh scans only hold arrival-pushed timers
+      e.exec = r.c_exec;
+      e.lat = r.c_lb;
+      e.size = r.c_size;
+      e.first = mp.off + r.qh;
+      e.model = m;
+      if (r.drops) atomicAdd(&mdrops[lo], (unsigned long long)r.drops);
+    }
   }
-  const FreshRec r = fresh_scan(shards[s], m, e.first - mp.off, kFreshMaxSteps);
-  e.t = r.mt_t;
-  e.a = r.mt_a;
-  e.tp = r.mt_tp;
-  e.ap = r.mt_ap;
-  e.chain = 0;  // fresh scans only hold arrival-pushed timers
-  e.exec = r.c_exec;
-  e.lat = r.c_lb;
-  e.size = r.c_size;
-  e.first = mp.off + r.qh;
-  e.model = m;
-  if (r.drops) atomicAdd(&mdrops[lo], (unsigned long long)r.drops);
+  // the batch's merge key, in the per-model run layout
+  const int64_t t = e.t;
+  if (t < 0 || t >= (int64_t(1) << tb)) atomicOr(&fail[s], FP_CAPACITY);
+  keys[d] = ((uint64_t)s << tb) | (uint64_t)(t & ((int64_t(1) << tb) - 1));
+  vals[d] = (uint32_t)p;
 }
 
 // K3b: dense batch numbering: bbase[k] per model, sbase[s] per shard
@@ -1021,27 +1030,6 @@ __global__ void k_nb_scan(const int32_t* __restrict__ nb, int32_t M, int32_t P,
 }
 
 // K3c: (shard|tick) keys of every batch, value = its EvBatch index
-__global__ void k_batch_keys(const Shard* __restrict__ shards,
-                             const int32_t* __restrict__ slot_base, int32_t P,
-                             const ModelParam* __restrict__ mp_all,
-                             const int32_t* __restrict__ nb,
-                             const int32_t* __restrict__ bbase,
-                             const EvBatch* __restrict__ evb, int64_t n,
-                             uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                             uint32_t* __restrict__ fail, int tb,
-                             const int32_t* __restrict__ s_slot) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int lo = s_slot[p];
-  const int32_t j = (int32_t)(p - mp_all[lo].off);
-  if (j >= nb[lo]) return;
-  const int s = shard_of_slot(slot_base, P, lo);
-  const int64_t t = evb[p].t;
-  if (t < 0 || t >= (int64_t(1) << tb)) atomicOr(&fail[s], FP_CAPACITY);
-  const int64_t d = bbase[lo] + j;
-  keys[d] = ((uint64_t)s << tb) | (uint64_t)(t & ((int64_t(1) << tb) - 1));
-  vals[d] = (uint32_t)p;
-}
 
 // --- LSD radix sort of (u64 key, u32 value) pairs, 8-bit digits, stable ---
 
@@ -1118,7 +1106,7 @@ k_rscatter(const uint64_t* __restrict__ kin,
 }
 
 // K3d: order runs of equal (shard, tick) by the full event key
-// Batch order by merging instead of radix sorting.  k_batch_keys lays the
+// Batch order by merging instead of radix sorting.  k_chain_recs lays the
 // batches out as one run per model, each already in event order (a model's
 // chain), so the global order is a merge of M sorted runs: ceil(log2 M)
 // rounds of stable pairwise merge path.  Round r merges the runs of models
@@ -1767,10 +1755,9 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     if (nt > 0) {
       KL(k_chain_recs, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_shards, ctx->d_slot_base, P, M, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
-          ctx->d_special, nt, ctx->d_evb, (unsigned long long*)ctx->d_mdrops, ctx->d_closek));
-      KL(k_batch_keys, nblk(n, 256), 256, 0, st>>>(
-          ctx->d_shards, ctx->d_slot_base, P, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
-          ctx->d_evb, n, ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits, ctx->d_s_slot));
+          ctx->d_special, nt, ctx->d_evb, (unsigned long long*)ctx->d_mdrops, ctx->d_closek,
+          ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits));
+
       // key = (shard << tick_bits) | tick; only the bits in use are sorted
       int bits = tick_bits;
       while ((1 << (bits - tick_bits)) < P) bits++;
