@@ -7,7 +7,7 @@
 //   K1d k_scatter   stable scatter to the (shard, model)-sorted layout with
 //                   warp __match_any_sync ranking (per-warp offsets keep
 //                   stream order without any global atomics)
-//   K1e k_aself     canonical A' of every arrival (same-tick cascades)
+//   (A' of an arrival -- same-tick cascades -- is derived on the fly, aself_at)
 //   K2  k_fresh     fresh-start pre-scan (chain fallback only)
 //   K3  k_nxt_pp ... k_fast_emit  the parallel validated path (fastpath.cuh)
 //   K4  k_chain     one CTA per sub-cluster runs the live-event chain
@@ -82,8 +82,7 @@ struct Ctx {
   int64_t cap = 0, W_cap = 0;
   int64_t *d_ticks = nullptr, *d_s_tick = nullptr, *d_sh_tick = nullptr;
   int32_t *d_inv = nullptr, *d_bid = nullptr;  // stream -> sorted position, position -> record
-  int32_t *d_model = nullptr, *d_s_g = nullptr, *d_s_i = nullptr,
-          *d_s_aself = nullptr;
+  int32_t *d_model = nullptr, *d_s_g = nullptr, *d_s_i = nullptr;
   int32_t* d_hist = nullptr;        // [W][B]
   int32_t* d_bins = nullptr;        // [B+1] totals -> offsets
   int32_t* d_err = nullptr;
@@ -312,7 +311,8 @@ k_scatter(const int64_t* __restrict__ ticks,
           int32_t* __restrict__ s_g,
           int32_t* __restrict__ s_i,
           int64_t* __restrict__ sh_tick,
-          int32_t* __restrict__ inv, int32_t* __restrict__ s_slot) {
+          int32_t* __restrict__ inv, int32_t* __restrict__ s_slot,
+          int32_t* __restrict__ bid) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int B = M + P;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -435,28 +435,10 @@ k_scatter(const int64_t* __restrict__ ticks,
     s_g[pos] = st_g[e];
     s_i[pos] = st_i[e];
     s_slot[pos] = b;
+    bid[pos] = -1;  // "no batch" until k_bid
   }
 }
 
-// canonical A' of each arrival, in the sorted layout (engine_core.cuh)
-__global__ void k_aself(const int64_t* __restrict__ s_tick,
-                        const int32_t* __restrict__ s_g,
-                        const int64_t* __restrict__ sh_tick,
-                        const int32_t* __restrict__ shard_off, int32_t P,
-                        int64_t n, int32_t* __restrict__ s_aself,
-                        int32_t* __restrict__ bid) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  bid[p] = -1;  // "no batch" until k_bid (saves a fill pass over n)
-  const int32_t j = s_g[p];
-  int lo = 0, hi = P;  // last s with shard_off[s] <= j
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (shard_off[mid] <= j) lo = mid; else hi = mid;
-  }
-  const bool first = j == shard_off[lo];
-  s_aself[p] = (!first && sh_tick[j - 1] == s_tick[p]) ? j : A_BASE;
-}
 
 // --------------------------------------------------------------- K2 -------
 
@@ -1487,7 +1469,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
                    std::max<int64_t>(((c + kChunkR - 1) / kChunkR + 1) * kDigits,
                                      ((c + kChunkI - 1) / kChunkI + 1) * (ctx->M + ctx->P)) /
                            kScanItems + 2)) ||
-        (rc = grow(ctx, ctx->d_s_aself, c)) || (rc = grow(ctx, ctx->d_fresh, c)) ||
+        (rc = grow(ctx, ctx->d_fresh, c)) ||
         (rc = grow(ctx, ctx->d_recs, c + ctx->P)) ||
         (rc = grow(ctx, ctx->d_drop_t, c)) || (rc = grow(ctx, ctx->d_drop_ks, c)) ||
         (rc = grow(ctx, ctx->d_drop_ka, c)) || (rc = grow(ctx, ctx->d_evb, c)) ||
@@ -1631,7 +1613,10 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                                            ctx->d_bins + B + 1));
   int32_t herr2[2] = {INT32_MAX, INT32_MAX};
   int64_t last_tick = 0;
+  std::vector<int32_t> shard_off(P + 1, 0);  // first shard-stream index per shard
   CK(cudaMemcpyAsync(herr2, ctx->d_err, sizeof herr2, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(shard_off.data(), ctx->d_bins + B + 1, sizeof(int32_t) * (P + 1),
+                     cudaMemcpyDeviceToHost, st));
   if (n > 0)
     CK(cudaMemcpyAsync(&last_tick, d_ticks + (n - 1), sizeof last_tick,
                        cudaMemcpyDeviceToHost, st));
@@ -1659,11 +1644,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_scatter, W, 32 * kIngestWarps, scatter_smem(B), st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
-        ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot));
-  if (n > 0)
-    KL(k_aself, nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, ctx->d_s_g,
-                                          ctx->d_sh_tick, ctx->d_bins + B + 1,
-                                          P, n, ctx->d_s_aself, ctx->d_bid));
+        ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot, ctx->d_bid));
   CK(cudaGetLastError());
   pc.mark("ingest");
   CK(cudaEventRecord(ctx->ev[1], st));
@@ -1672,7 +1653,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     Shard& S = ctx->shards[s];
     S.s_tick = ctx->d_s_tick;
     S.s_g = ctx->d_s_g;
-    S.s_aself = ctx->d_s_aself;
+    S.sh_tick = ctx->d_sh_tick;
+    S.sh_base = shard_off[s];
     S.record_trace = trace ? 1 : 0;
     S.drop_t = ctx->d_drop_t;
     S.drop_ksub = ctx->d_drop_ks;
@@ -2264,7 +2246,7 @@ void sym_destroy(void* engine) {
                   ctx->d_pq,   ctx->d_gt,     ctx->d_mlt,   ctx->d_mbt,
                   ctx->d_mcs,  ctx->d_dirty,  ctx->d_free,  ctx->d_mcl,
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
-                  ctx->d_model, ctx->d_s_g,   ctx->d_s_i,   ctx->d_s_aself,
+                  ctx->d_model, ctx->d_s_g,   ctx->d_s_i,
                   ctx->d_inv, ctx->d_bid, ctx->d_scan_part, ctx->d_closek,
                   ctx->d_hist, ctx->d_bins,   ctx->d_err,   ctx->d_fresh,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,

@@ -169,8 +169,8 @@ struct Shard {
   const ModelParam* mp;        // [M]
   // arrivals, sorted by (model, stream order)
   const int64_t* s_tick;       // [n] tick of sorted position p
-  const int32_t* s_g;          // [n] stream index of sorted position p
-  const int32_t* s_aself;      // [n] A' of that arrival
+  const int32_t* s_g;          // [n] shard-stream index of sorted position p
+  const int64_t* sh_tick;      // [n] ticks in shard-stream order (for A')
   // mutable
   ModelState* ms;              // [M]
   int32_t* pq;                 // [2*Mp] tournament tree of models (next event)
@@ -194,8 +194,16 @@ struct Shard {
   int64_t chain_events, absorbed, fresh_adoptions;
   int64_t ops, evictions, registrations, handler_ops_max;
   int32_t error;
-  int32_t _pad3;
+  int32_t sh_base;             // first shard-stream index of this shard
 };
+
+// Canonical A' of the arrival at sorted position pos (engine_core.cuh top):
+// its shard-stream index if the previous arrival of the shard has the same
+// tick, else BASE.
+SYM_HD int32_t aself_at(const Shard& S, int32_t pos) {
+  const int32_t j = S.s_g[pos];
+  return (j > S.sh_base && S.sh_tick[j - 1] == S.s_tick[pos]) ? j : A_BASE;
+}
 
 enum : int32_t { ERR_NONE = 0, ERR_REC_OVERFLOW = 1, ERR_STATE = 2 };
 
@@ -640,7 +648,7 @@ SYM_HD void absorb_arrival(const Shard& S, int32_t m, ModelState& st) {
   const int64_t now = S.s_tick[pos];
   Pusher who;
   who.t = now;
-  who.a_self = S.s_aself[pos];
+  who.a_self = aself_at(S, pos);
   who.a_after = S.s_g[pos] + 1;
   who.sub = SUB_ARRIVAL;
   st.qt += 1;
@@ -656,7 +664,7 @@ SYM_HD void registered_arrival(Shard& S, int32_t m) {
   const int64_t now = S.s_tick[pos];
   Pusher who;
   who.t = now;
-  who.a_self = S.s_aself[pos];
+  who.a_self = aself_at(S, pos);
   who.a_after = S.s_g[pos] + 1;
   who.sub = SUB_ARRIVAL;
   st.qt += 1;
@@ -688,7 +696,7 @@ SYM_HD int32_t scan_model(const Shard& S, int32_t m, ModelState& st,
     if (st.qt < P.cnt) {
       const int32_t pos = P.off + st.qt;
       const int64_t ta = S.s_tick[pos];
-      const int32_t aa = S.s_aself[pos];
+      const int32_t aa = aself_at(S, pos);
       // an arrival precedes a timer iff (a, A') < (tick, A') (prio 4 > 3)
       const bool first = type == EV_NONE || ta < best.t ||
                          (ta == best.t && aa < best.a);

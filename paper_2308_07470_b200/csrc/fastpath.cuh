@@ -387,7 +387,7 @@ SYM_HD void lean_batch(const Shard& S, int32_t m, int32_t q, int32_t k, EvBatch&
   e.t = fire;
   e.a = fire == now ? S.s_g[pos] + 1 : A_BASE;  // push_key with pusher = arrival k
   e.tp = now;
-  e.ap = S.s_aself[pos];
+  e.ap = aself_at(S, pos);
   e.chain = 0;
   e.exec = exec;
   e.lat = lat[len - 1];

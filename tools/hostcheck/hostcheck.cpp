@@ -47,7 +47,7 @@ extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64
   S.M = M; S.G = G; S.Mp = Mp; S.Gp = Gp; while ((1 << S.Mlog) < Mp) S.Mlog++; while ((1 << S.Glog) < Gp) S.Glog++; S.kind = cfg->kind; S.gather = cfg->gather;
   S.record_trace = 1; S.d_ctrl = cfg->d_ctrl_ns; S.d_data = cfg->d_data_ns;
   S.lat_stride = cfg->lat_stride; S.lat = cfg->lat_ns; S.mp = mp.data();
-  S.s_tick = s_tick.data(); S.s_g = s_g.data(); S.s_aself = s_as.data();
+  S.s_tick = s_tick.data(); S.s_g = s_g.data(); S.sh_tick = ticks; S.sh_base = 0;
   S.ms = ms.data(); S.pq = pq.data(); S.free_at = fa.data(); S.gt = gt.data();
   S.mc_lat_tree = mlt.data(); S.mc_bs_tree = mbt.data(); S.mc_size = mcs.data(); S.mc_latest = mcl.data();
   S.recs = recs.data(); S.rec_cap = n + 1; S.drop_t = dt.data(); S.drop_ksub = dks.data(); S.drop_ka = dka.data();
