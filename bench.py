@@ -44,8 +44,9 @@ def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
     """Minimal DRAM bytes one launch of `kernel` must move for n requests and
     nb batches (DESIGN.md §5 derives each line)."""
     table = {
-        # stable partition: read tick+model, write s_tick, s_g, s_i, sh_tick
-        "k_scatter": n * (8 + 4 + 8 + 4 + 4 + 8),
+        # stable partition: read tick+model, write s_tick, s_g, s_i, sh_tick,
+        # the inverse map, the model slot and the batch-id reset
+        "k_scatter": n * (8 + 4 + 8 + 4 + 4 + 8 + 4 + 4 + 4),
         "k_hist": n * 4,
         "k_aself": n * (4 + 8 + 8 + 4),
         # fresh-start pre-scan: read each sorted arrival once (tick, A', g),
