@@ -123,3 +123,46 @@ def test_random_subclusters_in_one_call(combo):
                                           err_msg=f"combo {combo} shard {s} {k}")
         lo += len(ms)
     eng.close()
+
+
+@pytest.mark.parametrize("combo", range(20))
+def test_random_jittered_subclusters_in_one_call(combo):
+    """Sub-clusters of one call under a histogram network: sub-cluster s
+    draws its k-th dispatch delay from the engine's Philox stream exactly as
+    a separate reference Engine with the same seed would."""
+    import random
+    from dataclasses import replace
+    from oracle import oracle
+    from paper_2308_07470_b200.network import DelayDist, NetworkModel, jitter_tables
+    from paper_2308_07470_b200.profile import ModelSpec
+    from paper_2308_07470_b200.simulator import Engine
+    rng = random.Random(900 + combo)
+    parts = [_case(7000 + 10 * combo + k) for k in range(rng.randint(2, 4))]
+    net = NetworkModel(DelayDist.histogram([0, rng.randint(1, 400_000), 2_000_000],
+                                           [0.6, 0.3, 0.1], 0.7),
+                       DelayDist.histogram([0, 3_000, 50_000], [0.5, 0.4, 0.1]))
+    policy = replace(parts[0][2], d_ctrl_ns=net.plan_ctrl_ns, d_data_ns=net.plan_data_ns)
+    seed = 11 + combo
+    models, som, gps, ticks, midx = [], [], [], [], []
+    for s, (ms, g, _, t, m) in enumerate(parts):
+        base = len(models)
+        models += [ModelSpec(base + x.model_id, f"s{s}_{x.name}", x.profile, x.slo_ns) for x in ms]
+        som += [s] * len(ms)
+        gps.append(g)
+        ticks.append(np.asarray(t, np.int64))
+        midx.append(np.asarray(m, np.int64) + base)
+    t_all, m_all = np.concatenate(ticks), np.concatenate(midx)
+    order = np.argsort(t_all, kind="stable")
+    t_all, m_all = t_all[order], m_all[order]
+    eng = Engine(models, sum(gps), policy, net, seed=seed, shards=(som, gps))
+    res = eng.run_stream(t_all, m_all, 1.0)
+    lo = 0
+    for s, (ms, g, _, _, _) in enumerate(parts):
+        sel = np.nonzero((m_all >= lo) & (m_all < lo + len(ms)))[0]
+        ref = oracle.run(arr_ticks=t_all[sel], arr_midx=m_all[sel] - lo,
+                         net=jitter_tables(net, seed), **oracle_args(list(ms), g, policy))
+        for k in OUT:
+            np.testing.assert_array_equal(getattr(res, k)[sel], ref[k],
+                                          err_msg=f"combo {combo} shard {s} {k}")
+        lo += len(ms)
+    eng.close()
