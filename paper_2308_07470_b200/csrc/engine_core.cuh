@@ -932,7 +932,8 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
   int prof_type = 3;
 #endif
   SYM_PROF_T(t1);
-  if (S.gt_armed && (!have_m || key_less(S.gt_key, S.ms[m].nx_key))) {
+  const bool gpu_event = S.gt_armed && (!have_m || key_less(S.gt_key, S.ms[m].nx_key));
+  if (gpu_event) {
     Pusher who;
     who.t = S.gt_key.t;
     who.a_self = who.a_after = S.gt_key.a;
@@ -956,7 +957,6 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
         break;
       default: S.error = ERR_STATE; return false;
     }
-    dirty[nd++] = m;
   }
   SYM_PROF_T(t2);
   S.chain_events += 1;
@@ -964,11 +964,15 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
     const int64_t ops = (S.ops - ops0) - 2 * (S.evictions - ev0);
     if (ops > S.handler_ops_max) S.handler_ops_max = ops;
   }
-  for (int32_t i = 0; i < nd; i++) {
+  // a model event dirties only its own model (kept in a register); a GPU
+  // timer may dirty several (evictions), listed in `dirty`
+  const int32_t nref = gpu_event ? nd : 1;
+  for (int32_t i = 0; i < nref; i++) {
+    const int32_t dm = gpu_event ? dirty[i] : m;
     SYM_PROF_T(r0);
-    refresh_model(S, dirty[i], fresh);
+    refresh_model(S, dm, fresh);
     SYM_PROF_T(r1);
-    pq_update(S, dirty[i]);
+    pq_update(S, dm);
     SYM_PROF_T(r2);
     SYM_PROF_ADD(9, r1 - r0);
     SYM_PROF_ADD(10, r2 - r1);
@@ -976,7 +980,7 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
   SYM_PROF_ADD(prof_type, t2 - t1);
   SYM_PROF_ADD(4 + prof_type, 1);
   SYM_PROF_ADD(8, t1 - t0);
-  SYM_PROF_ADD(11, nd);
+  SYM_PROF_ADD(11, nref);
   return true;
 }
 
