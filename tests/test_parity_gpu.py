@@ -165,6 +165,7 @@ def test_window_counts_and_autoscale_on_device(golden):
     eng = Engine(list(sc.models), sc.gpu_count, sc.policy)
     res = eng.run_stream(ticks, midx, 0.6)
     assert autoscale_series(res, 0.025, 0.6) == golden["C5/autoscale_series@0.6"]
+    assert autoscale_series(res, 0.025, 0.6, engine=eng) == golden["C5/autoscale_series@0.6"]
     for lo, hi in ((0, 600_000_000), (60_000_000, 540_000_000), (1234567, 7654321)):
         dev = eng.window_counts(lo, hi)
         b = res.batches
