@@ -161,6 +161,20 @@ int32_t sym_window_counts(void *engine, int64_t lo_ns, int64_t hi_ns,
                           int64_t *model_late, int64_t *model_dropped,
                           int64_t *gpu_busy_ns);
 
+/* Everything else compute_stats (metrics.py:71-132) needs for the window,
+ * on the device: the counts and busy time above, plus per model the p99
+ * latency by nearest rank with drops as +inf (-1 = inf, 0 = no arrivals),
+ * the largest queueing delay of a served request, and the batch-size
+ * histogram of the batches starting in the window ([n_models][hist_stride],
+ * hist_stride > max batch size).  Needs the last run's per-request outputs
+ * on the device (valid until the next run). */
+int32_t sym_window_stats(void *engine, int64_t lo_ns, int64_t hi_ns,
+                         int64_t *model_arrivals, int64_t *model_completed,
+                         int64_t *model_late, int64_t *model_dropped,
+                         int64_t *gpu_busy_ns, int64_t *model_p99_ns,
+                         int64_t *model_max_qd_ns, int64_t *model_batch_hist,
+                         int32_t hist_stride);
+
 const char *sym_last_error(void *engine);
 
 /* JSON object {"kernel": [launches, total_ms], ...} accumulated over runs

@@ -79,8 +79,8 @@ class SymResult(C.Structure):
 
 EXPORTS = ("sym_create", "sym_destroy", "sym_run", "sym_run_device",
            "sym_window_counts", "sym_last_error", "sym_version", "sym_kernel_times",
-           "sym_last_batches", "sym_text_format", "sym_text_fetch", "sym_text_free",
-           "sym_part_brute_force", "sym_part_evaluate", "sym_part_solve")
+           "sym_last_batches", "sym_window_stats", "sym_text_format", "sym_text_fetch",
+           "sym_text_free", "sym_part_brute_force", "sym_part_evaluate", "sym_part_solve")
 
 TEXT_REQUESTS, TEXT_LATENCY = 0, 1
 
@@ -128,6 +128,9 @@ def load(path: str | None = None):
         fn.restype = C.c_int32
     lib.sym_window_counts.argtypes = [C.c_void_p, C.c_int64, C.c_int64] + [i64p] * 5
     lib.sym_window_counts.restype = C.c_int32
+    lib.sym_window_stats.argtypes = ([C.c_void_p, C.c_int64, C.c_int64] + [i64p] * 8 +
+                                     [C.c_int32])
+    lib.sym_window_stats.restype = C.c_int32
     lib.sym_last_error.argtypes = [C.c_void_p]
     lib.sym_last_error.restype = C.c_char_p
     lib.sym_version.restype = C.c_int32

@@ -119,6 +119,8 @@ struct Ctx {
   const int32_t* last_model = nullptr;
   std::vector<int64_t> last_nrecs, last_rec_base;
   const int64_t* last_outcome = nullptr;
+  const int64_t* last_start = nullptr;   // per-request start / finish of the
+  const int64_t* last_finish = nullptr;  // last expanded run (device)
   std::vector<uint32_t> last_fast_fail;
   bool has_run = false;
   std::map<std::string, std::pair<int64_t, double>> ktimes;  // name -> (launches, ms)
@@ -1365,6 +1367,92 @@ __global__ void k_window_busy(const BatchRec* __restrict__ recs,
   if (b > a) atomicAdd(&busy[gpu_base[s] + r.gpu], (unsigned long long)(b - a));
 }
 
+// ---- per-model window statistics (compute_stats, metrics.py:71-132) ------
+// Sort key of request i for the per-model p99: (model slot, latency) for
+// arrivals in the window, latency = finish - arrival or kStatInf for a drop
+// (the reference's +inf); arrivals outside go to a trailing dummy slot M.
+constexpr int kStatLatBits = 40;
+constexpr uint64_t kStatInf = (uint64_t(1) << kStatLatBits) - 1;
+
+__global__ void k_stat_keys(const int64_t* __restrict__ ticks, const int32_t* __restrict__ model,
+                            const int64_t* __restrict__ outcome,
+                            const int64_t* __restrict__ start, const int64_t* __restrict__ fin,
+                            const int32_t* __restrict__ slot_of_model, int64_t n, int64_t lo,
+                            int64_t hi, int32_t M, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals, unsigned long long* __restrict__ qd_max,
+                            int32_t* __restrict__ err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t t = ticks[i];
+  uint64_t key = (uint64_t)M << kStatLatBits;
+  if (t >= lo && t < hi) {
+    const int32_t m = model[i];
+    uint64_t lat = kStatInf;
+    if (outcome[i] != 2) {  // served: latency and queueing delay
+      const int64_t l = fin[i] - t;
+      if (l < 0 || (uint64_t)l >= kStatInf) atomicExch(err, 1);
+      lat = (uint64_t)l;
+      atomicMax(&qd_max[m], (unsigned long long)(start[i] - t));
+    }
+    key = ((uint64_t)slot_of_model[m] << kStatLatBits) | lat;
+  }
+  keys[i] = key;
+  vals[i] = 0;
+}
+
+// Batch-size histogram per model of the batches starting in the window.
+__global__ void k_stat_hist(const BatchRec* __restrict__ recs, const int64_t* __restrict__ rec_base,
+                            const int64_t* __restrict__ rec_count, int32_t P,
+                            const int32_t* __restrict__ slot_base,
+                            const int32_t* __restrict__ model_of_slot, int64_t total, int64_t lo,
+                            int64_t hi, int32_t stride, unsigned long long* __restrict__ hist) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= total) return;
+  int s = 0;
+  int64_t k = w;
+  while (s < P && k >= rec_count[s]) {
+    k -= rec_count[s];
+    s++;
+  }
+  const BatchRec& r = recs[rec_base[s] + k];
+  if (r.start < lo || r.start >= hi) return;
+  const int32_t gm = model_of_slot[slot_base[s] + r.model];
+  atomicAdd(&hist[(int64_t)gm * stride + r.size], 1ull);
+}
+
+// p99 (nearest rank, drops as +inf: metrics.py:54-61) per model from the
+// sorted keys: rank k = max(1, ceil(0.99 * arrivals)) in the model's segment.
+// One block; segments in slot order.
+__global__ void __launch_bounds__(1024)
+k_stat_p99(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ arrivals,
+           const int32_t* __restrict__ model_of_slot, int32_t M,
+           long long* __restrict__ p99 /* -1 = inf, by model id */) {
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int32_t b0 = 0; b0 < M; b0 += 1024) {
+    const int32_t slot = b0 + threadIdx.x;
+    const int32_t gm = slot < M ? model_of_slot[slot] : 0;
+    const int32_t cnt = slot < M ? (int32_t)arrivals[gm] : 0;
+    int32_t tot;
+    const int32_t ex = block_exclusive_scan(cnt, &tot);
+    const long long base = carry;
+    if (slot < M) {
+      if (cnt == 0) {
+        p99[gm] = 0;
+      } else {
+        long long k = (long long)ceil(0.99 * (double)cnt);
+        if (k < 1) k = 1;
+        const uint64_t lat = keys[base + ex + k - 1] & kStatInf;
+        p99[gm] = lat == kStatInf ? -1 : (long long)lat;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry = base + tot;
+    __syncthreads();
+  }
+}
+
 
 // ------------------------------------------- jittered network (K5') ------
 // numpy's Philox4x64-10 (philox.h) is counter based: word j of the engine's
@@ -1962,6 +2050,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   ctx->last_ticks = d_ticks;
   ctx->last_model = d_model;
   ctx->last_outcome = expand ? out->req_outcome : nullptr;
+  ctx->last_start = expand ? out->req_start : nullptr;
+  ctx->last_finish = expand ? out->req_finish : nullptr;
   ctx->last_nrecs = rec_count;
   ctx->last_rec_base = rec_base;
   ctx->has_run = true;
@@ -2463,6 +2553,82 @@ int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,
     model_dropped[m] = (int64_t)h[3 * M + m];
   }
   for (int32_t g = 0; g < G; g++) gpu_busy_ns[g] = (int64_t)h[4 * (size_t)M + g];
+  return SYM_OK;
+}
+
+int32_t sym_window_stats(void* engine, int64_t lo_ns, int64_t hi_ns, int64_t* model_arrivals,
+                         int64_t* model_completed, int64_t* model_late, int64_t* model_dropped,
+                         int64_t* gpu_busy_ns, int64_t* model_p99_ns, int64_t* model_max_qd_ns,
+                         int64_t* model_batch_hist, int32_t hist_stride) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx || hist_stride < 1) return SYM_EINVAL;
+  if (!ctx->has_run || !ctx->last_outcome || !ctx->last_start || !ctx->last_finish) {
+    ctx->err = "sym_window_stats: no expanded run to reduce";
+    return SYM_EINVAL;
+  }
+  int32_t rc = sym_window_counts(engine, lo_ns, hi_ns, model_arrivals, model_completed,
+                                 model_late, model_dropped, gpu_busy_ns);
+  if (rc != SYM_OK) return rc;
+  cudaStream_t st = ctx->stream;
+  const int32_t M = ctx->M, P = ctx->P, B = M + P;
+  const int64_t n = ctx->last_n;
+  for (int32_t m = 0; m < M; m++) model_max_qd_ns[m] = 0;
+  const size_t nh = (size_t)M * hist_stride;
+  // scratch: arrivals [M] | qd [M] | p99 [M] | hist [M*stride] | err
+  unsigned long long* d = nullptr;
+  CK(cudaMallocAsync((void**)&d, sizeof(unsigned long long) * (3 * (size_t)M + nh + 1), st));
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * (3 * (size_t)M + nh + 1), st));
+  std::vector<unsigned long long> arr(model_arrivals, model_arrivals + M);
+  CK(cudaMemcpyAsync(d, arr.data(), sizeof(unsigned long long) * M, cudaMemcpyHostToDevice, st));
+  unsigned long long* d_qd = d + M;
+  long long* d_p99 = reinterpret_cast<long long*>(d + 2 * M);
+  unsigned long long* d_hist = d + 3 * (size_t)M;
+  int32_t* d_err = reinterpret_cast<int32_t*>(d + 3 * (size_t)M + nh);
+  const int32_t* model_of_slot = ctx->d_bins + B + P + 2;
+  if (n > 0) {
+    k_stat_keys<<<nblk(n, 256), 256, 0, st>>>(ctx->last_ticks, ctx->last_model,
+                                              ctx->last_outcome, ctx->last_start,
+                                              ctx->last_finish, ctx->d_slot_of_model, n, lo_ns,
+                                              hi_ns, M, ctx->d_bkA, ctx->d_bvA, d_qd, d_err);
+    int bits = kStatLatBits;
+    while ((int64_t(1) << (bits - kStatLatBits)) <= M) bits++;
+    const int64_t W = (n + kChunkR - 1) / kChunkR;
+    for (int shift = 0; shift < bits; shift += kDigitBits) {
+      k_rhist<<<nblk(W, kRadixWarps), 32 * kRadixWarps, 0, st>>>(ctx->d_bkA, n, shift,
+                                                                 ctx->d_rhist, W);
+      const int64_t len = W * kDigits, nparts = (len + kScanItems - 1) / kScanItems;
+      k_scan_up<<<nparts, 1024, 0, st>>>(ctx->d_rhist, len, ctx->d_scan_part);
+      k_scan_mid<<<1, 1024, 0, st>>>(ctx->d_scan_part, nparts);
+      k_scan_down<<<nparts, 1024, 0, st>>>(ctx->d_rhist, len, ctx->d_scan_part);
+      k_rscatter<<<nblk(W, kRadixWarps), 32 * kRadixWarps, 0, st>>>(
+          ctx->d_bkA, ctx->d_bvA, n, shift, ctx->d_rhist, W, ctx->d_bkB, ctx->d_bvB);
+      std::swap(ctx->d_bkA, ctx->d_bkB);
+      std::swap(ctx->d_bvA, ctx->d_bvB);
+    }
+    k_stat_p99<<<1, 1024, 0, st>>>(ctx->d_bkA, d, model_of_slot, M, d_p99);
+  }
+  int64_t total = 0;
+  for (int64_t c : ctx->last_nrecs) total += c;
+  if (total > 0)  // d_meta still holds this run's rec_base / rec_count (sym_window_counts)
+    k_stat_hist<<<nblk(total, 256), 256, 0, st>>>(ctx->d_recs, ctx->d_meta,
+                                                   ctx->d_meta + P + 1, P, ctx->d_slot_base,
+                                                   model_of_slot, total, lo_ns, hi_ns,
+                                                   hist_stride, d_hist);
+  CK(cudaGetLastError());
+  std::vector<unsigned long long> h(3 * (size_t)M + nh + 1);
+  CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(),
+                     cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(d, st);
+  CK(cudaStreamSynchronize(st));
+  if (reinterpret_cast<int32_t*>(&h[3 * (size_t)M + nh])[0]) {
+    ctx->err = "sym_window_stats: a latency exceeds the 40-bit sort key";
+    return SYM_EINVAL;
+  }
+  for (int32_t m = 0; m < M; m++) {
+    model_max_qd_ns[m] = (int64_t)h[M + m];
+    model_p99_ns[m] = n > 0 ? (int64_t)(long long)h[2 * M + m] : 0;
+  }
+  for (size_t k = 0; k < nh; k++) model_batch_hist[k] = (int64_t)h[3 * (size_t)M + k];
   return SYM_OK;
 }
 

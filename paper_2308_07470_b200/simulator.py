@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+import weakref
 from collections.abc import Sequence
 from dataclasses import dataclass, field
 from types import SimpleNamespace
@@ -91,6 +92,18 @@ class RunResult:
     #: batch records (numpy structured array, _native.BATCH_DTYPE), the
     #: compact form gpu_logs is derived from
     batches: np.ndarray | None = None
+    #: (weakref to the Engine, its run id): while the engine's last run is
+    #: this one, compute_stats can reduce on the device (sym_window_stats)
+    _source: tuple | None = field(default=None, repr=False, compare=False)
+
+    def device_engine(self):
+        """The Engine still holding this run on the device, else None."""
+        if self._source is None:
+            return None
+        eng = self._source[0]()
+        if eng is None or eng._handle is None or eng._run_id != self._source[1]:
+            return None
+        return eng
 
     @property
     def n_requests(self) -> int:
@@ -151,6 +164,7 @@ class Engine:
         self._timeout = np.array([policy.resolve_timeout_ns(m.slo_ns) for m in self.models],
                                  np.int64)
         self._handle = None
+        self._run_id = 0
         self._lib = None
         # reference-style counters (RankPlane.ops/evictions/registrations,
         # Engine.handler_ops_max), filled after each run
@@ -282,6 +296,7 @@ class Engine:
             res.drop_t = drop_t.ctypes.data_as(_native.i64p)
             res.drop_key_sub = drop_ks.ctypes.data_as(_native.i64p)
             res.drop_key_a = drop_ka.ctypes.data_as(_native.i32p)
+        self._run_id += 1
         rc = self._lib.sym_run(self._handle, ticks.ctypes.data, midx.ctypes.data, n,
                                self._flags() | _native.FLAG_MODEL_I64, C.byref(res))
         copier.join()
@@ -306,7 +321,7 @@ class Engine:
             # (simulator.py:251-252)
             completions=n - int(res.drops),
             late=int(np.count_nonzero(outc == OUTCOME_LATE)) if self._jitter is not None else 0,
-            batches=batches)
+            batches=batches, _source=(weakref.ref(self), self._run_id))
         if self.record_trace:
             result.trace = self._build_trace(ticks, midx, batches, drop_t, drop_ks, drop_ka)
         if self.check_invariants:
@@ -333,6 +348,32 @@ class Engine:
         if rc != _native.SYM_OK:
             self._raise(rc, _native.SymResult())
         out["gpu_busy_ns"] = busy
+        return out
+
+    def window_stats(self, lo_ns: int, hi_ns: int) -> dict:
+        """window_counts plus the rest of compute_stats' per-model inputs,
+        reduced on the device from the last run (sym_window_stats): p99
+        latency by nearest rank (drops as +inf; -1 = inf, 0 = no arrivals),
+        largest queueing delay of a served request, and the batch-size
+        histogram of batches starting in the window ([M][max_batch + 1])."""
+        if self._handle is None:
+            raise RuntimeError("no run to reduce")
+        M, G = len(self.models), self.gpu_count
+        stride = int(self._max_batch.max()) + 1 if M else 1
+        keys = ("arrivals", "completed", "late", "dropped")
+        out = {k: np.zeros(M, np.int64) for k in keys + ("p99_ns", "max_qd_ns")}
+        busy = np.zeros(G, np.int64)
+        hist = np.zeros((M, stride), np.int64)
+        rc = self._lib.sym_window_stats(
+            self._handle, int(lo_ns), int(hi_ns),
+            *(out[k].ctypes.data_as(_native.i64p) for k in keys),
+            busy.ctypes.data_as(_native.i64p), out["p99_ns"].ctypes.data_as(_native.i64p),
+            out["max_qd_ns"].ctypes.data_as(_native.i64p), hist.ctypes.data_as(_native.i64p),
+            stride)
+        if rc != _native.SYM_OK:
+            self._raise(rc, _native.SymResult())
+        out["gpu_busy_ns"] = busy
+        out["batch_hist"] = hist
         return out
 
     def kernel_times(self, reset: bool = True) -> dict:
@@ -377,6 +418,7 @@ class Engine:
         if kernel_times:
             flags |= _native.FLAG_KERNEL_TIMES
         torch.cuda.current_stream(dev).synchronize()
+        self._run_id += 1
         rc = self._lib.sym_run_device(self._handle, ticks.data_ptr(), model.data_ptr(), n,
                                       flags, C.byref(res))
         if rc != _native.SYM_OK:
