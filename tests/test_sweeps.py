@@ -27,6 +27,7 @@ def _check(rows, want):
 def test_sweep_rows_oracle(case, golden, monkeypatch):
     from resultcheck import oracle_run_scenario
     monkeypatch.setattr(metrics, "run_scenario", oracle_run_scenario)
+    monkeypatch.setattr(metrics, "BATCH_PROBES", False)
     monkeypatch.setattr(sweeps, "run_scenario", oracle_run_scenario)
     dim, name, grid, pols, peak = case
     rows = sweeps.run_sweep(dim, load_scenario(name), grid, pols, peak)
@@ -56,6 +57,7 @@ def test_speculative_search_equals_sequential(speculate, golden, monkeypatch):
     rate, same recorded probes (metrics.py:229-256 known answers)."""
     from resultcheck import oracle_run_scenario
     monkeypatch.setattr(metrics, "run_scenario", oracle_run_scenario)
+    monkeypatch.setattr(metrics, "BATCH_PROBES", False)
     for name, want in golden["known_answers"]["goodput_search"].items():
         res = metrics.goodput_search(load_scenario(name), speculate=speculate)
         assert res.rate_rps == want["rate_rps"]
@@ -65,6 +67,7 @@ def test_speculative_search_equals_sequential(speculate, golden, monkeypatch):
 def test_speculative_search_respects_max_iters(monkeypatch):
     from resultcheck import oracle_run_scenario
     monkeypatch.setattr(metrics, "run_scenario", oracle_run_scenario)
+    monkeypatch.setattr(metrics, "BATCH_PROBES", False)
     sc = load_scenario("table2_inceptionresnet")
     for it in (1, 2, 4):
         a = metrics.goodput_search(sc, max_iters=it, keep_stats=True)
@@ -82,3 +85,29 @@ def test_sweep_rows_engine_speculative(case, golden):
     rows = sweeps.run_sweep(dim, load_scenario(name), grid, pols, peak, workers=4,
                             speculate=3)
     _check(rows, golden["sweeps"][f"{dim}/{name}"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("speculate", [2, 3])
+def test_batched_speculative_search_on_engine(speculate, golden):
+    """Speculative rounds as sub-clusters of one engine call reproduce the
+    sequential search exactly (rate and recorded probes)."""
+    for name, want in golden["known_answers"]["goodput_search"].items():
+        res = metrics.goodput_search(load_scenario(name), speculate=speculate, keep_stats=True)
+        assert res.rate_rps == want["rate_rps"]
+        assert [list(p) for p in res.probes] == [list(p) for p in want["probes"]]
+        seq = metrics.goodput_search(load_scenario(name), keep_stats=True)
+        assert res.stats_at_rate == seq.stats_at_rate
+
+
+@pytest.mark.gpu
+def test_probe_batch_equals_single_probes():
+    sc = load_scenario("fig4b_timeout_zoo")
+    rates = [sc.workload.rate_rps * f for f in (0.5, 0.9, 1.3, 2.0)] if hasattr(
+        sc.workload, "rate_rps") else None
+    if rates is None:
+        pytest.skip("scenario has no scalar rate")
+    batched = metrics.probe_batch(sc, rates)
+    for r, (ok, st) in zip(rates, batched):
+        ok1, st1 = metrics.probe_feasible(sc, r)
+        assert ok == ok1 and st == st1
