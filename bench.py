@@ -40,13 +40,15 @@ BATCH_REC_BYTES = 64   # sizeof(BatchRec) / sizeof(sym_batch)
 EV_BATCH_BYTES = 56    # sizeof(EvBatch)
 
 
-def algorithmic_bytes(kernel: str, n: int, nb: int) -> float | None:
+def algorithmic_bytes(kernel: str, n: int, nb: int, shards: int = 1) -> float | None:
     """Minimal DRAM bytes one launch of `kernel` must move for n requests and
-    nb batches (DESIGN.md §5 derives each line)."""
+    nb batches over `shards` sub-clusters (DESIGN.md §5 derives each line)."""
     table = {
-        # stable partition: read tick+model, write s_tick, s_g, s_i, sh_tick,
-        # the inverse map, the model slot and the batch-id reset
-        "k_scatter": n * (8 + 4 + 8 + 4 + 4 + 8 + 4 + 4 + 4),
+        # stable partition: read tick+model, write s_tick, s_i, the inverse
+        # map, the model slot and the batch-id reset; with several shards
+        # also the shard-stream index s_g and the shard-ordered ticks sh_tick
+        # (one shard: those alias s_i and the input ticks)
+        "k_scatter": n * (8 + 4 + 8 + 4 + 4 + 4 + 4 + (4 + 8 if shards > 1 else 0)),
         "k_hist": n * 4,
         "k_aself": n * (4 + 8 + 8 + 4),
         # fresh-start pre-scan: read each sorted arrival once (tick, A', g),

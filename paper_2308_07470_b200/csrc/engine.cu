@@ -297,11 +297,15 @@ __global__ void k_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t M,
 // offsets (warp order = stream order), and a second pass over the values
 // kept in registers ranks every element.  The chunk is staged in shared
 // memory in bin order and written out as bin runs of ~kChunkI/M elements.
+// With one shard the shard stream is the stream itself (j == i): the
+// <false> instance writes neither s_g nor sh_tick, which then alias s_i and
+// the input ticks.
 __host__ __device__ inline size_t scatter_smem(int B) {
   return (size_t)kChunkI * (sizeof(int64_t) + 3 * sizeof(int32_t)) +
          sizeof(int32_t) * ((size_t)kIngestWarps * B + 2 * (size_t)B + 32);
 }
 
+template <bool kShards>
 __global__ void __launch_bounds__(32 * kIngestWarps)
 k_scatter(const int64_t* __restrict__ ticks,
           const int32_t* __restrict__ model, int64_t n,
@@ -348,8 +352,10 @@ k_scatter(const int64_t* __restrict__ ticks,
       t[r] = ticks[i];
     }
     if (sl[r] >= 0) atomicAdd_block(&mine[sl[r]], 1);  // counting only
-    const unsigned pd = __match_any_sync(0xffffffffu, sd[r]);
-    if (sl[r] >= 0 && (pd >> lane) == 1u) atomicAdd_block(&mine[sd[r]], __popc(pd));
+    if (kShards) {
+      const unsigned pd = __match_any_sync(0xffffffffu, sd[r]);
+      if (sl[r] >= 0 && (pd >> lane) == 1u) atomicAdd_block(&mine[sd[r]], __popc(pd));
+    }
     __syncwarp();
   }
   // bases from the scanned histogram; per-warp offsets; local bin starts
@@ -408,22 +414,25 @@ k_scatter(const int64_t* __restrict__ ticks,
     const int64_t i = wlo + r * 32 + lane;
     const bool act = i < hi;
     const unsigned ps = __match_any_sync(0xffffffffu, sl[r]);
-    const unsigned pd = __match_any_sync(0xffffffffu, sd[r]);
+    unsigned pd = 0;
+    if (kShards) pd = __match_any_sync(0xffffffffu, sd[r]);
     int32_t e = 0, j = 0;
     if (act) {
       e = mine[sl[r]] + __popc(ps & lt);
-      j = gbase[sd[r]] + mine[sd[r]] + __popc(pd & lt);
+      if (kShards) j = gbase[sd[r]] + mine[sd[r]] + __popc(pd & lt);
     }
     __syncwarp();
     if (act) {
       if ((ps >> lane) == 1u) mine[sl[r]] += __popc(ps);  // highest peer advances
-      if ((pd >> lane) == 1u) mine[sd[r]] += __popc(pd);
       const int32_t le = lstart[sl[r]] + e;
       st_t[le] = t[r];
-      st_g[le] = j;
       st_i[le] = (int32_t)i;
       st_b[le] = sl[r];
-      sh_tick[j] = t[r];
+      if (kShards) {
+        if ((pd >> lane) == 1u) mine[sd[r]] += __popc(pd);
+        st_g[le] = j;
+        sh_tick[j] = t[r];
+      }
       inv[i] = gbase[sl[r]] + e;  // coalesced in i
     }
     __syncwarp();
@@ -434,7 +443,7 @@ k_scatter(const int64_t* __restrict__ ticks,
     const int32_t b = st_b[e];
     const int32_t pos = gbase[b] + (e - lstart[b]);
     s_tick[pos] = st_t[e];
-    s_g[pos] = st_g[e];
+    if (kShards) s_g[pos] = st_g[e];
     s_i[pos] = st_i[e];
     s_slot[pos] = b;
     bid[pos] = -1;  // "no batch" until k_bid
@@ -1650,7 +1659,9 @@ struct KernelTimer {
       cudaEventSynchronize(m.second.second);
       float ms = 0;
       cudaEventElapsedTime(&ms, m.second.first, m.second.second);
-      auto& acc = ctx->ktimes[m.first];
+      std::string key(m.first);
+      key = key.substr(0, key.find('<'));  // one entry per kernel template
+      auto& acc = ctx->ktimes[key];
       acc.first += 1;
       acc.second += ms;
       cudaEventDestroy(m.second.first);
@@ -1728,8 +1739,13 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     ctx->err = "arrival ticks must be non-decreasing";
     return SYM_EINVAL;
   }
-  if (W > 0)
-    KL(k_scatter, W, 32 * kIngestWarps, scatter_smem(B), st>>>(
+  if (W > 0 && P > 1)
+    KL(k_scatter<true>, W, 32 * kIngestWarps, scatter_smem(B), st>>>(
+        d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
+        ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
+        ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot, ctx->d_bid));
+  else if (W > 0)
+    KL(k_scatter<false>, W, 32 * kIngestWarps, scatter_smem(B), st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
         ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot, ctx->d_bid));
@@ -1740,8 +1756,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   for (int s = 0; s < P; s++) {
     Shard& S = ctx->shards[s];
     S.s_tick = ctx->d_s_tick;
-    S.s_g = ctx->d_s_g;
-    S.sh_tick = ctx->d_sh_tick;
+    S.s_g = P > 1 ? ctx->d_s_g : ctx->d_s_i;  // one shard: j == i
+    S.sh_tick = P > 1 ? ctx->d_sh_tick : d_ticks;
     S.sh_base = shard_off[s];
     S.record_trace = trace ? 1 : 0;
     S.drop_t = ctx->d_drop_t;
@@ -2318,7 +2334,9 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
       return fail("smem attribute", e);
     const size_t sc = scatter_smem(ctx->M + ctx->P);
     if (sc > (size_t)dev_max) return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
-    if ((e = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(k_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sc)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sc)) != cudaSuccess)
       return fail("scatter smem attribute", e);
   }
