@@ -140,6 +140,16 @@ def test_edge_cases():
     assert r.drops == 100  # d_ctrl + d_data + l(1) > SLO: everything dropped
     with pytest.raises(ProtocolError):
         Engine(unit, 1, pol).run_stream(np.array([0, 1]), np.array([0, 2]), 1.0)
+    # many models, almost all idle; a large GPU pool with one request
+    many = [ModelSpec(i, f"m{i}", LatencyProfile.linear(0.25 + 0.01 * (i % 7), 1.0 + i % 5, 256),
+                      ms_to_ns(20.0 + i % 13)) for i in range(1000)]
+    both([0, 0, 3, 1_000_000], [999, 0, 500, 999], gpus=8192, models=many)
+    # one tick, full max_batch batches across several models and GPUs, each policy
+    burst_t = [7_000] * 3000
+    burst_m = [(k * 7) % 5 for k in range(3000)]
+    for pk in ("deferred", "eager", "timeout"):
+        kw = {"timeout_slo_frac": 0.3} if pk == "timeout" else {}
+        both(burst_t, burst_m, gpus=4, models=many[:5], policy=PolicyConfig(pk, **kw))
 
 
 def test_goodput_search_known_answers(golden):
