@@ -1719,6 +1719,10 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   if (n > 0)
     CK(cudaMemcpyAsync(&last_tick, d_ticks + (n - 1), sizeof last_tick,
                        cudaMemcpyDeviceToHost, st));
+  // per-model arrival counts (k_binoff) ride on the same readback
+  std::vector<ModelParam> mp(M);
+  CK(cudaMemcpyAsync(mp.data(), ctx->d_mp, sizeof(ModelParam) * M,
+                     cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   // every event tick and finish time of a validated run is below the last
   // arrival + SLO; the bound is generous and checked (FP_CAPACITY)
@@ -1765,10 +1769,6 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     S.drop_ka = ctx->d_drop_ka;
   }
   // record capacity per shard: its arrival count (+1)
-  std::vector<ModelParam> mp(M);
-  CK(cudaMemcpyAsync(mp.data(), ctx->d_mp, sizeof(ModelParam) * M,
-                     cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
   std::vector<int64_t> rec_base(P + 1, 0);
   for (int s = 0; s < P; s++) {
     int64_t cnt = 0;
@@ -1945,12 +1945,14 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   CK(cudaGetLastError());
   pc.mark("chain");
   CK(cudaEventRecord(ctx->ev[3], st));
-  CK(cudaMemcpyAsync(ctx->shards.data(), ctx->d_shards, sizeof(Shard) * P,
-                     cudaMemcpyDeviceToHost, st));
   std::vector<ModelState> ms(M);
-  CK(cudaMemcpyAsync(ms.data(), ctx->d_ms, sizeof(ModelState) * M,
-                     cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if (n_chain > 0) {  // otherwise the host copy is current and ms is unused
+    CK(cudaMemcpyAsync(ctx->shards.data(), ctx->d_shards, sizeof(Shard) * P,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ms.data(), ctx->d_ms, sizeof(ModelState) * M,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
   int64_t total = 0;
   std::vector<int64_t> rec_count(P);
   for (int s = 0; s < P; s++) {
