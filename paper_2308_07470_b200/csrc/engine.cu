@@ -300,13 +300,13 @@ __global__ void k_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t M,
 // With one shard the shard stream is the stream itself (j == i): the
 // <false> instance writes neither s_g nor sh_tick, which then alias s_i and
 // the input ticks.
-__host__ __device__ inline size_t scatter_smem(int B) {
-  return (size_t)kChunkI * (sizeof(int64_t) + 3 * sizeof(int32_t)) +
+__host__ __device__ inline size_t scatter_smem(int B, bool shards) {
+  return (size_t)kChunkI * (sizeof(int64_t) + (shards ? 2 : 1) * sizeof(int32_t) + sizeof(int16_t)) +
          sizeof(int32_t) * ((size_t)kIngestWarps * B + 2 * (size_t)B + 32);
 }
 
 template <bool kShards>
-__global__ void __launch_bounds__(32 * kIngestWarps)
+__global__ void __launch_bounds__(32 * kIngestWarps, kShards ? 4 : 6)
 k_scatter(const int64_t* __restrict__ ticks,
           const int32_t* __restrict__ model, int64_t n,
           const int32_t* __restrict__ slot_of_model,
@@ -324,13 +324,14 @@ k_scatter(const int64_t* __restrict__ ticks,
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = blockIdx.x;
   int64_t* st_t = reinterpret_cast<int64_t*>(smem_raw);
-  int32_t* st_g = reinterpret_cast<int32_t*>(st_t + kChunkI);
-  int32_t* st_i = st_g + kChunkI;
-  int32_t* st_b = st_i + kChunkI;
-  int32_t* wcnt = st_b + kChunkI;          // [warp][bin] counts -> offsets
+  int32_t* st_g = reinterpret_cast<int32_t*>(st_t + kChunkI);  // kShards only
+  int32_t* st_i = kShards ? st_g + kChunkI : st_g;
+  int32_t* wcnt = st_i + kChunkI;          // [warp][bin] counts -> offsets
   int32_t* gbase = wcnt + kIngestWarps * B;  // global base of (bin, chunk)
   int32_t* lstart = gbase + B;             // local start of a slot bin
   int32_t* scratch = lstart + B;           // [32] block scan of bin counts
+  // bin of each staged element; B < 2^15 (the smem check in sym_create)
+  int16_t* st_b = reinterpret_cast<int16_t*>(scratch + 32);
   int32_t* mine = wcnt + wib * B;
   for (int b = lane; b < B; b += 32) mine[b] = 0;
   // pass 1: load this lane's elements once, count the warp's bins
@@ -427,7 +428,7 @@ k_scatter(const int64_t* __restrict__ ticks,
       const int32_t le = lstart[sl[r]] + e;
       st_t[le] = t[r];
       st_i[le] = (int32_t)i;
-      st_b[le] = sl[r];
+      st_b[le] = (int16_t)sl[r];
       if (kShards) {
         if ((pd >> lane) == 1u) mine[sd[r]] += __popc(pd);
         st_g[le] = j;
@@ -1744,12 +1745,12 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     return SYM_EINVAL;
   }
   if (W > 0 && P > 1)
-    KL(k_scatter<true>, W, 32 * kIngestWarps, scatter_smem(B), st>>>(
+    KL(k_scatter<true>, W, 32 * kIngestWarps, scatter_smem(B, true), st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
         ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot, ctx->d_bid));
   else if (W > 0)
-    KL(k_scatter<false>, W, 32 * kIngestWarps, scatter_smem(B), st>>>(
+    KL(k_scatter<false>, W, 32 * kIngestWarps, scatter_smem(B, false), st>>>(
         d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
         ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot, ctx->d_bid));
@@ -2334,8 +2335,8 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     if ((e = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ctx->chain_smem)) != cudaSuccess)
       return fail("smem attribute", e);
-    const size_t sc = scatter_smem(ctx->M + ctx->P);
-    if (sc > (size_t)dev_max) return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
+    const size_t sc = scatter_smem(ctx->M + ctx->P, true);  // >= the <false> size
+    if (sc > (size_t)dev_max || ctx->M + ctx->P >= 32768) return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
     if ((e = cudaFuncSetAttribute(k_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sc)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(k_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
