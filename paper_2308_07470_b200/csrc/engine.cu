@@ -825,14 +825,28 @@ k_evolve(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base
 // forward by ~a batch per hop), so four doublings' worth of pointer chasing
 // costs one read, three L2-local gathers and one write per position.
 // first: jin is the raw chain pointer (NX_* sentinels -> -1).
-__global__ void k_jump4(const int32_t* __restrict__ jin, int32_t* __restrict__ jout,
-                        int64_t n) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  int32_t v = jin[p];
+// Each thread follows kJumpIlp independent chains (block-strided, so loads
+// and stores stay coalesced) with their gathers interleaved: the pass is
+// bound by dependent L2 latency, not bytes.
+constexpr int kJumpIlp = 4;
+__global__ void __launch_bounds__(256)
+k_jump4(const int32_t* __restrict__ jin, int32_t* __restrict__ jout, int64_t n) {
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x * kJumpIlp + threadIdx.x;
+  int32_t v[kJumpIlp];
 #pragma unroll
-  for (int h = 0; h < 3; h++) v = v >= 0 ? jin[v] : -1;
-  jout[p] = v >= 0 ? v : -1;
+  for (int k = 0; k < kJumpIlp; k++) {
+    const int64_t p = base + (int64_t)k * blockDim.x;
+    v[k] = p < n ? jin[p] : -1;
+  }
+#pragma unroll
+  for (int h = 0; h < 3; h++)
+#pragma unroll
+    for (int k = 0; k < kJumpIlp; k++) v[k] = v[k] >= 0 ? jin[v[k]] : -1;
+#pragma unroll
+  for (int k = 0; k < kJumpIlp; k++) {
+    const int64_t p = base + (int64_t)k * blockDim.x;
+    if (p < n) jout[p] = v[k] >= 0 ? v[k] : -1;
+  }
 }
 
 constexpr int kJump = 64;  // batches per checkpoint (J_64)
@@ -1813,10 +1827,10 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     const int64_t ncp = n / kJump + M + 2;
     CK(cudaMemsetAsync(ctx->d_cp_model, 0xff, sizeof(int32_t) * ncp, st));
     // J_4, J_16, J_64 (kept in jC), J_256 by quadrupling the chain pointer
-    KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_nxt, ctx->d_jA, n));
-    KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jA, ctx->d_jB, n));
-    KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jB, ctx->d_jC, n));
-    KL(k_jump4, nblk(n, 256), 256, 0, st>>>(ctx->d_jC, ctx->d_jA, n));
+    KL(k_jump4, nblk(n, 256 * kJumpIlp), 256, 0, st>>>(ctx->d_nxt, ctx->d_jA, n));
+    KL(k_jump4, nblk(n, 256 * kJumpIlp), 256, 0, st>>>(ctx->d_jA, ctx->d_jB, n));
+    KL(k_jump4, nblk(n, 256 * kJumpIlp), 256, 0, st>>>(ctx->d_jB, ctx->d_jC, n));
+    KL(k_jump4, nblk(n, 256 * kJumpIlp), 256, 0, st>>>(ctx->d_jC, ctx->d_jA, n));
     KL(k_walk, nblk(M, 64), 64, 0, st>>>(ctx->d_mp, M, ctx->d_nxt, ctx->d_jB, ctx->d_jC,
                                          ctx->d_jA,
                                          ctx->d_cp_pos, ctx->d_cp_model, ctx->d_nb,
