@@ -1121,7 +1121,7 @@ k_rscatter(const uint64_t* __restrict__ kin,
 // [2^(r+1) p, 2^(r+1) p + 2^r) and [.. + 2^r, 2^(r+1) (p+1)).  The key is
 // (shard << tb | tick); equal keys fall back to the full batch_cmp order
 // (A', pusher position, chain before arrival), so no fix-up pass is needed.
-constexpr int kMergeItems = 8;  // outputs per thread
+constexpr int kMergeItems = 4;  // outputs per thread
 
 __device__ __forceinline__ int64_t run_bound(const int32_t* __restrict__ bbase, int32_t M,
                                              int64_t nt, int64_t m) {
