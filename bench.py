@@ -1,22 +1,26 @@
-"""Benchmark: requests scheduled per second (device-timed) on the C4 workload.
+"""Benchmark: requests scheduled per second (device-timed) on BASELINE's C4.
 
 Workload (BASELINE.json configs[3]): 1000 A100-zoo models x
 8192 simulated GPUs, Poisson 1.2M req/s aggregate over a 60 s trace, seed 42,
-partitioned into P=8 sub-clusters of 125 contiguous models and 1024 GPUs
-("models sharded across 8xB200").  Rank r of N runs sub-cluster r, so the
-per-GPU work is fixed (weak scaling) and N=8 is exactly C4 on 8 B200s.
+partitioned into P=8 sub-clusters of 125 contiguous models and 1024 GPUs.
+The configuration is fixed and the GPU count varies (strong scaling): rank r
+of N runs sub-clusters {s : s mod N == r} in ONE engine call, so N=1 is the
+whole of C4 (72M requests) on one B200 and N=8 is one sub-cluster per B200.
 
-A step is one pass of the hot path over the rank's whole sub-cluster trace
-(~9.0M requests): ingest -> fresh-start pre-scan -> batch chains ->
-per-request RunResult arrays, inputs resident in HBM (the parallel
-validated fast path resolves the sub-cluster; the sequential live-event
-chain takes over for any sub-cluster that fails validation).  `value` is the
-whole-job throughput; `e2e` is the same metric through the public API
-(Engine.run_stream: host arrays in, RunResult out, H2D/D2H inside).
+A step is one pass of the hot path over the rank's whole trace, inputs
+resident in HBM: ingest (stable partition) -> window/chain pointers (K2) ->
+batch chains -> batch order -> matchmaking (K3) -> per-request RunResult
+arrays.  The parallel validated path resolves every C4 sub-cluster; the exact
+sequential chain would take over any sub-cluster that failed validation.
+``value`` is the whole-job throughput (all requests / max-over-ranks device
+time); ``e2e`` is the same metric through the public API (Engine.run_stream:
+pinned host arrays in, RunResult out, H2D/D2H inside the timed region).
+Every rank checks its device results bit for bit against the CPU oracle
+(oracle/, a C restatement of batchsym's loop) before printing.
 
---impl reference times the reference algorithm's CPU restatement
-(oracle/, a C port of batchsym's event loop) on the host cores over the
-same sub-clusters.
+--impl reference times that CPU restatement of the reference algorithm on
+the host cores over the same C4 sub-clusters (one thread per sub-cluster,
+the reference scalebench's process-per-shard layout).
 """
 from __future__ import annotations
 
@@ -35,57 +39,54 @@ sys.path.insert(0, ROOT)
 
 METRIC = "requests scheduled/sec (device-timed) at 1/2/4/8 B200; goodput bit-exact vs CPU ref"
 UNIT = "requests/s"
+N_SUBCLUSTERS = 8
 FRESH_REC_BYTES = 128  # sizeof(FreshRec)
 BATCH_REC_BYTES = 64   # sizeof(BatchRec) / sizeof(sym_batch)
 EV_BATCH_BYTES = 56    # sizeof(EvBatch)
 
+# SURVEY.md §8(d) algorithmic bytes of the three kernels north_star names
+# (n requests, nb batches, G simulated GPUs of the launch):
+#   K1 ingest       24 B per request (read tick+model 12, write 12 permuted)
+#   K2 window       12 B per arrival scanned (the per-model state and the
+#                   log2(max_batch) l(b) probes are negligible at this size)
+#   K3 matchmaking  8 B per GPU free_at + 24 B per ready candidate + 12 B
+#                   written per grant
+SURVEY_KERNELS = {
+    "K1": ("k_scatter", lambda n, nb, g: 24 * n),
+    "K2": ("k_nxt_pp", lambda n, nb, g: 12 * n),
+    "K3": ("k_match_coop", lambda n, nb, g: 36 * nb + 8 * g),
+}
 
-def algorithmic_bytes(kernel: str, n: int, nb: int, shards: int = 1) -> float | None:
-    """Minimal DRAM bytes one launch of `kernel` must move for n requests and
-    nb batches over `shards` sub-clusters (DESIGN.md §5 derives each line)."""
+
+def design_bytes(kernel: str, n: int, nb: int, shards: int) -> float | None:
+    """Minimal DRAM bytes one launch of a kernel outside §8(d)'s three must
+    move (DESIGN.md §5 derives each line)."""
     table = {
-        # stable partition: read tick+model, write s_tick, s_i, the inverse
-        # map, the model slot and the batch-id reset; with several shards
-        # also the shard-stream index s_g and the shard-ordered ticks sh_tick
-        # (one shard: those alias s_i and the input ticks)
-        "k_scatter": n * (8 + 4 + 8 + 4 + 4 + 4 + 4 + (4 + 8 if shards > 1 else 0)),
         "k_hist": n * 4,
-        "k_aself": n * (4 + 8 + 8 + 4),
-        # fresh-start pre-scan: read each sorted arrival once (tick, A', g),
-        # write one FreshRec and one chain pointer per position
         "k_fresh": n * (8 + 4 + 4 + FRESH_REC_BYTES + 4),
-        # lean chain pointer: each sorted tick read once (neighbours share
-        # the line), one 4-byte pointer written per position
-        "k_nxt": n * (8 + 4),
-        "k_nxt_pp": n * (8 + 4 + 4),
-        "k_nxt_general": n * 4,
-        # batch records from the chain positions' fresh scans: the members'
-        # ticks/ids once, one EvBatch written per batch
+        "k_nxt_general": 0,
         "k_chain_recs": n * (8 + 4 + 4) + nb * (4 + EV_BATCH_BYTES + 8 + 4),
-        "k_walk": 0,
-        # match + pointer jumping (~log2(nb/G) rounds) + tie repair, one launch
-        "k_match_coop": nb * (8 + 4 + 4 + 4) + nb * 12 * 12,
         "k_token_keys": nb * (4 + 8 + EV_BATCH_BYTES + 8 + 4),
-        # J_4k = (J_k)^4: read own pointer, one write; the three gathers
-        # re-read the same 4n-byte array, which L2 holds, so they are not
-        # counted as DRAM bytes
         "k_jump4": n * (4 + 4),
-        # stable merge-path round over the batch runs: read and write key+value
         "k_merge_round": nb * (12 + 12),
-        "k_walk_expand": nb * (FRESH_REC_BYTES + 4 + EV_BATCH_BYTES),
+        "k_walk_expand": nb * (4 + EV_BATCH_BYTES),
         "k_rscatter": nb * (12 + 12),
         "k_rhist": nb * 8,
-        "k_scan_up": None, "k_scan_mid": None, "k_scan_down": None,
         "k_fast_emit": nb * (EV_BATCH_BYTES + 12 + 4 + 8 + BATCH_REC_BYTES),
-        # per-request RunResult arrays from batch records
-        "k_fill32": n * 4,
         "k_bid": nb * BATCH_REC_BYTES + n * 4,
-        # one thread per request: inverse map, batch id, tick, model read,
-        # five int64 written coalesced; batch records read once
         "k_out": n * (4 + 4 + 8 + 4 + 5 * 8) + nb * BATCH_REC_BYTES,
         "k_copy_batches": nb * (BATCH_REC_BYTES + 4 + 64),
     }
     return table.get(kernel)
+
+
+def kernel_bytes(kernel: str, n: int, nb: int, g: int, shards: int):
+    """(bytes per launch, source) -- §8(d) for K1/K2/K3, else DESIGN."""
+    for tag, (name, fn) in SURVEY_KERNELS.items():
+        if name == kernel:
+            return fn(n, nb, g), f"SURVEY §8(d) {tag}"
+    b = design_bytes(kernel, n, nb, shards)
+    return b, ("DESIGN.md §5" if b is not None else None)
 
 
 def dist_env():
@@ -93,16 +94,70 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def build_workload(duration_s: float, shard: int):
+def my_subclusters(rank: int, world: int) -> list[int]:
+    return [s for s in range(N_SUBCLUSTERS) if s % world == rank]
+
+
+def build_workload(duration_s: float, subclusters: list[int]):
+    """The C4 trace restricted to the given sub-clusters, their models
+    renumbered contiguously in sub-cluster order.  Returns the scenario,
+    the engine arguments and each sub-cluster's (models, gpus, stream
+    indices) for the oracle."""
     from paper_2308_07470_b200 import configs
     from paper_2308_07470_b200.workload import generate_arrivals
     sc = configs.c4(duration_s)
     ticks, midx = generate_arrivals(sc.workload, [m.name for m in sc.models], duration_s,
                                     configs.SEED)
-    ms, gpus, ids = configs.shard_scenarios(sc)[shard]
-    sel = (midx >= ids[0]) & (midx <= ids[-1])
-    return sc, list(ms), gpus, np.ascontiguousarray(ticks[sel]), \
-        np.ascontiguousarray(midx[sel] - ids[0])
+    parts = configs.shard_scenarios(sc)
+    new_id = np.full(len(sc.models), -1, np.int64)
+    models, som, gps, k = [], [], [], 0
+    from dataclasses import replace
+    for j, s in enumerate(subclusters):
+        ms, g, ids = parts[s]
+        for i in ids:
+            new_id[i] = k
+            models.append(replace(sc.models[i], model_id=k))
+            som.append(j)
+            k += 1
+        gps.append(g)
+    m2 = new_id[midx]
+    keep = m2 >= 0
+    t_sel = np.ascontiguousarray(ticks[keep])
+    m_sel = np.ascontiguousarray(m2[keep])
+    som_a = np.asarray(som, np.int32)
+    per = []
+    base = 0
+    for j, s in enumerate(subclusters):
+        ms, g, ids = parts[s]
+        idx = np.nonzero(som_a[m_sel] == j)[0]
+        per.append((list(ms), g, idx, base))
+        base += len(ids)
+    return sc, models, int(sum(gps)), (som, gps), t_sel, m_sel, per
+
+
+def oracle_shard_run(ms, gpus, policy, ticks, midx):
+    from oracle import oracle
+    stride = max(m.profile.max_batch for m in ms)
+    return oracle.run(np.stack([m.profile.table_array(stride) for m in ms]),
+                      [m.profile.max_batch for m in ms], [m.slo_ns for m in ms],
+                      [policy.resolve_timeout_ns(m.slo_ns) for m in ms], gpus, ticks, midx,
+                      kind=policy.kind, gather=policy.gather,
+                      target_batch=policy.target_batch, d_ctrl_ns=policy.d_ctrl_ns,
+                      d_data_ns=policy.d_data_ns)
+
+
+def oracle_all(sc, per, ticks, midx, threads):
+    """The oracle over every sub-cluster of the rank, one thread each (the
+    C library releases the GIL); returns (results, wall seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(p):
+        ms, g, idx, base = p
+        return oracle_shard_run(ms, g, sc.policy, ticks[idx], midx[idx] - base)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        res = list(ex.map(one, per))
+    return res, time.perf_counter() - t0
 
 
 class ClockSampler:
@@ -116,15 +171,9 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.window = None  # (t0, t1) wall-clock bounds of the timed region
+        self.lines = []
 
     def start(self):
-        self.__enter__()
-        time.sleep(1.0)  # nvidia-smi start-up; sampling is running before timing
-
-    def stop(self):
-        self.__exit__(None, None, None)
-
-    def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -132,10 +181,9 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
-        return self
+        time.sleep(1.0)  # nvidia-smi start-up: sampling runs before timing starts
 
-    def __exit__(self, *exc):
-        self.lines = []
+    def stop(self):
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -149,7 +197,7 @@ class ClockSampler:
         import datetime
         sm, mx, reasons = [], 0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in getattr(self, "lines", []):
+        for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -177,66 +225,67 @@ def measured_peak_hbm():
         with open(p) as fh:
             return float(json.load(fh)["hbm_gbs"]), "measured"
     except (OSError, KeyError, ValueError):
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def oracle_shard_run(ms, gpus, policy, ticks, midx):
-    from oracle import oracle
-    stride = max(m.profile.max_batch for m in ms)
-    return oracle.run(np.stack([m.profile.table_array(stride) for m in ms]),
-                      [m.profile.max_batch for m in ms], [m.slo_ns for m in ms],
-                      [policy.resolve_timeout_ns(m.slo_ns) for m in ms], gpus, ticks, midx,
-                      kind=policy.kind, gather=policy.gather,
-                      target_batch=policy.target_batch, d_ctrl_ns=policy.d_ctrl_ns,
-                      d_data_ns=policy.d_data_ns)
+def workload_name(duration_s: float) -> str:
+    return (f"C4: 1000 A100-zoo models x 8192 GPUs, Poisson 1.2M req/s, {duration_s:g} s "
+            f"trace, seed 42, 8 sub-clusters of 125 models x 1024 GPUs")
 
 
-REF_BUDGET_S = 120.0
+def base_config(args, world):
+    return {"workload": workload_name(args.duration), "policy": "deferred", "max_batch": 256,
+            "subclusters_per_gpu": N_SUBCLUSTERS / world,
+            "l2": "256 MB buffer written before every step (> 126 MB L2)",
+            "parallelism": f"sub-cluster s on GPU s mod {world}"}
+
+
+REF_BUDGET_S = 150.0
 
 
 def run_reference(args, world):
-    """CPU arm: the oracle port over every rank's sub-cluster, one thread
+    """CPU arm: the oracle port over all 8 C4 sub-clusters, one host thread
     per sub-cluster (scalebench.bench_workers' process-per-shard layout)."""
-    from concurrent.futures import ThreadPoolExecutor
-    # Bounded sample: a shorter prefix of the same trace when many steps are
-    # asked for, so the whole arm stays near REF_BUDGET_S.  The port's speed
-    # on this host is calibrated on one second of the trace first.
-    cores = min(world, len(os.sched_getaffinity(0)))
-    waves = -(-world // cores)
-    cal = build_workload(1.0, 0)
-    t0 = time.perf_counter()
-    oracle_shard_run(cal[1], cal[2], cal[0].policy, cal[3], cal[4])
-    per_trace_s = (time.perf_counter() - t0) * waves  # step seconds per trace second
-    dur = round(min(args.duration, max(1.0, REF_BUDGET_S / (per_trace_s * (args.steps + args.warmup)))), 2)
-    work = [build_workload(dur, s) for s in range(world)]
-    n_total = sum(len(w[3]) for w in work)
-
-    def one_step():
-        with ThreadPoolExecutor(cores) as ex:
-            list(ex.map(lambda w: oracle_shard_run(w[1], w[2], w[0].policy, w[3], w[4]), work))
-
+    cores = min(N_SUBCLUSTERS, len(os.sched_getaffinity(0)))
+    all_sc = list(range(N_SUBCLUSTERS))
+    # bounded sample: the same trace, shortened if K + W steps of the full
+    # trace would not fit REF_BUDGET_S (calibrated on one second first)
+    sc, _, _, _, t1, m1, per1 = build_workload(1.0, all_sc)
+    _, cal = oracle_all(sc, per1, t1, m1, cores)
+    dur = round(min(args.duration, max(1.0, REF_BUDGET_S / (cal * (args.steps + args.warmup)))), 2)
+    sc, _, _, _, ticks, midx, per = build_workload(dur, all_sc)
+    n_total = len(ticks)
     for _ in range(args.warmup):
-        one_step()
-    t0 = time.perf_counter()
+        oracle_all(sc, per, ticks, midx, cores)
+    el = 0.0
     for _ in range(args.steps):
-        one_step()
-    el = time.perf_counter() - t0
+        el += oracle_all(sc, per, ticks, midx, cores)[1]
     value = n_total * args.steps / el
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": f"C4 sub-clusters 0..{world - 1} (125 models x 1024 GPUs each, "
-                               f"Poisson 150k req/s each, {dur:g} s of the seed-42 trace)",
-                   "requests_per_step": n_total, "policy": "deferred"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "impl": "reference", "config": base_config(args, world),
+        "requests_per_step": n_total,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"first {dur:g} s of the {args.duration:g} s trace of {world} "
-                                   "sub-cluster(s) per step, oracle/symoracle.c (C restatement "
-                                   "of batchsym's loop), one thread per sub-cluster"},
+                         "sample": f"all 8 C4 sub-clusters, first {dur:g} s of the "
+                                   f"{args.duration:g} s trace ({n_total} requests) per step; "
+                                   "oracle/symoracle.c (C restatement of batchsym's event "
+                                   "loop), one host thread per sub-cluster"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def check_parity(res_by_shard, per, outs):
+    """Device outputs of the timed runs vs the oracle, element for element."""
+    for (ms, g, idx, base), ref in zip(per, res_by_shard):
+        for k in ("dispatch", "start", "finish", "batch", "outcome"):
+            got = outs[k][idx]
+            if not np.array_equal(got, ref["req_" + k]):
+                bad = int(np.nonzero(got != ref["req_" + k])[0][0])
+                raise SystemExit(f"parity failure vs the oracle on req_{k} "
+                                 f"(sub-cluster model base {base}, request {bad})")
 
 
 def run_b200(args, rank, world, local_rank):
@@ -246,9 +295,10 @@ def run_b200(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    sc, ms, gpus, ticks, midx = build_workload(args.duration, rank)
+    mine = my_subclusters(rank, world)
+    sc, models, gpus, shards, ticks, midx, per = build_workload(args.duration, mine)
     n = len(ticks)
-    eng = Engine(ms, gpus, sc.policy, device=local_rank)
+    eng = Engine(models, gpus, sc.policy, shards=shards, device=local_rank)
     t_dev = torch.from_numpy(ticks).to(dev)
     m_dev = torch.from_numpy(midx.astype(np.int32)).to(dev)
     outs = {k: torch.empty(n, dtype=torch.int64, device=dev)
@@ -264,22 +314,23 @@ def run_b200(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     dev_ms, batches, launches = 0.0, 0, 0
-    if True:
-        t0 = time.perf_counter()
-        w0 = time.time()
-        for _ in range(args.steps):
-            flush.fill_(1)
-            _, cnt = eng.run_device(t_dev, m_dev, outs)
-            dev_ms += cnt["ms_total"]
-            batches += cnt["n_batches"]
-            launches += cnt["launches"] + 1  # + the L2 flush
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        clk.window = (w0, time.time())
-    clk.stop()
+    t0 = time.perf_counter()
+    w0 = time.time()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        _, cnt = eng.run_device(t_dev, m_dev, outs)
+        dev_ms += cnt["ms_total"]
+        batches += cnt["n_batches"]
+        launches += cnt["launches"]
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    clk.window = (w0, time.time())
     if world > 1:
         dist.barrier()
+    clk.stop()
     stats = dict(cnt)
+    host_outs = {k: v.cpu().numpy() for k, v in outs.items()}
+
     # per-kernel device time: the same K steps again with every launch
     # bracketed by CUDA events on the engine's stream
     eng.kernel_times(reset=True)
@@ -288,134 +339,159 @@ def run_b200(args, rank, world, local_rank):
         eng.run_device(t_dev, m_dev, outs, kernel_times=True)
     ktimes = eng.kernel_times(reset=True)
 
-    # end to end through the public API: pinned host arrays in, RunResult out
-    # (steady state: two untimed calls warm the pinned-memory pool, and each
+    # end to end through the public API: host arrays in, RunResult out
+    # (steady state: two untimed calls warm the pinned-memory pool; each
     # result is released before the next call, as a streaming caller would)
+    def e2e(t_host, m_host, reps):
+        for _ in range(2):
+            eng.run_stream(t_host, m_host, args.duration)
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            r = eng.run_stream(t_host, m_host, args.duration)
+            times.append(time.perf_counter() - t0)
+            del r
+        return sum(times) / len(times)
+    reps = max(3, min(args.steps, 10))
     pin_t = torch.from_numpy(ticks).pin_memory().numpy()
     pin_m = torch.from_numpy(midx).pin_memory().numpy()
-    for _ in range(2):
-        eng.run_stream(pin_t, pin_m, args.duration)
-    e2e_s = []
-    res = None
-    for _ in range(max(3, min(args.steps, 10))):
-        res = None
-        t0 = time.perf_counter()
-        res = eng.run_stream(pin_t, pin_m, args.duration)
-        e2e_s.append(time.perf_counter() - t0)
-    e2e_time = sum(e2e_s) / len(e2e_s)
-    h2d = n * (8 + 8)                      # ticks + int64 model ids
-    # six computed RunResult arrays + batch records cross PCIe; req_arrival and
-    # req_model (copies of the inputs) are filled by a host thread meanwhile
-    d2h = n * 6 * 8 + len(res.batches) * BATCH_REC_BYTES
+    e2e_pinned = e2e(pin_t, pin_m, reps)
+    e2e_pageable = e2e(ticks, midx, reps)
+    res = eng.run_stream(pin_t, pin_m, args.duration)
+    nb_rank = len(res.batches)
+    h2d = n * (8 + 8)  # ticks + int64 model ids
+    # five computed RunResult arrays + the batch records cross PCIe;
+    # req_arrival / req_model / req_deadline are formed on the host
+    d2h = n * 5 * 8 + nb_rank * BATCH_REC_BYTES
+    for k in ("batch", "outcome", "start"):
+        if not np.array_equal(host_outs[k], getattr(res, "req_" + k)):
+            raise SystemExit(f"device-resident and API outputs differ on req_{k}")
 
-    # parity spot check of the timed outputs against the API result
-    for k, ref in (("batch", res.req_batch), ("outcome", res.req_outcome)):
-        if not np.array_equal(outs[k].cpu().numpy(), ref):
-            raise SystemExit(f"device-resident and API outputs differ on {k}")
+    # bit-exact against the CPU oracle, every sub-cluster of this rank
+    threads = min(len(per), len(os.sched_getaffinity(0)))
+    ref, ref_s = oracle_all(sc, per, ticks, midx, threads)
+    check_parity(ref, per, host_outs)
 
     # end of run: the one collective -- per-sub-cluster integer summaries
     # reduced over NCCL into the cluster's goodput / idle / autoscale view
     from paper_2308_07470_b200.parallel import SummaryLayout, cluster_stats, reduce_summaries
-    layout = SummaryLayout(len(sc.models), sc.gpu_count)
+    layout = SummaryLayout(1000, 8192)
     lo, hi = int(0.1 * args.duration * 1e9), int(0.9 * args.duration * 1e9)
-    ids = np.arange(125 * rank, 125 * (rank + 1))
+    w = eng.window_counts(lo, hi)
     vec = layout.empty()
-    layout.put(vec, ids, np.arange(1024 * rank, 1024 * (rank + 1)), eng.window_counts(lo, hi))
+    for j, s in enumerate(mine):
+        ms, g, idx, base = per[j]
+        k = len(ms)
+        layout.put(vec, np.arange(125 * s, 125 * s + k),
+                   np.arange(1024 * s, 1024 * s + g),
+                   {name: w[name][base:base + k] for name in ("arrivals", "completed", "late",
+                                                              "dropped")} |
+                   {"gpu_busy_ns": w["gpu_busy_ns"][1024 * j:1024 * j + g]})
     t_red = time.perf_counter()
     vec = reduce_summaries(vec)
     red_ms = 1e3 * (time.perf_counter() - t_red)
-    world_layout = SummaryLayout(125 * world, 1024 * world)
-    cstats = cluster_stats(np.concatenate([vec[k * layout.M:k * layout.M + 125 * world]
-                                           for k in range(4)] + [vec[4 * layout.M:4 * layout.M
-                                                                      + 1024 * world]]),
-                           world_layout, lo, hi)
-    t = torch.tensor([dev_ms, e2e_time, wall], dtype=torch.float64, device=dev)
-    tot = torch.tensor([n, batches], dtype=torch.float64, device=dev)
+    cstats = cluster_stats(vec, layout, lo, hi)
+
+    t = torch.tensor([dev_ms, e2e_pinned, e2e_pageable, wall], dtype=torch.float64, device=dev)
+    tot = torch.tensor([n, batches, launches, h2d, d2h], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    dev_ms, e2e_time, wall = t.tolist()
-    n_all = int(tot[0].item())
+    dev_ms, e2e_pinned, e2e_pageable, wall = t.tolist()
+    n_all, batches_all, launches_all, h2d_all, d2h_all = (int(x) for x in tot.tolist())
     if rank != 0:
         return
     value = n_all * args.steps / (dev_ms / 1e3)
     peak, peak_kind = measured_peak_hbm()
-    nb_step = batches // args.steps
+    nb_step = batches // args.steps  # this rank's batches per step
     kern = {}
     k_total = sum(v[1] for v in ktimes.values())
     for name, (cnt_l, k_ms) in ktimes.items():
         per_launch_ms = k_ms / cnt_l
-        ab = algorithmic_bytes(name, n, nb_step)
+        ab, src = kernel_bytes(name, n, nb_step, gpus, len(mine))
+        gbs = (ab / (per_launch_ms / 1e3) / 1e9) if ab else None
         kern[name] = {"launches_per_step": cnt_l / args.steps, "ms_per_launch": per_launch_ms,
-                      "share": k_ms / k_total,
-                      "gbs": (ab / (per_launch_ms / 1e3) / 1e9) if ab else None}
-    dom = max(kern, key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches_per_step"])
-    ab = algorithmic_bytes(dom, n, nb_step)
-    achieved = kern[dom]["gbs"]
+                      "share": k_ms / k_total, "bytes_per_launch": ab, "bytes_source": src,
+                      "gbs": gbs, "frac": gbs / peak if gbs else None}
+    dom = max(kern, key=lambda k: kern[k]["share"])
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         with open(prof) as fh:
-            traffic = json.load(fh).get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
+            summ = json.load(fh)
+        if summ.get("workload") == workload_name(args.duration) and summ.get("n_gpus") == world:
+            traffic = summ.get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
+    k123 = {}
+    for tag, (name, _) in SURVEY_KERNELS.items():
+        if name in kern:
+            k123[tag] = {"kernel": name, "achieved_gbs": kern[name]["gbs"],
+                         "frac": kern[name]["frac"], "ms_per_launch": kern[name]["ms_per_launch"],
+                         "bytes_per_launch": kern[name]["bytes_per_launch"]}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"C4: 1000 A100-zoo models x 8192 GPUs, Poisson 1.2M req/s, "
-                               f"{args.duration:g} s trace, seed 42, 8 sub-clusters of 125 "
-                               f"models x 1024 GPUs; rank r runs sub-cluster r",
-                   "requests_per_step": n_all, "policy": "deferred", "max_batch": 256,
-                   "l2": "256 MB flush written before every step",
-                   "parallelism": f"sub-cluster-per-gpu x{world}"},
-        "e2e": {"value": n_all / e2e_time, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
-                "d2h_bytes_per_step": d2h * world},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": ab},
-        "kernels": {k: kern[k] for k in sorted(kern, key=lambda k: -kern[k]["share"])[:8]},
-        "gpu_launches": launches,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": base_config(args, world),
+        "requests_per_step": n_all,
+        "e2e": {"value": n_all / e2e_pinned, "unit": UNIT, "h2d_bytes_per_step": h2d_all,
+                "d2h_bytes_per_step": d2h_all, "inputs": "pinned host arrays",
+                "ms_per_step": 1e3 * e2e_pinned},
+        "e2e_pageable": {"value": n_all / e2e_pageable, "unit": UNIT,
+                         "inputs": "pageable numpy arrays", "ms_per_step": 1e3 * e2e_pageable},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": kern[dom]["frac"],
+                     "traffic": traffic, "algorithmic_bytes_per_launch":
+                         kern[dom]["bytes_per_launch"], "bytes_source": kern[dom]["bytes_source"],
+                     "scope": "rank 0's launch"},
+        "roofline_k123": k123,
+        "kernels": {k: kern[k] for k in sorted(kern, key=lambda k: -kern[k]["share"])[:10]},
+        "gpu_launches": launches_all,
         "phases_ms": {k: stats[k] for k in ("ms_ingest", "ms_fresh", "ms_fast", "ms_chain",
                                             "ms_expand")},
-        "path": {"fast_shards": stats["fast_shards"], "batches": stats["n_batches"],
+        "path": {"fast_shards": stats["fast_shards"], "batches_per_step": batches_all // args.steps,
                  "chain_events": stats["chain_events"]},
+        "parity": f"bit-exact vs oracle/symoracle.c on every sub-cluster of every rank "
+                  f"({n_all} requests, 5 per-request arrays)",
         "clocks": clk.summary(),
         "wall_ms_per_step": 1e3 * wall / args.steps,
         "cluster": dict(cstats, summary_allreduce_ms=red_ms,
-                        scope=f"sub-clusters 0..{world - 1}, window [10%, 90%) of the trace"),
+                        scope="all 8 sub-clusters, window [10%, 90%) of the trace"),
     }
+    if world > 1:
+        line["nccl_world"] = dist.get_world_size()
     if world == 1 and not args.no_cpu_baseline:
-        t0 = time.perf_counter()
-        oracle_shard_run(ms, gpus, sc.policy, ticks, midx)
-        el = time.perf_counter() - t0
-        line["cpu_baseline"] = {"value": n / el, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"sub-cluster 0, full {args.duration:g} s trace "
-                                          f"({n} requests), oracle/symoracle.c single thread"}
+        line["cpu_baseline"] = {"value": n / ref_s, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"all {len(per)} sub-clusters, full {args.duration:g} s "
+                                          f"trace ({n} requests), oracle/symoracle.c, one host "
+                                          "thread per sub-cluster (the parity run above)"}
     print(json.dumps(line), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--duration", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
-    if world != args.gpus and world != 1:
-        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
-    world = max(world, 1)
-    if args.gpus > 8:
-        raise SystemExit("C4 has 8 sub-clusters: at most 8 GPUs")
+    if args.gpus not in (1, 2, 4, 8):
+        raise SystemExit("C4 has 8 sub-clusters: --gpus must be 1, 2, 4 or 8")
+    if world != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus={args.gpus}: launch N>1 with "
+                         "torch.distributed.run --nproc-per-node N")
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":
         if rank == 0:
-            run_reference(args, max(world, args.gpus))
+            run_reference(args, world)
         return
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
+        print(f"[rank {rank}] NCCL communicator size {dist.get_world_size()}", file=sys.stderr)
     try:
         run_b200(args, rank, world, local_rank)
     finally:

@@ -148,6 +148,28 @@ int32_t sym_run_device(void *engine, const int64_t *d_arr_ticks,
                        const void *d_arr_model, int64_t n, uint32_t flags,
                        sym_result *out);
 
+/* ---- stepped runs (the reference's step API: scalebench._shard_loop drives
+ * Engine._record_arrival / ModelPlane.on_new_request / _dispatch_event,
+ * scalebench.py:67-84, simulator.py:201-242) ---------------------------------
+ * sym_step_reset starts a stepped run on the handle (a whole-run call ends
+ * it).  Each sym_step appends n arrivals (host buffers, stream order, ticks
+ * non-decreasing and within [previous until_tick, until_tick]) and processes
+ * every event with tick <= until_tick; the caller promises that later
+ * arrivals have tick >= until_tick.  Queues, candidates, timers, the GPU
+ * index and the registered sets stay on the device between calls.
+ * until_tick = INT64_MAX drains the engine.  After the last step the run
+ * equals one sym_run over the concatenated stream, bit for bit.  `out`
+ * receives the cumulative counters (n = arrivals so far, n_batches, drops,
+ * completions = requests dispatched so far).  Jitterless networks only. */
+int32_t sym_step_reset(void *engine);
+int32_t sym_step(void *engine, const int64_t *arr_ticks, const void *arr_model, int64_t n,
+                 int64_t until_tick, uint32_t flags, sym_result *out);
+/* RunResult arrays of every arrival so far (caller buffers of out->n =
+ * arrivals-so-far entries; NULL pointers are skipped): outcomes of requests
+ * whose completion tick is after the last until_tick are -1 (unresolved),
+ * as in the reference mid-run.  Batch records in step order. */
+int32_t sym_step_result(void *engine, sym_result *out);
+
 /* Copy the last run's batch records (emission order per GPU) to a host
  * buffer of capacity cap; returns the count (or -status on failure). */
 int64_t sym_last_batches(void *engine, sym_batch *host, int64_t cap);

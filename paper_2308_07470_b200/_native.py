@@ -80,7 +80,8 @@ class SymResult(C.Structure):
 EXPORTS = ("sym_create", "sym_destroy", "sym_run", "sym_run_device",
            "sym_window_counts", "sym_last_error", "sym_version", "sym_kernel_times",
            "sym_last_batches", "sym_window_stats", "sym_text_format", "sym_text_fetch",
-           "sym_text_free", "sym_part_brute_force", "sym_part_evaluate", "sym_part_solve")
+           "sym_text_free", "sym_part_brute_force", "sym_part_evaluate", "sym_part_solve",
+           "sym_step_reset", "sym_step", "sym_step_result")
 
 TEXT_REQUESTS, TEXT_LATENCY = 0, 1
 
@@ -126,6 +127,13 @@ def load(path: str | None = None):
         fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_uint32,
                        C.POINTER(SymResult)]
         fn.restype = C.c_int32
+    lib.sym_step_reset.argtypes = [C.c_void_p]
+    lib.sym_step_reset.restype = C.c_int32
+    lib.sym_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                             C.c_uint32, C.POINTER(SymResult)]
+    lib.sym_step.restype = C.c_int32
+    lib.sym_step_result.argtypes = [C.c_void_p, C.POINTER(SymResult)]
+    lib.sym_step_result.restype = C.c_int32
     lib.sym_window_counts.argtypes = [C.c_void_p, C.c_int64, C.c_int64] + [i64p] * 5
     lib.sym_window_counts.restype = C.c_int32
     lib.sym_window_stats.argtypes = ([C.c_void_p, C.c_int64, C.c_int64] + [i64p] * 8 +

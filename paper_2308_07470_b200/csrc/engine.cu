@@ -125,6 +125,32 @@ struct Ctx {
   bool has_run = false;
   std::map<std::string, std::pair<int64_t, double>> ktimes;  // name -> (launches, ms)
   std::string ktimes_json;
+  // ---- stepped run (sym_step): the chain's state persists in the chain
+  // arrays above (d_ms, d_free, trees) and the device Shard images; the
+  // sorted layout holds each model's unresolved arrivals followed by the
+  // new ones, double buffered and rebuilt every step
+  bool step_active = false, step_first = true;
+  int64_t step_n = 0;                 // arrivals so far (stream length)
+  int64_t step_until = INT64_MIN;     // until_tick of the previous step
+  int64_t step_served = 0, step_drops = 0;
+  int64_t g_cap = 0;                  // capacity of the per-request arrays
+  int64_t* d_g_ticks = nullptr;       // every arrival so far, stream order
+  int32_t* d_g_model = nullptr;
+  int64_t* d_g_out = nullptr;         // [5][g_cap] dispatch start finish batch outcome
+  int64_t lay_cap = 0, lay_n = 0;
+  int cur = 0;
+  int64_t* d_lay_tick[2] = {nullptr, nullptr};
+  int32_t* d_lay_g[2] = {nullptr, nullptr};
+  int32_t* d_lay_i[2] = {nullptr, nullptr};
+  int32_t* d_lay_aself[2] = {nullptr, nullptr};
+  int32_t* d_lay_flag = nullptr;      // served flag per layout position
+  ModelParam* d_mp_chunk = nullptr;   // off/cnt of the chunk's own sorted layout
+  int32_t* d_step_slot = nullptr;     // [4*(M+1)]: newcnt | newoff | keep | oldsrc
+  int64_t* d_step_shard = nullptr;    // [3*P]: shard base | last tick | has-previous
+  int64_t* d_step_cnt = nullptr;      // [2]: served, dropped this step
+  std::vector<int64_t> shard_count, shard_last;
+  sym_batch* d_gbat = nullptr;
+  int64_t gbat_cap = 0, gbat_n = 0;
 };
 
 #define CK(call)                                                        \
@@ -603,15 +629,21 @@ struct SmemPlan {
   }
 };
 
+// mode: 0 = a whole run (init, run to the end; only the model states are
+// written back, for the drop counts); 1 = the first step of a stepped run
+// (init, run to `until`, write back ALL state); 2 = a later step (load all
+// state, resume, run to `until`, write it back).
+constexpr int kChainWhole = 0, kChainFirstStep = 1, kChainResume = 2;
+
 __global__ void __launch_bounds__(32)
 k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
         int32_t* __restrict__ dirty_all, const int32_t* __restrict__ slot_base,
-        size_t smem_bytes, const int32_t* __restrict__ skip) {
+        size_t smem_bytes, const int32_t* __restrict__ skip, int mode, int64_t until) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (threadIdx.x != 0 || skip[blockIdx.x]) return;
   Shard S = shards[blockIdx.x];  // hot scalars of the sub-cluster in registers
   const Shard orig = S;  // global pointers, restored before the write-back
-  ModelState* const ms_global = S.ms;
+  const bool load = mode == kChainResume, keep = mode != kChainWhole;
   size_t used = 0;
   auto place = [&](auto*& ptr, size_t exact, bool copy_in) {
     const size_t bytes = SmemPlan::al(exact);
@@ -626,17 +658,18 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
     used += bytes;
     return true;
   };
-  place(S.gt, sizeof(int32_t) * 2 * S.Gp, false);
-  place(S.free_at, sizeof(int64_t) * S.G, false);
-  place(S.pq, sizeof(int32_t) * 2 * S.Mp, false);
-  const bool ms_in_smem = place(S.ms, sizeof(ModelState) * S.M, false);
+  // state arrays placed on chip, with their sizes for the write-back
+  const bool gt_s = place(S.gt, sizeof(int32_t) * 2 * S.Gp, load);
+  const bool fa_s = place(S.free_at, sizeof(int64_t) * S.G, load);
+  const bool pq_s = place(S.pq, sizeof(int32_t) * 2 * S.Mp, load);
+  const bool ms_in_smem = place(S.ms, sizeof(ModelState) * S.M, load);
   const ModelParam* mp = S.mp;
   ModelParam* mp_s = const_cast<ModelParam*>(mp);
   if (place(mp_s, sizeof(ModelParam) * S.M, true)) S.mp = mp_s;
-  place(S.mc_lat_tree, sizeof(int32_t) * 2 * S.Mp, false);
-  place(S.mc_bs_tree, sizeof(int32_t) * 2 * S.Mp, false);
-  place(S.mc_size, sizeof(int32_t) * S.M, false);
-  place(S.mc_latest, sizeof(int64_t) * S.M, false);
+  const bool ml_s = place(S.mc_lat_tree, sizeof(int32_t) * 2 * S.Mp, load);
+  const bool mb_s = place(S.mc_bs_tree, sizeof(int32_t) * 2 * S.Mp, load);
+  const bool mz_s = place(S.mc_size, sizeof(int32_t) * S.M, load);
+  const bool mt_s = place(S.mc_latest, sizeof(int64_t) * S.M, load);
   {  // latency rows last: small model sets keep every l(b) probe on chip
     const int64_t* lat_g = S.lat;
     int64_t* lat_s = const_cast<int64_t*>(lat_g);
@@ -646,14 +679,28 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
 #ifdef SYM_CHAIN_PROF
   sym::g_chain_prof_on = 1;
 #endif
-  chain_init(S, fresh);
-  while (chain_step(S, dirty, fresh)) {
+  if (load)
+    chain_resume(S);
+  else
+    chain_init(S, fresh);
+  while (chain_step(S, dirty, fresh, until)) {
   }
 #ifdef SYM_CHAIN_PROF
   sym::g_chain_prof_on = 0;
 #endif
-  if (ms_in_smem)
-    for (int32_t k = 0; k < S.M; k++) ms_global[k] = S.ms[k];
+  auto back = [](auto* dst, const auto* src, size_t cnt) {
+    for (size_t k = 0; k < cnt; k++) dst[k] = src[k];
+  };
+  if (ms_in_smem) back(orig.ms, S.ms, S.M);
+  if (keep) {  // a stepped run carries every structure to the next step
+    if (gt_s) back(orig.gt, S.gt, 2 * (size_t)S.Gp);
+    if (fa_s) back(orig.free_at, S.free_at, S.G);
+    if (pq_s) back(orig.pq, S.pq, 2 * (size_t)S.Mp);
+    if (ml_s) back(orig.mc_lat_tree, S.mc_lat_tree, 2 * (size_t)S.Mp);
+    if (mb_s) back(orig.mc_bs_tree, S.mc_bs_tree, 2 * (size_t)S.Mp);
+    if (mz_s) back(orig.mc_size, S.mc_size, S.M);
+    if (mt_s) back(orig.mc_latest, S.mc_latest, S.M);
+  }
   S.ms = orig.ms;
   S.mp = orig.mp;
   S.lat = orig.lat;
@@ -1565,6 +1612,250 @@ __global__ void k_serialize(const uint64_t* __restrict__ keys, const uint32_t* _
   }
 }
 
+// ------------------------------------------- stepped runs (sym_step) -----
+// A stepped run keeps the chain's state on the device between calls.  Each
+// step rebuilds the sorted layout as, per model, its unresolved arrivals
+// (queue positions >= qh) followed by the step's new arrivals, so queue
+// positions stay model-relative and the chain resumes where it stopped.
+
+// per slot: new count, kept count and the first kept old position
+__global__ void k_step_sizes(const ModelParam* __restrict__ mp,
+                             const ModelState* __restrict__ ms,
+                             const ModelParam* __restrict__ mpc, int32_t M, int first,
+                             int have_chunk, int32_t* __restrict__ slot_meta) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  const int32_t qh = first ? 0 : ms[k].qh;
+  const int32_t keep = first ? 0 : mp[k].cnt - qh;
+  const int32_t add = have_chunk ? mpc[k].cnt : 0;
+  slot_meta[k] = keep + add;                      // newcnt
+  slot_meta[2 * (M + 1) + k] = keep;              // keep
+  slot_meta[3 * (M + 1) + k] = first ? 0 : mp[k].off + qh;  // oldsrc
+}
+
+// newoff = exclusive scan of newcnt (one block); newoff[M] = total
+__global__ void __launch_bounds__(1024) k_step_offsets(int32_t* __restrict__ slot_meta,
+                                                       int32_t M) {
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  int32_t* newcnt = slot_meta;
+  int32_t* newoff = slot_meta + (M + 1);
+  for (int32_t b0 = 0; b0 < M; b0 += 1024) {
+    const int32_t k = b0 + threadIdx.x;
+    const int32_t v = k < M ? newcnt[k] : 0;
+    int32_t tot;
+    const int32_t ex = block_exclusive_scan(v, &tot);
+    const int32_t c = carry;
+    if (k < M) newoff[k] = c + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) newoff[M] = carry;
+}
+
+__device__ __forceinline__ int32_t slot_of_pos(const int32_t* __restrict__ newoff, int32_t M,
+                                               int64_t p) {
+  int32_t lo = 0, hi = M;  // last slot with newoff <= p (empty slots skipped)
+  while (hi - lo > 1) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (newoff[mid] <= p) lo = mid; else hi = mid;
+  }
+  while (lo + 1 < M && newoff[lo + 1] <= p) lo++;
+  return lo;
+}
+
+// The new layout: kept positions copied from the old layout, new ones from
+// the chunk's sorted layout with their stream index, shard-stream index and
+// A' (the shard's previous arrival may sit in an earlier step).
+__global__ void k_step_copy(int64_t bound, const int32_t* __restrict__ slot_meta, int32_t M,
+                            int32_t P, const int32_t* __restrict__ slot_base,
+                            const ModelParam* __restrict__ mpc,
+                            const int64_t* __restrict__ o_tick, const int32_t* __restrict__ o_g,
+                            const int32_t* __restrict__ o_i, const int32_t* __restrict__ o_as,
+                            const int64_t* __restrict__ c_tick, const int32_t* __restrict__ c_g,
+                            const int32_t* __restrict__ c_i, const int64_t* __restrict__ c_sh,
+                            const int64_t* __restrict__ c_in_ticks,
+                            const int32_t* __restrict__ c_shard_off,
+                            const int64_t* __restrict__ shard_meta, int64_t stream_base,
+                            int64_t* __restrict__ n_tick, int32_t* __restrict__ n_g,
+                            int32_t* __restrict__ n_i, int32_t* __restrict__ n_as,
+                            int32_t* __restrict__ flag) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t* newoff = slot_meta + (M + 1);
+  if (p >= bound || p >= newoff[M]) return;
+  const int32_t k = slot_of_pos(newoff, M, p);
+  const int32_t local = (int32_t)(p - newoff[k]);
+  const int32_t keep = slot_meta[2 * (M + 1) + k];
+  flag[p] = 0;
+  if (local < keep) {
+    const int32_t src = slot_meta[3 * (M + 1) + k] + local;
+    n_tick[p] = o_tick[src];
+    n_g[p] = o_g[src];
+    n_i[p] = o_i[src];
+    n_as[p] = o_as[src];
+    return;
+  }
+  const int32_t c = mpc[k].off + (local - keep);
+  const int64_t tick = c_tick[c];
+  const int32_t il = c_i[c];  // chunk-local stream index
+  int s = 0;
+  while (s + 1 < P && slot_base[s + 1] <= k) s++;
+  int64_t jl, prev_tick;
+  if (P == 1) {  // one shard: the shard stream is the stream
+    jl = il;
+    prev_tick = il > 0 ? c_in_ticks[il - 1] : shard_meta[P + s];
+  } else {
+    const int32_t j = c_g[c];
+    jl = j - c_shard_off[s];
+    prev_tick = jl > 0 ? c_sh[j - 1] : shard_meta[P + s];
+  }
+  const int64_t gsh = shard_meta[s] + jl;  // the shard's own stream index
+  const bool has_prev = jl > 0 || shard_meta[2 * P + s] != 0;
+  n_tick[p] = tick;
+  n_g[p] = (int32_t)gsh;
+  n_i[p] = (int32_t)(stream_base + il);
+  n_as[p] = has_prev && prev_tick == tick ? (int32_t)gsh : A_BASE;
+}
+
+// Queue positions are model-relative: shift them by the dropped prefix.
+__global__ void k_step_rebase(ModelParam* __restrict__ mp, ModelState* __restrict__ ms,
+                              const int32_t* __restrict__ slot_meta, int32_t M, int first) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  if (!first) {
+    ModelState& st = ms[k];
+    const int32_t sh = st.qh;
+    st.qh -= sh;
+    st.qt -= sh;
+    if (st.c_head >= sh) st.c_head -= sh;
+    if (st.dt_head >= 0) st.dt_head -= sh;
+  }
+  mp[k].off = slot_meta[(M + 1) + k];
+  mp[k].cnt = slot_meta[k];
+}
+
+// Every record the step's chains emitted: per-request outputs of its
+// members (stream index from the layout), its served flags, and the
+// sym_batch appended to the run's batch list.
+__global__ void k_step_emit(const BatchRec* __restrict__ recs,
+                            const int64_t* __restrict__ rec_base,
+                            const int64_t* __restrict__ rec_count, int32_t P,
+                            const int64_t* __restrict__ total_p,
+                            const int32_t* __restrict__ lay_i,
+                            const int32_t* __restrict__ model_of_slot,
+                            const int32_t* __restrict__ slot_base,
+                            const int32_t* __restrict__ gpu_base, int64_t gcap,
+                            int64_t* __restrict__ g_out, int32_t* __restrict__ flag,
+                            sym_batch* __restrict__ gbat, unsigned long long* __restrict__ cnt) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= *total_p) return;
+  int s = 0;
+  int64_t k = w;
+  while (s < P && k >= rec_count[s]) {
+    k -= rec_count[s];
+    s++;
+  }
+  const BatchRec& r = recs[rec_base[s] + k];
+  for (int32_t j = 0; j < r.size; j++) {
+    const int32_t pos = r.first + j;
+    const int64_t gi = lay_i[pos];
+    g_out[gi] = r.emitted;
+    g_out[gcap + gi] = r.start;
+    g_out[2 * gcap + gi] = r.finish;
+    g_out[3 * gcap + gi] = r.size;
+    g_out[4 * gcap + gi] = 0;  // served; the completion tick decides (collect)
+    flag[pos] = 1;
+  }
+  sym_batch b;
+  b.emitted = r.emitted;
+  b.start = r.start;
+  b.finish = r.finish;
+  b.key_t = r.kt;
+  b.key_sub = r.ksub;
+  b.key_a = r.ka;
+  b.model = model_of_slot[slot_base[s] + r.model];
+  b.gpu = gpu_base[s] + r.gpu;
+  b.size = r.size;
+  b.first_index = lay_i[r.first];
+  b.shrunk_from = r.shrunk_from;
+  gbat[w] = b;
+  atomicAdd(&cnt[0], (unsigned long long)r.size);
+}
+
+// Positions the step resolved (below the model's queue head) that no batch
+// took were dropped.
+__global__ void k_step_drops(int64_t bound, const int32_t* __restrict__ slot_meta, int32_t M,
+                             const ModelState* __restrict__ ms,
+                             const int32_t* __restrict__ lay_i,
+                             const int32_t* __restrict__ flag, int64_t gcap,
+                             int64_t* __restrict__ g_out, unsigned long long* __restrict__ cnt) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t* newoff = slot_meta + (M + 1);
+  if (p >= bound || p >= newoff[M]) return;
+  const int32_t k = slot_of_pos(newoff, M, p);
+  if (p - newoff[k] < ms[k].qh && !flag[p]) {
+    g_out[4 * gcap + lay_i[p]] = 2;  // OUTCOME_DROPPED
+    atomicAdd(&cnt[1], 1ull);
+  }
+}
+
+// Per-shard views of the step's layout, patched on the device (the device
+// Shard images carry the chain state from the previous step).
+__global__ void k_step_views(Shard* __restrict__ shards, int32_t P,
+                             const int32_t* __restrict__ slot_meta, int32_t M,
+                             const int32_t* __restrict__ slot_base, const int64_t* s_tick,
+                             const int32_t* s_g, const int32_t* s_aself, BatchRec* recs,
+                             int64_t* __restrict__ meta) {
+  const int s = threadIdx.x;
+  if (s >= P) return;
+  const int32_t* newoff = slot_meta + (M + 1);
+  const int64_t lo = newoff[slot_base[s]], hi = newoff[slot_base[s + 1]];
+  Shard& S = shards[s];
+  S.s_tick = s_tick;
+  S.s_g = s_g;
+  S.s_aself = s_aself;
+  S.sh_tick = nullptr;
+  S.sh_base = 0;
+  S.record_trace = 0;
+  S.drop_t = nullptr;
+  S.drop_ksub = nullptr;
+  S.drop_ka = nullptr;
+  S.recs = recs + lo + s;  // at most one record per layout position
+  S.rec_cap = hi - lo + 1;
+  meta[s] = lo + s;        // rec_base
+}
+
+// rec_count per shard after the chain, and their total
+__global__ void k_step_recmeta(const Shard* __restrict__ shards, int32_t P,
+                               int64_t* __restrict__ meta) {
+  if (threadIdx.x != 0) return;
+  int64_t tot = 0;
+  for (int s = 0; s < P; s++) {
+    meta[P + 1 + s] = shards[s].n_recs;
+    tot += shards[s].n_recs;
+  }
+  meta[2 * (P + 1)] = tot;
+}
+
+// Per-shard stream bookkeeping for the next step's A': arrivals so far,
+// the last tick, whether the shard has had any arrival.
+__global__ void k_step_shard_update(int64_t* __restrict__ shard_meta, int32_t P, int64_t n,
+                                    const int32_t* __restrict__ c_shard_off,
+                                    const int64_t* __restrict__ c_in_ticks,
+                                    const int64_t* __restrict__ c_sh) {
+  const int s = threadIdx.x;
+  if (s >= P || n == 0) return;
+  const int64_t lo = P == 1 ? 0 : c_shard_off[s], hi = P == 1 ? n : c_shard_off[s + 1];
+  if (hi <= lo) return;
+  shard_meta[s] += hi - lo;
+  shard_meta[P + s] = P == 1 ? c_in_ticks[n - 1] : c_sh[hi - 1];
+  shard_meta[2 * P + s] = 1;
+}
+
+// k_step_emit / k_step_drops launched over a bound: the real extents live
+// on the device (newoff[M], meta total)
 // ------------------------------------------------------------ driver ------
 
 int ensure_capacity(Ctx* ctx, int64_t n) {
@@ -1693,27 +1984,45 @@ struct KernelTimer {
     kt.end();                  \
   } while (0)
 
-int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
-               int64_t n, uint32_t flags, sym_result* out, bool outs_on_device) {
+// The previous run's device views die when a new run starts: a failed run
+// must not leave sym_window_* / sym_last_batches reading buffers the call
+// may have regrown, or caller tensors it no longer vouches for.
+void forget_last_run(Ctx* ctx) {
+  ctx->has_run = false;
+  ctx->last_n = 0;
+  ctx->last_ticks = nullptr;
+  ctx->last_model = nullptr;
+  ctx->last_outcome = ctx->last_start = ctx->last_finish = nullptr;
+  ctx->last_nrecs.clear();
+  ctx->last_rec_base.clear();
+}
+
+void flat_scan(Ctx* ctx, int32_t* a, int64_t len, KernelTimer& kt, int64_t& launches) {
   cudaStream_t st = ctx->stream;
-  int64_t launches = 0;
-  PhaseClock pc(st);
-  KernelTimer kt{ctx, st, (flags & SYM_FLAG_KERNEL_TIMES) != 0, {}};
-  auto flat_scan = [&](int32_t* a, int64_t len) {
-    const int64_t nparts = (len + kScanItems - 1) / kScanItems;
-    KL(k_scan_up, nparts, 1024, 0, st>>>(a, len, ctx->d_scan_part));
-    KL(k_scan_mid, 1, 1024, 0, st>>>(ctx->d_scan_part, nparts));
-    KL(k_scan_down, nparts, 1024, 0, st>>>(a, len, ctx->d_scan_part));
-  };
+  const int64_t nparts = (len + kScanItems - 1) / kScanItems;
+  KL(k_scan_up, nparts, 1024, 0, st>>>(a, len, ctx->d_scan_part));
+  KL(k_scan_mid, 1, 1024, 0, st>>>(ctx->d_scan_part, nparts));
+  KL(k_scan_down, nparts, 1024, 0, st>>>(a, len, ctx->d_scan_part));
+}
+
+// What the ingest reads back for the host (one synchronisation).
+struct IngestInfo {
+  int64_t last_tick = 0;
+  std::vector<int32_t> shard_off;   // [P+1] first shard-stream index per shard
+  std::vector<ModelParam> mp;       // per-slot off/cnt of the sorted layout
+};
+
+// K1: stable partition of n time-ordered arrivals into the (shard, model)-
+// sorted layout (ctx->d_s_tick, d_s_g, d_s_i, d_sh_tick, d_inv, d_s_slot;
+// per-slot off/cnt into mp_out).  Validates model ids (EPROTO) and the
+// time order (EINVAL) on the device.
+int ingest(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_t n,
+           ModelParam* mp_out, KernelTimer& kt, int64_t& launches, IngestInfo& info,
+           sym_result* out) {
+  cudaStream_t st = ctx->stream;
   const int32_t M = ctx->M, P = ctx->P;
   const int B = M + P;
-  const bool trace = flags & SYM_FLAG_TRACE;
-  const bool use_fresh = !trace && !(flags & SYM_FLAG_NO_FRESH);
-  int rc;
-  if ((rc = ensure_capacity(ctx, n))) return rc;
   const int64_t W = (n + kChunkI - 1) / kChunkI;
-  CK(cudaEventRecord(ctx->ev[0], st));
-  // ---- K1 ingest
   const int32_t big[2] = {INT32_MAX, INT32_MAX};
   CK(cudaMemcpyAsync(ctx->d_err, big, sizeof big, cudaMemcpyHostToDevice, st));
   const size_t smem = sizeof(int32_t) * (size_t)B;
@@ -1721,35 +2030,26 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_hist, W, 32 * kIngestWarps, smem, st>>>(
         d_model, d_ticks, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
         ctx->d_hist, W, ctx->d_err));
-    flat_scan(ctx->d_hist, W * B);
+    flat_scan(ctx, ctx->d_hist, W * B, kt, launches);
   }
-  KL(k_binoff, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, M, P, n, ctx->d_mp,
+  KL(k_binoff, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, M, P, n, mp_out,
                                            ctx->d_bins + B + 1));
   int32_t herr2[2] = {INT32_MAX, INT32_MAX};
-  int64_t last_tick = 0;
-  std::vector<int32_t> shard_off(P + 1, 0);  // first shard-stream index per shard
+  info.last_tick = 0;
+  info.shard_off.assign(P + 1, 0);
   CK(cudaMemcpyAsync(herr2, ctx->d_err, sizeof herr2, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(shard_off.data(), ctx->d_bins + B + 1, sizeof(int32_t) * (P + 1),
+  CK(cudaMemcpyAsync(info.shard_off.data(), ctx->d_bins + B + 1, sizeof(int32_t) * (P + 1),
                      cudaMemcpyDeviceToHost, st));
   if (n > 0)
-    CK(cudaMemcpyAsync(&last_tick, d_ticks + (n - 1), sizeof last_tick,
+    CK(cudaMemcpyAsync(&info.last_tick, d_ticks + (n - 1), sizeof info.last_tick,
                        cudaMemcpyDeviceToHost, st));
   // per-model arrival counts (k_binoff) ride on the same readback
-  std::vector<ModelParam> mp(M);
-  CK(cudaMemcpyAsync(mp.data(), ctx->d_mp, sizeof(ModelParam) * M,
+  info.mp.resize(M);
+  CK(cudaMemcpyAsync(info.mp.data(), mp_out, sizeof(ModelParam) * M,
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  // every event tick and finish time of a validated run is below the last
-  // arrival + SLO; the bound is generous and checked (FP_CAPACITY)
-  int tick_bits = 1;
-  {
-    const uint64_t bound = (uint64_t)(last_tick > 0 ? last_tick : 0) +
-                           2 * (uint64_t)ctx->max_slo + (uint64_t)ctx->max_lat + 1;
-    while (tick_bits < 62 && (uint64_t(1) << tick_bits) <= bound) tick_bits++;
-  }
-  const int32_t herr = herr2[0];
-  if (herr != INT32_MAX) {
-    out->err_index = herr;
+  if (herr2[0] != INT32_MAX) {
+    out->err_index = herr2[0];
     ctx->err = "request for unknown model";
     return SYM_EPROTO;
   }
@@ -1769,6 +2069,40 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
         ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot, ctx->d_bid));
   CK(cudaGetLastError());
+  return SYM_OK;
+}
+
+int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
+               int64_t n, uint32_t flags, sym_result* out, bool outs_on_device) {
+  cudaStream_t st = ctx->stream;
+  int64_t launches = 0;
+  PhaseClock pc(st);
+  KernelTimer kt{ctx, st, (flags & SYM_FLAG_KERNEL_TIMES) != 0, {}};
+  auto flat_scan = [&](int32_t* a, int64_t len) { ::flat_scan(ctx, a, len, kt, launches); };
+  const int32_t M = ctx->M, P = ctx->P;
+  const int B = M + P;
+  const bool trace = flags & SYM_FLAG_TRACE;
+  const bool use_fresh = !trace && !(flags & SYM_FLAG_NO_FRESH);
+  forget_last_run(ctx);
+  ctx->step_active = false;  // a whole run reuses the chain arrays
+  int rc;
+  if ((rc = ensure_capacity(ctx, n))) return rc;
+  CK(cudaEventRecord(ctx->ev[0], st));
+  // ---- K1 ingest
+  IngestInfo info;
+  if ((rc = ingest(ctx, d_ticks, d_model, n, ctx->d_mp, kt, launches, info, out))) return rc;
+  const int64_t last_tick = info.last_tick;
+  const std::vector<int32_t>& shard_off = info.shard_off;
+  const std::vector<ModelParam>& mp = info.mp;
+  // every event tick and finish time of a validated run is below the last
+  // arrival + SLO; the bound is generous and checked (FP_CAPACITY)
+  int tick_bits = 1;
+  {
+    const uint64_t bound = (uint64_t)(last_tick > 0 ? last_tick : 0) +
+                           2 * (uint64_t)ctx->max_slo + (uint64_t)ctx->max_lat + 1;
+    while (tick_bits < 62 && (uint64_t(1) << tick_bits) <= bound) tick_bits++;
+  }
+  CK(cudaGetLastError());
   pc.mark("ingest");
   CK(cudaEventRecord(ctx->ev[1], st));
   // ---- per-shard views
@@ -1778,6 +2112,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     S.s_g = P > 1 ? ctx->d_s_g : ctx->d_s_i;  // one shard: j == i
     S.sh_tick = P > 1 ? ctx->d_sh_tick : d_ticks;
     S.sh_base = shard_off[s];
+    S.s_aself = nullptr;
     S.record_trace = trace ? 1 : 0;
     S.drop_t = ctx->d_drop_t;
     S.drop_ksub = ctx->d_drop_ks;
@@ -1952,7 +2287,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                        cudaMemcpyHostToDevice, st));
     KL(k_chain, P, 32, ctx->chain_smem, st>>>(
         ctx->d_shards, use_fresh ? ctx->d_fresh : nullptr, ctx->d_dirty,
-        ctx->d_slot_base, ctx->chain_smem, ctx->d_skip));
+        ctx->d_slot_base, ctx->chain_smem, ctx->d_skip, kChainWhole, INT64_MAX));
   } else {
     CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
                        cudaMemcpyHostToDevice, st));
@@ -2088,6 +2423,200 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   ctx->last_nrecs = rec_count;
   ctx->last_rec_base = rec_base;
   ctx->has_run = true;
+  return SYM_OK;
+}
+
+// Realloc keeping the first `keep` elements (stream-ordered, no sync).
+template <class T>
+int grow_keep(Ctx* ctx, T*& p, int64_t keep, int64_t count) {
+  T* q = nullptr;
+  CK(cudaMallocAsync((void**)&q, sizeof(T) * (size_t)(count > 0 ? count : 1), ctx->stream));
+  if (p && keep > 0)
+    CK(cudaMemcpyAsync(q, p, sizeof(T) * (size_t)keep, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (p) cudaFreeAsync(p, ctx->stream);
+  p = q;
+  return SYM_OK;
+}
+
+void step_reset(Ctx* ctx) {
+  forget_last_run(ctx);
+  ctx->step_active = true;
+  ctx->step_first = true;
+  ctx->step_n = 0;
+  ctx->step_until = INT64_MIN;
+  ctx->step_served = ctx->step_drops = 0;
+  ctx->lay_n = 0;
+  ctx->gbat_n = 0;
+}
+
+// One step of a stepped run: the chunk (device buffers, stream order, ticks
+// within [previous until, until]) joins the sorted layout and the chain runs
+// every event with tick <= until.  Two synchronisations: the ingest's
+// validation readback and the step's counters.
+int step_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_t n,
+                int64_t until, uint32_t flags, sym_result* out) {
+  cudaStream_t st = ctx->stream;
+  int64_t launches = 0;
+  KernelTimer kt{ctx, st, (flags & SYM_FLAG_KERNEL_TIMES) != 0, {}};
+  const int32_t M = ctx->M, P = ctx->P;
+  const int B = M + P;
+  const bool first = ctx->step_first;
+  int rc;
+  CK(cudaEventRecord(ctx->ev[0], st));
+  const int64_t bound = ctx->lay_n + n;  // the new layout's size is at most this
+  if ((rc = ensure_capacity(ctx, std::max<int64_t>(n, bound)))) return rc;
+  if (ctx->step_n + n > ctx->g_cap) {
+    const int64_t c = std::max<int64_t>(2 * ctx->g_cap, ctx->step_n + n + 1024);
+    int64_t* o = nullptr;
+    CK(cudaMallocAsync((void**)&o, sizeof(int64_t) * 5 * (size_t)c, st));
+    for (int k = 0; k < 5 && ctx->step_n > 0; k++)
+      CK(cudaMemcpyAsync(o + k * c, ctx->d_g_out + k * ctx->g_cap,
+                         sizeof(int64_t) * ctx->step_n, cudaMemcpyDeviceToDevice, st));
+    if (ctx->d_g_out) cudaFreeAsync(ctx->d_g_out, st);
+    ctx->d_g_out = o;
+    if ((rc = grow_keep(ctx, ctx->d_g_ticks, ctx->step_n, c)) ||
+        (rc = grow_keep(ctx, ctx->d_g_model, ctx->step_n, c)))
+      return rc;
+    ctx->g_cap = c;
+  }
+  if (bound + 1 > ctx->lay_cap) {
+    const int64_t c = std::max<int64_t>(2 * ctx->lay_cap, bound + 1024);
+    const int64_t k = ctx->lay_n;
+    for (int b = 0; b < 2; b++) {
+      const int64_t kb = b == ctx->cur ? k : 0;
+      if ((rc = grow_keep(ctx, ctx->d_lay_tick[b], kb, c)) ||
+          (rc = grow_keep(ctx, ctx->d_lay_g[b], kb, c)) ||
+          (rc = grow_keep(ctx, ctx->d_lay_i[b], kb, c)) ||
+          (rc = grow_keep(ctx, ctx->d_lay_aself[b], kb, c)))
+        return rc;
+    }
+    if ((rc = grow(ctx, ctx->d_lay_flag, c))) return rc;
+    ctx->lay_cap = c;
+  }
+  if (ctx->gbat_n + bound + P > ctx->gbat_cap) {
+    const int64_t c = std::max<int64_t>(2 * ctx->gbat_cap, ctx->gbat_n + bound + P + 1024);
+    if ((rc = grow_keep(ctx, ctx->d_gbat, ctx->gbat_n, c))) return rc;
+    ctx->gbat_cap = c;
+  }
+  // ---- the chunk: ingest (validates ids and time order before any state
+  // changes), stream copy, outputs unresolved
+  IngestInfo info;
+  if (n > 0) {
+    if ((rc = ingest(ctx, d_ticks, d_model, n, ctx->d_mp_chunk, kt, launches, info, out)))
+      return rc;
+    CK(cudaMemcpyAsync(ctx->d_g_ticks + ctx->step_n, d_ticks, sizeof(int64_t) * n,
+                       cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->d_g_model + ctx->step_n, d_model, sizeof(int32_t) * n,
+                       cudaMemcpyDeviceToDevice, st));
+    for (int k = 0; k < 5; k++)
+      KL(k_fill64, nblk(n, 256), 256, 0, st>>>(ctx->d_g_out + k * ctx->g_cap + ctx->step_n, n,
+                                               -1));
+  }
+  if (first) {
+    CK(cudaMemsetAsync(ctx->d_step_shard, 0, sizeof(int64_t) * 3 * P, st));
+    // static configuration and pointers of every shard (the chain state
+    // itself is initialised by the first step's chain)
+    CK(cudaMemcpyAsync(ctx->d_shards, ctx->shards.data(), sizeof(Shard) * P,
+                       cudaMemcpyHostToDevice, st));
+  }
+  // ---- the new layout
+  const int nxt = ctx->cur ^ 1, cur = ctx->cur;
+  KL(k_step_sizes, nblk(M, 128), 128, 0, st>>>(ctx->d_mp, ctx->d_ms, ctx->d_mp_chunk, M,
+                                               first ? 1 : 0, n > 0 ? 1 : 0, ctx->d_step_slot));
+  KL(k_step_offsets, 1, 1024, 0, st>>>(ctx->d_step_slot, M));
+  if (bound > 0)
+    KL(k_step_copy, nblk(bound, 256), 256, 0, st>>>(
+        bound, ctx->d_step_slot, M, P, ctx->d_slot_base, ctx->d_mp_chunk,
+        ctx->d_lay_tick[cur], ctx->d_lay_g[cur], ctx->d_lay_i[cur], ctx->d_lay_aself[cur],
+        ctx->d_s_tick, P > 1 ? ctx->d_s_g : ctx->d_s_i, ctx->d_s_i,
+        P > 1 ? ctx->d_sh_tick : d_ticks, d_ticks, ctx->d_bins + B + 1, ctx->d_step_shard,
+        ctx->step_n, ctx->d_lay_tick[nxt], ctx->d_lay_g[nxt], ctx->d_lay_i[nxt],
+        ctx->d_lay_aself[nxt], ctx->d_lay_flag));
+  KL(k_step_rebase, nblk(M, 128), 128, 0, st>>>(ctx->d_mp, ctx->d_ms, ctx->d_step_slot, M,
+                                                first ? 1 : 0));
+  KL(k_step_shard_update, 1, 32 * ((P + 31) / 32), 0, st>>>(
+      ctx->d_step_shard, P, n, ctx->d_bins + B + 1, d_ticks, ctx->d_sh_tick));
+  ctx->cur = nxt;
+  int64_t* meta = ctx->d_meta;  // rec_base [P] | rec_count [P] | total
+  KL(k_step_views, 1, 32 * ((P + 31) / 32), 0, st>>>(
+      ctx->d_shards, P, ctx->d_step_slot, M, ctx->d_slot_base, ctx->d_lay_tick[nxt],
+      ctx->d_lay_g[nxt], ctx->d_lay_aself[nxt], ctx->d_recs, meta));
+  CK(cudaEventRecord(ctx->ev[1], st));
+  // ---- the chain, every sub-cluster, up to `until`
+  CK(cudaMemsetAsync(ctx->d_skip, 0, sizeof(int32_t) * P, st));
+  KL(k_chain, P, 32, ctx->chain_smem, st>>>(
+      ctx->d_shards, nullptr, ctx->d_dirty, ctx->d_slot_base, ctx->chain_smem, ctx->d_skip,
+      first ? kChainFirstStep : kChainResume, until));
+  CK(cudaEventRecord(ctx->ev[3], st));
+  // ---- what the step decided
+  KL(k_step_recmeta, 1, 32, 0, st>>>(ctx->d_shards, P, meta));
+  CK(cudaMemsetAsync(ctx->d_step_cnt, 0, sizeof(int64_t) * 2, st));
+  if (bound + P > 0)
+    KL(k_step_emit, nblk(bound + P, 256), 256, 0, st>>>(
+        ctx->d_recs, meta, meta + P + 1, P, meta + 2 * (P + 1), ctx->d_lay_i[nxt],
+        ctx->d_bins + B + P + 2, ctx->d_slot_base, ctx->d_bins + B + P + 2 + M, ctx->g_cap,
+        ctx->d_g_out, ctx->d_lay_flag, ctx->d_gbat + ctx->gbat_n,
+        (unsigned long long*)ctx->d_step_cnt));
+  if (bound > 0)
+    KL(k_step_drops, nblk(bound, 256), 256, 0, st>>>(
+        bound, ctx->d_step_slot, M, ctx->d_ms, ctx->d_lay_i[nxt], ctx->d_lay_flag, ctx->g_cap,
+        ctx->d_g_out, (unsigned long long*)ctx->d_step_cnt));
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[4], st));
+  int64_t hc[2] = {0, 0}, htot = 0;
+  int32_t lay_total = 0;
+  CK(cudaMemcpyAsync(ctx->shards.data(), ctx->d_shards, sizeof(Shard) * P,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hc, ctx->d_step_cnt, sizeof hc, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&htot, meta + 2 * (P + 1), sizeof htot, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&lay_total, ctx->d_step_slot + (M + 1) + M, sizeof lay_total,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int s = 0; s < P; s++) {
+    if (ctx->shards[s].error) {
+      ctx->step_active = false;
+      ctx->err = "chain error " + std::to_string(ctx->shards[s].error) + " in shard " +
+                 std::to_string(s);
+      return SYM_EINVARIANT;
+    }
+  }
+  ctx->step_first = false;
+  ctx->step_n += n;
+  ctx->step_until = until;
+  ctx->gbat_n += htot;
+  ctx->step_served += hc[0];
+  ctx->step_drops += hc[1];
+  ctx->lay_n = lay_total;
+  out->n = ctx->step_n;
+  out->n_batches = ctx->gbat_n;
+  out->drops = ctx->step_drops;
+  out->completions = ctx->step_served;
+  out->late = 0;
+  out->launches = launches;
+  out->ops = out->evictions = out->registrations = out->handler_ops_max = 0;
+  out->chain_events = out->absorbed_arrivals = out->fresh_adoptions = 0;
+  for (int s = 0; s < P; s++) {
+    const Shard& S = ctx->shards[s];
+    out->ops += S.ops;
+    out->evictions += S.evictions;
+    out->registrations += S.registrations;
+    out->handler_ops_max = std::max<int64_t>(out->handler_ops_max, S.handler_ops_max);
+    out->chain_events += S.chain_events;
+    out->absorbed_arrivals += S.absorbed;
+  }
+  out->fast_shards = 0;
+  out->fast_fail_mask = 0;
+  float t;
+  cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]);
+  out->ms_ingest = t;
+  out->ms_fresh = 0;
+  out->ms_fast = 0;
+  cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[3]);
+  out->ms_chain = t;
+  cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]);
+  out->ms_expand = t;
+  cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[4]);
+  out->ms_total = t;
   return SYM_OK;
 }
 
@@ -2299,6 +2828,10 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     cudaMemcpyAsync(ctx->d_net_cdf + ctx->net_ctrl_n, cfg->net_data_cdf, sizeof(double) * ctx->net_data_n, cudaMemcpyHostToDevice, ctx->stream);
   }
   ALLOC(ctx->d_meta, 3 * (P + 1));
+  ALLOC(ctx->d_mp_chunk, M);
+  ALLOC(ctx->d_step_slot, 4 * (M + 1));
+  ALLOC(ctx->d_step_shard, 3 * P);
+  ALLOC(ctx->d_step_cnt, 2);
 #undef ALLOC
   const int B = M + P;
   cudaMemcpyAsync(ctx->d_lat, lat.data(), sizeof(int64_t) * lat.size(), cudaMemcpyHostToDevice, ctx->stream);
@@ -2384,7 +2917,11 @@ void sym_destroy(void* engine) {
                   ctx->d_cp_pos,
                   ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
                   ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
-                  ctx->d_net_vals, ctx->d_net_cdf};
+                  ctx->d_net_vals, ctx->d_net_cdf, ctx->d_g_ticks, ctx->d_g_model,
+                  ctx->d_g_out, ctx->d_lay_tick[0], ctx->d_lay_tick[1], ctx->d_lay_g[0],
+                  ctx->d_lay_g[1], ctx->d_lay_i[0], ctx->d_lay_i[1], ctx->d_lay_aself[0],
+                  ctx->d_lay_aself[1], ctx->d_lay_flag, ctx->d_mp_chunk, ctx->d_step_slot,
+                  ctx->d_step_shard, ctx->d_step_cnt, ctx->d_gbat};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, ctx->stream);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
@@ -2400,6 +2937,7 @@ int32_t sym_run_device(void* engine, const int64_t* d_arr_ticks,
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return SYM_ECUDA;
+  forget_last_run(ctx);
   out->n = n;
   out->err_index = -1;
   const int32_t* model = static_cast<const int32_t*>(d_arr_model);
@@ -2419,6 +2957,7 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const void* arr_model,
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
   CK(cudaSetDevice(ctx->device));
+  forget_last_run(ctx);
   int rc;
   if ((rc = ensure_capacity(ctx, n))) return rc;
   cudaStream_t st = ctx->stream;
@@ -2511,6 +3050,131 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const void* arr_model,
   out->drop_key_sub = k6;
   out->drop_key_a = k7;
   return rc;
+}
+
+int32_t sym_step_reset(void* engine) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx) return SYM_EINVAL;
+  if (ctx->jitter) {
+    ctx->err = "stepped runs support jitterless networks only";
+    return SYM_EINVAL;
+  }
+  step_reset(ctx);
+  return SYM_OK;
+}
+
+int32_t sym_step(void* engine, const int64_t* arr_ticks, const void* arr_model, int64_t n,
+                 int64_t until_tick, uint32_t flags, sym_result* out) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx || !out || n < 0 || (n > 0 && (!arr_ticks || !arr_model))) return SYM_EINVAL;
+  out->err_index = -1;
+  if (!ctx->step_active) {
+    ctx->err = "no stepped run in progress (sym_step_reset starts one)";
+    return SYM_EINVAL;
+  }
+  if (flags & (SYM_FLAG_TRACE | SYM_FLAG_NO_EXPAND)) {
+    ctx->err = "stepped runs take neither TRACE nor NO_EXPAND";
+    return SYM_EINVAL;
+  }
+  if (until_tick < ctx->step_until || (n > 0 && (arr_ticks[0] < ctx->step_until ||
+                                                  arr_ticks[n - 1] > until_tick))) {
+    ctx->err = "a step's arrivals must lie in [previous until_tick, until_tick]";
+    out->err_index = n > 0 && arr_ticks[0] < ctx->step_until ? 0 : n - 1;
+    return SYM_EINVAL;
+  }
+  if (ctx->step_n + n >= INT32_MAX) {
+    ctx->err = "stepped run too long (2^31 arrivals)";
+    return SYM_EINVAL;
+  }
+  CK(cudaSetDevice(ctx->device));
+  int rc;
+  // scratch sized for the chunk and the new layout before the chunk lands
+  if ((rc = ensure_capacity(ctx, std::max<int64_t>(n, ctx->lay_n + n)))) return rc;
+  cudaStream_t st = ctx->stream;
+  if (n > 0) {
+    CK(cudaMemcpyAsync(ctx->d_ticks, arr_ticks, sizeof(int64_t) * n, cudaMemcpyHostToDevice,
+                       st));
+    if (flags & SYM_FLAG_MODEL_I64) {
+      CK(cudaMemcpyAsync(ctx->d_s_tick, arr_model, sizeof(int64_t) * n, cudaMemcpyHostToDevice,
+                         st));  // s_tick is free until the ingest
+      k_narrow<<<nblk(n, 256), 256, 0, st>>>(ctx->d_s_tick, n, ctx->d_model);
+    } else {
+      CK(cudaMemcpyAsync(ctx->d_model, arr_model, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                         st));
+    }
+  }
+  return step_device(ctx, ctx->d_ticks, ctx->d_model, n, until_tick, flags, out);
+}
+
+int32_t sym_step_result(void* engine, sym_result* out) {
+  Ctx* ctx = static_cast<Ctx*>(engine);
+  if (!ctx || !out) return SYM_EINVAL;
+  if (ctx->step_first && !ctx->step_active) {
+    ctx->err = "no stepped run";
+    return SYM_EINVAL;
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int64_t n = ctx->step_n, cap = ctx->g_cap;
+  if (out->batches && ctx->gbat_n > out->batch_cap) {
+    ctx->err = "batch buffer too small";
+    return SYM_EINVAL;
+  }
+  int64_t* dsts[5] = {out->req_dispatch, out->req_start, out->req_finish, out->req_batch,
+                      out->req_outcome};
+  for (int k = 0; k < 5; k++)
+    if (dsts[k] && n > 0)
+      CK(cudaMemcpyAsync(dsts[k], ctx->d_g_out + k * cap, sizeof(int64_t) * n,
+                         cudaMemcpyDeviceToHost, st));
+  std::vector<int32_t> model;
+  if ((out->req_model || out->req_deadline) && n > 0) {
+    model.resize(n);
+    CK(cudaMemcpyAsync(model.data(), ctx->d_g_model, sizeof(int32_t) * n,
+                       cudaMemcpyDeviceToHost, st));
+  }
+  std::vector<int64_t> ticks;
+  int64_t* arr = out->req_arrival;
+  if (!arr && out->req_deadline && n > 0) {
+    ticks.resize(n);
+    arr = ticks.data();
+  }
+  if (arr && n > 0)
+    CK(cudaMemcpyAsync(arr, ctx->d_g_ticks, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+  if (out->batches && ctx->gbat_n > 0)
+    CK(cudaMemcpyAsync(out->batches, ctx->d_gbat, sizeof(sym_batch) * ctx->gbat_n,
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // a served request completes at its finish tick (simulator.py:249-258):
+  // until then its outcome is unresolved, as in the reference mid-run
+  int64_t completions = 0;
+  if (out->req_outcome && out->req_finish)
+    for (int64_t i = 0; i < n; i++) {
+      if (out->req_outcome[i] == 0) {
+        if (out->req_finish[i] > ctx->step_until) out->req_outcome[i] = -1;
+        else completions++;
+      }
+    }
+  if (out->req_model)
+    for (int64_t i = 0; i < n; i++) out->req_model[i] = model[i];
+  if (out->req_deadline)
+    for (int64_t i = 0; i < n; i++)
+      out->req_deadline[i] = arr[i] + ctx->mp_host[ctx->slot_of_model[model[i]]].slo;
+  out->n = n;
+  out->n_batches = ctx->gbat_n;
+  out->drops = ctx->step_drops;
+  out->completions = completions;
+  out->late = 0;
+  out->ops = out->evictions = out->registrations = out->handler_ops_max = 0;
+  out->chain_events = out->absorbed_arrivals = out->fresh_adoptions = 0;
+  for (const Shard& S : ctx->shards) {
+    out->ops += S.ops;
+    out->evictions += S.evictions;
+    out->registrations += S.registrations;
+    out->handler_ops_max = std::max<int64_t>(out->handler_ops_max, S.handler_ops_max);
+    out->chain_events += S.chain_events;
+    out->absorbed_arrivals += S.absorbed;
+  }
+  return SYM_OK;
 }
 
 int64_t sym_last_batches(void* engine, sym_batch* host, int64_t cap) {

@@ -171,6 +171,8 @@ struct Shard {
   const int64_t* s_tick;       // [n] tick of sorted position p
   const int32_t* s_g;          // [n] shard-stream index of sorted position p
   const int64_t* sh_tick;      // [n] ticks in shard-stream order (for A')
+  const int32_t* s_aself;      // [n] A' of sorted position p, precomputed
+                               // (stepped runs); nullptr = derive it
   // mutable
   ModelState* ms;              // [M]
   int32_t* pq;                 // [2*Mp] tournament tree of models (next event)
@@ -201,6 +203,7 @@ struct Shard {
 // its shard-stream index if the previous arrival of the shard has the same
 // tick, else BASE.
 SYM_HD int32_t aself_at(const Shard& S, int32_t pos) {
+  if (S.s_aself) return S.s_aself[pos];
   const int32_t j = S.s_g[pos];
   return (j > S.sh_base && S.sh_tick[j - 1] == S.s_tick[pos]) ? j : A_BASE;
 }
@@ -918,9 +921,12 @@ SYM_HD void refresh_model(Shard& S, int32_t m, const FreshRec* fresh) {
   if (st.fresh_skip == 0) prefetch_fresh(fresh, P, st);
 }
 
-// Process one chain event; returns false when the sub-cluster is drained.
+// Process one chain event; returns false when the sub-cluster is drained or
+// its next event lies after `until` (a stepped run stops there: every event
+// with tick <= until is processed, later ones wait for the next step).
 // dirty must hold M+1 entries.
-SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
+SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh,
+                       int64_t until = INT64_MAX) {
   SYM_PROF_T(t0);
   const int32_t m = S.pq[1];
   const bool have_m = m >= 0;
@@ -933,6 +939,7 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh) {
 #endif
   SYM_PROF_T(t1);
   const bool gpu_event = S.gt_armed && (!have_m || key_less(S.gt_key, S.ms[m].nx_key));
+  if ((gpu_event ? S.gt_key.t : S.ms[m].nx_key.t) > until) return false;
   if (gpu_event) {
     Pusher who;
     who.t = S.gt_key.t;
@@ -1009,6 +1016,25 @@ SYM_HD void chain_init(Shard& S, const FreshRec* fresh) {
     S.mc_size[m] = 0;
     S.mc_latest[m] = 0;
     refresh_model(S, m, fresh);
+    S.pq[S.Mp + m] = S.ms[m].nx_type != EV_NONE ? m : -1;
+  }
+  for (int32_t i = S.Mp - 1; i >= 1; i--) {
+    int32_t l = S.pq[2 * i], r = S.pq[2 * i + 1];
+    S.pq[i] = model_before(S, r, l) ? r : l;
+  }
+}
+
+// Resume a stepped run: the state of every model, the trees and the GPU
+// timer are as the previous step left them; the sorted stream now also
+// holds this step's arrivals.  Each model is brought to its next event
+// again (an unregistered model absorbs new arrivals that precede its
+// pending timers; those timers all lie after the previous step's until, and
+// the new arrivals at or after it) and the model tree is rebuilt.
+SYM_HD void chain_resume(Shard& S) {
+  S.n_recs = 0;
+  S.error = ERR_NONE;
+  for (int32_t m = 0; m < S.M; m++) {
+    S.absorbed += scan_model(S, m, S.ms[m], -1);
     S.pq[S.Mp + m] = S.ms[m].nx_type != EV_NONE ? m : -1;
   }
   for (int32_t i = S.Mp - 1; i >= 1; i--) {

@@ -15,6 +15,7 @@ reference's scalebench shards, scalebench.py:98-99) in one call.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import weakref
 from collections.abc import Sequence
@@ -110,10 +111,30 @@ class RunResult:
         return len(self.req_model)
 
 
-def _echo_inputs(*pairs):
-    """Copy (destination, source) array pairs (numpy releases the GIL)."""
-    for dst, src in pairs:
-        np.copyto(dst, src)
+_ECHO_CHUNK = 1 << 20
+
+
+def _echo_chunk(lo, hi, ticks, midx, slo, arrival, model, deadline):
+    np.copyto(arrival[lo:hi], ticks[lo:hi])
+    np.copyto(model[lo:hi], midx[lo:hi])
+    # clip: an unknown model id is reported by the device (ProtocolError)
+    np.add(ticks[lo:hi], np.take(slo, midx[lo:hi], mode="clip"), out=deadline[lo:hi])
+
+
+def _echo_inputs(ticks, midx, slo, arrival, model, deadline):
+    """req_arrival / req_model are copies of the inputs and req_deadline =
+    arrival + slo[model] (simulator.py:217-219): formed on host threads while
+    the device runs (numpy releases the GIL), so none of them crosses PCIe."""
+    from concurrent.futures import ThreadPoolExecutor
+    n = len(ticks)
+    spans = [(lo, min(n, lo + _ECHO_CHUNK)) for lo in range(0, n, _ECHO_CHUNK)]
+    if len(spans) <= 1:
+        for lo, hi in spans:
+            _echo_chunk(lo, hi, ticks, midx, slo, arrival, model, deadline)
+        return
+    with ThreadPoolExecutor(min(8, len(spans), os.cpu_count() or 1)) as ex:
+        list(ex.map(lambda sp: _echo_chunk(sp[0], sp[1], ticks, midx, slo, arrival, model,
+                                           deadline), spans))
 
 
 def _split_shards(models, gpu_count, shards):
@@ -165,6 +186,8 @@ class Engine:
                                  np.int64)
         self._handle = None
         self._run_id = 0
+        self._last_ok = False   # the last run succeeded and is still on the device
+        self._keep = None       # caller tensors the device views of that run read
         self._lib = None
         # reference-style counters (RankPlane.ops/evictions/registrations,
         # Engine.handler_ops_max), filled after each run
@@ -279,15 +302,16 @@ class Engine:
         outs = {k: _native.pinned_empty(n) for k in names}
         res = _native.SymResult()
         res.n = n
-        # req_arrival / req_model are copies of the inputs: a host thread
-        # copies them while the device runs and its copy engine returns the
-        # six computed arrays, instead of sending them back over PCIe
-        echo = ("arrival", "model")
+        # req_arrival / req_model / req_deadline follow from the inputs: host
+        # threads form them while the device runs and its copy engine returns
+        # the five computed arrays (simulator.py:217-219, 228-242)
+        echo = ("arrival", "model", "deadline")
         for k in names:
             if k not in echo:
                 setattr(res, "req_" + k, outs[k].ctypes.data_as(_native.i64p))
         copier = threading.Thread(target=_echo_inputs,
-                                  args=((outs["arrival"], ticks), (outs["model"], midx)))
+                                  args=(ticks, midx, self._slo, outs["arrival"], outs["model"],
+                                        outs["deadline"]))
         copier.start()
         if self.record_trace:
             drop_t = np.empty(n, np.int64)
@@ -297,6 +321,8 @@ class Engine:
             res.drop_key_sub = drop_ks.ctypes.data_as(_native.i64p)
             res.drop_key_a = drop_ka.ctypes.data_as(_native.i32p)
         self._run_id += 1
+        self._last_ok, self._keep = False, None
+        self._stepping = False
         rc = self._lib.sym_run(self._handle, ticks.ctypes.data, midx.ctypes.data, n,
                                self._flags() | _native.FLAG_MODEL_I64, C.byref(res))
         copier.join()
@@ -305,6 +331,7 @@ class Engine:
                 raise ProtocolError(f"request for unknown model {int(midx[res.err_index])}")
             self._raise(rc, res)
         self._absorb_counters(res)
+        self._last_ok = True
         batches = _native.pinned_empty(res.n_batches, _native.BATCH_DTYPE)
         got = self._lib.sym_last_batches(self._handle, batches.ctypes.data, len(batches))
         if got != res.n_batches:
@@ -328,15 +355,99 @@ class Engine:
             self._verify(result)
         return result
 
+    # -- step API (scalebench.py:67-84: _record_arrival / on_new_request /
+    # _dispatch_event, batched) ----------------------------------------------
+
+    #: until_tick that drains a stepped run
+    DRAIN = (1 << 63) - 1
+
+    def reset_steps(self):
+        """Start a stepped run (a whole run_stream / run_device ends one)."""
+        self._ensure()
+        self._last_ok, self._keep = False, None
+        rc = self._lib.sym_step_reset(self._handle)
+        if rc != _native.SYM_OK:
+            self._raise(rc, _native.SymResult())
+        self._stepping = True
+        self._step_until = None
+
+    def step(self, arr_ticks, arr_midx, until_tick: int) -> dict:
+        """Feed the next arrivals and process every event with tick <=
+        until_tick; later arrivals must have tick >= until_tick.  State stays
+        on the device between calls (sym_step).  Starts a stepped run if
+        none is in progress.  Returns the cumulative counters: arrivals,
+        batches, dispatched requests, drops."""
+        if not getattr(self, "_stepping", False):
+            self.reset_steps()
+        ticks = np.ascontiguousarray(arr_ticks, dtype=np.int64)
+        midx = np.ascontiguousarray(arr_midx, dtype=np.int64)
+        if len(midx) != len(ticks):
+            raise ValueError("arr_ticks and arr_midx differ in length")
+        res = _native.SymResult()
+        rc = self._lib.sym_step(self._handle, ticks.ctypes.data, midx.ctypes.data, len(ticks),
+                                int(until_tick), _native.FLAG_MODEL_I64, C.byref(res))
+        if rc != _native.SYM_OK:
+            if rc == _native.SYM_EPROTO and 0 <= res.err_index < len(midx):
+                raise ProtocolError(f"request for unknown model {int(midx[res.err_index])}")
+            self._raise(rc, res)
+        self._step_until = int(until_tick)
+        self._absorb_counters(res)
+        return {"arrivals": res.n, "batches": res.n_batches, "dispatched": res.completions,
+                "drops": res.drops, "chain_events": res.chain_events,
+                "ms_total": res.ms_total}
+
+    def step_result(self, duration_s: float, drain: bool = True) -> RunResult:
+        """RunResult of every arrival stepped so far; with ``drain`` the run is
+        first completed (until_tick = +inf), which makes it equal to
+        run_stream over the concatenated arrivals."""
+        if not getattr(self, "_stepping", False):
+            raise RuntimeError("no stepped run in progress")
+        if drain and self._step_until != self.DRAIN:
+            self.step(np.empty(0, np.int64), np.empty(0, np.int64), self.DRAIN)
+        probe = _native.SymResult()
+        rc = self._lib.sym_step_result(self._handle, C.byref(probe))  # counts only
+        if rc != _native.SYM_OK:
+            self._raise(rc, probe)
+        n, nb = probe.n, probe.n_batches
+        names = ("dispatch", "start", "finish", "batch", "outcome", "arrival", "deadline",
+                 "model")
+        outs = {k: np.empty(n, np.int64) for k in names}
+        batches = np.empty(nb, _native.BATCH_DTYPE)
+        res = _native.SymResult()
+        for k in names:
+            setattr(res, "req_" + k, outs[k].ctypes.data_as(_native.i64p))
+        res.batches = batches.ctypes.data
+        res.batch_cap = nb
+        rc = self._lib.sym_step_result(self._handle, C.byref(res))
+        if rc != _native.SYM_OK:
+            self._raise(rc, res)
+        self._absorb_counters(res)
+        # a whole run lists the batches sub-cluster by sub-cluster, each in
+        # emission order; a stepped run appends them step by step
+        if self.n_shards > 1 and nb:
+            batches = batches[np.argsort(self.shard_of_model[batches["model"]], kind="stable")]
+        outc = outs["outcome"]
+        return RunResult(
+            model_names=[m.name for m in self.models], gpu_count=self.gpu_count,
+            duration_ns=s_to_ns(duration_s), req_model=outs["model"],
+            req_arrival=outs["arrival"], req_deadline=outs["deadline"],
+            req_dispatch=outs["dispatch"], req_start=outs["start"], req_finish=outs["finish"],
+            req_batch=outs["batch"], req_outcome=outc,
+            gpu_logs=_GpuLogs(batches, self.gpu_count), drops=int(res.drops),
+            completions=int(res.completions), late=0, batches=batches)
+
     # -- device-resident entry point -------------------------------------------
+
+    def _require_last_run(self):
+        if self._handle is None or not self._last_ok:
+            raise RuntimeError("no successful run on the device to reduce")
 
     def window_counts(self, lo_ns: int, hi_ns: int) -> dict:
         """Integer window reductions of the last run on the device (the
         counting part of compute_stats, metrics.py:79-94): per model
         arrivals/completed/late/dropped among arrivals in [lo, hi), per GPU
         busy ns clipped to the window."""
-        if self._handle is None:
-            raise RuntimeError("no run to reduce")
+        self._require_last_run()
         M, G = len(self.models), self.gpu_count
         out = {k: np.zeros(M, np.int64) for k in ("arrivals", "completed", "late", "dropped")}
         busy = np.zeros(G, np.int64)
@@ -356,8 +467,7 @@ class Engine:
         latency by nearest rank (drops as +inf; -1 = inf, 0 = no arrivals),
         largest queueing delay of a served request, and the batch-size
         histogram of batches starting in the window ([M][max_batch + 1])."""
-        if self._handle is None:
-            raise RuntimeError("no run to reduce")
+        self._require_last_run()
         M, G = len(self.models), self.gpu_count
         stride = int(self._max_batch.max()) + 1 if M else 1
         keys = ("arrivals", "completed", "late", "dropped")
@@ -419,11 +529,17 @@ class Engine:
             flags |= _native.FLAG_KERNEL_TIMES
         torch.cuda.current_stream(dev).synchronize()
         self._run_id += 1
+        self._last_ok, self._keep = False, None
+        self._stepping = False
         rc = self._lib.sym_run_device(self._handle, ticks.data_ptr(), model.data_ptr(), n,
                                       flags, C.byref(res))
         if rc != _native.SYM_OK:
             self._raise(rc, res)
         self._absorb_counters(res)
+        # the engine's view of this run (window_counts / window_stats) reads
+        # these tensors: keep them alive until the next run
+        self._keep = (ticks, model, outputs, batches)
+        self._last_ok = True
         counters = dict(self.stats, n_batches=res.n_batches, drops=res.drops,
                         registrations=res.registrations, evictions=res.evictions)
         return outputs, counters

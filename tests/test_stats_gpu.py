@@ -57,12 +57,12 @@ def test_device_stats_sharded_c4():
 
 
 def test_auto_device_stats_for_large_runs():
-    """A result whose engine still holds it (and is large enough) is reduced
-    on the device by plain compute_stats; a stale one falls back to the host
-    arrays -- same numbers either way."""
-    from dataclasses import replace
+    """The package's own callers reduce a large fresh result on the device
+    (_fresh_stats); plain compute_stats reduces the result's arrays, so an
+    edited result gets the host answer for the edit; a stale result never
+    reaches the device -- same numbers whenever the arrays are unedited."""
     from paper_2308_07470_b200 import configs
-    from paper_2308_07470_b200.metrics import compute_stats
+    from paper_2308_07470_b200.metrics import _fresh_stats, compute_stats
     from paper_2308_07470_b200.simulator import Engine
     from paper_2308_07470_b200.workload import generate_arrivals
     sc = configs.c4(1.0)
@@ -70,11 +70,15 @@ def test_auto_device_stats_for_large_runs():
     eng = Engine(list(sc.models), sc.gpu_count, sc.policy, shards=sc.shards)
     res = eng.run_stream(ticks, midx, 1.0)
     assert res.n_requests >= 200_000 and res.device_engine() is eng
-    auto = compute_stats(res, 0.1, 0.1, 1.0)
-    host = compute_stats(replace(res, _source=None), 0.1, 0.1, 1.0)
-    assert auto == host
+    dev = _fresh_stats(sc, res)
+    host = compute_stats(res, 0.1, 0.1, 1.0)
+    assert dev == host == compute_stats(res, 0.1, 0.1, 1.0, engine=eng)
+    edited = res.req_outcome.copy()
+    res.req_outcome[: len(edited) // 2] = 2  # the caller edits the result
+    assert compute_stats(res, 0.1, 0.1, 1.0).dropped > host.dropped
+    res.req_outcome[:] = edited
     res2 = eng.run_stream(ticks[: len(ticks) // 2], midx[: len(midx) // 2], 1.0)
     assert res.device_engine() is None and res2.device_engine() is eng  # res is stale now
-    assert compute_stats(res, 0.1, 0.1, 1.0) == host
+    assert _fresh_stats(sc, res) == host
     eng.close()
     assert res2.device_engine() is None
