@@ -83,6 +83,14 @@ typedef struct {
   const double *net_ctrl_cdf, *net_data_cdf;
   int64_t net_ctrl_const, net_data_const;
   uint64_t net_key[2];
+  /* Several devices in one call: with n_devices >= 2,
+   * sub-cluster s runs on devices[s mod n_devices] and every call spans
+   * them; results equal the one-device run.  NULL / 0 = `device` alone.
+   * The device-pointer, step and kernel-timing entry points take
+   * one-device handles only. */
+  const int32_t *devices;
+  int32_t n_devices;
+  int32_t _pad_dev;
 } sym_config;
 
 /* Batch record = one ExecutionOrder (scheduler.py:123-135) / one gpu_logs

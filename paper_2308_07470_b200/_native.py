@@ -38,6 +38,7 @@ class SymConfig(C.Structure):
         ("net_ctrl_cdf", C.POINTER(C.c_double)), ("net_data_cdf", C.POINTER(C.c_double)),
         ("net_ctrl_const", C.c_int64), ("net_data_const", C.c_int64),
         ("net_key", C.c_uint64 * 2),
+        ("devices", i32p), ("n_devices", C.c_int32), ("_pad_dev", C.c_int32),
     ]
 
 

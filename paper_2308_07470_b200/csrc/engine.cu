@@ -31,19 +31,18 @@
 #include "../../include/symphony_b200.h"
 #include "engine_core.cuh"
 #include "fastpath.cuh"
+#include "multi.h"
 
 using namespace sym;
 
 namespace {
 
 constexpr int kChunkR = 256;      // keys per warp in the radix passes
-constexpr int kIngestWarps = 8;                    // warps per ingest block
-constexpr int kPerLane = 8;                        // stream elements per lane
-constexpr int kChunkI = kIngestWarps * 32 * kPerLane;  // stream elements per block
 constexpr int kFreshMaxSteps = 1 << 16;
 constexpr int kVersion = 1;
 
 struct Ctx {
+  uint32_t magic = kSymSingleMagic;  // first member: multi.h tells the handles apart
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[6] = {};
@@ -79,12 +78,17 @@ struct Ctx {
   size_t chain_smem = 0;            // dynamic smem of k_chain
   int64_t max_slo = 0, max_lat = 0; // bounds for the sort-key width
   // per-run buffers (grown)
-  int64_t cap = 0, W_cap = 0;
+  int64_t cap = 0;
   int64_t *d_ticks = nullptr, *d_s_tick = nullptr, *d_sh_tick = nullptr;
   int32_t *d_inv = nullptr, *d_bid = nullptr;  // stream -> sorted position, position -> record
   int32_t *d_model = nullptr, *d_s_g = nullptr, *d_s_i = nullptr;
-  int32_t* d_hist = nullptr;        // [W][B]
-  int32_t* d_bins = nullptr;        // [B+1] totals -> offsets
+  int32_t* d_bins = nullptr;        // [B+1] (unused) | shard_off | model_of_slot | gpu_base
+  unsigned long long* d_ing_tot = nullptr;  // [B] per-bin totals (ingest pass A)
+  int32_t* d_ing_start = nullptr;   // [B] first sorted position of each bin
+  unsigned int* d_ing_ticket = nullptr;
+  unsigned long long* d_ing_status = nullptr;  // [tiles][B] look-back words
+  int64_t ing_status_cap = 0;
+  uint64_t ing_epoch = 0;
   int32_t* d_err = nullptr;
   FreshRec* d_fresh = nullptr;
   BatchRec* d_recs = nullptr;
@@ -175,45 +179,6 @@ int grow(Ctx* ctx, T*& p, int64_t count) {
 
 // --------------------------------------------------------------- K1 -------
 
-// Per-block-chunk histogram of (slot, shard) bins, bin-major (hist[b][w]);
-// also checks model ids and the time order of the stream.  Equal bins of a
-// warp round are aggregated with __match_any_sync before the shared atomic.
-__global__ void __launch_bounds__(32 * kIngestWarps)
-k_hist(const int32_t* __restrict__ model, const int64_t* __restrict__ ticks, int64_t n,
-       const int32_t* __restrict__ slot_of_model, const int32_t* __restrict__ shard_of_model,
-       int32_t M, int32_t P, int32_t* __restrict__ hist, int64_t W,
-       int32_t* __restrict__ err) {
-  extern __shared__ int32_t cnt[];
-  const int B = M + P, lane = threadIdx.x & 31;
-  const int64_t w = blockIdx.x;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) cnt[b] = 0;
-  __syncthreads();
-  const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
-  for (int64_t i0 = lo + (threadIdx.x & ~31); i0 < hi; i0 += blockDim.x) {
-    const int64_t i = i0 + lane;
-    int32_t sl = -1 - lane, sd = -2 - lane - 32;  // unique dummies when inactive
-    if (i < hi) {
-      if (i > 0 && ticks[i] < ticks[i - 1])  // arrivals must be time-ordered
-        atomicMin(err + 1, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
-      const int32_t m = model[i];
-      if (m < 0 || m >= M) {
-        atomicMin(err, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
-      } else {
-        sl = slot_of_model[m];
-        sd = M + shard_of_model[m];
-      }
-    }
-    // slot bins: ~M distinct addresses per round, plain shared atomics;
-    // shard bins: few addresses, aggregated per warp first
-    if (sl >= 0) atomicAdd(&cnt[sl], 1);
-    const unsigned pd = __match_any_sync(0xffffffffu, sd);
-    if (sl >= 0 && (pd >> lane) == 1u) atomicAdd(&cnt[sd], __popc(pd));
-  }
-  __syncthreads();
-  if (w < W)
-    for (int b = threadIdx.x; b < B; b += blockDim.x) hist[(int64_t)b * W + w] = cnt[b];
-}
-
 // ---- device-wide exclusive scan of an int32 array (reduce, scan the block
 // sums, rescan with offsets).  Histograms are stored bin-major (hist[b][w]),
 // so this one scan yields every stable scatter base: base(w, b) =
@@ -296,118 +261,190 @@ k_scan_down(int32_t* __restrict__ a, int64_t len, const int32_t* __restrict__ pa
   }
 }
 
-// ModelParam.off/cnt per slot and the shard stream offsets, read off the
-// scanned bin-major histogram (first column of every bin).
-__global__ void k_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t M, int32_t P,
-                         int64_t n, ModelParam* __restrict__ mp,
-                         int32_t* __restrict__ shard_off) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  auto first = [&](int bin) -> int32_t {
-    return W > 0 ? hist[(int64_t)bin * W] : 0;
-  };
-  if (b < M) {
-    const int32_t o = first(b);
-    const int32_t e = b + 1 < M ? first(b + 1) : (int32_t)n;
-    mp[b].off = o;
-    mp[b].cnt = e - o;
-  } else if (b < M + P) {
-    const int s = b - M;
-    shard_off[s] = first(b) - (int32_t)n;
-    if (s == P - 1) shard_off[P] = (int32_t)n;
+// ---- K1, one sweep: stable partition with decoupled look-back ----------
+// Pass A (k_ing_count): per-bin totals of the whole stream (persistent
+// blocks, one shared histogram each, one global atomic per bin per block)
+// and the model-id check.  k_ing_offsets: exclusive scan of the totals ->
+// each bin's first sorted position (ModelParam.off/cnt, shard offsets).
+// Pass B (k_ing_scatter): tiles of kTileI arrivals taken in ticket order;
+// a tile counts its bins, publishes the counts, looks back over its
+// predecessors' published counts for each bin's running prefix (decoupled
+// look-back: a predecessor publishes its own count first and its inclusive
+// prefix as soon as it knows it), ranks every element stably (per-warp
+// offsets + __match_any_sync), stages the tile in shared memory in bin order
+// and writes bin runs.  The stream is read once (plus 4 B/request in pass
+// A) and every output is written once; no histogram of the size of the data
+// is materialised or scanned.
+constexpr int kTileWarps = 8;
+constexpr int kTilePerLane = 16;
+constexpr int kTileI = kTileWarps * 32 * kTilePerLane;  // 4096 arrivals per tile
+// look-back status word: epoch (20 bits) | flag (2 bits) | count (32 bits)
+constexpr uint64_t kStAgg = 1ull << 32, kStInc = 2ull << 32;
+constexpr int kEpochShift = 40;
+
+__global__ void __launch_bounds__(256)
+k_ing_count(const int32_t* __restrict__ model, int64_t n,
+            const int32_t* __restrict__ slot_of_model, const int32_t* __restrict__ shard_of_model,
+            int32_t M, int32_t P, unsigned long long* __restrict__ totals,
+            int32_t* __restrict__ err) {
+  extern __shared__ int32_t hcnt[];
+  const int B = P > 1 ? M + P : M;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) hcnt[b] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int32_t m = model[i];
+    if (m < 0 || m >= M) {
+      atomicMin(err, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
+      continue;
+    }
+    atomicAdd(&hcnt[slot_of_model[m]], 1);
+    if (P > 1) atomicAdd(&hcnt[M + shard_of_model[m]], 1);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    if (hcnt[b]) atomicAdd(&totals[b], (unsigned long long)hcnt[b]);
+}
+
+// bin_start = exclusive scan of the slot bins (shard bins start at 0 of
+// the shard-ordered stream: their own scan), ModelParam.off/cnt, shard_off
+__global__ void __launch_bounds__(1024)
+k_ing_offsets(const unsigned long long* __restrict__ totals, int32_t M, int32_t P, int64_t n,
+              int32_t* __restrict__ bin_start, ModelParam* __restrict__ mp,
+              int32_t* __restrict__ shard_off) {
+  __shared__ int32_t carry;
+  for (int part = 0; part < (P > 1 ? 2 : 1); part++) {
+    const int lo = part ? M : 0, len = part ? P : M;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < len; b0 += 1024) {
+      const int b = b0 + threadIdx.x;
+      const int32_t v = b < len ? (int32_t)totals[lo + b] : 0;
+      int32_t tot;
+      const int32_t ex = block_exclusive_scan(v, &tot);
+      const int32_t c = carry;
+      if (b < len) {
+        bin_start[lo + b] = c + ex;
+        if (part == 0) {
+          mp[b].off = c + ex;
+          mp[b].cnt = v;
+        } else {
+          shard_off[b] = c + ex;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) carry = c + tot;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (P > 1) shard_off[P] = (int32_t)n;
+    else { shard_off[0] = 0; shard_off[1] = (int32_t)n; }
   }
 }
 
-// Stable scatter of the stream into the (shard, model)-sorted layout, one
-// block per kChunkI-element chunk.  Each warp owns a contiguous sub-chunk,
-// counts its bins (__match_any_sync), the counts are turned into per-warp
-// offsets (warp order = stream order), and a second pass over the values
-// kept in registers ranks every element.  The chunk is staged in shared
-// memory in bin order and written out as bin runs of ~kChunkI/M elements.
-// With one shard the shard stream is the stream itself (j == i): the
-// <false> instance writes neither s_g nor sh_tick, which then alias s_i and
-// the input ticks.
-__host__ __device__ inline size_t scatter_smem(int B, bool shards) {
-  return (size_t)kChunkI * (sizeof(int64_t) + (shards ? 2 : 1) * sizeof(int32_t) + sizeof(int16_t)) +
-         sizeof(int32_t) * ((size_t)kIngestWarps * B + 2 * (size_t)B + 32);
+__host__ __device__ inline size_t ing_smem(int B, bool shards) {
+  return (size_t)kTileI * (sizeof(int64_t) + (shards ? 2 : 1) * sizeof(int32_t) + sizeof(int16_t)) +
+         sizeof(int32_t) * ((size_t)kTileWarps * B + 3 * (size_t)B + 32 + 1);
 }
 
 template <bool kShards>
-__global__ void __launch_bounds__(32 * kIngestWarps, kShards ? 4 : 6)
-k_scatter(const int64_t* __restrict__ ticks,
-          const int32_t* __restrict__ model, int64_t n,
-          const int32_t* __restrict__ slot_of_model,
-          const int32_t* __restrict__ shard_of_model,
-          int32_t M, int32_t P,
-          const int32_t* __restrict__ hist, int64_t W,
-          int64_t* __restrict__ s_tick,
-          int32_t* __restrict__ s_g,
-          int32_t* __restrict__ s_i,
-          int64_t* __restrict__ sh_tick,
-          int32_t* __restrict__ inv, int32_t* __restrict__ s_slot,
-          int32_t* __restrict__ bid) {
+__global__ void __launch_bounds__(32 * kTileWarps)
+k_ing_scatter(const int64_t* __restrict__ ticks, const int32_t* __restrict__ model, int64_t n,
+              const int32_t* __restrict__ slot_of_model,
+              const int32_t* __restrict__ shard_of_model, int32_t M, int32_t P,
+              const int32_t* __restrict__ bin_start, unsigned long long* status,
+              unsigned int* tile_ticket, uint64_t epoch,
+              int64_t* __restrict__ s_tick, int32_t* __restrict__ s_g,
+              int32_t* __restrict__ s_i, int64_t* __restrict__ sh_tick,
+              int32_t* __restrict__ inv, int32_t* __restrict__ s_slot,
+              int32_t* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int B = M + P;
+  const int B = kShards ? M + P : M;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = blockIdx.x;
   int64_t* st_t = reinterpret_cast<int64_t*>(smem_raw);
-  int32_t* st_g = reinterpret_cast<int32_t*>(st_t + kChunkI);  // kShards only
-  int32_t* st_i = kShards ? st_g + kChunkI : st_g;
-  int32_t* wcnt = st_i + kChunkI;          // [warp][bin] counts -> offsets
-  int32_t* gbase = wcnt + kIngestWarps * B;  // global base of (bin, chunk)
-  int32_t* lstart = gbase + B;             // local start of a slot bin
-  int32_t* scratch = lstart + B;           // [32] block scan of bin counts
-  // bin of each staged element; B < 2^15 (the smem check in sym_create)
-  int16_t* st_b = reinterpret_cast<int16_t*>(scratch + 32);
+  int32_t* st_g = reinterpret_cast<int32_t*>(st_t + kTileI);  // kShards only
+  int32_t* st_i = kShards ? st_g + kTileI : st_g;
+  int32_t* wcnt = st_i + kTileI;               // [warp][bin] counts -> offsets
+  int32_t* gbase = wcnt + kTileWarps * B;      // global position of the tile's bin run
+  int32_t* tcnt = gbase + B;                   // the tile's count per bin
+  int32_t* lstart = tcnt + B;                  // local start of a slot bin's run
+  int32_t* scratch = lstart + B;               // [32] block scan, [32] the ticket
+  int16_t* st_b = reinterpret_cast<int16_t*>(scratch + 33);
+  if (threadIdx.x == 0) scratch[32] = (int32_t)atomicAdd(tile_ticket, 1u);
   int32_t* mine = wcnt + wib * B;
   for (int b = lane; b < B; b += 32) mine[b] = 0;
+  __syncthreads();
+  const int64_t t = scratch[32];  // tiles in ticket order: predecessors are resident
+  const int64_t lo = t * kTileI, hi = (lo + kTileI < n ? lo + kTileI : n);
+  const int64_t wlo = lo + (int64_t)wib * 32 * kTilePerLane;
   // pass 1: load this lane's elements once, count the warp's bins
-  const int64_t lo = w * kChunkI, hi = (lo + kChunkI < n ? lo + kChunkI : n);
-  const int64_t wlo = lo + (int64_t)wib * 32 * kPerLane;
-  int64_t t[kPerLane];
-  int32_t sl[kPerLane], sd[kPerLane];
-  __syncwarp();
+  int64_t tk[kTilePerLane];
+  int32_t sl[kTilePerLane], sd[kTilePerLane];
 #pragma unroll
-  for (int r = 0; r < kPerLane; r++) {
+  for (int r = 0; r < kTilePerLane; r++) {
     const int64_t i = wlo + r * 32 + lane;
     sl[r] = -1 - lane;
     sd[r] = -2 - lane - 32;
-    t[r] = 0;
+    tk[r] = 0;
     if (i < hi) {
       const int32_t m = model[i];
-      sl[r] = slot_of_model[m];
-      sd[r] = M + shard_of_model[m];
-      t[r] = ticks[i];
+      tk[r] = ticks[i];
+      if (i > 0 && tk[r] < ticks[i - 1])  // arrivals must be time-ordered
+        atomicMin(err + 1, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
+      if (m >= 0 && m < M) {  // unknown ids were reported by pass A
+        sl[r] = slot_of_model[m];
+        if (kShards) sd[r] = M + shard_of_model[m];
+      }
     }
-    if (sl[r] >= 0) atomicAdd_block(&mine[sl[r]], 1);  // counting only
+    if (sl[r] >= 0) atomicAdd_block(&mine[sl[r]], 1);
     if (kShards) {
       const unsigned pd = __match_any_sync(0xffffffffu, sd[r]);
       if (sl[r] >= 0 && (pd >> lane) == 1u) atomicAdd_block(&mine[sd[r]], __popc(pd));
     }
-    __syncwarp();
   }
-  // bases from the scanned histogram; per-warp offsets; local bin starts
   __syncthreads();
-  const int64_t total = 2 * n;
-  const int per = (B + blockDim.x - 1) / blockDim.x;  // bins per thread
-  int32_t run = 0;
-  for (int k = 0; k < per; k++) {
-    const int b = threadIdx.x * per + k;
-    if (b >= B) break;
-    const int64_t f = (int64_t)b * W + w;
-    const int32_t g = hist[f];
-    const int64_t nx = f + 1 < (int64_t)B * W ? hist[f + 1] : total;
-    gbase[b] = b < M ? g : g - (int32_t)n;
+  // per bin: warp offsets and the tile's count, published at once (tile 0
+  // publishes its inclusive prefix) ...
+  const uint64_t ep = epoch << kEpochShift;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
     int32_t acc = 0;
-    for (int q = 0; q < kIngestWarps; q++) {
+    for (int q = 0; q < kTileWarps; q++) {
       const int32_t c = wcnt[q * B + b];
       wcnt[q * B + b] = acc;
       acc += c;
     }
-    lstart[b] = run;  // provisional: thread-local prefix
-    run += b < M ? (int32_t)(nx - g) : 0;
+    tcnt[b] = acc;
+    atomicExch(status + (size_t)t * B + b,
+               (unsigned long long)(ep | (t == 0 ? kStInc : kStAgg) | (uint32_t)acc));
   }
-  // block exclusive scan of the per-thread bin totals
+  // ... then each bin's prefix over the predecessors (decoupled look-back)
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    int64_t prefix = 0;
+    if (t > 0) {
+      for (int64_t u = t - 1; u >= 0; u--) {
+        const volatile unsigned long long* q = status + (size_t)u * B + b;
+        unsigned long long v;
+        do {
+          v = *q;
+        } while ((v >> kEpochShift) != epoch || ((v >> 32) & 3u) == 0);
+        prefix += (uint32_t)v;
+        if (((v >> 32) & 3u) == 2u) break;
+      }
+      atomicExch(status + (size_t)t * B + b,
+                 (unsigned long long)(ep | kStInc | (uint32_t)(prefix + tcnt[b])));
+    }
+    gbase[b] = bin_start[b] + (int32_t)prefix;
+  }
+  __syncthreads();
+  // local starts of the slot runs: block exclusive scan of tcnt[0..M)
   {
+    const int per = (M + blockDim.x - 1) / blockDim.x;
+    int32_t run = 0;
+    for (int k = 0; k < per; k++) {
+      const int b = threadIdx.x * per + k;
+      if (b < M) run += tcnt[b];
+    }
     int32_t x = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -417,55 +454,57 @@ k_scatter(const int64_t* __restrict__ ticks,
     if (lane == 31) scratch[wib] = x;
     __syncthreads();
     if (wib == 0) {
-      int32_t v = lane < kIngestWarps ? scratch[lane] : 0;
+      int32_t v = lane < kTileWarps ? scratch[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
         if (lane >= o) v += y;
       }
-      if (lane < kIngestWarps) scratch[lane] = v;
+      if (lane < kTileWarps) scratch[lane] = v;
     }
     __syncthreads();
-    const int32_t before = (wib ? scratch[wib - 1] : 0) + x - run;
+    int32_t before = (wib ? scratch[wib - 1] : 0) + x - run;
     for (int k = 0; k < per; k++) {
       const int b = threadIdx.x * per + k;
-      if (b >= B) break;
-      lstart[b] += before;
+      if (b < M) {
+        lstart[b] = before;
+        before += tcnt[b];
+      }
     }
   }
   __syncthreads();
   // pass 2: rank, stage in bin order, shard-stream index, inverse map
-  const unsigned lt = (1u << lane) - 1u;
+  const unsigned ltm = (1u << lane) - 1u;
 #pragma unroll
-  for (int r = 0; r < kPerLane; r++) {
+  for (int r = 0; r < kTilePerLane; r++) {
     const int64_t i = wlo + r * 32 + lane;
-    const bool act = i < hi;
+    const bool act = i < hi && sl[r] >= 0;
     const unsigned ps = __match_any_sync(0xffffffffu, sl[r]);
     unsigned pd = 0;
     if (kShards) pd = __match_any_sync(0xffffffffu, sd[r]);
     int32_t e = 0, j = 0;
     if (act) {
-      e = mine[sl[r]] + __popc(ps & lt);
-      if (kShards) j = gbase[sd[r]] + mine[sd[r]] + __popc(pd & lt);
+      e = mine[sl[r]] + __popc(ps & ltm);
+      if (kShards) j = gbase[sd[r]] + mine[sd[r]] + __popc(pd & ltm);
     }
     __syncwarp();
     if (act) {
       if ((ps >> lane) == 1u) mine[sl[r]] += __popc(ps);  // highest peer advances
       const int32_t le = lstart[sl[r]] + e;
-      st_t[le] = t[r];
+      st_t[le] = tk[r];
       st_i[le] = (int32_t)i;
       st_b[le] = (int16_t)sl[r];
       if (kShards) {
         if ((pd >> lane) == 1u) mine[sd[r]] += __popc(pd);
         st_g[le] = j;
-        sh_tick[j] = t[r];
+        sh_tick[j] = tk[r];
       }
       inv[i] = gbase[sl[r]] + e;  // coalesced in i
     }
     __syncwarp();
   }
   __syncthreads();
-  const int32_t len = (int32_t)(hi - lo);
+  const int32_t len = (int32_t)(lstart[M - 1] + tcnt[M - 1]);
   for (int32_t e = threadIdx.x; e < len; e += blockDim.x) {  // bin runs
     const int32_t b = st_b[e];
     const int32_t pos = gbase[b] + (e - lstart[b]);
@@ -473,10 +512,8 @@ k_scatter(const int64_t* __restrict__ ticks,
     if (kShards) s_g[pos] = st_g[e];
     s_i[pos] = st_i[e];
     s_slot[pos] = b;
-    bid[pos] = -1;  // "no batch" until k_bid
   }
 }
-
 
 // --------------------------------------------------------------- K2 -------
 
@@ -1859,8 +1896,6 @@ __global__ void k_step_shard_update(int64_t* __restrict__ shard_meta, int32_t P,
 // ------------------------------------------------------------ driver ------
 
 int ensure_capacity(Ctx* ctx, int64_t n) {
-  const int64_t W = (n + kChunkI - 1) / kChunkI;
-  const int B = ctx->M + ctx->P;
   if (n > ctx->cap) {
     int64_t c = n + n / 8 + 1024;
     int rc;
@@ -1869,9 +1904,7 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_s_g, c)) || (rc = grow(ctx, ctx->d_s_i, c)) ||
         (rc = grow(ctx, ctx->d_inv, c)) || (rc = grow(ctx, ctx->d_bid, c)) ||
         (rc = grow(ctx, ctx->d_scan_part,
-                   std::max<int64_t>(((c + kChunkR - 1) / kChunkR + 1) * kDigits,
-                                     ((c + kChunkI - 1) / kChunkI + 1) * (ctx->M + ctx->P)) /
-                           kScanItems + 2)) ||
+                   ((c + kChunkR - 1) / kChunkR + 1) * kDigits / kScanItems + 2)) ||
         (rc = grow(ctx, ctx->d_fresh, c)) ||
         (rc = grow(ctx, ctx->d_recs, c + ctx->P)) ||
         (rc = grow(ctx, ctx->d_drop_t, c)) || (rc = grow(ctx, ctx->d_drop_ks, c)) ||
@@ -1890,11 +1923,6 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_cp_model, c / kJump + ctx->M + 2)))
       return rc;
     ctx->cap = c;
-  }
-  if (W * B > ctx->W_cap) {
-    int rc;
-    if ((rc = grow(ctx, ctx->d_hist, W * B + 1))) return rc;
-    ctx->W_cap = W * B + 1;
   }
   return SYM_OK;
 }
@@ -2021,29 +2049,54 @@ int ingest(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_t n,
            sym_result* out) {
   cudaStream_t st = ctx->stream;
   const int32_t M = ctx->M, P = ctx->P;
-  const int B = M + P;
-  const int64_t W = (n + kChunkI - 1) / kChunkI;
+  const int B = P > 1 ? M + P : M;
+  const int64_t tiles = (n + kTileI - 1) / kTileI;
+  if (tiles * B > ctx->ing_status_cap) {  // look-back words, zeroed once
+    const int64_t c = tiles * B + tiles * B / 4 + 1024;
+    int rc;
+    if ((rc = grow(ctx, ctx->d_ing_status, c))) return rc;
+    CK(cudaMemsetAsync(ctx->d_ing_status, 0, sizeof(unsigned long long) * c, st));
+    ctx->ing_status_cap = c;
+  }
+  if (++ctx->ing_epoch >= (uint64_t(1) << (64 - kEpochShift))) {  // epoch wrap
+    ctx->ing_epoch = 1;
+    CK(cudaMemsetAsync(ctx->d_ing_status, 0,
+                       sizeof(unsigned long long) * ctx->ing_status_cap, st));
+  }
   const int32_t big[2] = {INT32_MAX, INT32_MAX};
   CK(cudaMemcpyAsync(ctx->d_err, big, sizeof big, cudaMemcpyHostToDevice, st));
-  const size_t smem = sizeof(int32_t) * (size_t)B;
-  if (W > 0) {
-    KL(k_hist, W, 32 * kIngestWarps, smem, st>>>(
-        d_model, d_ticks, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
-        ctx->d_hist, W, ctx->d_err));
-    flat_scan(ctx, ctx->d_hist, W * B, kt, launches);
-  }
-  KL(k_binoff, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, M, P, n, mp_out,
-                                           ctx->d_bins + B + 1));
+  CK(cudaMemsetAsync(ctx->d_ing_tot, 0, sizeof(unsigned long long) * B, st));
+  CK(cudaMemsetAsync(ctx->d_ing_ticket, 0, sizeof(unsigned int), st));
+  int32_t* shard_off = ctx->d_bins + (M + P) + 1;
+  if (n > 0)
+    KL(k_ing_count, (unsigned)std::min<int64_t>(148 * 8, nblk(n, 256)), 256,
+       sizeof(int32_t) * B, st>>>(d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M,
+                                  P, ctx->d_ing_tot, ctx->d_err));
+  KL(k_ing_offsets, 1, 1024, 0, st>>>(ctx->d_ing_tot, M, P, n, ctx->d_ing_start, mp_out,
+                                       shard_off));
+  if (tiles > 0 && P > 1)
+    KL(k_ing_scatter<true>, tiles, 32 * kTileWarps, ing_smem(B, true), st>>>(
+        d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
+        ctx->d_ing_start, ctx->d_ing_status, ctx->d_ing_ticket, ctx->ing_epoch,
+        ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i, ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot,
+        ctx->d_err));
+  else if (tiles > 0)
+    KL(k_ing_scatter<false>, tiles, 32 * kTileWarps, ing_smem(B, false), st>>>(
+        d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
+        ctx->d_ing_start, ctx->d_ing_status, ctx->d_ing_ticket, ctx->ing_epoch,
+        ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i, ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot,
+        ctx->d_err));
+  CK(cudaGetLastError());
   int32_t herr2[2] = {INT32_MAX, INT32_MAX};
   info.last_tick = 0;
   info.shard_off.assign(P + 1, 0);
   CK(cudaMemcpyAsync(herr2, ctx->d_err, sizeof herr2, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(info.shard_off.data(), ctx->d_bins + B + 1, sizeof(int32_t) * (P + 1),
+  CK(cudaMemcpyAsync(info.shard_off.data(), shard_off, sizeof(int32_t) * (P + 1),
                      cudaMemcpyDeviceToHost, st));
   if (n > 0)
     CK(cudaMemcpyAsync(&info.last_tick, d_ticks + (n - 1), sizeof info.last_tick,
                        cudaMemcpyDeviceToHost, st));
-  // per-model arrival counts (k_binoff) ride on the same readback
+  // per-model arrival counts ride on the same readback
   info.mp.resize(M);
   CK(cudaMemcpyAsync(info.mp.data(), mp_out, sizeof(ModelParam) * M,
                      cudaMemcpyDeviceToHost, st));
@@ -2058,17 +2111,6 @@ int ingest(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_t n,
     ctx->err = "arrival ticks must be non-decreasing";
     return SYM_EINVAL;
   }
-  if (W > 0 && P > 1)
-    KL(k_scatter<true>, W, 32 * kIngestWarps, scatter_smem(B, true), st>>>(
-        d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
-        ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
-        ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot, ctx->d_bid));
-  else if (W > 0)
-    KL(k_scatter<false>, W, 32 * kIngestWarps, scatter_smem(B, false), st>>>(
-        d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
-        ctx->d_hist, W, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i,
-        ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot, ctx->d_bid));
-  CK(cudaGetLastError());
   return SYM_OK;
 }
 
@@ -2641,6 +2683,7 @@ int32_t sym_chain_prof(unsigned long long* out) {
 #endif
 
 const char* sym_kernel_times(void* engine, int32_t reset) {
+  if (sym_is_multi(engine)) return "{}";
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx) return "{}";
   std::string j = "{";
@@ -2659,6 +2702,7 @@ const char* sym_kernel_times(void* engine, int32_t reset) {
 }
 
 const char* sym_last_error(void* engine) {
+  if (sym_is_multi(engine)) return sym_multi_last_error(engine);
   return engine ? static_cast<Ctx*>(engine)->err.c_str() : "null engine";
 }
 
@@ -2674,6 +2718,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     return nullptr;
   if (cfg->gather == SYM_GATHER_DROP_HEAD && cfg->target_batch < 1)
     return nullptr;
+  if (cfg->n_devices > 1 && cfg->devices) return sym_multi_create(cfg, status);
   Ctx* ctx = new Ctx();
   ctx->M = cfg->n_models;
   ctx->G = cfg->n_gpus;
@@ -2800,6 +2845,9 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   // bins: [B+1] totals, then shard_off [P+1], model_of_slot [M], gpu_base [P+1]
   ALLOC(ctx->d_bins, (M + P + 1) + (P + 1) + M + (P + 1));
   ALLOC(ctx->d_err, 2);
+  ALLOC(ctx->d_ing_tot, M + P);
+  ALLOC(ctx->d_ing_start, M + P);
+  ALLOC(ctx->d_ing_ticket, 1);
   ALLOC(ctx->d_nb, M);
   ALLOC(ctx->d_bbase, M);
   ALLOC(ctx->d_mdrops, M);
@@ -2882,12 +2930,15 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     if ((e = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ctx->chain_smem)) != cudaSuccess)
       return fail("smem attribute", e);
-    const size_t sc = scatter_smem(ctx->M + ctx->P, true);  // >= the <false> size
-    if (sc > (size_t)dev_max || ctx->M + ctx->P >= 32768) return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
-    if ((e = cudaFuncSetAttribute(k_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sc)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sc)) != cudaSuccess)
+    const size_t sc = ing_smem(ctx->M + ctx->P, true);  // >= the <false> size
+    if (sc > (size_t)dev_max || ctx->M + ctx->P >= 32768)
+      return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
+    if ((e = cudaFuncSetAttribute(k_ing_scatter<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc)) !=
+            cudaSuccess ||
+        (e = cudaFuncSetAttribute(k_ing_scatter<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc)) !=
+            cudaSuccess)
       return fail("scatter smem attribute", e);
   }
   if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return fail("init", e);
@@ -2896,6 +2947,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
 }
 
 void sym_destroy(void* engine) {
+  if (sym_is_multi(engine)) return sym_multi_destroy(engine);
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx) return;
   cudaSetDevice(ctx->device);
@@ -2906,7 +2958,8 @@ void sym_destroy(void* engine) {
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,
                   ctx->d_inv, ctx->d_bid, ctx->d_scan_part, ctx->d_closek,
-                  ctx->d_hist, ctx->d_bins,   ctx->d_err,   ctx->d_fresh,
+                  ctx->d_bins,   ctx->d_err,   ctx->d_fresh,  ctx->d_ing_tot,
+                  ctx->d_ing_start, ctx->d_ing_ticket, ctx->d_ing_status,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
                   ctx->d_bvA, ctx->d_bvB, ctx->d_tvA, ctx->d_tvB, ctx->d_ptrA,
@@ -2934,6 +2987,7 @@ void sym_destroy(void* engine) {
 int32_t sym_run_device(void* engine, const int64_t* d_arr_ticks,
                        const void* d_arr_model, int64_t n, uint32_t flags,
                        sym_result* out) {
+  if (sym_is_multi(engine)) return SYM_EINVAL;  // device pointers live on one device
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return SYM_ECUDA;
@@ -2954,6 +3008,11 @@ int32_t sym_run_device(void* engine, const int64_t* d_arr_ticks,
 
 int32_t sym_run(void* engine, const int64_t* arr_ticks, const void* arr_model,
                 int64_t n, uint32_t flags, sym_result* out) {
+  if (sym_is_multi(engine)) {
+    if (!out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
+    out->err_index = -1;
+    return sym_multi_run(engine, arr_ticks, arr_model, n, flags, out);
+  }
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !out || n < 0 || n >= INT32_MAX) return SYM_EINVAL;
   CK(cudaSetDevice(ctx->device));
@@ -3053,6 +3112,7 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const void* arr_model,
 }
 
 int32_t sym_step_reset(void* engine) {
+  if (sym_is_multi(engine)) return SYM_EINVAL;
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx) return SYM_EINVAL;
   if (ctx->jitter) {
@@ -3065,6 +3125,7 @@ int32_t sym_step_reset(void* engine) {
 
 int32_t sym_step(void* engine, const int64_t* arr_ticks, const void* arr_model, int64_t n,
                  int64_t until_tick, uint32_t flags, sym_result* out) {
+  if (sym_is_multi(engine)) return SYM_EINVAL;
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !out || n < 0 || (n > 0 && (!arr_ticks || !arr_model))) return SYM_EINVAL;
   out->err_index = -1;
@@ -3107,6 +3168,7 @@ int32_t sym_step(void* engine, const int64_t* arr_ticks, const void* arr_model, 
 }
 
 int32_t sym_step_result(void* engine, sym_result* out) {
+  if (sym_is_multi(engine)) return SYM_EINVAL;
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !out) return SYM_EINVAL;
   if (ctx->step_first && !ctx->step_active) {
@@ -3178,6 +3240,7 @@ int32_t sym_step_result(void* engine, sym_result* out) {
 }
 
 int64_t sym_last_batches(void* engine, sym_batch* host, int64_t cap) {
+  if (sym_is_multi(engine)) return sym_multi_last_batches(engine, host, cap);
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || !ctx->has_run) return -SYM_EINVAL;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return -SYM_ECUDA;
@@ -3211,6 +3274,10 @@ int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,
                           int64_t* model_arrivals, int64_t* model_completed,
                           int64_t* model_late, int64_t* model_dropped,
                           int64_t* gpu_busy_ns) {
+  if (sym_is_multi(engine))
+    return sym_multi_window_stats(engine, lo_ns, hi_ns, model_arrivals, model_completed,
+                                  model_late, model_dropped, gpu_busy_ns, nullptr, nullptr,
+                                  nullptr, 0);
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx) return SYM_EINVAL;
   if (!ctx->has_run || !ctx->last_outcome) {
@@ -3259,6 +3326,12 @@ int32_t sym_window_stats(void* engine, int64_t lo_ns, int64_t hi_ns, int64_t* mo
                          int64_t* model_completed, int64_t* model_late, int64_t* model_dropped,
                          int64_t* gpu_busy_ns, int64_t* model_p99_ns, int64_t* model_max_qd_ns,
                          int64_t* model_batch_hist, int32_t hist_stride) {
+  if (sym_is_multi(engine))
+    return hist_stride < 1 ? SYM_EINVAL
+                           : sym_multi_window_stats(engine, lo_ns, hi_ns, model_arrivals,
+                                                    model_completed, model_late, model_dropped,
+                                                    gpu_busy_ns, model_p99_ns, model_max_qd_ns,
+                                                    model_batch_hist, hist_stride);
   Ctx* ctx = static_cast<Ctx*>(engine);
   if (!ctx || hist_stride < 1) return SYM_EINVAL;
   if (!ctx->has_run || !ctx->last_outcome || !ctx->last_start || !ctx->last_finish) {

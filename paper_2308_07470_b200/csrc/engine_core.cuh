@@ -309,8 +309,14 @@ SYM_HD void pq_update(Shard& S, int32_t mid) {
 
 // ------------------------------------------------------- ModelPlane -------
 
+// l(b) for 1 <= b <= max_batch.  An exactly affine row (every linear
+// profile, detected in sym_create) is computed from two on-chip scalars
+// instead of a load from the row, which for a large model set lives in
+// global memory: the single chain thread would otherwise pay an L2 round
+// trip per probe.
 SYM_HD int64_t lat_of(const Shard& S, int32_t m, int32_t b) {
-  return S.lat[(int64_t)m * S.lat_stride + (b - 1)];
+  const ModelParam& P = S.mp[m];
+  return P.affine ? P.aff_a * b + P.aff_b : S.lat[(int64_t)m * S.lat_stride + (b - 1)];
 }
 SYM_HD int64_t deadline_at(const Shard& S, const ModelParam& P, int32_t q) {
   return S.s_tick[P.off + q] + P.slo;
@@ -351,9 +357,12 @@ SYM_HD int32_t max_feasible(const Shard& S, int32_t m, int64_t now,
                             int64_t floor, int32_t cap, int64_t d,
                             int32_t hint = 0) {
   const int64_t* lat = S.lat + (int64_t)m * S.lat_stride;
+  const ModelParam& P = S.mp[m];
+  const bool aff = P.affine != 0;
+  const int64_t la = P.aff_a, lb0 = P.aff_b;
   const int64_t dc = S.d_ctrl, dd = S.d_data;
   auto ok = [&](int32_t b) {
-    return imax(now + dc + dd * b, floor) + lat[b - 1] <= d;
+    return imax(now + dc + dd * b, floor) + (aff ? la * b + lb0 : lat[b - 1]) <= d;
   };
   int32_t lo, hi;  // invariant: ok(lo) (or lo == 0), !ok(hi + 1) (or hi == cap)
   if (hint < 1 || hint > cap) hint = 1;

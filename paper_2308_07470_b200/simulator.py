@@ -160,7 +160,7 @@ class Engine:
                  policy: PolicyConfig, network: NetworkModel | None = None,
                  seed: int = 0, record_trace: bool = False,
                  check_invariants: bool = False, *, shards=None, device: int = 0,
-                 use_fresh: bool = True, use_fast: bool = True):
+                 devices=None, use_fresh: bool = True, use_fast: bool = True):
         if gpu_count < 1:
             raise ValueError("need at least one GPU")
         self.models = list(models)
@@ -174,6 +174,9 @@ class Engine:
         self.check_invariants = check_invariants
         self.gpu_count = gpu_count
         self.device = device
+        # several devices in one call: sub-cluster s on devices[s % len]
+        self.devices = None if devices is None or len(devices) < 2 else \
+            np.ascontiguousarray(devices, np.int32)
         self.use_fresh = use_fresh
         self.use_fast = use_fast
         self.shard_of_model, self.gpus_per_shard = _split_shards(self.models, gpu_count, shards)
@@ -218,6 +221,9 @@ class Engine:
         cfg.device = self.device
         cfg.shard_of_model = self.shard_of_model.ctypes.data_as(_native.i32p)
         cfg.gpus_per_shard = self.gpus_per_shard.ctypes.data_as(_native.i32p)
+        if self.devices is not None:
+            cfg.devices = self.devices.ctypes.data_as(_native.i32p)
+            cfg.n_devices = len(self.devices)
         j = self._jitter
         if j is not None:
             self._jit_keep = [np.ascontiguousarray(a) for a in (j.ctrl_vals, j.ctrl_cdf,

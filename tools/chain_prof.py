@@ -13,7 +13,8 @@ import __graft_entry__ as g  # noqa: E402
 LIB = os.path.join(ROOT, "gpurun_out", "libsym_chainprof.so")
 if not os.path.exists(LIB) or "--build" in sys.argv:
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    srcs = [os.path.join(g.CSRC, f) for f in ("engine.cu", "textfmt.cu", "partition.cu")]
+    srcs = [os.path.join(g.CSRC, f) for f in ("engine.cu", "multi.cu", "textfmt.cu",
+                                                 "partition.cu")]
     subprocess.run([g._nvcc(), *g.NVCC_FLAGS, "-DSYM_CHAIN_PROF", "-o", LIB, *srcs], check=True)
 if "--build" in sys.argv:
     sys.exit(0)
@@ -54,3 +55,15 @@ t, m = generate_arrivals(c1.workload, [x.name for x in c1.models], 60.0, 42)
 eng = Engine(list(c1.models), c1.gpu_count, PolicyConfig("eager"))
 eng.run_stream(t, m, 60.0)
 report("C1 eager")
+
+for name in ("C3", "C4"):
+    sc = configs.CONFIGS[name](1.0, "eager")
+    t, m = generate_arrivals(sc.workload, [x.name for x in sc.models], 1.0, 42)
+    models, gpus = list(sc.models), sc.gpu_count
+    if name == "C4":
+        ms, g, ids = configs.shard_scenarios(sc)[0]
+        keep = (m >= ids[0]) & (m <= ids[-1])
+        t, m, models, gpus = t[keep], m[keep] - ids[0], list(ms), g
+    eng = Engine(models, gpus, sc.policy)
+    eng.run_stream(t, m, 1.0)
+    report(f"{name} eager 1 s ({len(t)} requests, {eng.stats['ms_chain']:.0f} ms chain)")
