@@ -52,8 +52,8 @@ EV_BATCH_BYTES = 56    # sizeof(EvBatch)
 #   K3 matchmaking  8 B per GPU free_at + 24 B per ready candidate + 12 B
 #                   written per grant
 SURVEY_KERNELS = {
-    "K1": ("k_scatter", lambda n, nb, g: 24 * n),
-    "K2": ("k_nxt_pp", lambda n, nb, g: 12 * n),
+    "K1": ("k_part", lambda n, nb, g: 24 * n),     # per partition pass (2 with P > 1)
+    "K2": ("k_nxt", lambda n, nb, g: 12 * n),
     "K3": ("k_match_coop", lambda n, nb, g: 36 * nb + 8 * g),
 }
 
@@ -62,7 +62,7 @@ def design_bytes(kernel: str, n: int, nb: int, shards: int) -> float | None:
     """Minimal DRAM bytes one launch of a kernel outside §8(d)'s three must
     move (DESIGN.md §5 derives each line)."""
     table = {
-        "k_hist": n * 4,
+        "k_part_count": n * 4,
         "k_fresh": n * (8 + 4 + 4 + FRESH_REC_BYTES + 4),
         "k_nxt_general": 0,
         "k_chain_recs": n * (8 + 4 + 4) + nb * (4 + EV_BATCH_BYTES + 8 + 4),
@@ -95,7 +95,8 @@ def dist_env():
 
 
 def my_subclusters(rank: int, world: int) -> list[int]:
-    return [s for s in range(N_SUBCLUSTERS) if s % world == rank]
+    from paper_2308_07470_b200.parallel import assign
+    return assign(N_SUBCLUSTERS, world)[rank]
 
 
 def build_workload(duration_s: float, subclusters: list[int]):

@@ -46,7 +46,13 @@ enum {
   SYM_FLAG_NO_EXPAND = 4u,  /* leave per-request arrays untouched (bench) */
   SYM_FLAG_NO_FAST = 8u,    /* always run the sequential live-event chain */
   SYM_FLAG_KERNEL_TIMES = 16u, /* CUDA-event time every kernel (profiling) */
-  SYM_FLAG_MODEL_I64 = 32u    /* arr_model holds int64 ids (numpy default) */
+  SYM_FLAG_MODEL_I64 = 32u,   /* arr_model holds int64 ids (numpy default) */
+  SYM_FLAG_CHECK_INVARIANTS = 64u, /* check_invariants=True: the exact chain
+                                 verifies the reference's invariants
+                                 (simulator.py:276-305) after every event;
+                                 a violation returns SYM_EINVARIANT */
+  SYM_FLAG_INJECT_FAULT = 128u /* test hook (with CHECK_INVARIANTS): corrupt
+                                 the state at the 10th chain event */
 };
 
 /* Engine configuration.  Models are numbered 0..n_models-1 in the order of

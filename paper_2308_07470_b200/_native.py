@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(HERE, LIB_NAME)
 SYM_OK, SYM_EPROTO, SYM_EINVAL, SYM_EINVARIANT, SYM_ECUDA, SYM_ENOMEM = range(6)
 FLAG_TRACE, FLAG_NO_FRESH, FLAG_NO_EXPAND, FLAG_NO_FAST, FLAG_KERNEL_TIMES = 1, 2, 4, 8, 16
 FLAG_MODEL_I64 = 32
+FLAG_CHECK_INVARIANTS, FLAG_INJECT_FAULT = 64, 128
 KIND = {"deferred": 0, "eager": 1, "timeout": 2}
 GATHER = {"prefix": 0, "drop_head": 1}
 

@@ -83,12 +83,10 @@ struct Ctx {
   int32_t *d_inv = nullptr, *d_bid = nullptr;  // stream -> sorted position, position -> record
   int32_t *d_model = nullptr, *d_s_g = nullptr, *d_s_i = nullptr;
   int32_t* d_bins = nullptr;        // [B+1] (unused) | shard_off | model_of_slot | gpu_base
-  unsigned long long* d_ing_tot = nullptr;  // [B] per-bin totals (ingest pass A)
-  int32_t* d_ing_start = nullptr;   // [B] first sorted position of each bin
-  unsigned int* d_ing_ticket = nullptr;
-  unsigned long long* d_ing_status = nullptr;  // [tiles][B] look-back words
-  int64_t ing_status_cap = 0;
-  uint64_t ing_epoch = 0;
+  int32_t *d_sh_i = nullptr, *d_sh_slot = nullptr, *d_inv1 = nullptr;  // P > 1: level 1
+  int32_t* d_hist = nullptr;        // [B][tiles] bin counts -> positions
+  int32_t* d_hist_part = nullptr;   // block sums of its scan
+  int64_t hist_cap = 0;
   int32_t* d_err = nullptr;
   FreshRec* d_fresh = nullptr;
   BatchRec* d_recs = nullptr;
@@ -108,13 +106,13 @@ struct Ctx {
   int32_t* d_dka = nullptr;
   sym_batch* d_bat = nullptr;
   int64_t stage_cap = 0, bat_cap = 0;
-  int32_t* d_closek = nullptr;      // closing arrival of lean-certified starts
+  int32_t* d_closek = nullptr;      // closing arrival of each batch start (-1: general)
+  int32_t* d_special = nullptr;     // [M] models left to the sequential evolution
   int32_t *d_jC = nullptr;          // J_64 kept while J_256 is built
-  int32_t *d_s_slot = nullptr;      // [n] model slot of each sorted position
   int32_t *d_unsure = nullptr;      // [n] positions the lean pointer could not certify
   int32_t *d_unsure_n = nullptr;    // [1] their count
   int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
-          *d_cp_model = nullptr, *d_special = nullptr;
+          *d_cp_model = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
   int32_t* d_drop_ka = nullptr;
   // last run (for sym_window_counts)
@@ -261,189 +259,140 @@ k_scan_down(int32_t* __restrict__ a, int64_t len, const int32_t* __restrict__ pa
   }
 }
 
-// ---- K1, one sweep: stable partition with decoupled look-back ----------
-// Pass A (k_ing_count): per-bin totals of the whole stream (persistent
-// blocks, one shared histogram each, one global atomic per bin per block)
-// and the model-id check.  k_ing_offsets: exclusive scan of the totals ->
-// each bin's first sorted position (ModelParam.off/cnt, shard offsets).
-// Pass B (k_ing_scatter): tiles of kTileI arrivals taken in ticket order;
-// a tile counts its bins, publishes the counts, looks back over its
-// predecessors' published counts for each bin's running prefix (decoupled
-// look-back: a predecessor publishes its own count first and its inclusive
-// prefix as soon as it knows it), ranks every element stably (per-warp
-// offsets + __match_any_sync), stages the tile in shared memory in bin order
-// and writes bin runs.  The stream is read once (plus 4 B/request in pass
-// A) and every output is written once; no histogram of the size of the data
-// is materialised or scanned.
+// ---- K1: stable partition of the stream into the (shard, model) layout ---
+// One building block, a stable partition of a time-ordered stream into few
+// bins by reduce-then-scan over tiles of kTileI arrivals:
+//   k_part_count  one block per tile counts its bins (shared atomics) and
+//                 checks the model ids -> hist[bin][tile]
+//   flat_scan     one exclusive scan of the bin-major histogram: every
+//                 (bin, tile)'s first output position
+//   k_part        one block per tile: stable ranks within the tile
+//                 (per-warp bin counts + __match_any_sync), the tile staged in
+//                 shared memory in bin order, bin runs written out
+// One sub-cluster (P = 1): one partition by model id.  Several (P > 1): by
+// sub-cluster first (P bins: the sub-cluster streams, whose ticks the chain
+// reads for A'), then each sub-cluster stream by model slot -- two
+// partitions with few bins each run far faster than one over M + P bins,
+// whose per-tile bin bookkeeping and shared memory (1016 bins for C4 on one
+// B200) starve the SMs.
+//   mode 0 (P = 1):  bin = model          out: s_tick, s_i = i, inv[i] = p
+//   mode 1 (level 1): bin = shard(model)  out: sh_tick, sh_i = i, sh_slot,
+//                                              inv1[i] = j
+//   mode 2 (level 2): bin = sh_slot       out: s_tick, s_g = j, s_i = sh_i[j],
+//                                              inv[j] = p
 constexpr int kTileWarps = 8;
-constexpr int kTilePerLane = 16;
-constexpr int kTileI = kTileWarps * 32 * kTilePerLane;  // 4096 arrivals per tile
-// look-back status word: epoch (20 bits) | flag (2 bits) | count (32 bits)
-constexpr uint64_t kStAgg = 1ull << 32, kStInc = 2ull << 32;
-constexpr int kEpochShift = 40;
+constexpr int kTilePerLane = 8;
+constexpr int kTileI = kTileWarps * 32 * kTilePerLane;  // 2048 arrivals per tile
 
+template <int kMode>
 __global__ void __launch_bounds__(256)
-k_ing_count(const int32_t* __restrict__ model, int64_t n,
-            const int32_t* __restrict__ slot_of_model, const int32_t* __restrict__ shard_of_model,
-            int32_t M, int32_t P, unsigned long long* __restrict__ totals,
-            int32_t* __restrict__ err) {
+k_part_count(const int32_t* __restrict__ key, int64_t n, int32_t M,
+             const int32_t* __restrict__ shard_of_model, int32_t B,
+             int32_t* __restrict__ hist, int64_t W, int32_t* __restrict__ err) {
   extern __shared__ int32_t hcnt[];
-  const int B = P > 1 ? M + P : M;
   for (int b = threadIdx.x; b < B; b += blockDim.x) hcnt[b] = 0;
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int32_t m = model[i];
-    if (m < 0 || m >= M) {
+  const int64_t w = blockIdx.x;
+  const int64_t lo = w * kTileI, hi = lo + kTileI < n ? lo + kTileI : n;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int32_t m = key[i];
+    if (kMode != 2 && (m < 0 || m >= M)) {
       atomicMin(err, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
       continue;
     }
-    atomicAdd(&hcnt[slot_of_model[m]], 1);
-    if (P > 1) atomicAdd(&hcnt[M + shard_of_model[m]], 1);
+    atomicAdd(&hcnt[kMode == 1 ? shard_of_model[m] : m], 1);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < B; b += blockDim.x)
-    if (hcnt[b]) atomicAdd(&totals[b], (unsigned long long)hcnt[b]);
+  for (int b = threadIdx.x; b < B; b += blockDim.x) hist[(int64_t)b * W + w] = hcnt[b];
 }
 
-// bin_start = exclusive scan of the slot bins (shard bins start at 0 of
-// the shard-ordered stream: their own scan), ModelParam.off/cnt, shard_off
-__global__ void __launch_bounds__(1024)
-k_ing_offsets(const unsigned long long* __restrict__ totals, int32_t M, int32_t P, int64_t n,
-              int32_t* __restrict__ bin_start, ModelParam* __restrict__ mp,
-              int32_t* __restrict__ shard_off) {
-  __shared__ int32_t carry;
-  for (int part = 0; part < (P > 1 ? 2 : 1); part++) {
-    const int lo = part ? M : 0, len = part ? P : M;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int b0 = 0; b0 < len; b0 += 1024) {
-      const int b = b0 + threadIdx.x;
-      const int32_t v = b < len ? (int32_t)totals[lo + b] : 0;
-      int32_t tot;
-      const int32_t ex = block_exclusive_scan(v, &tot);
-      const int32_t c = carry;
-      if (b < len) {
-        bin_start[lo + b] = c + ex;
-        if (part == 0) {
-          mp[b].off = c + ex;
-          mp[b].cnt = v;
-        } else {
-          shard_off[b] = c + ex;
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) carry = c + tot;
-      __syncthreads();
-    }
-  }
-  if (threadIdx.x == 0) {
-    if (P > 1) shard_off[P] = (int32_t)n;
-    else { shard_off[0] = 0; shard_off[1] = (int32_t)n; }
+// ModelParam.off/cnt per slot (slots == 1: shard_off instead) from the
+// first column of the scanned bin-major histogram
+__global__ void k_part_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t B, int64_t n,
+                              ModelParam* __restrict__ mp, int32_t* __restrict__ shard_off) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int32_t o = W > 0 ? hist[(int64_t)b * W] : 0;
+  const int32_t e = b + 1 < B ? (W > 0 ? hist[(int64_t)(b + 1) * W] : 0) : (int32_t)n;
+  if (mp) {
+    mp[b].off = o;
+    mp[b].cnt = e - o;
+  } else {
+    shard_off[b] = o;
+    if (b == B - 1) shard_off[B] = (int32_t)n;
   }
 }
 
-__host__ __device__ inline size_t ing_smem(int B, bool shards) {
-  return (size_t)kTileI * (sizeof(int64_t) + (shards ? 2 : 1) * sizeof(int32_t) + sizeof(int16_t)) +
-         sizeof(int32_t) * ((size_t)kTileWarps * B + 3 * (size_t)B + 32 + 1);
+__host__ __device__ inline size_t part_smem(int B) {
+  return (size_t)kTileI * (sizeof(int64_t) + 2 * sizeof(int32_t) + sizeof(int16_t)) +
+         sizeof(int32_t) * ((size_t)kTileWarps * B + 2 * (size_t)B + 32);
 }
 
-template <bool kShards>
-__global__ void __launch_bounds__(32 * kTileWarps)
-k_ing_scatter(const int64_t* __restrict__ ticks, const int32_t* __restrict__ model, int64_t n,
-              const int32_t* __restrict__ slot_of_model,
-              const int32_t* __restrict__ shard_of_model, int32_t M, int32_t P,
-              const int32_t* __restrict__ bin_start, unsigned long long* status,
-              unsigned int* tile_ticket, uint64_t epoch,
-              int64_t* __restrict__ s_tick, int32_t* __restrict__ s_g,
-              int32_t* __restrict__ s_i, int64_t* __restrict__ sh_tick,
-              int32_t* __restrict__ inv, int32_t* __restrict__ s_slot,
-              int32_t* __restrict__ err) {
+template <int kMode>
+__global__ void __launch_bounds__(32 * kTileWarps, 5)
+k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
+       const int32_t* __restrict__ aux_in, int64_t n, int32_t M,
+       const int32_t* __restrict__ shard_of_model, const int32_t* __restrict__ slot_of_model,
+       int32_t B, const int32_t* __restrict__ hist, int64_t W,
+       int64_t* __restrict__ out_tick, int32_t* __restrict__ out_idx,
+       int32_t* __restrict__ out_aux, int32_t* __restrict__ inv_out,
+       int32_t* __restrict__ err) {
+  constexpr bool kAux = kMode != 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int B = kShards ? M + P : M;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t* st_t = reinterpret_cast<int64_t*>(smem_raw);
-  int32_t* st_g = reinterpret_cast<int32_t*>(st_t + kTileI);  // kShards only
-  int32_t* st_i = kShards ? st_g + kTileI : st_g;
-  int32_t* wcnt = st_i + kTileI;               // [warp][bin] counts -> offsets
+  int32_t* st_i = reinterpret_cast<int32_t*>(st_t + kTileI);
+  int32_t* st_a = st_i + kTileI;               // kAux only
+  int32_t* wcnt = st_a + kTileI;               // [warp][bin] counts -> offsets
   int32_t* gbase = wcnt + kTileWarps * B;      // global position of the tile's bin run
-  int32_t* tcnt = gbase + B;                   // the tile's count per bin
-  int32_t* lstart = tcnt + B;                  // local start of a slot bin's run
-  int32_t* scratch = lstart + B;               // [32] block scan, [32] the ticket
-  int16_t* st_b = reinterpret_cast<int16_t*>(scratch + 33);
-  if (threadIdx.x == 0) scratch[32] = (int32_t)atomicAdd(tile_ticket, 1u);
+  int32_t* lstart = gbase + B;                 // local start of a bin's run
+  int32_t* scratch = lstart + B;               // [32] block scan
+  int16_t* st_b = reinterpret_cast<int16_t*>(scratch + 32);
   int32_t* mine = wcnt + wib * B;
+  const int64_t w = blockIdx.x;
   for (int b = lane; b < B; b += 32) mine[b] = 0;
-  __syncthreads();
-  const int64_t t = scratch[32];  // tiles in ticket order: predecessors are resident
-  const int64_t lo = t * kTileI, hi = (lo + kTileI < n ? lo + kTileI : n);
+  for (int b = threadIdx.x; b < B; b += blockDim.x) gbase[b] = hist[(int64_t)b * W + w];
+  const int64_t lo = w * kTileI, hi = (lo + kTileI < n ? lo + kTileI : n);
   const int64_t wlo = lo + (int64_t)wib * 32 * kTilePerLane;
+  __syncwarp();
   // pass 1: load this lane's elements once, count the warp's bins
   int64_t tk[kTilePerLane];
-  int32_t sl[kTilePerLane], sd[kTilePerLane];
+  int32_t bn[kTilePerLane], ax[kTilePerLane];
 #pragma unroll
   for (int r = 0; r < kTilePerLane; r++) {
     const int64_t i = wlo + r * 32 + lane;
-    sl[r] = -1 - lane;
-    sd[r] = -2 - lane - 32;
+    bn[r] = -1 - lane;
     tk[r] = 0;
+    ax[r] = 0;
     if (i < hi) {
-      const int32_t m = model[i];
-      tk[r] = ticks[i];
-      if (i > 0 && tk[r] < ticks[i - 1])  // arrivals must be time-ordered
+      const int32_t m = key[i];
+      tk[r] = tick_in[i];
+      if (kMode != 2 && i > 0 && tk[r] < tick_in[i - 1])  // arrivals must be time-ordered
         atomicMin(err + 1, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
-      if (m >= 0 && m < M) {  // unknown ids were reported by pass A
-        sl[r] = slot_of_model[m];
-        if (kShards) sd[r] = M + shard_of_model[m];
+      if (kMode == 2 || (m >= 0 && m < M)) {  // unknown ids were reported by k_part_count
+        bn[r] = kMode == 1 ? shard_of_model[m] : m;
+        if (kMode == 1) ax[r] = slot_of_model[m];
+        if (kMode == 2) ax[r] = aux_in[i];
       }
     }
-    if (sl[r] >= 0) atomicAdd_block(&mine[sl[r]], 1);
-    if (kShards) {
-      const unsigned pd = __match_any_sync(0xffffffffu, sd[r]);
-      if (sl[r] >= 0 && (pd >> lane) == 1u) atomicAdd_block(&mine[sd[r]], __popc(pd));
-    }
+    if (bn[r] >= 0) atomicAdd_block(&mine[bn[r]], 1);
   }
   __syncthreads();
-  // per bin: warp offsets and the tile's count, published at once (tile 0
-  // publishes its inclusive prefix) ...
-  const uint64_t ep = epoch << kEpochShift;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    int32_t acc = 0;
-    for (int q = 0; q < kTileWarps; q++) {
-      const int32_t c = wcnt[q * B + b];
-      wcnt[q * B + b] = acc;
-      acc += c;
-    }
-    tcnt[b] = acc;
-    atomicExch(status + (size_t)t * B + b,
-               (unsigned long long)(ep | (t == 0 ? kStInc : kStAgg) | (uint32_t)acc));
-  }
-  // ... then each bin's prefix over the predecessors (decoupled look-back)
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    int64_t prefix = 0;
-    if (t > 0) {
-      for (int64_t u = t - 1; u >= 0; u--) {
-        const volatile unsigned long long* q = status + (size_t)u * B + b;
-        unsigned long long v;
-        do {
-          v = *q;
-        } while ((v >> kEpochShift) != epoch || ((v >> 32) & 3u) == 0);
-        prefix += (uint32_t)v;
-        if (((v >> 32) & 3u) == 2u) break;
-      }
-      atomicExch(status + (size_t)t * B + b,
-                 (unsigned long long)(ep | kStInc | (uint32_t)(prefix + tcnt[b])));
-    }
-    gbase[b] = bin_start[b] + (int32_t)prefix;
-  }
-  __syncthreads();
-  // local starts of the slot runs: block exclusive scan of tcnt[0..M)
+  // per bin: warp offsets and the tile's count; local starts by a block scan
   {
-    const int per = (M + blockDim.x - 1) / blockDim.x;
+    const int per = (B + blockDim.x - 1) / blockDim.x;
     int32_t run = 0;
     for (int k = 0; k < per; k++) {
       const int b = threadIdx.x * per + k;
-      if (b < M) run += tcnt[b];
+      if (b >= B) break;
+      int32_t acc = 0;
+      for (int q = 0; q < kTileWarps; q++) {
+        const int32_t c = wcnt[q * B + b];
+        wcnt[q * B + b] = acc;
+        acc += c;
+      }
+      lstart[b] = acc;  // the bin's count, for now
+      run += acc;
     }
     int32_t x = run;
 #pragma unroll
@@ -466,136 +415,127 @@ k_ing_scatter(const int64_t* __restrict__ ticks, const int32_t* __restrict__ mod
     int32_t before = (wib ? scratch[wib - 1] : 0) + x - run;
     for (int k = 0; k < per; k++) {
       const int b = threadIdx.x * per + k;
-      if (b < M) {
-        lstart[b] = before;
-        before += tcnt[b];
-      }
+      if (b >= B) break;
+      const int32_t c = lstart[b];
+      lstart[b] = before;
+      before += c;
     }
   }
   __syncthreads();
-  // pass 2: rank, stage in bin order, shard-stream index, inverse map
+  // pass 2: stable rank, stage in bin order, inverse map
   const unsigned ltm = (1u << lane) - 1u;
 #pragma unroll
   for (int r = 0; r < kTilePerLane; r++) {
     const int64_t i = wlo + r * 32 + lane;
-    const bool act = i < hi && sl[r] >= 0;
-    const unsigned ps = __match_any_sync(0xffffffffu, sl[r]);
-    unsigned pd = 0;
-    if (kShards) pd = __match_any_sync(0xffffffffu, sd[r]);
-    int32_t e = 0, j = 0;
-    if (act) {
-      e = mine[sl[r]] + __popc(ps & ltm);
-      if (kShards) j = gbase[sd[r]] + mine[sd[r]] + __popc(pd & ltm);
-    }
+    const bool act = i < hi && bn[r] >= 0;
+    const unsigned ps = __match_any_sync(0xffffffffu, bn[r]);
+    int32_t e = 0;
+    if (act) e = mine[bn[r]] + __popc(ps & ltm);
     __syncwarp();
     if (act) {
-      if ((ps >> lane) == 1u) mine[sl[r]] += __popc(ps);  // highest peer advances
-      const int32_t le = lstart[sl[r]] + e;
+      if ((ps >> lane) == 1u) mine[bn[r]] += __popc(ps);  // highest peer advances
+      const int32_t le = lstart[bn[r]] + e;
       st_t[le] = tk[r];
       st_i[le] = (int32_t)i;
-      st_b[le] = (int16_t)sl[r];
-      if (kShards) {
-        if ((pd >> lane) == 1u) mine[sd[r]] += __popc(pd);
-        st_g[le] = j;
-        sh_tick[j] = tk[r];
-      }
-      inv[i] = gbase[sl[r]] + e;  // coalesced in i
+      st_b[le] = (int16_t)bn[r];
+      if (kAux) st_a[le] = ax[r];
+      inv_out[i] = gbase[bn[r]] + e;  // coalesced in i
     }
     __syncwarp();
   }
   __syncthreads();
-  const int32_t len = (int32_t)(lstart[M - 1] + tcnt[M - 1]);
+  const int32_t len = scratch[kTileWarps - 1];  // elements staged (valid ids)
   for (int32_t e = threadIdx.x; e < len; e += blockDim.x) {  // bin runs
     const int32_t b = st_b[e];
     const int32_t pos = gbase[b] + (e - lstart[b]);
-    s_tick[pos] = st_t[e];
-    if (kShards) s_g[pos] = st_g[e];
-    s_i[pos] = st_i[e];
-    s_slot[pos] = b;
+    out_tick[pos] = st_t[e];
+    out_idx[pos] = st_i[e];
+    if (kAux) out_aux[pos] = st_a[e];
   }
 }
 
 // --------------------------------------------------------------- K2 -------
 
-// K2' (fast path): the batch-chain pointer of every position by the lean
-// monotone sweep (fastpath.cuh), one thread per 32 consecutive positions;
-// close_k[p] keeps the closing arrival of certified starts for k_chain_recs.
-// One lane per sorted position (lanes in lock step on neighbouring ticks);
-// close_k = the closing arrival for k_chain_recs.
-//
-// Affine profiles (the common case) use lean_chain_next_affine's test on
-// u_j = tick_j + c1*j, but instead of every lane scanning forward to its own
-// closing arrival (a loop as long as the warp's longest batch), the warp
-// stages the ticks of its 64-position window in registers (two coalesced
-// loads) and each lane binary-searches its first u_j >= T through shuffles:
-// six uniform steps.  A closing index beyond the window (batches longer
-// than ~32) continues with the scalar scan.
+// K2 (window / candidate per fresh start, fast path): the batch-chain
+// pointer of every sorted position q -- where the batch a fresh start at q
+// forms closes (fastpath.cuh, lean_chain_next*) -- and its closing arrival
+// for k_chain_recs.  Each thread owns kNxtPer consecutive positions and
+// sweeps them with two pointers: for an affine l(b) (deferred, prefix) the
+// closing index is the first j > q with u_j >= u_q + (slo - a - b0 - d_ctrl)
+// on u_j = tick_j + (a + d_data) j (lean_chain_next_affine), and both
+// sides grow with q, so the search pointer only moves forward: ~1 load,
+// multiply-add and compare per position instead of a search per position.
+// Model boundaries come from the per-slot offsets (no per-position model
+// array).  Positions the lean test cannot certify are listed for the general
+// fresh scan (k_nxt_general); other profiles and policies take the scalar
+// lean forms per position.
+constexpr int kNxtPer = 8;
+
+__device__ __forceinline__ int32_t slot_of_position(const ModelParam* __restrict__ mp_all,
+                                                    int32_t M, int64_t p) {
+  int32_t lo = 0, hi = M;  // last slot with off <= p, skipping empty slots
+  while (hi - lo > 1) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+  }
+  while (lo + 1 < M && mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
+  return lo;
+}
+
 __global__ void __launch_bounds__(256)
-k_nxt_pp(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
-         const ModelParam* __restrict__ mp_all, int32_t P, int64_t n,
-         const int32_t* __restrict__ s_slot,
-         int32_t* __restrict__ nxt, int32_t* __restrict__ close_k,
-         int32_t* __restrict__ unsure, int32_t* __restrict__ unsure_n) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int64_t p0 = p - lane;  // window base (warp-uniform)
-  if (p0 >= n) return;          // whole warp out of range
-  const bool valid = p < n;
-  const int64_t pc = valid ? p : n - 1;
-  const int lo = s_slot[pc];  // model slot of the position (k_scatter)
-  int s = 0;
-  while (slot_base[s + 1] <= lo) s++;
-  const Shard& S = shards[s];
-  const int32_t m = lo - slot_base[s];
-  const ModelParam& mp = mp_all[lo];
-  const int64_t* tick_g = S.s_tick;
-  const int64_t w0 = p0 + lane < n ? tick_g[p0 + lane] : INT64_MAX;
-  const int64_t w1 = p0 + 32 + lane < n ? tick_g[p0 + 32 + lane] : INT64_MAX;
-  const int32_t q = (int32_t)(pc - mp.off);
-  const bool affine = mp.affine && S.kind == K_DEFERRED && S.gather == G_PREFIX;
-  // affine search state (absolute positions)
-  const int64_t a = mp.aff_a, b0 = mp.aff_b, dc = S.d_ctrl, dd = S.d_data, c1 = a + dd;
-  const int32_t mb = mp.max_batch, cnt = mp.cnt;
-  const int64_t off = mp.off;
-  const int64_t uq = valid ? w0 + c1 * q : 0;  // tick_p is this lane's w0
-  const int64_t T = uq + (mp.slo - a - b0 - dc);
-  const int32_t kmax = cnt - 2 < q + mb - 2 ? cnt - 2 : q + mb - 2;
-  const int64_t jend = off + (int64_t)kmax + 1;     // last candidate j (absolute)
-  const int64_t jw = jend < p0 + 63 ? jend : p0 + 63;  // last candidate in the window
-  int32_t jlo = (int32_t)(pc + 1 - p0), jhi = (int32_t)(jw - p0) + 1;  // [jlo, jhi)
-  if (!affine || !valid) jhi = jlo;
-#pragma unroll
-  for (int it = 0; it < 6; it++) {
-    const bool act = jlo < jhi;
-    const int mid = act ? (jlo + jhi) >> 1 : 0;
-    const int64_t v0 = __shfl_sync(0xffffffffu, w0, mid & 31);
-    const int64_t v1 = __shfl_sync(0xffffffffu, w1, mid & 31);
-    const int64_t t = mid < 32 ? v0 : v1;
-    if (act) {
-      if (t + c1 * (p0 + mid - off) >= T) jhi = mid;
-      else jlo = mid + 1;
-    }
-  }
-  if (!valid) return;
-  int32_t v;
-  if (affine) {
-    int64_t j = p0 + jlo;  // first j in the window with u_j >= T, or jw + 1
-    if (j > jw && jw < jend) {  // continue past the window
-      while (j <= jend && tick_g[j] + c1 * (j - off) < T) j++;
-    }
-    if (j <= jend) {  // closes at k = j - 1
-      const int64_t k = j - 1;
-      const int64_t OK = uq + (mp.slo - dc - b0 - c1);
-      v = tick_g[k] + c1 * (k - off) <= OK ? (int32_t)j : NX_UNSURE;
+k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
+      const ModelParam* __restrict__ mp_all, int32_t P, int32_t M, int64_t n,
+      int32_t* __restrict__ nxt, int32_t* __restrict__ close_k,
+      int32_t* __restrict__ unsure, int32_t* __restrict__ unsure_n) {
+  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kNxtPer;
+  if (p0 >= n) return;
+  const int64_t p1 = p0 + kNxtPer < n ? p0 + kNxtPer : n;
+  int32_t k = slot_of_position(mp_all, M, p0);
+  for (int64_t p = p0; p < p1;) {
+    while (mp_all[k].off + mp_all[k].cnt <= p) k++;  // next non-empty slot
+    const ModelParam mp = mp_all[k];
+    int s = 0;
+    while (slot_base[s + 1] <= k) s++;
+    const Shard& S = shards[s];
+    const int32_t m = k - slot_base[s];
+    const int64_t pe = mp.off + mp.cnt < p1 ? mp.off + mp.cnt : p1;  // this model's part
+    const int64_t* tick = S.s_tick;
+    if (mp.affine && S.kind == K_DEFERRED && S.gather == G_PREFIX) {
+      const int64_t a = mp.aff_a, b0 = mp.aff_b, dc = S.d_ctrl, dd = S.d_data, c1 = a + dd;
+      const int64_t off = mp.off;
+      const int32_t mb = mp.max_batch, cnt = mp.cnt;
+      int64_t j = p + 1;  // search pointer (absolute): u_i < T for every i in (q, j)
+      for (; p < pe; p++) {
+        const int32_t q = (int32_t)(p - off);
+        const int64_t uq = tick[p] + c1 * q;
+        const int64_t T = uq + (mp.slo - a - b0 - dc);
+        const int32_t kmax = cnt - 2 < q + mb - 2 ? cnt - 2 : q + mb - 2;
+        const int64_t jend = off + (int64_t)kmax + 1;  // last candidate j
+        if (j < p + 1) j = p + 1;
+        while (j <= jend && tick[j] + c1 * (j - off) < T) j++;
+        int32_t v;
+        if (j <= jend) {  // closes at k = j - 1, if ok(len) holds there
+          const int64_t kk = j - 1;
+          const int64_t OK = uq + (mp.slo - dc - b0 - c1);
+          v = tick[kk] + c1 * (kk - off) <= OK ? (int32_t)j : NX_UNSURE;
+        } else {
+          v = lean_chain_next_affine_tail(S, mp, q);
+        }
+        nxt[p] = v;
+        close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
+        if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = (int32_t)p;
+      }
     } else {
-      v = lean_chain_next_affine_tail(S, mp, q);
+      const bool r32 = rel32_ok(S, mp);
+      for (; p < pe; p++) {
+        const int32_t q = (int32_t)(p - mp.off);
+        const int32_t v = r32 ? lean_chain_next32(S, m, q) : lean_chain_next(S, m, q);
+        nxt[p] = v;
+        close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
+        if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = (int32_t)p;
+      }
     }
-  } else {
-    v = rel32_ok(S, mp) ? lean_chain_next32(S, m, q) : lean_chain_next(S, m, q);
   }
-  nxt[p] = v;
-  close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
-  if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = (int32_t)p;  // for k_nxt_general
 }
 
 // Positions the lean loop could not certify: the general fresh_scan.
@@ -781,7 +721,8 @@ __global__ void k_bid(const BatchRec* __restrict__ recs, const int64_t* __restri
 // RunResult arrays (simulator.py:74-78, 159-173, 249-258) in stream order:
 // one thread per request, reads scattered, writes coalesced.  A request no
 // batch covers was dropped (every request resolves).
-__global__ void k_out(int64_t n, const int32_t* __restrict__ inv,
+__global__ void k_out(int64_t n, const int32_t* __restrict__ inv1,
+                      const int32_t* __restrict__ inv,
                       const int32_t* __restrict__ bid, const BatchRec* __restrict__ recs,
                       const int64_t* __restrict__ ticks, const int32_t* __restrict__ model,
                       const int64_t* __restrict__ slo_by_model,
@@ -797,7 +738,9 @@ __global__ void k_out(int64_t n, const int32_t* __restrict__ inv,
   if (o_arr) o_arr[i] = tick;
   if (o_dl) o_dl[i] = dl;
   if (o_model) o_model[i] = mi;
-  const int32_t r = bid[inv[i]];
+  // sorted position: inv[i] (one sub-cluster) or inv[inv1[i]] (several:
+  // stream -> sub-cluster stream -> layout)
+  const int32_t r = bid[inv[inv1 ? inv1[i] : (int32_t)i]];
   if (r < 0) {
     disp[i] = -1;
     start[i] = -1;
@@ -1323,6 +1266,9 @@ __global__ void k_token_keys(const uint32_t* __restrict__ bvals, int64_t nt,
 // groups by the resolved gid, repeated until no group moves.  Grid-wide
 // syncs replace the host round trips; convergence flags alternate by parity
 // so a flag is reset one phase before it is written.
+constexpr int kTieMax = 64;    // tie groups repaired by relabelling
+constexpr int kTieGroup = 16;  // ... of at most this many tokens each
+
 __global__ void __launch_bounds__(256)
 k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bvals,
              int64_t nt, const int64_t* __restrict__ sbase,
@@ -1366,6 +1312,84 @@ k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bv
       }
     }
     grid.sync();
+    if (it == 0) {
+      // Few equal-finish token groups (5 in a 9M-request C4 sub-cluster): put
+      // each in gid order in token order, and move the GPU of everything
+      // downstream of a consumer whose creator changed -- a consumer y and
+      // its descendants are exactly the batches of y's GPU from y on, so a
+      // relabel of (gid og, index >= y) -> ng replaces a whole re-match.
+      int32_t* list = flags + 4;
+      int32_t* table = flags + 4 + kTieMax;  // [kTieGroup][3]: og, ng, y
+      for (int64_t i = tid0; i < nt; i += stride) {
+        if ((i > 0 && tkeys[i - 1] == tkeys[i]) || i + 1 >= nt || tkeys[i + 1] != tkeys[i])
+          continue;
+        int64_t e = i + 1;
+        while (e < nt && tkeys[e] == tkeys[i]) e++;
+        // a group too large for the relabel table sends the run to the loop
+        const int32_t k = atomicAdd(&flags[1], e - i > kTieGroup ? kTieMax + 1 : 1);
+        if (k < kTieMax) list[k] = (int32_t)i;
+      }
+      grid.sync();
+      const int32_t ng = __ldcg(&flags[1]);
+      if (ng <= kTieMax) {
+        if (tid0 == 0)  // the groups in token order
+          for (int32_t a = 1; a < ng; a++)
+            for (int32_t b = a; b > 0 && list[b - 1] > list[b]; b--) {
+              const int32_t t = list[b];
+              list[b] = list[b - 1];
+              list[b - 1] = t;
+            }
+        grid.sync();
+        for (int32_t q = 0; q < ng; q++) {
+          if (tid0 == 0) {
+            const int64_t i = list[q];
+            const int s = (int)(tkeys[i] >> tb);
+            const int64_t base = sbase[s], ns = sbase[s + 1] - base;
+            const int32_t G = shards[s].G;
+            int64_t e = i + 1;
+            while (e < nt && tkeys[e] == tkeys[i]) e++;
+            int32_t og[kTieGroup];
+            for (int64_t a = i; a < e; a++) og[a - i] = -__ldcg(ptrA + base + tvals[a]) - 1;
+            for (int64_t a = i + 1; a < e; a++) {  // stable insertion sort by gid
+              const uint32_t v = tvals[a];
+              const int32_t gv = -__ldcg(ptrA + base + v) - 1;
+              int64_t b = a;
+              while (b > i && -__ldcg(ptrA + base + tvals[b - 1]) - 1 > gv) {
+                tvals[b] = tvals[b - 1];
+                b--;
+              }
+              tvals[b] = v;
+            }
+            int32_t cnt = 0;
+            for (int64_t a = i; a < e; a++) {
+              const int32_t n_g = -__ldcg(ptrA + base + tvals[a]) - 1;
+              const int64_t y = a + G;  // the batch popping this token
+              if (n_g != og[a - i] && y - base < ns) {
+                table[3 * cnt] = og[a - i];
+                table[3 * cnt + 1] = n_g;
+                table[3 * cnt + 2] = (int32_t)y;
+                cnt++;
+              }
+            }
+            flags[2] = cnt;
+            __threadfence();
+          }
+          grid.sync();
+          const int32_t cnt = __ldcg(&flags[2]);
+          for (int64_t i = tid0; cnt > 0 && i < nt; i += stride) {
+            const int32_t g = -__ldcg(ptrA + i) - 1;
+            for (int32_t k = 0; k < cnt; k++)
+              if (g == __ldcg(&table[3 * k]) && i >= __ldcg(&table[3 * k + 2])) {
+                ptrA[i] = -__ldcg(&table[3 * k + 1]) - 1;
+                break;
+              }
+          }
+          grid.sync();
+        }
+        break;  // matched (k_fast_emit still checks every tie's order)
+      }
+      // many tie groups: the general fixed-point iteration below
+    }
     if (tid0 == 0) flags[2 + ((it + 1) & 1)] = 0;
     bool moved = false;
     for (int64_t i = tid0; i < nt; i += stride) {  // equal-finish groups by gid
@@ -1764,6 +1788,7 @@ __global__ void k_step_rebase(ModelParam* __restrict__ mp, ModelState* __restric
   if (!first) {
     ModelState& st = ms[k];
     const int32_t sh = st.qh;
+    st.qbase += sh;
     st.qh -= sh;
     st.qt -= sh;
     if (st.c_head >= sh) st.c_head -= sh;
@@ -1903,6 +1928,8 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_s_tick, c)) || (rc = grow(ctx, ctx->d_sh_tick, c)) ||
         (rc = grow(ctx, ctx->d_s_g, c)) || (rc = grow(ctx, ctx->d_s_i, c)) ||
         (rc = grow(ctx, ctx->d_inv, c)) || (rc = grow(ctx, ctx->d_bid, c)) ||
+        (rc = grow(ctx, ctx->d_sh_i, c)) || (rc = grow(ctx, ctx->d_sh_slot, c)) ||
+        (rc = grow(ctx, ctx->d_inv1, c)) ||
         (rc = grow(ctx, ctx->d_scan_part,
                    ((c + kChunkR - 1) / kChunkR + 1) * kDigits / kScanItems + 2)) ||
         (rc = grow(ctx, ctx->d_fresh, c)) ||
@@ -1915,10 +1942,10 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
         (rc = grow(ctx, ctx->d_tvA, c)) || (rc = grow(ctx, ctx->d_tvB, c)) ||
         (rc = grow(ctx, ctx->d_ptrA, c)) ||
         (rc = grow(ctx, ctx->d_rhist, ((c + kChunkR - 1) / kChunkR + 1) * kDigits)) ||
-        (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
         (rc = grow(ctx, ctx->d_closek, c)) ||
+        (rc = grow(ctx, ctx->d_nxt, c)) || (rc = grow(ctx, ctx->d_jA, c)) ||
         (rc = grow(ctx, ctx->d_jB, c)) || (rc = grow(ctx, ctx->d_jC, c)) ||
-        (rc = grow(ctx, ctx->d_s_slot, c)) || (rc = grow(ctx, ctx->d_unsure, c)) ||
+        (rc = grow(ctx, ctx->d_unsure, c)) ||
         (rc = grow(ctx, ctx->d_cp_pos, c / kJump + ctx->M + 2)) ||
         (rc = grow(ctx, ctx->d_cp_model, c / kJump + ctx->M + 2)))
       return rc;
@@ -2025,12 +2052,14 @@ void forget_last_run(Ctx* ctx) {
   ctx->last_rec_base.clear();
 }
 
-void flat_scan(Ctx* ctx, int32_t* a, int64_t len, KernelTimer& kt, int64_t& launches) {
+void flat_scan(Ctx* ctx, int32_t* a, int64_t len, KernelTimer& kt, int64_t& launches,
+               int32_t* part = nullptr) {
   cudaStream_t st = ctx->stream;
+  if (!part) part = ctx->d_scan_part;
   const int64_t nparts = (len + kScanItems - 1) / kScanItems;
-  KL(k_scan_up, nparts, 1024, 0, st>>>(a, len, ctx->d_scan_part));
-  KL(k_scan_mid, 1, 1024, 0, st>>>(ctx->d_scan_part, nparts));
-  KL(k_scan_down, nparts, 1024, 0, st>>>(a, len, ctx->d_scan_part));
+  KL(k_scan_up, nparts, 1024, 0, st>>>(a, len, part));
+  KL(k_scan_mid, 1, 1024, 0, st>>>(part, nparts));
+  KL(k_scan_down, nparts, 1024, 0, st>>>(a, len, part));
 }
 
 // What the ingest reads back for the host (one synchronisation).
@@ -2041,51 +2070,63 @@ struct IngestInfo {
 };
 
 // K1: stable partition of n time-ordered arrivals into the (shard, model)-
-// sorted layout (ctx->d_s_tick, d_s_g, d_s_i, d_sh_tick, d_inv, d_s_slot;
+// sorted layout (ctx->d_s_tick, d_s_g, d_s_i, d_sh_tick, d_inv;
 // per-slot off/cnt into mp_out).  Validates model ids (EPROTO) and the
 // time order (EINVAL) on the device.
+// One stable partition (k_part_count, flat_scan, k_part_binoff, k_part).
+template <int kMode>
+int partition(Ctx* ctx, const int64_t* tick_in, const int32_t* key, const int32_t* aux_in,
+              int64_t n, int32_t B, ModelParam* mp_out, int32_t* shard_off_out,
+              int64_t* out_tick, int32_t* out_idx, int32_t* out_aux, int32_t* inv_out,
+              KernelTimer& kt, int64_t& launches) {
+  cudaStream_t st = ctx->stream;
+  const int64_t W = (n + kTileI - 1) / kTileI;
+  if (W * B + 1 > ctx->hist_cap) {
+    int rc;
+    if ((rc = grow(ctx, ctx->d_hist, W * B + 1)) ||
+        (rc = grow(ctx, ctx->d_hist_part, (W * B + 1) / kScanItems + 2)))
+      return rc;
+    ctx->hist_cap = W * B + 1;
+  }
+  if (W > 0) {
+    KL(k_part_count<kMode>, W, 256, sizeof(int32_t) * B, st>>>(
+        key, n, ctx->M, ctx->d_shard_of_model, B, ctx->d_hist, W, ctx->d_err));
+    flat_scan(ctx, ctx->d_hist, W * B, kt, launches, ctx->d_hist_part);
+  }
+  KL(k_part_binoff, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, n, mp_out, shard_off_out));
+  if (W > 0)
+    KL(k_part<kMode>, W, 32 * kTileWarps, part_smem(B), st>>>(
+        tick_in, key, aux_in, n, ctx->M, ctx->d_shard_of_model, ctx->d_slot_of_model, B,
+        ctx->d_hist, W, out_tick, out_idx, out_aux, inv_out, ctx->d_err));
+  CK(cudaGetLastError());
+  return SYM_OK;
+}
+
 int ingest(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_t n,
            ModelParam* mp_out, KernelTimer& kt, int64_t& launches, IngestInfo& info,
            sym_result* out) {
   cudaStream_t st = ctx->stream;
   const int32_t M = ctx->M, P = ctx->P;
-  const int B = P > 1 ? M + P : M;
-  const int64_t tiles = (n + kTileI - 1) / kTileI;
-  if (tiles * B > ctx->ing_status_cap) {  // look-back words, zeroed once
-    const int64_t c = tiles * B + tiles * B / 4 + 1024;
-    int rc;
-    if ((rc = grow(ctx, ctx->d_ing_status, c))) return rc;
-    CK(cudaMemsetAsync(ctx->d_ing_status, 0, sizeof(unsigned long long) * c, st));
-    ctx->ing_status_cap = c;
-  }
-  if (++ctx->ing_epoch >= (uint64_t(1) << (64 - kEpochShift))) {  // epoch wrap
-    ctx->ing_epoch = 1;
-    CK(cudaMemsetAsync(ctx->d_ing_status, 0,
-                       sizeof(unsigned long long) * ctx->ing_status_cap, st));
-  }
   const int32_t big[2] = {INT32_MAX, INT32_MAX};
   CK(cudaMemcpyAsync(ctx->d_err, big, sizeof big, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(ctx->d_ing_tot, 0, sizeof(unsigned long long) * B, st));
-  CK(cudaMemsetAsync(ctx->d_ing_ticket, 0, sizeof(unsigned int), st));
   int32_t* shard_off = ctx->d_bins + (M + P) + 1;
-  if (n > 0)
-    KL(k_ing_count, (unsigned)std::min<int64_t>(148 * 8, nblk(n, 256)), 256,
-       sizeof(int32_t) * B, st>>>(d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M,
-                                  P, ctx->d_ing_tot, ctx->d_err));
-  KL(k_ing_offsets, 1, 1024, 0, st>>>(ctx->d_ing_tot, M, P, n, ctx->d_ing_start, mp_out,
-                                       shard_off));
-  if (tiles > 0 && P > 1)
-    KL(k_ing_scatter<true>, tiles, 32 * kTileWarps, ing_smem(B, true), st>>>(
-        d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
-        ctx->d_ing_start, ctx->d_ing_status, ctx->d_ing_ticket, ctx->ing_epoch,
-        ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i, ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot,
-        ctx->d_err));
-  else if (tiles > 0)
-    KL(k_ing_scatter<false>, tiles, 32 * kTileWarps, ing_smem(B, false), st>>>(
-        d_ticks, d_model, n, ctx->d_slot_of_model, ctx->d_shard_of_model, M, P,
-        ctx->d_ing_start, ctx->d_ing_status, ctx->d_ing_ticket, ctx->ing_epoch,
-        ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i, ctx->d_sh_tick, ctx->d_inv, ctx->d_s_slot,
-        ctx->d_err));
+  int rc;
+  if (P == 1) {
+    const int32_t zn[2] = {0, (int32_t)n};
+    CK(cudaMemcpyAsync(shard_off, zn, sizeof zn, cudaMemcpyHostToDevice, st));
+    if ((rc = partition<0>(ctx, d_ticks, d_model, nullptr, n, M, mp_out, nullptr,
+                           ctx->d_s_tick, ctx->d_s_i, nullptr, ctx->d_inv, kt, launches)))
+      return rc;
+  } else {
+    // by sub-cluster (the sub-cluster streams), then each of them by model
+    if ((rc = partition<1>(ctx, d_ticks, d_model, nullptr, n, P, nullptr, shard_off,
+                           ctx->d_sh_tick, ctx->d_sh_i, ctx->d_sh_slot, ctx->d_inv1, kt,
+                           launches)) ||
+        (rc = partition<2>(ctx, ctx->d_sh_tick, ctx->d_sh_slot, ctx->d_sh_i, n, M, mp_out,
+                           nullptr, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i, ctx->d_inv, kt,
+                           launches)))
+      return rc;
+  }
   CK(cudaGetLastError());
   int32_t herr2[2] = {INT32_MAX, INT32_MAX};
   info.last_tick = 0;
@@ -2124,6 +2165,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   const int32_t M = ctx->M, P = ctx->P;
   const int B = M + P;
   const bool trace = flags & SYM_FLAG_TRACE;
+  const bool check = flags & SYM_FLAG_CHECK_INVARIANTS;
   const bool use_fresh = !trace && !(flags & SYM_FLAG_NO_FRESH);
   forget_last_run(ctx);
   ctx->step_active = false;  // a whole run reuses the chain arrays
@@ -2156,6 +2198,8 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     S.sh_base = shard_off[s];
     S.s_aself = nullptr;
     S.record_trace = trace ? 1 : 0;
+    S.check = check ? 1 : 0;
+    S.inject = check && (flags & SYM_FLAG_INJECT_FAULT) ? 9 : -1;
     S.drop_t = ctx->d_drop_t;
     S.drop_ksub = ctx->d_drop_ks;
     S.drop_ka = ctx->d_drop_ka;
@@ -2176,13 +2220,14 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     KL(k_fill64, nblk(n, 256), 256, 0, st>>>(ctx->d_drop_t, n, -1));
   // ---- K2 fresh-start pre-scan: chain pointers for the fast path, full
   // records (needed only by the sequential chain) otherwise
-  const bool fast = use_fresh && !(flags & SYM_FLAG_NO_FAST) && n > 0;
+  // per-event invariants need the event-by-event chain (no fast path)
+  const bool fast = use_fresh && !check && !(flags & SYM_FLAG_NO_FAST) && n > 0;
   bool have_fresh = false;
   if (fast) {
     CK(cudaMemsetAsync(ctx->d_unsure_n, 0, sizeof(int32_t), st));
-    KL(k_nxt_pp, nblk(n, 256), 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, n,
-                                             ctx->d_s_slot, ctx->d_nxt, ctx->d_closek,
-                                             ctx->d_unsure, ctx->d_unsure_n));
+    KL(k_nxt, nblk((n + kNxtPer - 1) / kNxtPer, 256), 256, 0, st>>>(
+        ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, M, n, ctx->d_nxt, ctx->d_closek,
+        ctx->d_unsure, ctx->d_unsure_n));
     KL(k_nxt_general, 148 * 4, 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P,
                                              ctx->d_unsure, ctx->d_unsure_n, ctx->d_nxt,
                                              ctx->d_closek));
@@ -2350,8 +2395,17 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   for (int s = 0; s < P; s++) {
     const Shard& S = ctx->shards[s];
     if (S.error) {
-      ctx->err = "chain error " + std::to_string(S.error) + " in shard " +
-                 std::to_string(s);
+      static const char* what[] = {"", "record overflow", "bad chain state",
+                                   "conservation broken (arrivals != dispatched + dropped + "
+                                   "queued)",
+                                   "gpu state machine broken (grant outstanding across an "
+                                   "event, or free index out of sync)",
+                                   "rank candidate indices out of sync",
+                                   "candidate infeasible (exec_at > latest or misses its head "
+                                   "deadline)"};
+      ctx->err = std::string(S.error >= 1 && S.error <= 6 ? what[S.error] : "chain error") +
+                 " in sub-cluster " + std::to_string(s) + " after chain event " +
+                 std::to_string(S.chain_events);
       return SYM_EINVARIANT;
     }
     rec_count[s] = S.n_recs;
@@ -2391,10 +2445,13 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   }
   const bool expand = !(flags & SYM_FLAG_NO_EXPAND) && out->req_dispatch;
   if (expand && n > 0) {
+    // every position starts as "no batch" (dropped); k_bid stamps the members
+    CK(cudaMemsetAsync(ctx->d_bid, 0xff, sizeof(int32_t) * n, st));
     if (total > 0)
       KL(k_bid, nblk(total, 256), 256, 0, st>>>(ctx->d_recs, d_meta, d_meta + P + 1, P, total,
                                                 ctx->d_bid));
-    KL(k_out, nblk(n, 256), 256, 0, st>>>(n, ctx->d_inv, ctx->d_bid, ctx->d_recs, d_ticks,
+    KL(k_out, nblk(n, 256), 256, 0, st>>>(n, P > 1 ? ctx->d_inv1 : nullptr, ctx->d_inv,
+                                          ctx->d_bid, ctx->d_recs, d_ticks,
                                           d_model, ctx->d_slo_model, out->req_dispatch,
                                           out->req_start, out->req_finish, out->req_batch,
                                           out->req_outcome, out->req_arrival, out->req_deadline,
@@ -2555,6 +2612,10 @@ int step_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_
                                                -1));
   }
   if (first) {
+    for (Shard& S : ctx->shards) {
+      S.check = (flags & SYM_FLAG_CHECK_INVARIANTS) ? 1 : 0;
+      S.inject = -1;
+    }
     CK(cudaMemsetAsync(ctx->d_step_shard, 0, sizeof(int64_t) * 3 * P, st));
     // static configuration and pointers of every shard (the chain state
     // itself is initialised by the first step's chain)
@@ -2617,8 +2678,8 @@ int step_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_
   for (int s = 0; s < P; s++) {
     if (ctx->shards[s].error) {
       ctx->step_active = false;
-      ctx->err = "chain error " + std::to_string(ctx->shards[s].error) + " in shard " +
-                 std::to_string(s);
+      ctx->err = "chain error " + std::to_string(ctx->shards[s].error) + " in sub-cluster " +
+                 std::to_string(s) + " (invariant codes 3-6: see engine_core.cuh)";
       return SYM_EINVARIANT;
     }
   }
@@ -2845,16 +2906,14 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   // bins: [B+1] totals, then shard_off [P+1], model_of_slot [M], gpu_base [P+1]
   ALLOC(ctx->d_bins, (M + P + 1) + (P + 1) + M + (P + 1));
   ALLOC(ctx->d_err, 2);
-  ALLOC(ctx->d_ing_tot, M + P);
-  ALLOC(ctx->d_ing_start, M + P);
-  ALLOC(ctx->d_ing_ticket, 1);
+
   ALLOC(ctx->d_nb, M);
   ALLOC(ctx->d_bbase, M);
   ALLOC(ctx->d_mdrops, M);
   ALLOC(ctx->d_sbase, P + 1);
   ALLOC(ctx->d_fail, P);
   ALLOC(ctx->d_skip, P);
-  ALLOC(ctx->d_changed, 4);
+  ALLOC(ctx->d_changed, 4 + kTieMax + 3 * kTieGroup);
   ALLOC(ctx->d_unsure_n, 1);
   ALLOC(ctx->d_special, M);
   ALLOC(ctx->d_slo_model, M);
@@ -2930,16 +2989,16 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     if ((e = cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)ctx->chain_smem)) != cudaSuccess)
       return fail("smem attribute", e);
-    const size_t sc = ing_smem(ctx->M + ctx->P, true);  // >= the <false> size
+    const size_t sc = part_smem(std::max(ctx->M, ctx->P));
     if (sc > (size_t)dev_max || ctx->M + ctx->P >= 32768)
-      return fail("too many models for the ingest scatter", cudaErrorInvalidValue);
-    if ((e = cudaFuncSetAttribute(k_ing_scatter<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc)) !=
-            cudaSuccess ||
-        (e = cudaFuncSetAttribute(k_ing_scatter<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc)) !=
-            cudaSuccess)
-      return fail("scatter smem attribute", e);
+      return fail("too many models for the ingest partition", cudaErrorInvalidValue);
+    if ((e = cudaFuncSetAttribute(k_part<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sc)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k_part<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sc)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(k_part<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sc)) != cudaSuccess)
+      return fail("partition smem attribute", e);
   }
   if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return fail("init", e);
   *status = SYM_OK;
@@ -2958,17 +3017,16 @@ void sym_destroy(void* engine) {
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,
                   ctx->d_inv, ctx->d_bid, ctx->d_scan_part, ctx->d_closek,
-                  ctx->d_bins,   ctx->d_err,   ctx->d_fresh,  ctx->d_ing_tot,
-                  ctx->d_ing_start, ctx->d_ing_ticket, ctx->d_ing_status,
+                  ctx->d_bins,   ctx->d_err,   ctx->d_fresh, ctx->d_hist, ctx->d_hist_part, ctx->d_sh_i,
+                  ctx->d_sh_slot, ctx->d_inv1,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
                   ctx->d_bvA, ctx->d_bvB, ctx->d_tvA, ctx->d_tvB, ctx->d_ptrA,
                   ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
-                  ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_jC, ctx->d_s_slot,
-                  ctx->d_unsure, ctx->d_unsure_n,
-                  ctx->d_cp_pos,
-                  ctx->d_cp_model, ctx->d_special, ctx->d_meta, ctx->d_req,
+                  ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_jC,
+                  ctx->d_unsure, ctx->d_unsure_n, ctx->d_cp_pos, ctx->d_cp_model,
+                  ctx->d_special, ctx->d_meta, ctx->d_req,
                   ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
                   ctx->d_net_vals, ctx->d_net_cdf, ctx->d_g_ticks, ctx->d_g_model,
                   ctx->d_g_out, ctx->d_lay_tick[0], ctx->d_lay_tick[1], ctx->d_lay_g[0],

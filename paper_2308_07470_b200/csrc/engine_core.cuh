@@ -136,6 +136,7 @@ struct ModelState {
   EvKey dt_key;       // live drop timer (valid iff dt_head >= 0)
   EvKey nx_key;       // next chain event of this model
   int64_t drops;
+  int64_t qbase;      // arrivals compacted out of the layout by earlier steps
   int32_t qh, qt;     // queue = positions [off+qh, off+qt)
   int32_t has_cand, c_size;
   int32_t c_head;     // queue position of the candidate head (head rid)
@@ -197,6 +198,10 @@ struct Shard {
   int64_t ops, evictions, registrations, handler_ops_max;
   int32_t error;
   int32_t sh_base;             // first shard-stream index of this shard
+  // invariant mode (Engine(check_invariants=True), simulator.py:276-305)
+  int64_t served;              // requests dispatched so far (sum of batch sizes)
+  int32_t check;               // verify the state after every chain event
+  int32_t inject;              // test hook: corrupt the state at chain event `inject` (-1 off)
 };
 
 // Canonical A' of the arrival at sorted position pos (engine_core.cuh top):
@@ -208,7 +213,14 @@ SYM_HD int32_t aself_at(const Shard& S, int32_t pos) {
   return (j > S.sh_base && S.sh_tick[j - 1] == S.s_tick[pos]) ? j : A_BASE;
 }
 
-enum : int32_t { ERR_NONE = 0, ERR_REC_OVERFLOW = 1, ERR_STATE = 2 };
+enum : int32_t {
+  ERR_NONE = 0, ERR_REC_OVERFLOW = 1, ERR_STATE = 2,
+  // per-event invariants (simulator.py:276-305), checked with Shard.check
+  ERR_INV_CONSERVATION = 3,  // processed arrivals != dispatched + dropped + queued
+  ERR_INV_GPU = 4,           // a GPU left OUTSTANDING across an event, or index out of sync
+  ERR_INV_INDEX = 5,         // registered-candidate indices out of sync
+  ERR_INV_CANDIDATE = 6      // candidate exec_at > latest, or misses its head deadline
+};
 
 SYM_HD int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
 SYM_HD int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -611,6 +623,7 @@ SYM_HD void granted_gpu(Shard& S, int32_t m, int32_t gid, int64_t gpu_free_at,
     S.error = ERR_REC_OVERFLOW;
   }
   S.n_recs += 1;
+  S.served += b;
   st.qh += b;
   const int64_t believed_free = st.c_exec + lat_b;
   st.has_cand = 0;
@@ -930,6 +943,42 @@ SYM_HD void refresh_model(Shard& S, int32_t m, const FreshRec* fresh) {
   if (st.fresh_skip == 0) prefetch_fresh(fresh, P, st);
 }
 
+// The reference's _verify (simulator.py:276-305) on the chain state after an
+// event, O(M + G): conservation (every processed arrival is dispatched,
+// dropped or queued), the GPU state machine (no grant outstanding across an
+// event boundary, the free index equal to min (free_at, gid)), the
+// registered-candidate indices in sync with the registered flags, and every
+// candidate feasible (exec_at <= latest, exec_at + l(b) <= head deadline).
+SYM_HD int32_t verify_state(const Shard& S) {
+  int64_t queued_total = 0, processed = 0, dropped = 0;
+  int32_t min_lat = -1, max_bs = -1;
+  for (int32_t m = 0; m < S.M; m++) {
+    const ModelState& st = S.ms[m];
+    if (st.qh < 0 || st.qh > st.qt || st.qt > S.mp[m].cnt) return ERR_INV_CONSERVATION;
+    queued_total += st.qt - st.qh;
+    processed += st.qbase + st.qt;
+    dropped += st.drops;
+    if (st.has_cand) {
+      if (st.c_exec > st.c_latest) return ERR_INV_CANDIDATE;
+      if (st.c_exec + lat_of(S, m, st.c_size) > st.c_d) return ERR_INV_CANDIDATE;
+    }
+    if (st.registered) {
+      if (!st.has_cand) return ERR_INV_INDEX;
+      if (lat_before(S, m, min_lat)) min_lat = m;
+      if (bs_before(S, m, max_bs)) max_bs = m;
+    }
+  }
+  if (processed != S.served + dropped + queued_total) return ERR_INV_CONSERVATION;
+  if (S.mc_lat_tree[1] != min_lat || S.mc_bs_tree[1] != max_bs) return ERR_INV_INDEX;
+  int32_t best = -1;
+  for (int32_t g = 0; g < S.G; g++) {
+    if (S.free_at[g] == OUTSTANDING) return ERR_INV_GPU;
+    if (gpu_before(S, g, best)) best = g;
+  }
+  if (S.gt[1] != best) return ERR_INV_GPU;
+  return ERR_NONE;
+}
+
 // Process one chain event; returns false when the sub-cluster is drained or
 // its next event lies after `until` (a stepped run stops there: every event
 // with tick <= until is processed, later ones wait for the next step).
@@ -997,6 +1046,20 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh,
   SYM_PROF_ADD(4 + prof_type, 1);
   SYM_PROF_ADD(8, t1 - t0);
   SYM_PROF_ADD(11, nref);
+  if (S.check) {
+    if (S.inject >= 0 && S.chain_events == S.inject + 1) {
+      // test hook: lose the head of the model that just moved without
+      // counting a drop, or (empty queue) leave GPU 0 outstanding
+      const int32_t cm = gpu_event ? (nd > 0 ? dirty[0] : 0) : m;
+      if (S.ms[cm].qh < S.ms[cm].qt) S.ms[cm].qh += 1;
+      else S.free_at[0] = OUTSTANDING;
+    }
+    const int32_t e = verify_state(S);
+    if (e) {
+      S.error = e;
+      return false;
+    }
+  }
   return true;
 }
 
@@ -1016,12 +1079,14 @@ SYM_HD void chain_init(Shard& S, const FreshRec* fresh) {
   }
   S.gt_armed = 0;
   S.n_recs = 0;
+  S.served = 0;
   S.chain_events = S.absorbed = S.fresh_adoptions = 0;
   S.ops = S.evictions = S.registrations = S.handler_ops_max = 0;
   S.error = ERR_NONE;
   for (int32_t m = 0; m < S.M; m++) {
     fresh_state(S.ms[m], 0);
     S.ms[m].fresh_skip = 0;
+    S.ms[m].qbase = 0;
     S.mc_size[m] = 0;
     S.mc_latest[m] = 0;
     refresh_model(S, m, fresh);

@@ -275,6 +275,11 @@ class Engine:
             f |= _native.FLAG_NO_FRESH
         if not self.use_fast:
             f |= _native.FLAG_NO_FAST
+        if self.check_invariants:
+            # per-event _verify (simulator.py:276-305) inside the device chain
+            f |= _native.FLAG_CHECK_INVARIANTS
+            if getattr(self, "_inject_fault", False):  # test hook
+                f |= _native.FLAG_INJECT_FAULT
         return f
 
     def _absorb_counters(self, res: _native.SymResult):
@@ -390,8 +395,11 @@ class Engine:
         if len(midx) != len(ticks):
             raise ValueError("arr_ticks and arr_midx differ in length")
         res = _native.SymResult()
+        flags = _native.FLAG_MODEL_I64
+        if self.check_invariants:
+            flags |= _native.FLAG_CHECK_INVARIANTS
         rc = self._lib.sym_step(self._handle, ticks.ctypes.data, midx.ctypes.data, len(ticks),
-                                int(until_tick), _native.FLAG_MODEL_I64, C.byref(res))
+                                int(until_tick), flags, C.byref(res))
         if rc != _native.SYM_OK:
             if rc == _native.SYM_EPROTO and 0 <= res.err_index < len(midx):
                 raise ProtocolError(f"request for unknown model {int(midx[res.err_index])}")
@@ -591,8 +599,10 @@ class Engine:
         return [r[6] for r in rows]
 
     def _verify(self, res: RunResult):
-        """End-of-run invariants (the per-event _verify of simulator.py:276-305
-        cannot observe device-internal states; these are their results)."""
+        """End-of-run invariants on the returned arrays.  The per-event
+        _verify of simulator.py:276-305 runs inside the device chain
+        (SYM_FLAG_CHECK_INVARIANTS, engine_core.cuh verify_state) after
+        every event of a check_invariants run."""
         o = res.req_outcome
         if np.any((o < 0) | (o > 2)):
             raise InvariantViolation("unresolved request outcome")

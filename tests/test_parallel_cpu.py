@@ -1,4 +1,4 @@
-"""Multi-rank host logic of the sharded path on CPU (gloo, world_size 2):
+"""Multi-rank host logic of the sharded path on CPU (gloo, world sizes 2 and 8):
 sub-cluster assignment, per-rank integer summaries, the single all-reduce,
 and the cluster statistics rebuilt from it -- checked against
 compute_stats on the whole run.  Each rank resolves its sub-clusters with
@@ -7,6 +7,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -61,20 +62,24 @@ def test_assignment_is_fixed_by_scenario():
     assert assign(8, 1) == [list(range(8))]
     assert assign(8, 2) == [[0, 2, 4, 6], [1, 3, 5, 7]]
     assert sorted(sum(assign(8, 4), [])) == list(range(8))
+    assert assign(8, 8) == [[s] for s in range(8)]  # C4 on 8 B200s: one sub-cluster each
 
 
-def test_two_rank_gloo_summary_matches_whole_run_stats():
+@pytest.mark.parametrize("world", [2, 8])
+def test_gloo_summary_matches_whole_run_stats(world):
+    """world ranks (gloo, one process each; 8 = C4 on a full box) reduce
+    their sub-clusters' summaries into the whole run's statistics."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=300) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert got[0] == got[1]  # every rank sees the same cluster view
+    assert all(got[r] == got[0] for r in range(world))  # every rank sees the same view
     # whole run, single process: compute_stats on the concatenated results
     from paper_2308_07470_b200.metrics import compute_stats
     from paper_2308_07470_b200.simulator import RunResult

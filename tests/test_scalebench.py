@@ -75,3 +75,29 @@ def test_scale_bench_runs():
     r = SB.scale_bench([1, 2], [4], 0.05, total_models=16, total_gpus=32)
     assert [p.workers for p in r["workers"]] == [1, 2]
     assert all(p.requests > 0 and p.elapsed_s > 0 for p in r["workers"] + r["gpus"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", KEYS)
+def test_schedule_engine_stepped(key, golden):
+    """The reference loop's granularity through the step API (scalebench.py:
+    67-84): chunks of arrivals, each step up to the next chunk's first
+    tick, state on the device between steps -- the reference schedule."""
+    from paper_2308_07470_b200.simulator import Engine
+    g, M, G, keep = _g(golden, key)
+    ticks, midx = SB.shard_stream(2 * keep, M, G)
+    eng = Engine(SB.shard_models(M), G, PolicyConfig("deferred"))
+    chunk = max(1, keep // 7)
+    for lo in range(0, len(ticks), chunk):
+        hi = min(len(ticks), lo + chunk)
+        eng.step(ticks[lo:hi], midx[lo:hi], int(ticks[hi]) if hi < len(ticks) else eng.DRAIN)
+    res = eng.step_result(1.0)
+    assert D.requests_digest(*[getattr(res, k)[:keep] for k in OUT]) == g["requests"]
+    eng.close()
+
+
+@pytest.mark.gpu
+def test_scale_bench_step_mode_runs():
+    r = SB.scale_bench([1, 2], [4], 0.05, total_models=16, total_gpus=32, mode="step")
+    assert [p.workers for p in r["workers"]] == [1, 2]
+    assert all(p.requests > 0 and p.elapsed_s > 0 for p in r["workers"] + r["gpus"])

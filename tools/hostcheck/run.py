@@ -54,7 +54,12 @@ for case in list(cases.bundled()) + list(cases.stress()) + list(cases.config_cas
     rc = lib.hc_run(1, C.addressof(cfg), t.ctypes.data, m.ctypes.data, n, req.ctypes.data,
                     ords.ctypes.data, C.addressof(nord), cnt.ctypes.data)
     bad = int(cnt[9])
-    total_bad += bad
-    if rc or bad:
-        print(key, "rc", rc, "mismatch", bad, "certified", int(cnt[8]), flush=True)
+    ref = oracle.run(arr_ticks=ticks, arr_midx=midx, **oracle_args(models, gpus, policy))
+    diff = [k for j, k in enumerate(("req_dispatch", "req_start", "req_finish", "req_batch",
+                                      "req_outcome")) if not np.array_equal(req[j * n:(j + 1) * n],
+                                                                            ref[k])]
+    total_bad += bad + len(diff)
+    if rc or bad or diff:
+        print(key, "rc", rc, "mismatch", bad, "certified", int(cnt[8]), "parity", diff or "ok",
+              flush=True)
 print("cases done; total mismatch", total_bad)
