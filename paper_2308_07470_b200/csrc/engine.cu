@@ -86,6 +86,8 @@ struct Ctx {
   int32_t *d_sh_i = nullptr, *d_sh_slot = nullptr, *d_inv1 = nullptr;  // P > 1: level 1
   int32_t* d_hist = nullptr;        // [B][tiles] bin counts -> positions
   int32_t* d_hist_part = nullptr;   // block sums of its scan
+  int32_t *d_bkt = nullptr, *d_bkt_part = nullptr;  // bucket sort counts / ends
+  int64_t bkt_cap = 0;
   int64_t hist_cap = 0;
   int32_t* d_err = nullptr;
   FreshRec* d_fresh = nullptr;
@@ -482,7 +484,7 @@ __device__ __forceinline__ int32_t slot_of_position(const ModelParam* __restrict
   return lo;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
       const ModelParam* __restrict__ mp_all, int32_t P, int32_t M, int64_t n,
       int32_t* __restrict__ nxt, int32_t* __restrict__ close_k,
@@ -499,7 +501,7 @@ k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
     const Shard& S = shards[s];
     const int32_t m = k - slot_base[s];
     const int64_t pe = mp.off + mp.cnt < p1 ? mp.off + mp.cnt : p1;  // this model's part
-    const int64_t* tick = S.s_tick;
+    const int64_t* __restrict__ tick = S.s_tick;
     if (mp.affine && S.kind == K_DEFERRED && S.gather == G_PREFIX) {
       const int64_t a = mp.aff_a, b0 = mp.aff_b, dc = S.d_ctrl, dd = S.d_data, c1 = a + dd;
       const int64_t off = mp.off;
@@ -507,17 +509,31 @@ k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
       int64_t j = p + 1;  // search pointer (absolute): u_i < T for every i in (q, j)
       for (; p < pe; p++) {
         const int32_t q = (int32_t)(p - off);
-        const int64_t uq = tick[p] + c1 * q;
+        const int64_t uq = __ldg(tick + p) + c1 * q;
         const int64_t T = uq + (mp.slo - a - b0 - dc);
         const int32_t kmax = cnt - 2 < q + mb - 2 ? cnt - 2 : q + mb - 2;
         const int64_t jend = off + (int64_t)kmax + 1;  // last candidate j
         if (j < p + 1) j = p + 1;
-        while (j <= jend && tick[j] + c1 * (j - off) < T) j++;
+        // four candidates per round, loaded together: the scan is bound by
+        // load latency, not by the few extra loads past the closing index
+        while (j <= jend) {
+          const int64_t base = T - c1 * (j - off);  // u_x >= T <=> tick_x >= base - c1 (x - j)
+          const int64_t t0 = __ldg(tick + j);
+          const int64_t t1 = j + 1 <= jend ? __ldg(tick + j + 1) : INT64_MAX;
+          const int64_t t2 = j + 2 <= jend ? __ldg(tick + j + 2) : INT64_MAX;
+          const int64_t t3 = j + 3 <= jend ? __ldg(tick + j + 3) : INT64_MAX;
+          if (t0 >= base) break;
+          if (t1 >= base - c1) { j += 1; break; }
+          if (t2 >= base - 2 * c1) { j += 2; break; }
+          if (t3 >= base - 3 * c1) { j += 3; break; }
+          j += 4;
+        }
+        if (j > jend + 1) j = jend + 1;
         int32_t v;
         if (j <= jend) {  // closes at k = j - 1, if ok(len) holds there
           const int64_t kk = j - 1;
           const int64_t OK = uq + (mp.slo - dc - b0 - c1);
-          v = tick[kk] + c1 * (kk - off) <= OK ? (int32_t)j : NX_UNSURE;
+          v = __ldg(tick + kk) + c1 * (kk - off) <= OK ? (int32_t)j : NX_UNSURE;
         } else {
           v = lean_chain_next_affine_tail(S, mp, q);
         }
@@ -1140,101 +1156,64 @@ k_rscatter(const uint64_t* __restrict__ kin,
   }
 }
 
-// K3d: order runs of equal (shard, tick) by the full event key
-// Batch order by merging instead of radix sorting.  k_chain_recs lays the
-// batches out as one run per model, each already in event order (a model's
-// chain), so the global order is a merge of M sorted runs: ceil(log2 M)
-// rounds of stable pairwise merge path.  Round r merges the runs of models
-// [2^(r+1) p, 2^(r+1) p + 2^r) and [.. + 2^r, 2^(r+1) (p+1)).  The key is
-// (shard << tb | tick); equal keys fall back to the full batch_cmp order
-// (A', pusher position, chain before arrival), so no fix-up pass is needed.
-constexpr int kMergeItems = 4;  // outputs per thread
-
-__device__ __forceinline__ int64_t run_bound(const int32_t* __restrict__ bbase, int32_t M,
-                                             int64_t nt, int64_t m) {
-  return m < M ? bbase[m] : nt;
+// ---- bucket sort of (shard|time key, value) pairs -------------------------
+// Batch grant ticks and finish times are spread over the run, ~1 per bucket
+// of 2^S ns when there are about as many buckets as keys: count per bucket
+// (atomics), one exclusive scan, scatter (atomic slot per bucket, order
+// within a bucket arbitrary), then one thread per bucket insertion-sorts its
+// few keys by the full order.  Four launches instead of a radix sort's
+// five passes of histogram + scan + scatter (or ceil(log2 M) merge rounds),
+// and the result is the same total order: ties beyond the key are broken by
+// the batch event order (batches, FP_KEY_TIE if that ties too) or the value
+// (tokens: the creator's rank, i.e. the stable order).
+__global__ void k_bkt_count(const uint64_t* __restrict__ keys, int64_t n, int shift,
+                            int32_t* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&cnt[keys[i] >> shift], 1);
 }
 
-// x strictly before y in batch order
-__device__ __forceinline__ bool batch_less(uint64_t kx, uint32_t vx, uint64_t ky, uint32_t vy,
-                                           const EvBatch* __restrict__ evb) {
-  if (kx != ky) return kx < ky;
-  return batch_cmp(evb[vx], evb[vy]) < 0;
+__global__ void k_bkt_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                              int64_t n, int shift, int32_t* __restrict__ next,
+                              uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = kin[i];
+  const int32_t pos = atomicAdd(&next[k >> shift], 1);  // ends up at the bucket's end
+  kout[pos] = k;
+  vout[pos] = vin[i];
 }
 
-__global__ void __launch_bounds__(256)
-k_merge_round(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-              uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t nt,
-              const int32_t* __restrict__ bbase, int32_t M, int round,
-              const EvBatch* __restrict__ evb) {
-  const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergeItems;
-  if (k0 >= nt) return;
-  const int64_t span = int64_t(1) << (round + 1), half = span >> 1;
-  // the pair containing output k0: last p with bound(p * span) <= k0
-  int64_t lo = 0, hi = (M + span - 1) / span;  // pairs [lo, hi)
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (run_bound(bbase, M, nt, mid * span) <= k0) lo = mid; else hi = mid;
-  }
-  const int64_t a0 = run_bound(bbase, M, nt, lo * span);
-  const int64_t a1 = run_bound(bbase, M, nt, lo * span + half);
-  const int64_t b1 = run_bound(bbase, M, nt, (lo + 1) * span);
-  const int64_t la = a1 - a0, lb = b1 - a1;
-  const int64_t diag = k0 - a0;
-  // merge path: i = elements of A among the first diag outputs (A first on ties)
-  int64_t i_lo = diag > lb ? diag - lb : 0, i_hi = diag < la ? diag : la;
-  while (i_lo < i_hi) {
-    const int64_t mid = (i_lo + i_hi) >> 1;
-    const int64_t j = diag - 1 - mid;
-    if (batch_less(kin[a1 + j], vin[a1 + j], kin[a0 + mid], vin[a0 + mid], evb))
-      i_hi = mid;
-    else
-      i_lo = mid + 1;
-  }
-  int64_t ia = a0 + i_lo, ib = a1 + (diag - i_lo);
-  const int64_t kend = k0 + kMergeItems < b1 ? k0 + kMergeItems : b1;
-  for (int64_t k = k0; k < kend; k++) {
-    bool take_a;
-    if (ia >= a1) take_a = false;
-    else if (ib >= b1) take_a = true;
-    else take_a = !batch_less(kin[ib], vin[ib], kin[ia], vin[ia], evb);
-    const int64_t src = take_a ? ia++ : ib++;
-    kout[k] = kin[src];
-    vout[k] = vin[src];
-  }
-  // outputs beyond this pair in the same thread chunk belong to the next
-  // pair(s): handled by walking on with fresh searches
-  for (int64_t k = kend; k < k0 + kMergeItems && k < nt;) {
-    int64_t p2 = lo + 1;
-    while (run_bound(bbase, M, nt, (p2 + 1) * span) <= k) p2++;
-    const int64_t c0 = run_bound(bbase, M, nt, p2 * span);
-    const int64_t c1 = run_bound(bbase, M, nt, p2 * span + half);
-    const int64_t d1 = run_bound(bbase, M, nt, (p2 + 1) * span);
-    const int64_t lc = c1 - c0, ld = d1 - c1, dg = k - c0;
-    int64_t x_lo = dg > ld ? dg - ld : 0, x_hi = dg < lc ? dg : lc;
-    while (x_lo < x_hi) {
-      const int64_t mid = (x_lo + x_hi) >> 1;
-      const int64_t j = dg - 1 - mid;
-      if (batch_less(kin[c1 + j], vin[c1 + j], kin[c0 + mid], vin[c0 + mid], evb))
-        x_hi = mid;
-      else
-        x_lo = mid + 1;
+template <bool kBatches>
+__global__ void k_bkt_sort(const int32_t* __restrict__ end, int64_t nbuckets,
+                           uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                           const EvBatch* __restrict__ evb) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbuckets) return;
+  const int32_t lo = b ? end[b - 1] : 0, hi = end[b];
+  for (int32_t a = lo + 1; a < hi; a++) {
+    const uint64_t k = keys[a];
+    const uint32_t v = vals[a];
+    int32_t c = a;
+    for (; c > lo; c--) {
+      const uint64_t pk = keys[c - 1];
+      const uint32_t pv = vals[c - 1];
+      bool before;  // (k, v) strictly before (pk, pv)
+      if (k != pk) {
+        before = k < pk;
+      } else if (kBatches) {
+        const int o = batch_cmp(evb[v], evb[pv]);
+        before = o != 0 ? o < 0 : v < pv;
+      } else {
+        before = v < pv;
+      }
+      if (!before) break;
+      keys[c] = pk;
+      vals[c] = pv;
     }
-    int64_t xa = c0 + x_lo, xb = c1 + (dg - x_lo);
-    const int64_t e2 = k0 + kMergeItems < d1 ? k0 + kMergeItems : d1;
-    for (; k < e2 && k < nt; k++) {
-      bool take_a;
-      if (xa >= c1) take_a = false;
-      else if (xb >= d1) take_a = true;
-      else take_a = !batch_less(kin[xb], vin[xb], kin[xa], vin[xa], evb);
-      const int64_t src = take_a ? xa++ : xb++;
-      kout[k] = kin[src];
-      vout[k] = vin[src];
-    }
-    lo = p2;
+    keys[c] = k;
+    vals[c] = v;
   }
 }
-
 
 // K3e: finish-time token of every sorted batch: key (shard|finish),
 // value = the batch's rank within its shard
@@ -1257,18 +1236,11 @@ __global__ void k_token_keys(const uint32_t* __restrict__ bvals, int64_t nt,
   tvals[i] = (uint32_t)(i - sbase[s]);
 }
 
-
-
-
-
 // The whole matching phase in one cooperative launch: match (batch r pops
 // token r) -> pointer jumping to convergence -> re-sort equal-finish token
 // groups by the resolved gid, repeated until no group moves.  Grid-wide
 // syncs replace the host round trips; convergence flags alternate by parity
 // so a flag is reset one phase before it is written.
-constexpr int kTieMax = 64;    // tie groups repaired by relabelling
-constexpr int kTieGroup = 16;  // ... of at most this many tokens each
-
 __global__ void __launch_bounds__(256)
 k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bvals,
              int64_t nt, const int64_t* __restrict__ sbase,
@@ -1312,84 +1284,6 @@ k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bv
       }
     }
     grid.sync();
-    if (it == 0) {
-      // Few equal-finish token groups (5 in a 9M-request C4 sub-cluster): put
-      // each in gid order in token order, and move the GPU of everything
-      // downstream of a consumer whose creator changed -- a consumer y and
-      // its descendants are exactly the batches of y's GPU from y on, so a
-      // relabel of (gid og, index >= y) -> ng replaces a whole re-match.
-      int32_t* list = flags + 4;
-      int32_t* table = flags + 4 + kTieMax;  // [kTieGroup][3]: og, ng, y
-      for (int64_t i = tid0; i < nt; i += stride) {
-        if ((i > 0 && tkeys[i - 1] == tkeys[i]) || i + 1 >= nt || tkeys[i + 1] != tkeys[i])
-          continue;
-        int64_t e = i + 1;
-        while (e < nt && tkeys[e] == tkeys[i]) e++;
-        // a group too large for the relabel table sends the run to the loop
-        const int32_t k = atomicAdd(&flags[1], e - i > kTieGroup ? kTieMax + 1 : 1);
-        if (k < kTieMax) list[k] = (int32_t)i;
-      }
-      grid.sync();
-      const int32_t ng = __ldcg(&flags[1]);
-      if (ng <= kTieMax) {
-        if (tid0 == 0)  // the groups in token order
-          for (int32_t a = 1; a < ng; a++)
-            for (int32_t b = a; b > 0 && list[b - 1] > list[b]; b--) {
-              const int32_t t = list[b];
-              list[b] = list[b - 1];
-              list[b - 1] = t;
-            }
-        grid.sync();
-        for (int32_t q = 0; q < ng; q++) {
-          if (tid0 == 0) {
-            const int64_t i = list[q];
-            const int s = (int)(tkeys[i] >> tb);
-            const int64_t base = sbase[s], ns = sbase[s + 1] - base;
-            const int32_t G = shards[s].G;
-            int64_t e = i + 1;
-            while (e < nt && tkeys[e] == tkeys[i]) e++;
-            int32_t og[kTieGroup];
-            for (int64_t a = i; a < e; a++) og[a - i] = -__ldcg(ptrA + base + tvals[a]) - 1;
-            for (int64_t a = i + 1; a < e; a++) {  // stable insertion sort by gid
-              const uint32_t v = tvals[a];
-              const int32_t gv = -__ldcg(ptrA + base + v) - 1;
-              int64_t b = a;
-              while (b > i && -__ldcg(ptrA + base + tvals[b - 1]) - 1 > gv) {
-                tvals[b] = tvals[b - 1];
-                b--;
-              }
-              tvals[b] = v;
-            }
-            int32_t cnt = 0;
-            for (int64_t a = i; a < e; a++) {
-              const int32_t n_g = -__ldcg(ptrA + base + tvals[a]) - 1;
-              const int64_t y = a + G;  // the batch popping this token
-              if (n_g != og[a - i] && y - base < ns) {
-                table[3 * cnt] = og[a - i];
-                table[3 * cnt + 1] = n_g;
-                table[3 * cnt + 2] = (int32_t)y;
-                cnt++;
-              }
-            }
-            flags[2] = cnt;
-            __threadfence();
-          }
-          grid.sync();
-          const int32_t cnt = __ldcg(&flags[2]);
-          for (int64_t i = tid0; cnt > 0 && i < nt; i += stride) {
-            const int32_t g = -__ldcg(ptrA + i) - 1;
-            for (int32_t k = 0; k < cnt; k++)
-              if (g == __ldcg(&table[3 * k]) && i >= __ldcg(&table[3 * k + 2])) {
-                ptrA[i] = -__ldcg(&table[3 * k + 1]) - 1;
-                break;
-              }
-          }
-          grid.sync();
-        }
-        break;  // matched (k_fast_emit still checks every tie's order)
-      }
-      // many tie groups: the general fixed-point iteration below
-    }
     if (tid0 == 0) flags[2 + ((it + 1) & 1)] = 0;
     bool moved = false;
     for (int64_t i = tid0; i < nt; i += stride) {  // equal-finish groups by gid
@@ -1954,6 +1848,17 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
   return SYM_OK;
 }
 
+int ensure_buckets(Ctx* ctx, int64_t nbk) {
+  if (nbk + 1 > ctx->bkt_cap) {
+    int rc;
+    if ((rc = grow(ctx, ctx->d_bkt, nbk + 1)) ||
+        (rc = grow(ctx, ctx->d_bkt_part, (nbk + 1) / kScanItems + 2)))
+      return rc;
+    ctx->bkt_cap = nbk + 1;
+  }
+  return SYM_OK;
+}
+
 // Opt-in host-side phase timing (SYM_DEBUG_TIMING=1): synchronises the
 // stream at each mark and prints the wall time since the previous mark.
 struct PhaseClock {
@@ -2281,35 +2186,38 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
           ctx->d_special, nt, ctx->d_evb, (unsigned long long*)ctx->d_mdrops, ctx->d_closek,
           ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits));
 
-      // key = (shard << tick_bits) | tick; only the bits in use are sorted
+      // key = (shard << tick_bits) | tick: bits in use
       int bits = tick_bits;
       while ((1 << (bits - tick_bits)) < P) bits++;
-      const int64_t Wr = (nt + kChunkR - 1) / kChunkR;
-      auto radix = [&](uint64_t*& ka, uint32_t*& va, uint64_t*& kb, uint32_t*& vb) {
-        for (int shift = 0; shift < bits; shift += kDigitBits) {
-          KL(k_rhist, nblk(Wr, kRadixWarps), 32 * kRadixWarps, 0, st>>>(ka, nt, shift,
-                                                                          ctx->d_rhist, Wr));
-          flat_scan(ctx->d_rhist, Wr * kDigits);
-          KL(k_rscatter, nblk(Wr, kRadixWarps), 32 * kRadixWarps, 0, st>>>(
-              ka, va, nt, shift, ctx->d_rhist, Wr, kb, vb));
-          std::swap(ka, kb);
-          std::swap(va, vb);
-        }
-      };
   pc.mark("batch_keys");
-      for (int round = 0; (int64_t(1) << round) < M; round++) {
-        KL(k_merge_round, nblk((nt + kMergeItems - 1) / kMergeItems, 256), 256, 0, st>>>(
-            ctx->d_bkA, ctx->d_bvA, ctx->d_bkB, ctx->d_bvB, nt, ctx->d_bbase, M, round,
-            ctx->d_evb));
-        std::swap(ctx->d_bkA, ctx->d_bkB);
-        std::swap(ctx->d_bvA, ctx->d_bvB);
-      }
+      // bucket sorts: ~1 key per bucket of 2^shift ns over the (shard|tick) range
+      int shift = 0;
+      while ((int64_t(1) << (bits - shift)) > 2 * nt && shift < bits) shift++;
+      const int64_t nbk = ((int64_t)P << tick_bits) >> shift;
+      if ((rc = ensure_buckets(ctx, nbk))) return rc;
+      auto bucket_sort = [&](uint64_t*& ka, uint32_t*& va, uint64_t*& kb, uint32_t*& vb,
+                             bool batches) {
+        CK(cudaMemsetAsync(ctx->d_bkt, 0, sizeof(int32_t) * (nbk + 1), st));
+        KL(k_bkt_count, nblk(nt, 256), 256, 0, st>>>(ka, nt, shift, ctx->d_bkt));
+        ::flat_scan(ctx, ctx->d_bkt, nbk, kt, launches, ctx->d_bkt_part);
+        KL(k_bkt_scatter, nblk(nt, 256), 256, 0, st>>>(ka, va, nt, shift, ctx->d_bkt, kb, vb));
+        if (batches)
+          KL(k_bkt_sort<true>, nblk(nbk, 256), 256, 0, st>>>(ctx->d_bkt, nbk, kb, vb,
+                                                             ctx->d_evb));
+        else
+          KL(k_bkt_sort<false>, nblk(nbk, 256), 256, 0, st>>>(ctx->d_bkt, nbk, kb, vb,
+                                                              ctx->d_evb));
+        std::swap(ka, kb);
+        std::swap(va, vb);
+        return SYM_OK;
+      };
+      if ((rc = bucket_sort(ctx->d_bkA, ctx->d_bvA, ctx->d_bkB, ctx->d_bvB, true))) return rc;
   pc.mark("sort_batches");
       KL(k_token_keys, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_bvA, nt, ctx->d_bkA, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
           ctx->d_fail, tick_bits));
   pc.mark("token_keys");
-      radix(ctx->d_tkA, ctx->d_tvA, ctx->d_tkB, ctx->d_tvB);
+      if ((rc = bucket_sort(ctx->d_tkA, ctx->d_tvA, ctx->d_tkB, ctx->d_tvB, false))) return rc;
   pc.mark("sort_tokens");
       {
         int bps = 0;
@@ -2913,7 +2821,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_sbase, P + 1);
   ALLOC(ctx->d_fail, P);
   ALLOC(ctx->d_skip, P);
-  ALLOC(ctx->d_changed, 4 + kTieMax + 3 * kTieGroup);
+  ALLOC(ctx->d_changed, 4);
   ALLOC(ctx->d_unsure_n, 1);
   ALLOC(ctx->d_special, M);
   ALLOC(ctx->d_slo_model, M);
@@ -3017,7 +2925,7 @@ void sym_destroy(void* engine) {
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,
                   ctx->d_inv, ctx->d_bid, ctx->d_scan_part, ctx->d_closek,
-                  ctx->d_bins,   ctx->d_err,   ctx->d_fresh, ctx->d_hist, ctx->d_hist_part, ctx->d_sh_i,
+                  ctx->d_bins,   ctx->d_err,   ctx->d_fresh, ctx->d_hist, ctx->d_hist_part, ctx->d_bkt, ctx->d_bkt_part, ctx->d_sh_i,
                   ctx->d_sh_slot, ctx->d_inv1,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
