@@ -87,6 +87,7 @@ struct Ctx {
   int32_t* d_hist = nullptr;        // [B][tiles] bin counts -> positions
   int32_t* d_hist_part = nullptr;   // block sums of its scan
   int32_t *d_bkt = nullptr, *d_bkt_part = nullptr;  // bucket sort counts / ends
+  int64_t* d_seg = nullptr;         // [4*(P+1)] segmented partition geometry
   int64_t bkt_cap = 0;
   int64_t hist_cap = 0;
   int32_t* d_err = nullptr;
@@ -286,36 +287,122 @@ constexpr int kTileWarps = 8;
 constexpr int kTilePerLane = 8;
 constexpr int kTileI = kTileWarps * 32 * kTilePerLane;  // 2048 arrivals per tile
 
+// Geometry of tile t.  Modes 0 and 1: tiles of the whole stream, global
+// bins, hist[bin][tile].  Mode 2 (segmented): the input is the sub-cluster
+// streams back to back, and tiles never straddle two of them: tile t of
+// sub-cluster s partitions its arrivals by the sub-cluster's own model slots
+// (local bins 0..B_s), and the histogram is stored sub-cluster by
+// sub-cluster, [local bin][tile] within each, so one flat scan still yields
+// global output positions.  seg: tile_base[P+1] | hist_base[P+1] |
+// shard_off[P+1] | slot_base[P+1].
+struct TileGeom {
+  int64_t lo, hi, hbase, hstride, col;
+  int32_t B, bin0;
+};
+
+template <int kMode>
+__device__ __forceinline__ bool tile_geom(int64_t t, int64_t n, int32_t B, int64_t W,
+                                          const int64_t* __restrict__ seg, int32_t P,
+                                          TileGeom& g) {
+  if (kMode != 2) {
+    g.lo = t * kTileI;
+    g.hi = g.lo + kTileI < n ? g.lo + kTileI : n;
+    g.B = B;
+    g.bin0 = 0;
+    g.hbase = 0;
+    g.hstride = W;
+    g.col = t;
+    return true;
+  }
+  const int64_t* tile_base = seg;
+  const int64_t* hist_base = seg + (P + 1);
+  const int64_t* shard_off = seg + 2 * (P + 1);
+  const int64_t* slot_base = seg + 3 * (P + 1);
+  if (t >= tile_base[P]) return false;
+  int s = 0;
+  while (tile_base[s + 1] <= t) s++;
+  const int64_t lt = t - tile_base[s];
+  g.lo = shard_off[s] + lt * kTileI;
+  g.hi = g.lo + kTileI < shard_off[s + 1] ? g.lo + kTileI : shard_off[s + 1];
+  g.B = (int32_t)(slot_base[s + 1] - slot_base[s]);
+  g.bin0 = (int32_t)slot_base[s];
+  g.hbase = hist_base[s];
+  g.hstride = tile_base[s + 1] - tile_base[s];
+  g.col = lt;
+  return true;
+}
+
+// mode 2's geometry from the level-1 sub-cluster offsets (one thread)
+__global__ void k_part_seg(const int32_t* __restrict__ shard_off,
+                           const int32_t* __restrict__ slot_base, int32_t P,
+                           int64_t* __restrict__ seg) {
+  if (threadIdx.x != 0) return;
+  int64_t tb = 0, hb = 0;
+  for (int s = 0; s <= P; s++) {
+    seg[s] = tb;
+    seg[(P + 1) + s] = hb;
+    seg[2 * (P + 1) + s] = shard_off[s];
+    seg[3 * (P + 1) + s] = slot_base[s];
+    if (s < P) {
+      const int64_t tiles = (shard_off[s + 1] - shard_off[s] + kTileI - 1) / kTileI;
+      tb += tiles;
+      hb += tiles * (slot_base[s + 1] - slot_base[s]);
+    }
+  }
+}
+
 template <int kMode>
 __global__ void __launch_bounds__(256)
 k_part_count(const int32_t* __restrict__ key, int64_t n, int32_t M,
              const int32_t* __restrict__ shard_of_model, int32_t B,
-             int32_t* __restrict__ hist, int64_t W, int32_t* __restrict__ err) {
+             int32_t* __restrict__ hist, int64_t W, const int64_t* __restrict__ seg,
+             int32_t P, int32_t* __restrict__ err) {
   extern __shared__ int32_t hcnt[];
-  for (int b = threadIdx.x; b < B; b += blockDim.x) hcnt[b] = 0;
+  TileGeom g;
+  if (!tile_geom<kMode>(blockIdx.x, n, B, W, seg, P, g)) return;
+  for (int b = threadIdx.x; b < g.B; b += blockDim.x) hcnt[b] = 0;
   __syncthreads();
-  const int64_t w = blockIdx.x;
-  const int64_t lo = w * kTileI, hi = lo + kTileI < n ? lo + kTileI : n;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+  for (int64_t i = g.lo + threadIdx.x; i < g.hi; i += blockDim.x) {
     const int32_t m = key[i];
     if (kMode != 2 && (m < 0 || m >= M)) {
       atomicMin(err, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
       continue;
     }
-    atomicAdd(&hcnt[kMode == 1 ? shard_of_model[m] : m], 1);
+    atomicAdd(&hcnt[kMode == 1 ? shard_of_model[m] : m - g.bin0], 1);
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < B; b += blockDim.x) hist[(int64_t)b * W + w] = hcnt[b];
+  for (int b = threadIdx.x; b < g.B; b += blockDim.x)
+    hist[g.hbase + (int64_t)b * g.hstride + g.col] = hcnt[b];
 }
 
-// ModelParam.off/cnt per slot (slots == 1: shard_off instead) from the
-// first column of the scanned bin-major histogram
+// ModelParam.off/cnt per slot (mp == null: shard_off instead) from the
+// first tile column of the scanned histogram
+template <int kMode>
 __global__ void k_part_binoff(const int32_t* __restrict__ hist, int64_t W, int32_t B, int64_t n,
+                              const int64_t* __restrict__ seg, int32_t P,
                               ModelParam* __restrict__ mp, int32_t* __restrict__ shard_off) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
-  const int32_t o = W > 0 ? hist[(int64_t)b * W] : 0;
-  const int32_t e = b + 1 < B ? (W > 0 ? hist[(int64_t)(b + 1) * W] : 0) : (int32_t)n;
+  int32_t o, e;
+  if (kMode != 2) {
+    o = W > 0 ? hist[(int64_t)b * W] : 0;
+    e = b + 1 < B ? (W > 0 ? hist[(int64_t)(b + 1) * W] : 0) : (int32_t)n;
+  } else {
+    const int64_t* tile_base = seg;
+    const int64_t* hist_base = seg + (P + 1);
+    const int64_t* soff = seg + 2 * (P + 1);
+    const int64_t* slot_base = seg + 3 * (P + 1);
+    int s = 0;
+    while (slot_base[s + 1] <= b) s++;
+    const int64_t lb = b - slot_base[s], tiles = tile_base[s + 1] - tile_base[s];
+    if (tiles == 0) {
+      o = e = (int32_t)soff[s];
+    } else {
+      o = hist[hist_base[s] + lb * tiles];
+      e = lb + 1 < slot_base[s + 1] - slot_base[s] ? hist[hist_base[s] + (lb + 1) * tiles]
+                                                     : (int32_t)soff[s + 1];
+    }
+  }
   if (mp) {
     mp[b].off = o;
     mp[b].cnt = e - o;
@@ -335,12 +422,16 @@ __global__ void __launch_bounds__(32 * kTileWarps, 5)
 k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
        const int32_t* __restrict__ aux_in, int64_t n, int32_t M,
        const int32_t* __restrict__ shard_of_model, const int32_t* __restrict__ slot_of_model,
-       int32_t B, const int32_t* __restrict__ hist, int64_t W,
+       int32_t Bmax, const int32_t* __restrict__ hist, int64_t W,
+       const int64_t* __restrict__ seg, int32_t P,
        int64_t* __restrict__ out_tick, int32_t* __restrict__ out_idx,
        int32_t* __restrict__ out_aux, int32_t* __restrict__ inv_out,
        int32_t* __restrict__ err) {
   constexpr bool kAux = kMode != 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileGeom geo;
+  if (!tile_geom<kMode>(blockIdx.x, n, Bmax, W, seg, P, geo)) return;
+  const int32_t B = geo.B;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t* st_t = reinterpret_cast<int64_t*>(smem_raw);
   int32_t* st_i = reinterpret_cast<int32_t*>(st_t + kTileI);
@@ -351,10 +442,10 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
   int32_t* scratch = lstart + B;               // [32] block scan
   int16_t* st_b = reinterpret_cast<int16_t*>(scratch + 32);
   int32_t* mine = wcnt + wib * B;
-  const int64_t w = blockIdx.x;
   for (int b = lane; b < B; b += 32) mine[b] = 0;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) gbase[b] = hist[(int64_t)b * W + w];
-  const int64_t lo = w * kTileI, hi = (lo + kTileI < n ? lo + kTileI : n);
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    gbase[b] = hist[geo.hbase + (int64_t)b * geo.hstride + geo.col];
+  const int64_t lo = geo.lo, hi = geo.hi;
   const int64_t wlo = lo + (int64_t)wib * 32 * kTilePerLane;
   __syncwarp();
   // pass 1: load this lane's elements once, count the warp's bins
@@ -372,7 +463,7 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
       if (kMode != 2 && i > 0 && tk[r] < tick_in[i - 1])  // arrivals must be time-ordered
         atomicMin(err + 1, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
       if (kMode == 2 || (m >= 0 && m < M)) {  // unknown ids were reported by k_part_count
-        bn[r] = kMode == 1 ? shard_of_model[m] : m;
+        bn[r] = kMode == 1 ? shard_of_model[m] : m - geo.bin0;
         if (kMode == 1) ax[r] = slot_of_model[m];
         if (kMode == 2) ax[r] = aux_in[i];
       }
@@ -484,7 +575,7 @@ __device__ __forceinline__ int32_t slot_of_position(const ModelParam* __restrict
   return lo;
 }
 
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256)
 k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
       const ModelParam* __restrict__ mp_all, int32_t P, int32_t M, int64_t n,
       int32_t* __restrict__ nxt, int32_t* __restrict__ close_k,
@@ -514,21 +605,7 @@ k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
         const int32_t kmax = cnt - 2 < q + mb - 2 ? cnt - 2 : q + mb - 2;
         const int64_t jend = off + (int64_t)kmax + 1;  // last candidate j
         if (j < p + 1) j = p + 1;
-        // four candidates per round, loaded together: the scan is bound by
-        // load latency, not by the few extra loads past the closing index
-        while (j <= jend) {
-          const int64_t base = T - c1 * (j - off);  // u_x >= T <=> tick_x >= base - c1 (x - j)
-          const int64_t t0 = __ldg(tick + j);
-          const int64_t t1 = j + 1 <= jend ? __ldg(tick + j + 1) : INT64_MAX;
-          const int64_t t2 = j + 2 <= jend ? __ldg(tick + j + 2) : INT64_MAX;
-          const int64_t t3 = j + 3 <= jend ? __ldg(tick + j + 3) : INT64_MAX;
-          if (t0 >= base) break;
-          if (t1 >= base - c1) { j += 1; break; }
-          if (t2 >= base - 2 * c1) { j += 2; break; }
-          if (t3 >= base - 3 * c1) { j += 3; break; }
-          j += 4;
-        }
-        if (j > jend + 1) j = jend + 1;
+        while (j <= jend && __ldg(tick + j) + c1 * (j - off) < T) j++;
         int32_t v;
         if (j <= jend) {  // closes at k = j - 1, if ok(len) holds there
           const int64_t kk = j - 1;
@@ -1979,30 +2056,45 @@ struct IngestInfo {
 // per-slot off/cnt into mp_out).  Validates model ids (EPROTO) and the
 // time order (EINVAL) on the device.
 // One stable partition (k_part_count, flat_scan, k_part_binoff, k_part).
+// Mode 2 partitions each sub-cluster stream by its own slots (tiles within
+// one sub-cluster, local bins: Bmax = the largest sub-cluster's model count).
 template <int kMode>
 int partition(Ctx* ctx, const int64_t* tick_in, const int32_t* key, const int32_t* aux_in,
               int64_t n, int32_t B, ModelParam* mp_out, int32_t* shard_off_out,
               int64_t* out_tick, int32_t* out_idx, int32_t* out_aux, int32_t* inv_out,
               KernelTimer& kt, int64_t& launches) {
   cudaStream_t st = ctx->stream;
+  const int32_t P = ctx->P;
   const int64_t W = (n + kTileI - 1) / kTileI;
-  if (W * B + 1 > ctx->hist_cap) {
+  int32_t Bmax = B;
+  int64_t grid = W, hlen = W * B;
+  int64_t* seg = ctx->d_seg;
+  if (kMode == 2) {
+    Bmax = 1;
+    for (int s = 0; s < P; s++) Bmax = std::max(Bmax, ctx->slot_base[s + 1] - ctx->slot_base[s]);
+    grid = W + P;              // >= sum over sub-clusters of their tiles
+    hlen = (int64_t)Bmax * (W + P);
+    KL(k_part_seg, 1, 32, 0, st>>>(ctx->d_bins + (ctx->M + P) + 1, ctx->d_slot_base, P, seg));
+  }
+  if (hlen + 1 > ctx->hist_cap) {
     int rc;
-    if ((rc = grow(ctx, ctx->d_hist, W * B + 1)) ||
-        (rc = grow(ctx, ctx->d_hist_part, (W * B + 1) / kScanItems + 2)))
+    if ((rc = grow(ctx, ctx->d_hist, hlen + 1)) ||
+        (rc = grow(ctx, ctx->d_hist_part, (hlen + 1) / kScanItems + 2)))
       return rc;
-    ctx->hist_cap = W * B + 1;
+    ctx->hist_cap = hlen + 1;
   }
   if (W > 0) {
-    KL(k_part_count<kMode>, W, 256, sizeof(int32_t) * B, st>>>(
-        key, n, ctx->M, ctx->d_shard_of_model, B, ctx->d_hist, W, ctx->d_err));
-    flat_scan(ctx, ctx->d_hist, W * B, kt, launches, ctx->d_hist_part);
+    if (kMode == 2) CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(int32_t) * hlen, st));
+    KL(k_part_count<kMode>, grid, 256, sizeof(int32_t) * Bmax, st>>>(
+        key, n, ctx->M, ctx->d_shard_of_model, B, ctx->d_hist, W, seg, P, ctx->d_err));
+    flat_scan(ctx, ctx->d_hist, hlen, kt, launches, ctx->d_hist_part);
   }
-  KL(k_part_binoff, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, n, mp_out, shard_off_out));
+  KL(k_part_binoff<kMode>, nblk(B, 128), 128, 0, st>>>(ctx->d_hist, W, B, n, seg, P, mp_out,
+                                                        shard_off_out));
   if (W > 0)
-    KL(k_part<kMode>, W, 32 * kTileWarps, part_smem(B), st>>>(
-        tick_in, key, aux_in, n, ctx->M, ctx->d_shard_of_model, ctx->d_slot_of_model, B,
-        ctx->d_hist, W, out_tick, out_idx, out_aux, inv_out, ctx->d_err));
+    KL(k_part<kMode>, grid, 32 * kTileWarps, part_smem(Bmax), st>>>(
+        tick_in, key, aux_in, n, ctx->M, ctx->d_shard_of_model, ctx->d_slot_of_model, Bmax,
+        ctx->d_hist, W, seg, P, out_tick, out_idx, out_aux, inv_out, ctx->d_err));
   CK(cudaGetLastError());
   return SYM_OK;
 }
@@ -2823,6 +2915,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_skip, P);
   ALLOC(ctx->d_changed, 4);
   ALLOC(ctx->d_unsure_n, 1);
+  ALLOC(ctx->d_seg, 4 * (P + 1));
   ALLOC(ctx->d_special, M);
   ALLOC(ctx->d_slo_model, M);
   ctx->net_ctrl_n = cfg->net_ctrl_n > 0 ? cfg->net_ctrl_n : 0;
@@ -2925,7 +3018,7 @@ void sym_destroy(void* engine) {
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,
                   ctx->d_inv, ctx->d_bid, ctx->d_scan_part, ctx->d_closek,
-                  ctx->d_bins,   ctx->d_err,   ctx->d_fresh, ctx->d_hist, ctx->d_hist_part, ctx->d_bkt, ctx->d_bkt_part, ctx->d_sh_i,
+                  ctx->d_bins,   ctx->d_err,   ctx->d_fresh, ctx->d_hist, ctx->d_hist_part, ctx->d_bkt, ctx->d_bkt_part, ctx->d_seg, ctx->d_sh_i,
                   ctx->d_sh_slot, ctx->d_inv1,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
