@@ -814,40 +814,80 @@ __global__ void k_bid(const BatchRec* __restrict__ recs, const int64_t* __restri
 // RunResult arrays (simulator.py:74-78, 159-173, 249-258) in stream order:
 // one thread per request, reads scattered, writes coalesced.  A request no
 // batch covers was dropped (every request resolves).
-__global__ void k_out(int64_t n, const int32_t* __restrict__ inv1,
-                      const int32_t* __restrict__ inv,
-                      const int32_t* __restrict__ bid, const BatchRec* __restrict__ recs,
-                      const int64_t* __restrict__ ticks, const int32_t* __restrict__ model,
-                      const int64_t* __restrict__ slo_by_model,
-                      int64_t* __restrict__ disp, int64_t* __restrict__ start,
-                      int64_t* __restrict__ fin, int64_t* __restrict__ bat,
-                      int64_t* __restrict__ outc, int64_t* __restrict__ o_arr,
-                      int64_t* __restrict__ o_dl, int64_t* __restrict__ o_model) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t tick = ticks[i];
-  const int32_t mi = model[i];
-  const int64_t dl = tick + slo_by_model[mi];
-  if (o_arr) o_arr[i] = tick;
-  if (o_dl) o_dl[i] = dl;
-  if (o_model) o_model[i] = mi;
-  // sorted position: inv[i] (one sub-cluster) or inv[inv1[i]] (several:
-  // stream -> sub-cluster stream -> layout)
-  const int32_t r = bid[inv[inv1 ? inv1[i] : (int32_t)i]];
+// Two requests per thread: the stream-order loads and the five output
+// stores are 16-byte vector accesses (the kernel is bound by the LSU queue
+// and by the gather chain inv -> bid -> record, whose loads for the two
+// requests are issued together).  Outputs must be 16-byte aligned (torch
+// and the pinned host pool allocate 256-byte aligned buffers); an odd n
+// leaves the last request to a scalar tail.
+struct OutRow {
+  int64_t disp, start, fin, bat, outc;
+};
+
+__device__ __forceinline__ OutRow out_row(int32_t r, const BatchRec* __restrict__ recs,
+                                          int64_t dl) {
+  OutRow o;
   if (r < 0) {
-    disp[i] = -1;
-    start[i] = -1;
-    fin[i] = -1;
-    bat[i] = -1;
-    outc[i] = 2;  // OUTCOME_DROPPED
-    return;
+    o.disp = o.start = o.fin = o.bat = -1;
+    o.outc = 2;  // OUTCOME_DROPPED
+    return o;
   }
   const BatchRec& b = recs[r];
-  disp[i] = b.emitted;
-  start[i] = b.start;
-  fin[i] = b.finish;
-  bat[i] = b.size;
-  outc[i] = b.finish <= dl ? 0 : 1;
+  o.disp = b.emitted;
+  o.start = b.start;
+  o.fin = b.finish;
+  o.bat = b.size;
+  o.outc = b.finish <= dl ? 0 : 1;
+  return o;
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(256)
+k_out(int64_t n, const int32_t* __restrict__ inv1, const int32_t* __restrict__ inv,
+      const int32_t* __restrict__ bid, const BatchRec* __restrict__ recs,
+      const int64_t* __restrict__ ticks, const int32_t* __restrict__ model,
+      const int64_t* __restrict__ slo_by_model,
+      int64_t* __restrict__ disp, int64_t* __restrict__ start,
+      int64_t* __restrict__ fin, int64_t* __restrict__ bat,
+      int64_t* __restrict__ outc, int64_t* __restrict__ o_arr,
+      int64_t* __restrict__ o_dl, int64_t* __restrict__ o_model) {
+  const int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (i >= n) return;
+  if (!kVec || i + 1 >= n) {  // scalar: unaligned caller buffers, or the tail
+    for (int64_t k = i; k < i + 2 && k < n; k++) {
+      const int64_t tick = ticks[k];
+      const int32_t mi = model[k];
+      const int64_t dl = tick + slo_by_model[mi];
+      if (o_arr) o_arr[k] = tick;
+      if (o_dl) o_dl[k] = dl;
+      if (o_model) o_model[k] = mi;
+      const OutRow o = out_row(bid[inv[inv1 ? inv1[k] : (int32_t)k]], recs, dl);
+      disp[k] = o.disp;
+      start[k] = o.start;
+      fin[k] = o.fin;
+      bat[k] = o.bat;
+      outc[k] = o.outc;
+    }
+    return;
+  }
+  const longlong2 t2 = *reinterpret_cast<const longlong2*>(ticks + i);
+  const int2 m2 = *reinterpret_cast<const int2*>(model + i);
+  // sorted position: inv[i] (one sub-cluster) or inv[inv1[i]] (several:
+  // stream -> sub-cluster stream -> layout)
+  int2 j2 = make_int2((int32_t)i, (int32_t)i + 1);
+  if (inv1) j2 = *reinterpret_cast<const int2*>(inv1 + i);
+  const int32_t p0 = inv[j2.x], p1 = inv[j2.y];
+  const int32_t r0 = bid[p0], r1 = bid[p1];
+  const int64_t dl0 = t2.x + slo_by_model[m2.x], dl1 = t2.y + slo_by_model[m2.y];
+  const OutRow a = out_row(r0, recs, dl0), b = out_row(r1, recs, dl1);
+  if (o_arr) *reinterpret_cast<longlong2*>(o_arr + i) = t2;
+  if (o_dl) *reinterpret_cast<longlong2*>(o_dl + i) = make_longlong2(dl0, dl1);
+  if (o_model) *reinterpret_cast<longlong2*>(o_model + i) = make_longlong2(m2.x, m2.y);
+  *reinterpret_cast<longlong2*>(disp + i) = make_longlong2(a.disp, b.disp);
+  *reinterpret_cast<longlong2*>(start + i) = make_longlong2(a.start, b.start);
+  *reinterpret_cast<longlong2*>(fin + i) = make_longlong2(a.fin, b.fin);
+  *reinterpret_cast<longlong2*>(bat + i) = make_longlong2(a.bat, b.bat);
+  *reinterpret_cast<longlong2*>(outc + i) = make_longlong2(a.outc, b.outc);
 }
 
 __global__ void k_drop_out(int64_t n, const int32_t* __restrict__ s_i,
@@ -2450,12 +2490,21 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     if (total > 0)
       KL(k_bid, nblk(total, 256), 256, 0, st>>>(ctx->d_recs, d_meta, d_meta + P + 1, P, total,
                                                 ctx->d_bid));
-    KL(k_out, nblk(n, 256), 256, 0, st>>>(n, P > 1 ? ctx->d_inv1 : nullptr, ctx->d_inv,
-                                          ctx->d_bid, ctx->d_recs, d_ticks,
-                                          d_model, ctx->d_slo_model, out->req_dispatch,
-                                          out->req_start, out->req_finish, out->req_batch,
-                                          out->req_outcome, out->req_arrival, out->req_deadline,
-                                          out->req_model));
+    auto al16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
+    const bool vec = al16(d_ticks) && ((uintptr_t)d_model & 7u) == 0 &&
+                     al16(out->req_dispatch) && al16(out->req_start) &&
+                     al16(out->req_finish) && al16(out->req_batch) && al16(out->req_outcome) &&
+                     al16(out->req_arrival) && al16(out->req_deadline) && al16(out->req_model);
+    if (vec)
+      KL(k_out<true>, nblk((n + 1) / 2, 256), 256, 0, st>>>(
+          n, P > 1 ? ctx->d_inv1 : nullptr, ctx->d_inv, ctx->d_bid, ctx->d_recs, d_ticks,
+          d_model, ctx->d_slo_model, out->req_dispatch, out->req_start, out->req_finish,
+          out->req_batch, out->req_outcome, out->req_arrival, out->req_deadline, out->req_model));
+    else
+      KL(k_out<false>, nblk((n + 1) / 2, 256), 256, 0, st>>>(
+          n, P > 1 ? ctx->d_inv1 : nullptr, ctx->d_inv, ctx->d_bid, ctx->d_recs, d_ticks,
+          d_model, ctx->d_slo_model, out->req_dispatch, out->req_start, out->req_finish,
+          out->req_batch, out->req_outcome, out->req_arrival, out->req_deadline, out->req_model));
   }
   if (trace && out->drop_t && n > 0)
     KL(k_drop_out, nblk(n, 256), 256, 0, st>>>(
@@ -3096,10 +3145,11 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const void* arr_model,
   const bool want_req = out->req_dispatch && !(flags & SYM_FLAG_NO_EXPAND);
   const bool want_drop = (flags & SYM_FLAG_TRACE) && out->drop_t;
   if (n + 1 > ctx->stage_cap) {
-    if ((rc = grow(ctx, ctx->d_req, 8 * (n + 1))) || (rc = grow(ctx, ctx->d_drop, 2 * (n + 1))) ||
-        (rc = grow(ctx, ctx->d_dka, n + 1)))
+    const int64_t c = (n + 32) & ~int64_t(31);  // every staged array 256-byte aligned
+    if ((rc = grow(ctx, ctx->d_req, 8 * c)) || (rc = grow(ctx, ctx->d_drop, 2 * c)) ||
+        (rc = grow(ctx, ctx->d_dka, c)))
       return rc;
-    ctx->stage_cap = n + 1;
+    ctx->stage_cap = c;
   }
   if (out->batches && out->batch_cap + 1 > ctx->bat_cap) {
     if ((rc = grow(ctx, ctx->d_bat, out->batch_cap + 1))) return rc;
