@@ -66,12 +66,10 @@ def design_bytes(kernel: str, n: int, nb: int, shards: int) -> float | None:
         "k_fresh": n * (8 + 4 + 4 + FRESH_REC_BYTES + 4),
         "k_nxt_general": 0,
         "k_chain_recs": n * (8 + 4 + 4) + nb * (4 + EV_BATCH_BYTES + 8 + 4),
+        "k_walk_expand": nb * (4 + EV_BATCH_BYTES),
         "k_token_keys": nb * (4 + 8 + EV_BATCH_BYTES + 8 + 4),
         "k_jump4": n * (4 + 4),
-        "k_merge_round": nb * (12 + 12),
-        "k_walk_expand": nb * (4 + EV_BATCH_BYTES),
-        "k_rscatter": nb * (12 + 12),
-        "k_rhist": nb * 8,
+        "k_bkt_scatter": nb * (12 + 12),
         "k_fast_emit": nb * (EV_BATCH_BYTES + 12 + 4 + 8 + BATCH_REC_BYTES),
         "k_bid": nb * BATCH_REC_BYTES + n * 4,
         "k_out": n * (4 + 4 + 8 + 4 + 5 * 8) + nb * BATCH_REC_BYTES,
@@ -490,8 +488,10 @@ def main():
             run_reference(args, world)
         return
     if world > 1:
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         print(f"[rank {rank}] NCCL communicator size {dist.get_world_size()}", file=sys.stderr)
     try:
         run_b200(args, rank, world, local_rank)

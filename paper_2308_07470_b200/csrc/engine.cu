@@ -72,6 +72,7 @@ struct Ctx {
   ModelState* d_ms = nullptr;
   int32_t *d_pq = nullptr, *d_gt = nullptr, *d_mlt = nullptr,
           *d_mbt = nullptr, *d_mcs = nullptr, *d_dirty = nullptr;
+  int64_t *d_pqt = nullptr, *d_gtf = nullptr, *d_mltv = nullptr, *d_mbtv = nullptr;
   int64_t *d_free = nullptr, *d_mcl = nullptr;
   Shard* d_shards = nullptr;
   std::vector<Shard> shards;        // host images
@@ -691,11 +692,12 @@ k_fresh(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
 struct SmemPlan {
   static SYM_HD size_t al(size_t x) { return (x + 15) & ~size_t(15); }
   static SYM_HD size_t need(const Shard& S) {
-    return al(sizeof(int32_t) * 2 * S.Gp) + al(sizeof(int64_t) * S.G) +
-           al(sizeof(int32_t) * 2 * S.Mp) + al(sizeof(ModelState) * S.M) +
+    return al(sizeof(int32_t) * 2 * S.Gp) + al(sizeof(int64_t) * 2 * S.Gp) +
+           al(sizeof(int64_t) * S.G) + al(sizeof(int32_t) * 2 * S.Mp) +
+           al(sizeof(int64_t) * 2 * S.Mp) + al(sizeof(ModelState) * S.M) +
            al(sizeof(ModelParam) * S.M) + 2 * al(sizeof(int32_t) * 2 * S.Mp) +
-           al(sizeof(int32_t) * S.M) + al(sizeof(int64_t) * S.M) +
-           al(sizeof(int64_t) * S.M * S.lat_stride);
+           2 * al(sizeof(int64_t) * 2 * S.Mp) + al(sizeof(int32_t) * S.M) +
+           al(sizeof(int64_t) * S.M) + al(sizeof(int64_t) * S.M * S.lat_stride);
   }
 };
 
@@ -730,14 +732,18 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
   };
   // state arrays placed on chip, with their sizes for the write-back
   const bool gt_s = place(S.gt, sizeof(int32_t) * 2 * S.Gp, load);
+  const bool gf_s = place(S.gt_f, sizeof(int64_t) * 2 * S.Gp, load);
   const bool fa_s = place(S.free_at, sizeof(int64_t) * S.G, load);
   const bool pq_s = place(S.pq, sizeof(int32_t) * 2 * S.Mp, load);
+  const bool pt_s = place(S.pq_t, sizeof(int64_t) * 2 * S.Mp, load);
   const bool ms_in_smem = place(S.ms, sizeof(ModelState) * S.M, load);
   const ModelParam* mp = S.mp;
   ModelParam* mp_s = const_cast<ModelParam*>(mp);
   if (place(mp_s, sizeof(ModelParam) * S.M, true)) S.mp = mp_s;
   const bool ml_s = place(S.mc_lat_tree, sizeof(int32_t) * 2 * S.Mp, load);
   const bool mb_s = place(S.mc_bs_tree, sizeof(int32_t) * 2 * S.Mp, load);
+  const bool mlv_s = place(S.mlt_v, sizeof(int64_t) * 2 * S.Mp, load);
+  const bool mbv_s = place(S.mbt_v, sizeof(int64_t) * 2 * S.Mp, load);
   const bool mz_s = place(S.mc_size, sizeof(int32_t) * S.M, load);
   const bool mt_s = place(S.mc_latest, sizeof(int64_t) * S.M, load);
   {  // latency rows last: small model sets keep every l(b) probe on chip
@@ -764,10 +770,14 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
   if (ms_in_smem) back(orig.ms, S.ms, S.M);
   if (keep) {  // a stepped run carries every structure to the next step
     if (gt_s) back(orig.gt, S.gt, 2 * (size_t)S.Gp);
+    if (gf_s) back(orig.gt_f, S.gt_f, 2 * (size_t)S.Gp);
     if (fa_s) back(orig.free_at, S.free_at, S.G);
     if (pq_s) back(orig.pq, S.pq, 2 * (size_t)S.Mp);
+    if (pt_s) back(orig.pq_t, S.pq_t, 2 * (size_t)S.Mp);
     if (ml_s) back(orig.mc_lat_tree, S.mc_lat_tree, 2 * (size_t)S.Mp);
     if (mb_s) back(orig.mc_bs_tree, S.mc_bs_tree, 2 * (size_t)S.Mp);
+    if (mlv_s) back(orig.mlt_v, S.mlt_v, 2 * (size_t)S.Mp);
+    if (mbv_s) back(orig.mbt_v, S.mbt_v, 2 * (size_t)S.Mp);
     if (mz_s) back(orig.mc_size, S.mc_size, S.M);
     if (mt_s) back(orig.mc_latest, S.mc_latest, S.M);
   }
@@ -775,10 +785,14 @@ k_chain(Shard* shards, const FreshRec* __restrict__ fresh,
   S.mp = orig.mp;
   S.lat = orig.lat;
   S.gt = orig.gt;
+  S.gt_f = orig.gt_f;
   S.free_at = orig.free_at;
   S.pq = orig.pq;
+  S.pq_t = orig.pq_t;
   S.mc_lat_tree = orig.mc_lat_tree;
   S.mc_bs_tree = orig.mc_bs_tree;
+  S.mlt_v = orig.mlt_v;
+  S.mbt_v = orig.mbt_v;
   S.mc_size = orig.mc_size;
   S.mc_latest = orig.mc_latest;
   shards[blockIdx.x] = S;
@@ -2947,6 +2961,10 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_mlt, tot_m2);
   ALLOC(ctx->d_mbt, tot_m2);
   ALLOC(ctx->d_gt, tot_g2);
+  ALLOC(ctx->d_pqt, tot_m2);
+  ALLOC(ctx->d_gtf, tot_g2);
+  ALLOC(ctx->d_mltv, tot_m2);
+  ALLOC(ctx->d_mbtv, tot_m2);
   ALLOC(ctx->d_mcs, M);
   ALLOC(ctx->d_mcl, M);
   ALLOC(ctx->d_free, ctx->G);
@@ -3020,9 +3038,13 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     S.mp = ctx->d_mp + ctx->slot_base[s];
     S.ms = ctx->d_ms + ctx->slot_base[s];
     S.pq = ctx->d_pq + om;
+    S.pq_t = ctx->d_pqt + om;
     S.mc_lat_tree = ctx->d_mlt + om;
     S.mc_bs_tree = ctx->d_mbt + om;
+    S.mlt_v = ctx->d_mltv + om;
+    S.mbt_v = ctx->d_mbtv + om;
     S.gt = ctx->d_gt + og;
+    S.gt_f = ctx->d_gtf + og;
     S.mc_size = ctx->d_mcs + ctx->slot_base[s];
     S.mc_latest = ctx->d_mcl + ctx->slot_base[s];
     S.free_at = ctx->d_free + ctx->gpu_base[s];
@@ -3064,6 +3086,7 @@ void sym_destroy(void* engine) {
                   ctx->d_shard_of_model, ctx->d_slot_base, ctx->d_ms,
                   ctx->d_pq,   ctx->d_gt,     ctx->d_mlt,   ctx->d_mbt,
                   ctx->d_mcs,  ctx->d_dirty,  ctx->d_free,  ctx->d_mcl,
+                  ctx->d_pqt, ctx->d_gtf, ctx->d_mltv, ctx->d_mbtv,
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,
                   ctx->d_inv, ctx->d_bid, ctx->d_scan_part, ctx->d_closek,

@@ -177,6 +177,13 @@ struct Shard {
   // mutable
   ModelState* ms;              // [M]
   int32_t* pq;                 // [2*Mp] tournament tree of models (next event)
+  // the winners' keys held inline beside every tree node (INT64_MAX / -1 =
+  // none), so a climb compares its sibling's key without first loading the
+  // sibling's id and then its key: one shared-memory round trip per level
+  int64_t* pq_t;               // [2*Mp] winner's next-event tick
+  int64_t* gt_f;               // [2*Gp] winner's free_at
+  int64_t* mlt_v;              // [2*Mp] winner's registered latest
+  int64_t* mbt_v;              // [2*Mp] winner's registered size
   int64_t* free_at;            // [G]
   int32_t* gt;                 // [2*Gp] tournament tree, min (free_at, gid)
   int32_t* mc_lat_tree;        // [2*Mp] min (latest, mid) over registered
@@ -246,18 +253,18 @@ SYM_HD void gpu_tree_update(Shard& S, int32_t gid) {
   int32_t node = S.Gp + gid;
   const int64_t f = S.free_at[gid];
   int32_t cur = f == OUTSTANDING ? -1 : gid;
-  int64_t ck = f;
+  int64_t ck = f == OUTSTANDING ? INT64_MAX : f;
   S.gt[node] = cur;
+  S.gt_f[node] = ck;
   for (; node > 1; node >>= 1) {
     const int32_t o = S.gt[node ^ 1];
-    if (o >= 0) {
-      const int64_t ok = S.free_at[o];
-      if (cur < 0 || ok < ck || (ok == ck && o < cur)) {
-        cur = o;
-        ck = ok;
-      }
+    const int64_t ok = S.gt_f[node ^ 1];
+    if (o >= 0 && (cur < 0 || ok < ck || (ok == ck && o < cur))) {
+      cur = o;
+      ck = ok;
     }
     S.gt[node >> 1] = cur;
+    S.gt_f[node >> 1] = ck;
   }
 }
 
@@ -280,15 +287,30 @@ SYM_HD bool bs_before(const Shard& S, int32_t x, int32_t y) {
 
 SYM_HD void mc_tree_update(Shard& S, int32_t mid) {
   int32_t i = S.Mp + mid;
-  int32_t v = S.ms[mid].registered ? mid : -1;
-  S.mc_lat_tree[i] = v;
-  S.mc_bs_tree[i] = v;
-  for (i >>= 1; i >= 1; i >>= 1) {
-    int32_t l = S.mc_lat_tree[2 * i], r = S.mc_lat_tree[2 * i + 1];
-    S.mc_lat_tree[i] = lat_before(S, r, l) ? r : l;
-    l = S.mc_bs_tree[2 * i];
-    r = S.mc_bs_tree[2 * i + 1];
-    S.mc_bs_tree[i] = bs_before(S, r, l) ? r : l;
+  const bool reg = S.ms[mid].registered;
+  int32_t lw = reg ? mid : -1, bw = lw;
+  int64_t lv = reg ? S.mc_latest[mid] : INT64_MAX, bv = reg ? S.mc_size[mid] : -1;
+  S.mc_lat_tree[i] = lw;
+  S.mlt_v[i] = lv;
+  S.mc_bs_tree[i] = bw;
+  S.mbt_v[i] = bv;
+  for (; i > 1; i >>= 1) {
+    const int32_t sib = i ^ 1;
+    const int32_t lo = S.mc_lat_tree[sib], bo = S.mc_bs_tree[sib];
+    const int64_t lov = S.mlt_v[sib], bov = S.mbt_v[sib];
+    // min (latest, mid) and max (size, mid): ids break ties (lat_before / bs_before)
+    if (lo >= 0 && (lw < 0 || lov < lv || (lov == lv && lo < lw))) {
+      lw = lo;
+      lv = lov;
+    }
+    if (bo >= 0 && (bw < 0 || bov > bv || (bov == bv && bo > bw))) {
+      bw = bo;
+      bv = bov;
+    }
+    S.mc_lat_tree[i >> 1] = lw;
+    S.mlt_v[i >> 1] = lv;
+    S.mc_bs_tree[i >> 1] = bw;
+    S.mbt_v[i >> 1] = bv;
   }
 }
 
@@ -303,19 +325,31 @@ SYM_HD bool model_before(const Shard& S, int32_t x, int32_t y) {
 SYM_HD void pq_update(Shard& S, int32_t mid) {
   int32_t node = S.Mp + mid;
   int32_t cur = S.ms[mid].nx_type != EV_NONE ? mid : -1;
-  int64_t ck = S.ms[mid].nx_key.t;
+  int64_t ck = cur >= 0 ? S.ms[mid].nx_key.t : INT64_MAX;
   S.pq[node] = cur;
+  S.pq_t[node] = ck;
   for (; node > 1; node >>= 1) {
     const int32_t o = S.pq[node ^ 1];
-    // leaves of models without a next event are -1, so o >= 0 has one
-    if (o >= 0) {
-      const int64_t ot = S.ms[o].nx_key.t;
-      if (cur < 0 || ot < ck || (ot == ck && key_less(S.ms[o].nx_key, S.ms[cur].nx_key))) {
-        cur = o;
-        ck = ot;
-      }
+    const int64_t ot = S.pq_t[node ^ 1];
+    // leaves of models without a next event are -1, so o >= 0 has one;
+    // equal ticks (rare) fall back to the full key
+    if (o >= 0 &&
+        (cur < 0 || ot < ck || (ot == ck && key_less(S.ms[o].nx_key, S.ms[cur].nx_key)))) {
+      cur = o;
+      ck = ot;
     }
     S.pq[node >> 1] = cur;
+    S.pq_t[node >> 1] = ck;
+  }
+}
+
+// (Re)build a tree's internal nodes from its leaves.
+SYM_HD void pq_build(Shard& S) {
+  for (int32_t i = S.Mp - 1; i >= 1; i--) {
+    const int32_t l = S.pq[2 * i], r = S.pq[2 * i + 1];
+    const bool right = model_before(S, r, l);
+    S.pq[i] = right ? r : l;
+    S.pq_t[i] = right ? S.pq_t[2 * i + 1] : S.pq_t[2 * i];
   }
 }
 
@@ -1066,16 +1100,27 @@ SYM_HD bool chain_step(Shard& S, int32_t* dirty, const FreshRec* fresh,
 // Initialise trees and bring every model to its first chain event.
 SYM_HD void chain_init(Shard& S, const FreshRec* fresh) {
   for (int32_t g = 0; g < S.G; g++) S.free_at[g] = 0;
-  for (int32_t i = 0; i < 2 * S.Gp; i++) S.gt[i] = -1;
-  for (int32_t g = 0; g < S.G; g++) S.gt[S.Gp + g] = g;
+  for (int32_t i = 0; i < 2 * S.Gp; i++) {
+    S.gt[i] = -1;
+    S.gt_f[i] = INT64_MAX;
+  }
+  for (int32_t g = 0; g < S.G; g++) {
+    S.gt[S.Gp + g] = g;
+    S.gt_f[S.Gp + g] = 0;
+  }
   for (int32_t i = S.Gp - 1; i >= 1; i--) {
-    int32_t l = S.gt[2 * i], r = S.gt[2 * i + 1];
-    S.gt[i] = gpu_before(S, r, l) ? r : l;
+    const int32_t l = S.gt[2 * i], r = S.gt[2 * i + 1];
+    const bool right = gpu_before(S, r, l);
+    S.gt[i] = right ? r : l;
+    S.gt_f[i] = right ? S.gt_f[2 * i + 1] : S.gt_f[2 * i];
   }
   for (int32_t i = 0; i < 2 * S.Mp; i++) {
     S.pq[i] = -1;
+    S.pq_t[i] = INT64_MAX;
     S.mc_lat_tree[i] = -1;
     S.mc_bs_tree[i] = -1;
+    S.mlt_v[i] = INT64_MAX;
+    S.mbt_v[i] = -1;
   }
   S.gt_armed = 0;
   S.n_recs = 0;
@@ -1090,12 +1135,11 @@ SYM_HD void chain_init(Shard& S, const FreshRec* fresh) {
     S.mc_size[m] = 0;
     S.mc_latest[m] = 0;
     refresh_model(S, m, fresh);
-    S.pq[S.Mp + m] = S.ms[m].nx_type != EV_NONE ? m : -1;
+    const bool act = S.ms[m].nx_type != EV_NONE;
+    S.pq[S.Mp + m] = act ? m : -1;
+    S.pq_t[S.Mp + m] = act ? S.ms[m].nx_key.t : INT64_MAX;
   }
-  for (int32_t i = S.Mp - 1; i >= 1; i--) {
-    int32_t l = S.pq[2 * i], r = S.pq[2 * i + 1];
-    S.pq[i] = model_before(S, r, l) ? r : l;
-  }
+  pq_build(S);
 }
 
 // Resume a stepped run: the state of every model, the trees and the GPU
@@ -1109,12 +1153,11 @@ SYM_HD void chain_resume(Shard& S) {
   S.error = ERR_NONE;
   for (int32_t m = 0; m < S.M; m++) {
     S.absorbed += scan_model(S, m, S.ms[m], -1);
-    S.pq[S.Mp + m] = S.ms[m].nx_type != EV_NONE ? m : -1;
+    const bool act = S.ms[m].nx_type != EV_NONE;
+    S.pq[S.Mp + m] = act ? m : -1;
+    S.pq_t[S.Mp + m] = act ? S.ms[m].nx_key.t : INT64_MAX;
   }
-  for (int32_t i = S.Mp - 1; i >= 1; i--) {
-    int32_t l = S.pq[2 * i], r = S.pq[2 * i + 1];
-    S.pq[i] = model_before(S, r, l) ? r : l;
-  }
+  pq_build(S);
 }
 
 SYM_HD int64_t total_drops(const Shard& S) {

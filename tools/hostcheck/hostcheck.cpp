@@ -40,7 +40,7 @@ extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64
   int32_t Gp = 1; while (Gp < G) Gp <<= 1;
   std::vector<ModelState> ms(M);
   std::vector<int32_t> pq(2 * Mp), gt(2 * Gp), mlt(2 * Mp), mbt(2 * Mp), mcs(M);
-  std::vector<int64_t> fa(G), mcl(M);
+  std::vector<int64_t> fa(G), mcl(M), pqt(2 * Mp), gtf(2 * Gp), mltv(2 * Mp), mbtv(2 * Mp);
   std::vector<BatchRec> recs(n + 1);
   std::vector<int64_t> dt(n, -1), dks(n); std::vector<int32_t> dka(n);
   Shard S; memset(&S, 0, sizeof S);
@@ -50,6 +50,8 @@ extern "C" int32_t hc_run(int32_t use_fresh, const symo_config* cfg, const int64
   S.s_tick = s_tick.data(); S.s_g = s_g.data(); S.sh_tick = ticks; S.sh_base = 0;
   S.ms = ms.data(); S.pq = pq.data(); S.free_at = fa.data(); S.gt = gt.data();
   S.mc_lat_tree = mlt.data(); S.mc_bs_tree = mbt.data(); S.mc_size = mcs.data(); S.mc_latest = mcl.data();
+  S.pq_t = pqt.data(); S.gt_f = gtf.data(); S.mlt_v = mltv.data(); S.mbt_v = mbtv.data();
+  S.check = 1; S.inject = -1;  // verify_state after every event
   S.recs = recs.data(); S.rec_cap = n + 1; S.drop_t = dt.data(); S.drop_ksub = dks.data(); S.drop_ka = dka.data();
   S.record_trace = use_fresh ? 0 : 1;
   std::vector<FreshRec> fresh;
