@@ -170,3 +170,25 @@ def test_step_errors():
     res = eng.step_result(1.0)
     assert res.n_requests == 3 and set(res.req_outcome.tolist()) <= {0, 2}
     eng.close()
+
+
+def test_slo_beyond_32_bits():
+    """SLOs beyond 2^32 ns (4.3 s) keep every tick int64 end to end (finish -
+    arrival above 2^32): same results as the oracle."""
+    from paper_2308_07470_b200 import Engine, PolicyConfig
+    from paper_2308_07470_b200.profile import LatencyProfile, ModelSpec
+    from paper_2308_07470_b200.workload import WorkloadSpec, generate_arrivals
+    for slo_ms in (50.0, 9000.0):
+        models = [ModelSpec(i, f"m{i}", LatencyProfile.linear(1.0 + i, 5.0, 32),
+                            int(slo_ms * 1e6)) for i in range(3)]
+        ticks, midx = generate_arrivals(WorkloadSpec("poisson", 3000.0),
+                                        [m.name for m in models], 20.0, 3)
+        ref = oracle.run(arr_ticks=ticks, arr_midx=midx,
+                         **oracle_args(models, 4, PolicyConfig("deferred")))
+        eng = Engine(models, 4, PolicyConfig("deferred"))
+        res = eng.run_stream(ticks, midx, 20.0)
+        for k in ("req_dispatch", "req_start", "req_finish", "req_batch", "req_outcome"):
+            np.testing.assert_array_equal(getattr(res, k), ref[k], err_msg=f"{slo_ms} {k}")
+        if slo_ms > 5000:
+            assert int((res.req_finish - res.req_arrival).max()) > (1 << 32)
+        eng.close()

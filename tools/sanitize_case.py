@@ -35,6 +35,7 @@ for c in list(cases.bundled()) + list(cases.stress(20)):
     eng = Engine(models, gpus, policy)
     half = len(ticks) // 2
     eng.step(ticks[:half], midx[:half], int(ticks[half]) if half < len(ticks) else eng.DRAIN)
+    eng.step(ticks[half:], midx[half:], eng.DRAIN)
     res = eng.step_result(dur)
     assert np.array_equal(res.req_outcome, ref["req_outcome"]), (key, "step")
     eng.close()
