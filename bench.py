@@ -240,6 +240,43 @@ def base_config(args, world):
 
 
 REF_BUDGET_S = 150.0
+PYREF_DIR = os.path.join(ROOT, "baseline", "_ref")
+PYREF_SECONDS = 2.0
+
+
+def python_reference_sample():
+    """The unmodified Python reference (batchsym, pip-installed into
+    baseline/_ref from the reference package) timed on one host
+    core: its Engine.run_stream over the first PYREF_SECONDS of C4
+    sub-cluster 0, its result checked against the oracle's.  None when the
+    install is absent."""
+    if not os.path.isdir(os.path.join(PYREF_DIR, "batchsym")):
+        return None
+    sys.path.insert(0, PYREF_DIR)
+    try:
+        import batchsym.profile as RP
+        import batchsym.scheduler as RS
+        from batchsym.simulator import Engine as REngine
+    finally:
+        sys.path.remove(PYREF_DIR)
+    sc, _, _, _, ticks, midx, per = build_workload(PYREF_SECONDS, [0])
+    ms, g, idx, base = per[0]
+    t, m = ticks[idx], midx[idx] - base
+    rmodels = [RP.ModelSpec(x.model_id, x.name,
+                            RP.LatencyProfile(x.profile.kind, x.profile.max_batch,
+                                              x.profile.alpha_ns, x.profile.beta_ns,
+                                              x.profile.lat_ns), x.slo_ns) for x in ms]
+    eng = REngine(rmodels, g, RS.PolicyConfig(sc.policy.kind))
+    t0 = time.perf_counter()
+    res = eng.run_stream(t, m, PYREF_SECONDS)
+    el = time.perf_counter() - t0
+    ref = oracle_shard_run(ms, g, sc.policy, t, m)
+    same = all(np.array_equal(np.asarray(getattr(res, "req_" + k)), ref["req_" + k])
+               for k in ("dispatch", "start", "finish", "batch", "outcome"))
+    return {"value": len(t) / el, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"batchsym Engine.run_stream (baseline/_ref), C4 sub-cluster 0, first "
+                      f"{PYREF_SECONDS:g} s of the trace ({len(t)} requests)",
+            "equals_oracle": bool(same)}
 
 
 def run_reference(args, world):
@@ -273,6 +310,12 @@ def run_reference(args, world):
                                    "loop), one host thread per sub-cluster"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        py = python_reference_sample()
+    except Exception as exc:  # the reported arm stays the C port
+        py = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+    if py is not None:
+        line["python_reference"] = py
     print(json.dumps(line), flush=True)
 
 

@@ -33,7 +33,9 @@ enum {
                          scheduler.py:70-82) */
   SYM_EINVARIANT = 3, /* InvariantViolation (simulator.py:90-91) */
   SYM_ECUDA = 4,      /* CUDA runtime failure -> RuntimeError */
-  SYM_ENOMEM = 5
+  SYM_ENOMEM = 5,
+  SYM_EGUARD = 6      /* guard mode (SYM_GUARD=1): a device write outside its
+                         buffer -> RuntimeError naming the buffer */
 };
 
 enum { SYM_KIND_DEFERRED = 0, SYM_KIND_EAGER = 1, SYM_KIND_TIMEOUT = 2 };

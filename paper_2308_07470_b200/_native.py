@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libsymphony_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 
-SYM_OK, SYM_EPROTO, SYM_EINVAL, SYM_EINVARIANT, SYM_ECUDA, SYM_ENOMEM = range(6)
+SYM_OK, SYM_EPROTO, SYM_EINVAL, SYM_EINVARIANT, SYM_ECUDA, SYM_ENOMEM, SYM_EGUARD = range(7)
 FLAG_TRACE, FLAG_NO_FRESH, FLAG_NO_EXPAND, FLAG_NO_FAST, FLAG_KERNEL_TIMES = 1, 2, 4, 8, 16
 FLAG_MODEL_I64 = 32
 FLAG_CHECK_INVARIANTS, FLAG_INJECT_FAULT = 64, 128

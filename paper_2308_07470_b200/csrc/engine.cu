@@ -157,6 +157,13 @@ struct Ctx {
   std::vector<int64_t> shard_count, shard_last;
   sym_batch* d_gbat = nullptr;
   int64_t gbat_cap = 0, gbat_n = 0;
+  // guard mode (SYM_GUARD=1 when the engine is created): every device buffer
+  // sits between two redzones, its body filled with a poison byte
+  // (SYM_GUARD_POISON), and each run ends by checking every redzone
+  bool guard = false;
+  bool guard_selftest = false;
+  unsigned char poison = 0xff;
+  std::map<void*, std::pair<size_t, const char*>> guards;  // body -> (bytes, name)
 };
 
 #define CK(call)                                                        \
@@ -171,13 +178,75 @@ struct Ctx {
 // Device memory is stream-ordered (the device's default pool, release
 // threshold at max): no allocation or free synchronises the device, so
 // several engines (threads, streams) run their kernels concurrently.
-template <class T>
-int grow(Ctx* ctx, T*& p, int64_t count) {
-  if (p) cudaFreeAsync(p, ctx->stream);
-  p = nullptr;
-  CK(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)(count > 0 ? count : 1), ctx->stream));
+//
+// Guard mode stands in for compute-sanitizer's memcheck and initcheck (the
+// pool's GPUs cannot run it): a write outside any buffer lands in a redzone
+// and fails the run; a read of memory the engine never wrote sees the poison
+// byte, so two runs with different poison bytes that both equal the oracle
+// read nothing uninitialised that matters.
+constexpr size_t kRedzone = 4096;
+constexpr unsigned char kRedByte = 0xa5;
+
+cudaError_t dmalloc(Ctx* ctx, void** p, size_t bytes, cudaStream_t st, const char* name) {
+  if (!ctx->guard) return cudaMallocAsync(p, bytes, st);
+  char* base = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&base, bytes + 2 * kRedzone, st);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(base, kRedByte, kRedzone, st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(base + kRedzone, ctx->poison, bytes, st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(base + kRedzone + bytes, kRedByte, kRedzone, st)) != cudaSuccess)
+    return e;
+  *p = base + kRedzone;
+  ctx->guards[*p] = {bytes, name};
+  return cudaSuccess;
+}
+
+void dfree(Ctx* ctx, void* p, cudaStream_t st) {
+  if (!p) return;
+  if (!ctx->guard) {
+    cudaFreeAsync(p, st);
+    return;
+  }
+  ctx->guards.erase(p);
+  cudaFreeAsync(static_cast<char*>(p) - kRedzone, st);
+}
+
+// Synchronises and reads every redzone back: SYM_EGUARD naming the first
+// buffer written outside its bounds.
+int guard_check(Ctx* ctx) {
+  if (!ctx->guard) return SYM_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->guard_selftest && !ctx->guards.empty()) {  // test hook: one byte past a buffer
+    auto it = ctx->guards.begin();
+    CK(cudaMemset(static_cast<char*>(it->first) + it->second.first, 0, 1));
+  }
+  std::vector<unsigned char> zone(kRedzone);
+  for (auto& g : ctx->guards) {
+    char* body = static_cast<char*>(g.first);
+    for (int side = 0; side < 2; side++) {
+      CK(cudaMemcpy(zone.data(), side ? body + g.second.first : body - kRedzone, kRedzone,
+                    cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < kRedzone; i++)
+        if (zone[i] != kRedByte) {
+          const size_t off = side ? i + 1 : kRedzone - i;
+          ctx->err = std::string("guard: byte ") + std::to_string(off) +
+                     (side ? " past the end of " : " before the start of ") +
+                     g.second.second + " (" + std::to_string(g.second.first) + " bytes)";
+          return SYM_EGUARD;
+        }
+    }
+  }
   return SYM_OK;
 }
+
+template <class T>
+int grow_named(Ctx* ctx, T*& p, int64_t count, const char* name) {
+  dfree(ctx, p, ctx->stream);
+  p = nullptr;
+  CK(dmalloc(ctx, (void**)&p, sizeof(T) * (size_t)(count > 0 ? count : 1), ctx->stream, name));
+  return SYM_OK;
+}
+#define grow(ctx, p, count) grow_named(ctx, p, count, #p)
 
 // --------------------------------------------------------------- K1 -------
 
@@ -2590,15 +2659,16 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
 
 // Realloc keeping the first `keep` elements (stream-ordered, no sync).
 template <class T>
-int grow_keep(Ctx* ctx, T*& p, int64_t keep, int64_t count) {
+int grow_keep_named(Ctx* ctx, T*& p, int64_t keep, int64_t count, const char* name) {
   T* q = nullptr;
-  CK(cudaMallocAsync((void**)&q, sizeof(T) * (size_t)(count > 0 ? count : 1), ctx->stream));
+  CK(dmalloc(ctx, (void**)&q, sizeof(T) * (size_t)(count > 0 ? count : 1), ctx->stream, name));
   if (p && keep > 0)
     CK(cudaMemcpyAsync(q, p, sizeof(T) * (size_t)keep, cudaMemcpyDeviceToDevice, ctx->stream));
-  if (p) cudaFreeAsync(p, ctx->stream);
+  dfree(ctx, p, ctx->stream);
   p = q;
   return SYM_OK;
 }
+#define grow_keep(ctx, p, keep, count) grow_keep_named(ctx, p, keep, count, #p)
 
 void step_reset(Ctx* ctx) {
   forget_last_run(ctx);
@@ -2630,11 +2700,11 @@ int step_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_
   if (ctx->step_n + n > ctx->g_cap) {
     const int64_t c = std::max<int64_t>(2 * ctx->g_cap, ctx->step_n + n + 1024);
     int64_t* o = nullptr;
-    CK(cudaMallocAsync((void**)&o, sizeof(int64_t) * 5 * (size_t)c, st));
+    CK(dmalloc(ctx, (void**)&o, sizeof(int64_t) * 5 * (size_t)c, st, "d_g_out"));
     for (int k = 0; k < 5 && ctx->step_n > 0; k++)
       CK(cudaMemcpyAsync(o + k * c, ctx->d_g_out + k * ctx->g_cap,
                          sizeof(int64_t) * ctx->step_n, cudaMemcpyDeviceToDevice, st));
-    if (ctx->d_g_out) cudaFreeAsync(ctx->d_g_out, st);
+    dfree(ctx, ctx->d_g_out, st);
     ctx->d_g_out = o;
     if ((rc = grow_keep(ctx, ctx->d_g_ticks, ctx->step_n, c)) ||
         (rc = grow_keep(ctx, ctx->d_g_model, ctx->step_n, c)))
@@ -2853,6 +2923,11 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ctx->d_ctrl = cfg->d_ctrl_ns;
   ctx->d_data = cfg->d_data_ns;
   ctx->device = cfg->device;
+  if (const char* g = getenv("SYM_GUARD")) {
+    ctx->guard = g[0] && g[0] != '0';
+    if (const char* v = getenv("SYM_GUARD_POISON")) ctx->poison = (unsigned char)strtol(v, nullptr, 0);
+    ctx->guard_selftest = getenv("SYM_GUARD_SELFTEST") != nullptr;
+  }
   const int M = ctx->M, P = ctx->P;
   // shard membership and slot order (shard-major, model id within shard)
   ctx->shard_of_model.assign(M, 0);
@@ -2948,8 +3023,8 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     tot_g2 += 2 * b;
   }
 #define ALLOC(p, cnt)                                                        \
-  if ((e = cudaMallocAsync((void**)&(p), sizeof(*(p)) * (size_t)(cnt),       \
-                           ctx->stream)) != cudaSuccess)                      \
+  if ((e = dmalloc(ctx, (void**)&(p), sizeof(*(p)) * (size_t)(cnt),         \
+                   ctx->stream, #p)) != cudaSuccess)                          \
     return fail(#p, e);
   ALLOC(ctx->d_lat, (int64_t)M * ctx->lat_stride);
   ALLOC(ctx->d_mp, M);
@@ -3106,8 +3181,7 @@ void sym_destroy(void* engine) {
                   ctx->d_lay_g[1], ctx->d_lay_i[0], ctx->d_lay_i[1], ctx->d_lay_aself[0],
                   ctx->d_lay_aself[1], ctx->d_lay_flag, ctx->d_mp_chunk, ctx->d_step_slot,
                   ctx->d_step_shard, ctx->d_step_cnt, ctx->d_gbat};
-  for (void* p : ptrs)
-    if (p) cudaFreeAsync(p, ctx->stream);
+  for (void* p : ptrs) dfree(ctx, p, ctx->stream);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
@@ -3134,7 +3208,8 @@ int32_t sym_run_device(void* engine, const int64_t* d_arr_ticks,
                                                         n, ctx->d_model);
     model = ctx->d_model;
   }
-  return run_device(ctx, d_arr_ticks, model, n, flags, out, true);
+  const int rc = run_device(ctx, d_arr_ticks, model, n, flags, out, true);
+  return rc == SYM_OK ? guard_check(ctx) : rc;
 }
 
 int32_t sym_run(void* engine, const int64_t* arr_ticks, const void* arr_model,
@@ -3240,7 +3315,7 @@ int32_t sym_run(void* engine, const int64_t* arr_ticks, const void* arr_model,
   out->drop_t = k5;
   out->drop_key_sub = k6;
   out->drop_key_a = k7;
-  return rc;
+  return rc == SYM_OK ? guard_check(ctx) : rc;
 }
 
 int32_t sym_step_reset(void* engine) {
@@ -3296,7 +3371,8 @@ int32_t sym_step(void* engine, const int64_t* arr_ticks, const void* arr_model, 
                          st));
     }
   }
-  return step_device(ctx, ctx->d_ticks, ctx->d_model, n, until_tick, flags, out);
+  const int rc2 = step_device(ctx, ctx->d_ticks, ctx->d_model, n, until_tick, flags, out);
+  return rc2 == SYM_OK ? guard_check(ctx) : rc2;
 }
 
 int32_t sym_step_result(void* engine, sym_result* out) {
@@ -3399,6 +3475,7 @@ int64_t sym_last_batches(void* engine, sym_batch* host, int64_t cap) {
                       st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     return -SYM_ECUDA;
+  if (const int g = guard_check(ctx)) return -g;
   return total;
 }
 
@@ -3421,7 +3498,8 @@ int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,
   const int32_t M = ctx->M, P = ctx->P, G = ctx->G;
   const int64_t n = ctx->last_n;
   unsigned long long* d = nullptr;
-  CK(cudaMallocAsync((void**)&d, sizeof(unsigned long long) * (4 * (size_t)M + G), st));
+  CK(dmalloc(ctx, (void**)&d, sizeof(unsigned long long) * (4 * (size_t)M + G), st,
+             "window counts"));
   CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * (4 * (size_t)M + G), st));
   if (n > 0)
     k_window_req<<<nblk(n, 256), 256, 0, st>>>(ctx->last_ticks, ctx->last_model,
@@ -3442,8 +3520,10 @@ int32_t sym_window_counts(void* engine, int64_t lo_ns, int64_t hi_ns,
   std::vector<unsigned long long> h(4 * (size_t)M + G);
   CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(),
                      cudaMemcpyDeviceToHost, st));
-  cudaFreeAsync(d, st);
+  int grc = guard_check(ctx);
+  dfree(ctx, d, st);
   CK(cudaStreamSynchronize(st));
+  if (grc) return grc;
   for (int32_t m = 0; m < M; m++) {
     model_arrivals[m] = (int64_t)h[m];
     model_completed[m] = (int64_t)h[M + m];
@@ -3480,7 +3560,8 @@ int32_t sym_window_stats(void* engine, int64_t lo_ns, int64_t hi_ns, int64_t* mo
   const size_t nh = (size_t)M * hist_stride;
   // scratch: arrivals [M] | qd [M] | p99 [M] | hist [M*stride] | err
   unsigned long long* d = nullptr;
-  CK(cudaMallocAsync((void**)&d, sizeof(unsigned long long) * (3 * (size_t)M + nh + 1), st));
+  CK(dmalloc(ctx, (void**)&d, sizeof(unsigned long long) * (3 * (size_t)M + nh + 1), st,
+             "window stats"));
   CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * (3 * (size_t)M + nh + 1), st));
   std::vector<unsigned long long> arr(model_arrivals, model_arrivals + M);
   CK(cudaMemcpyAsync(d, arr.data(), sizeof(unsigned long long) * M, cudaMemcpyHostToDevice, st));
@@ -3522,8 +3603,10 @@ int32_t sym_window_stats(void* engine, int64_t lo_ns, int64_t hi_ns, int64_t* mo
   std::vector<unsigned long long> h(3 * (size_t)M + nh + 1);
   CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(),
                      cudaMemcpyDeviceToHost, st));
-  cudaFreeAsync(d, st);
+  int grc = guard_check(ctx);
+  dfree(ctx, d, st);
   CK(cudaStreamSynchronize(st));
+  if (grc) return grc;
   if (reinterpret_cast<int32_t*>(&h[3 * (size_t)M + nh])[0]) {
     ctx->err = "sym_window_stats: a latency exceeds the 40-bit sort key";
     return SYM_EINVAL;

@@ -345,6 +345,8 @@ class Engine:
         self._last_ok = True
         batches = _native.pinned_empty(res.n_batches, _native.BATCH_DTYPE)
         got = self._lib.sym_last_batches(self._handle, batches.ctypes.data, len(batches))
+        if got < 0:
+            self._raise(-got, res)
         if got != res.n_batches:
             raise RuntimeError(f"sym_last_batches returned {got}")
         outc = outs["outcome"]
