@@ -51,10 +51,13 @@ EV_BATCH_BYTES = 56    # sizeof(EvBatch)
 #                   log2(max_batch) l(b) probes are negligible at this size)
 #   K3 matchmaking  8 B per GPU free_at + 24 B per ready candidate + 12 B
 #                   written per grant
+# K1's 24 B/request cover the whole stable partition; with several
+# sub-clusters in one engine it runs as two k_part passes (by sub-cluster,
+# then by model), so each pass is credited its share (24 B / passes).
 SURVEY_KERNELS = {
-    "K1": ("k_part", lambda n, nb, g: 24 * n),     # per partition pass (2 with P > 1)
-    "K2": ("k_nxt", lambda n, nb, g: 12 * n),
-    "K3": ("k_match_coop", lambda n, nb, g: 36 * nb + 8 * g),
+    "K1": ("k_part", lambda n, nb, g, passes=1: 24 * n / passes),
+    "K2": ("k_nxt_bs", lambda n, nb, g, passes=1: 12 * n),
+    "K3": ("k_match_coop", lambda n, nb, g, passes=1: 36 * nb + 8 * g),
 }
 
 
@@ -78,11 +81,12 @@ def design_bytes(kernel: str, n: int, nb: int, shards: int) -> float | None:
     return table.get(kernel)
 
 
-def kernel_bytes(kernel: str, n: int, nb: int, g: int, shards: int):
+def kernel_bytes(kernel: str, n: int, nb: int, g: int, shards: int, passes: float = 1):
     """(bytes per launch, source) -- §8(d) for K1/K2/K3, else DESIGN."""
     for tag, (name, fn) in SURVEY_KERNELS.items():
         if name == kernel:
-            return fn(n, nb, g), f"SURVEY §8(d) {tag}"
+            return fn(n, nb, g, passes), f"SURVEY §8(d) {tag}" + (
+                f" / {passes:g} passes" if passes != 1 else "")
     b = design_bytes(kernel, n, nb, shards)
     return b, ("DESIGN.md §5" if b is not None else None)
 
@@ -450,7 +454,7 @@ def run_b200(args, rank, world, local_rank):
     k_total = sum(v[1] for v in ktimes.values())
     for name, (cnt_l, k_ms) in ktimes.items():
         per_launch_ms = k_ms / cnt_l
-        ab, src = kernel_bytes(name, n, nb_step, gpus, len(mine))
+        ab, src = kernel_bytes(name, n, nb_step, gpus, len(mine), cnt_l / args.steps)
         gbs = (ab / (per_launch_ms / 1e3) / 1e9) if ab else None
         kern[name] = {"launches_per_step": cnt_l / args.steps, "ms_per_launch": per_launch_ms,
                       "share": k_ms / k_total, "bytes_per_launch": ab, "bytes_source": src,
@@ -469,6 +473,10 @@ def run_b200(args, rank, world, local_rank):
             k123[tag] = {"kernel": name, "achieved_gbs": kern[name]["gbs"],
                          "frac": kern[name]["frac"], "ms_per_launch": kern[name]["ms_per_launch"],
                          "bytes_per_launch": kern[name]["bytes_per_launch"]}
+    if "K1" in k123:  # the whole ingest phase (counts, scans, passes, readback) vs 24 B/request
+        ph = stats["ms_ingest"]
+        k123["K1"]["phase"] = {"ms": ph, "achieved_gbs": 24 * n / (ph / 1e3) / 1e9,
+                               "frac": 24 * n / (ph / 1e3) / 1e9 / peak}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,

@@ -162,6 +162,7 @@ struct Ctx {
   // (SYM_GUARD_POISON), and each run ends by checking every redzone
   bool guard = false;
   bool guard_selftest = false;
+  int n_sm = 148;
   unsigned char poison = 0xff;
   std::map<void*, std::pair<size_t, const char*>> guards;  // body -> (bytes, name)
 };
@@ -622,82 +623,188 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
 // K2 (window / candidate per fresh start, fast path): the batch-chain
 // pointer of every sorted position q -- where the batch a fresh start at q
 // forms closes (fastpath.cuh, lean_chain_next*) -- and its closing arrival
-// for k_chain_recs.  Each thread owns kNxtPer consecutive positions and
-// sweeps them with two pointers: for an affine l(b) (deferred, prefix) the
-// closing index is the first j > q with u_j >= u_q + (slo - a - b0 - d_ctrl)
-// on u_j = tick_j + (a + d_data) j (lean_chain_next_affine), and both
-// sides grow with q, so the search pointer only moves forward: ~1 load,
-// multiply-add and compare per position instead of a search per position.
-// Model boundaries come from the per-slot offsets (no per-position model
-// array).  Positions the lean test cannot certify are listed for the general
-// fresh scan (k_nxt_general); other profiles and policies take the scalar
-// lean forms per position.
-constexpr int kNxtPer = 8;
+// for k_chain_recs.  For an affine l(b) (deferred, prefix) the closing index
+// is the first j > q with u_j >= u_q + (slo - a - b0 - d_ctrl) on the
+// non-decreasing u_j = tick_j + (a + d_data) j (lean_chain_next_affine): a
+// lower bound in a sorted sequence, found per lane by a fixed binary search
+// over shared memory (k_nxt_tma).  Model boundaries come from the per-slot
+// offsets (no per-position model array).  Positions the lean test cannot
+// certify are listed for the general fresh scan (k_nxt_general); other
+// profiles and policies take the scalar lean forms per position
+// (also in k_nxt_tma).
 
-__device__ __forceinline__ int32_t slot_of_position(const ModelParam* __restrict__ mp_all,
-                                                    int32_t M, int64_t p) {
-  int32_t lo = 0, hi = M;  // last slot with off <= p, skipping empty slots
+// k_nxt_tma: a warp owns kNxtRounds x 32 consecutive positions (lane =
+// position), their u plus a look-ahead staged in shared memory.  For the
+// affine deferred/prefix form the closing index of a fresh start p is the
+// first j in (p, jend] with u_j >= T_p, so a lane finds it by a fixed 5-step
+// binary search over the 32 staged u after p -- every lane runs the same
+// instructions, no data-dependent loop -- and stores nxt/close_k coalesced.
+// Batches longer than 32 arrivals, the last arrivals of a model and the
+// max-batch tail take the scalar lean_chain_next_affine.
+constexpr int kNxtRounds = 16;
+constexpr int kNxtTile = 32 * kNxtRounds;  // positions per warp
+constexpr int kNxtWin = 32;                // binary-search window after q
+constexpr int kNxtStage = kNxtTile + 2 * kNxtWin;
+
+__device__ __forceinline__ bool lean_affine(const Shard& S, const ModelParam& mp) {
+  return mp.affine && S.kind == K_DEFERRED && S.gather == G_PREFIX;
+}
+
+__device__ __forceinline__ int shard_of_slot_linear(const int32_t* __restrict__ slot_base,
+                                                    int32_t k) {
+  int sh = 0;
+  while (slot_base[sh + 1] <= k) sh++;
+  return sh;
+}
+
+// ---- TMA-staged K2 (the launch used).  A persistent warp walks tiles
+// t = w, w + W, ...; the tile's ticks [t0, t0 + kNxtStage) arrive in shared
+// memory by one bulk copy (cp.async.bulk, completion on an mbarrier) issued
+// one tile ahead into the warp's other buffer, so the DRAM latency of tile
+// t+W hides behind the search of tile t.  The ticks become u in place
+// (u_j = tick_j + (a + d_data)(j - off)), one model segment at a time.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "NXT_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra NXT_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Last slot with off <= p (empty slots skipped): a 32-ary search, one load
+// per lane per level (two levels up to 1024 slots).
+__device__ __forceinline__ int32_t warp_slot_of_position(const ModelParam* __restrict__ mp_all,
+                                                         int32_t M, int32_t p, int lane) {
+  int32_t lo = 0, hi = M;  // answer in [lo, hi)
   while (hi - lo > 1) {
-    const int32_t mid = (lo + hi) >> 1;
-    if (mp_all[mid].off <= p) lo = mid; else hi = mid;
+    const int32_t step = (hi - lo + 31) / 32;
+    const int32_t idx = lo + lane * step;
+    const bool le = idx < hi && (idx == lo || mp_all[idx].off <= p);
+    const unsigned b = __ballot_sync(0xffffffffu, le);
+    const int32_t L = 31 - __clz(b);
+    lo = lo + L * step;
+    hi = min(lo + step, hi);
   }
   while (lo + 1 < M && mp_all[lo].off + mp_all[lo].cnt <= p) lo++;
   return lo;
 }
 
-__global__ void __launch_bounds__(256)
-k_nxt(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_base,
-      const ModelParam* __restrict__ mp_all, int32_t P, int32_t M, int64_t n,
-      int32_t* __restrict__ nxt, int32_t* __restrict__ close_k,
-      int32_t* __restrict__ unsure, int32_t* __restrict__ unsure_n) {
-  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kNxtPer;
-  if (p0 >= n) return;
-  const int64_t p1 = p0 + kNxtPer < n ? p0 + kNxtPer : n;
-  int32_t k = slot_of_position(mp_all, M, p0);
-  for (int64_t p = p0; p < p1;) {
-    while (mp_all[k].off + mp_all[k].cnt <= p) k++;  // next non-empty slot
-    const ModelParam mp = mp_all[k];
-    int s = 0;
-    while (slot_base[s + 1] <= k) s++;
-    const Shard& S = shards[s];
-    const int32_t m = k - slot_base[s];
-    const int64_t pe = mp.off + mp.cnt < p1 ? mp.off + mp.cnt : p1;  // this model's part
-    const int64_t* __restrict__ tick = S.s_tick;
-    if (mp.affine && S.kind == K_DEFERRED && S.gather == G_PREFIX) {
-      const int64_t a = mp.aff_a, b0 = mp.aff_b, dc = S.d_ctrl, dd = S.d_data, c1 = a + dd;
-      const int64_t off = mp.off;
-      const int32_t mb = mp.max_batch, cnt = mp.cnt;
-      int64_t j = p + 1;  // search pointer (absolute): u_i < T for every i in (q, j)
-      for (; p < pe; p++) {
-        const int32_t q = (int32_t)(p - off);
-        const int64_t uq = __ldg(tick + p) + c1 * q;
-        const int64_t T = uq + (mp.slo - a - b0 - dc);
-        const int32_t kmax = cnt - 2 < q + mb - 2 ? cnt - 2 : q + mb - 2;
-        const int64_t jend = off + (int64_t)kmax + 1;  // last candidate j
-        if (j < p + 1) j = p + 1;
-        while (j <= jend && __ldg(tick + j) + c1 * (j - off) < T) j++;
-        int32_t v;
-        if (j <= jend) {  // closes at k = j - 1, if ok(len) holds there
-          const int64_t kk = j - 1;
-          const int64_t OK = uq + (mp.slo - dc - b0 - c1);
-          v = __ldg(tick + kk) + c1 * (kk - off) <= OK ? (int32_t)j : NX_UNSURE;
-        } else {
-          v = lean_chain_next_affine_tail(S, mp, q);
-        }
-        nxt[p] = v;
-        close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
-        if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = (int32_t)p;
-      }
-    } else {
-      const bool r32 = rel32_ok(S, mp);
-      for (; p < pe; p++) {
-        const int32_t q = (int32_t)(p - mp.off);
-        const int32_t v = r32 ? lean_chain_next32(S, m, q) : lean_chain_next(S, m, q);
-        nxt[p] = v;
-        close_k[p] = v >= 0 ? v - 1 - mp.off : (v == NX_LAST ? mp.cnt - 1 : -1);
-        if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = (int32_t)p;
-      }
+constexpr int kNxtTmaWarps = 8;
+constexpr int kNxtTmaBlocksPerSm = 3;
+constexpr int kNxtTmaSmemBuf = kNxtTmaWarps * 2 * kNxtStage * 8;
+constexpr int kNxtTmaSmem = kNxtTmaSmemBuf + kNxtTmaWarps * 2 * 8;  // + mbarriers
+
+__global__ void __launch_bounds__(32 * kNxtTmaWarps, kNxtTmaBlocksPerSm)
+k_nxt_tma(const int64_t* __restrict__ tick, const Shard* __restrict__ shards,
+          const int32_t* __restrict__ slot_base, const ModelParam* __restrict__ mp_all,
+          int32_t P, int32_t M, int32_t n, int32_t* __restrict__ nxt,
+          int32_t* __restrict__ close_k, int32_t* __restrict__ unsure,
+          int32_t* __restrict__ unsure_n) {
+  extern __shared__ __align__(128) unsigned char nxt_smem[];
+  auto sbuf = reinterpret_cast<int64_t(*)[2][kNxtStage]>(nxt_smem);
+  auto sbar = reinterpret_cast<uint64_t(*)[2]>(nxt_smem + kNxtTmaSmemBuf);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t ntiles = (n + kNxtTile - 1) / kNxtTile;
+  const int32_t W = gridDim.x * kNxtTmaWarps;
+  int32_t t = blockIdx.x * kNxtTmaWarps + w;
+  if (lane == 0) {
+    mbar_init(&sbar[w][0], 1);
+    mbar_init(&sbar[w][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int32_t tt, int b) {
+    const int32_t t0 = tt * kNxtTile;
+    const int32_t cnt = n - t0 < kNxtStage ? n - t0 : kNxtStage;
+    // whole 16-byte units: an odd tail reads one element past n (capacity
+    // n + 1024), never used
+    bulk_load(sbuf[w][b], tick + t0, (uint32_t)((cnt + 1) & ~1) * 8u, &sbar[w][b]);
+  };
+  if (lane == 0 && t < ntiles) issue(t, 0);
+  uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+  for (int b = 0; t < ntiles; t += W, b ^= 1) {
+    if (lane == 0 && t + W < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(t + W, b ^ 1);
     }
+    const int32_t t0 = t * kNxtTile;
+    const int32_t send = n - t0 < kNxtStage ? n : t0 + kNxtStage;
+    int32_t k = warp_slot_of_position(mp_all, M, t0, lane);
+    const int32_t pend = n - t0 < kNxtTile ? n : t0 + kNxtTile;
+    int64_t* __restrict__ u = sbuf[w][b];
+    mbar_wait(&sbar[w][b], (phase >> b) & 1);
+    phase ^= 1u << b;
+    // the tile's positions, one model segment at a time (warp-uniform loop;
+    // usually one segment)
+    for (int32_t a = t0; a < pend;) {
+      while (mp_all[k].off + mp_all[k].cnt <= a) k++;
+      const ModelParam& mk = mp_all[k];
+      const int sh = shard_of_slot_linear(slot_base, k);
+      const Shard& S = shards[sh];
+      const int32_t off = mk.off, cnt = mk.cnt;
+      const int32_t seg_end = off + cnt < pend ? off + cnt : pend;
+      if (lean_affine(S, mk)) {
+        const int64_t c1 = mk.aff_a + S.d_data;
+        const int64_t D1 = mk.slo - mk.aff_a - mk.aff_b - S.d_ctrl;
+        const int64_t D2 = mk.slo - S.d_ctrl - mk.aff_b - c1;
+        // jend = min(off + cnt - 1, p + mb - 1) >= p + 32  <=>  p <= pfull
+        const int32_t pfull = mk.max_batch - 1 >= kNxtWin ? off + cnt - 1 - kNxtWin : INT32_MIN;
+        const int32_t ub = off + cnt < send ? off + cnt : send;  // this model's staged part
+        for (int32_t e = a - t0 + lane; e < ub - t0; e += 32) u[e] += c1 * (t0 + e - off);
+        __syncwarp();
+#pragma unroll 1
+        for (int32_t p = a + lane; p < seg_end; p += 32) {
+          const int e = p - t0;
+          const int64_t uq = u[e];
+          const int64_t T = uq + D1;
+          int32_t v;
+          if (p <= pfull && u[e + kNxtWin] >= T) {
+            // the batch closes within 32 arrivals: first j in (p, p+32] with u_j >= T
+            int32_t x = 0;
+#pragma unroll
+            for (int st = kNxtWin / 2; st >= 1; st >>= 1)
+              if (u[e + x + st] < T) x += st;
+            v = u[e + x] <= uq + D2 ? p + x + 1 : NX_UNSURE;
+          } else {  // a long batch or the model's last arrivals: the scalar form
+            v = lean_chain_next_affine(S, mk, p - off);
+          }
+          nxt[p] = v;
+          close_k[p] = v >= 0 ? v - 1 - off : (v == NX_LAST ? cnt - 1 : -1);
+          if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = p;
+        }
+      } else {  // other profiles / policies: the scalar lean forms
+        const int32_t m = k - slot_base[sh];
+        const bool r32 = rel32_ok(S, mk);
+        for (int32_t p = a + lane; p < seg_end; p += 32) {
+          const int32_t q = p - off;
+          const int32_t v = r32 ? lean_chain_next32(S, m, q) : lean_chain_next(S, m, q);
+          nxt[p] = v;
+          close_k[p] = v >= 0 ? v - 1 - off : (v == NX_LAST ? cnt - 1 : -1);
+          if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = p;
+        }
+      }
+      a = seg_end;
+    }
+    __syncwarp();  // every lane is done with buffer b before it is refilled
   }
 }
 
@@ -1506,6 +1613,7 @@ k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bv
     }
     if (moved) flags[2 + (it & 1)] = 1;
     grid.sync();
+    if (tid0 == 0) flags[1] = it + 1;  // passes run (SYM_DEBUG_TIMING=1 prints it)
     if (flags[2 + (it & 1)] == 0) break;
     grid.sync();
   }
@@ -2345,9 +2453,12 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   bool have_fresh = false;
   if (fast) {
     CK(cudaMemsetAsync(ctx->d_unsure_n, 0, sizeof(int32_t), st));
-    KL(k_nxt, nblk((n + kNxtPer - 1) / kNxtPer, 256), 256, 0, st>>>(
-        ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, M, n, ctx->d_nxt, ctx->d_closek,
-        ctx->d_unsure, ctx->d_unsure_n));
+    const int64_t tiles = (n + kNxtTile - 1) / kNxtTile;
+    const int64_t want = (tiles + kNxtTmaWarps - 1) / kNxtTmaWarps;
+    KL(k_nxt_tma, (unsigned)std::min<int64_t>(want, (int64_t)ctx->n_sm * kNxtTmaBlocksPerSm),
+       32 * kNxtTmaWarps, kNxtTmaSmem, st>>>(
+           ctx->d_s_tick, ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P, M, (int32_t)n,
+           ctx->d_nxt, ctx->d_closek, ctx->d_unsure, ctx->d_unsure_n));
     KL(k_nxt_general, 148 * 4, 256, 0, st>>>(ctx->d_shards, ctx->d_slot_base, ctx->d_mp, P,
                                              ctx->d_unsure, ctx->d_unsure_n, ctx->d_nxt,
                                              ctx->d_closek));
@@ -2451,6 +2562,11 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         kt.end();
       }
   pc.mark("match_loop");
+      if (pc.mode == 1) {
+        int32_t passes = 0;
+        cudaMemcpy(&passes, ctx->d_changed + 1, sizeof(int32_t), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[sym] match passes %d (%lld batches)\n", passes, (long long)nt);
+      }
       int64_t* d_rb = ctx->d_meta + 2 * (P + 1);
       CK(cudaMemcpyAsync(d_rb, rec_base.data(), sizeof(int64_t) * (P + 1),
                          cudaMemcpyHostToDevice, st));
@@ -3000,6 +3116,11 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
     return fail("stream", e);
   for (auto& ev : ctx->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail("event", e);
+  if ((e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, ctx->device)) !=
+          cudaSuccess ||
+      (e = cudaFuncSetAttribute(k_nxt_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kNxtTmaSmem)) != cudaSuccess)
+    return fail("k_nxt_tma attributes", e);
   {  // keep pool memory mapped across synchronisations (no remap stalls)
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
