@@ -56,7 +56,7 @@ EV_BATCH_BYTES = 56    # sizeof(EvBatch)
 # then by model), so each pass is credited its share (24 B / passes).
 SURVEY_KERNELS = {
     "K1": ("k_part", lambda n, nb, g, passes=1: 24 * n / passes),
-    "K2": ("k_nxt_bs", lambda n, nb, g, passes=1: 12 * n),
+    "K2": ("k_nxt_tma", lambda n, nb, g, passes=1: 12 * n),
     "K3": ("k_match_coop", lambda n, nb, g, passes=1: 36 * nb + 8 * g),
 }
 

@@ -641,7 +641,16 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
 // instructions, no data-dependent loop -- and stores nxt/close_k coalesced.
 // Batches longer than 32 arrivals, the last arrivals of a model and the
 // max-batch tail take the scalar lean_chain_next_affine.
-constexpr int kNxtRounds = 16;
+#ifndef SYM_NXT_ROUNDS
+#define SYM_NXT_ROUNDS 16
+#endif
+#ifndef SYM_NXT_BPS
+#define SYM_NXT_BPS 3
+#endif
+#ifndef SYM_NXT_WARPS
+#define SYM_NXT_WARPS 8
+#endif
+constexpr int kNxtRounds = SYM_NXT_ROUNDS;
 constexpr int kNxtTile = 32 * kNxtRounds;  // positions per warp
 constexpr int kNxtWin = 32;                // binary-search window after q
 constexpr int kNxtStage = kNxtTile + 2 * kNxtWin;
@@ -708,8 +717,8 @@ __device__ __forceinline__ int32_t warp_slot_of_position(const ModelParam* __res
   return lo;
 }
 
-constexpr int kNxtTmaWarps = 8;
-constexpr int kNxtTmaBlocksPerSm = 3;
+constexpr int kNxtTmaWarps = SYM_NXT_WARPS;
+constexpr int kNxtTmaBlocksPerSm = SYM_NXT_BPS;
 constexpr int kNxtTmaSmemBuf = kNxtTmaWarps * 2 * kNxtStage * 8;
 constexpr int kNxtTmaSmem = kNxtTmaSmemBuf + kNxtTmaWarps * 2 * 8;  // + mbarriers
 
@@ -988,17 +997,29 @@ __global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __r
 __global__ void k_bid(const BatchRec* __restrict__ recs, const int64_t* __restrict__ rec_base,
                       const int64_t* __restrict__ rec_count, int32_t P, int64_t total,
                       int32_t* __restrict__ bid) {
+  // a warp takes 32 records; each record's run of positions is written by
+  // the whole warp (one coalesced store per record) instead of by one lane
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= total) return;
-  int s = 0;
-  int64_t k = w;
-  while (s < P && k >= rec_count[s]) {
-    k -= rec_count[s];
-    s++;
+  const int lane = threadIdx.x & 31;
+  int32_t ri = -1, first = 0, size = 0;
+  if (w < total) {
+    int s = 0;
+    int64_t k = w;
+    while (s < P && k >= rec_count[s]) {
+      k -= rec_count[s];
+      s++;
+    }
+    ri = (int32_t)(rec_base[s] + k);
+    const BatchRec& r = recs[ri];
+    first = r.first;
+    size = r.size;
   }
-  const int64_t ri = rec_base[s] + k;
-  const BatchRec& r = recs[ri];
-  for (int32_t j = 0; j < r.size; j++) bid[r.first + j] = (int32_t)ri;
+  for (int b = 0; b < 32; b++) {
+    const int32_t rb = __shfl_sync(0xffffffffu, ri, b);
+    const int32_t fb = __shfl_sync(0xffffffffu, first, b);
+    const int32_t sb = __shfl_sync(0xffffffffu, size, b);
+    for (int32_t j = lane; j < sb; j += 32) bid[fb + j] = rb;
+  }
 }
 
 // RunResult arrays (simulator.py:74-78, 159-173, 249-258) in stream order:
