@@ -433,13 +433,32 @@ k_part_count(const int32_t* __restrict__ key, int64_t n, int32_t M,
   if (!tile_geom<kMode>(blockIdx.x, n, B, W, seg, P, g)) return;
   for (int b = threadIdx.x; b < g.B; b += blockDim.x) hcnt[b] = 0;
   __syncthreads();
-  for (int64_t i = g.lo + threadIdx.x; i < g.hi; i += blockDim.x) {
-    const int32_t m = key[i];
+  // launched with 256 threads: every element's key load issued before any
+  // counting (kTileI / 256 per thread)
+  constexpr int kPer = kTileI / 256;
+  int32_t mk[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; k++) {
+    const int64_t i = g.lo + threadIdx.x + k * 256;
+    mk[k] = i < g.hi ? key[i] : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; k++) {
+    const int64_t i = g.lo + threadIdx.x + k * 256;
+    const int32_t m = mk[k];
+    if (i >= g.hi) break;
     if (kMode != 2 && (m < 0 || m >= M)) {
       atomicMin(err, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
+      mk[k] = -1;
       continue;
     }
-    atomicAdd(&hcnt[kMode == 1 ? shard_of_model[m] : m - g.bin0], 1);
+    mk[k] = kMode == 1 ? shard_of_model[m] : m - g.bin0;
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; k++) {
+    const int64_t i = g.lo + threadIdx.x + k * 256;
+    if (i >= g.hi) break;
+    if (mk[k] >= 0) atomicAdd(&hcnt[mk[k]], 1);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < g.B; b += blockDim.x)
@@ -489,7 +508,7 @@ __host__ __device__ inline size_t part_smem(int B) {
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(32 * kTileWarps, 5)
+__global__ void __launch_bounds__(32 * kTileWarps, 4)
 k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
        const int32_t* __restrict__ aux_in, int64_t n, int32_t M,
        const int32_t* __restrict__ shard_of_model, const int32_t* __restrict__ slot_of_model,
@@ -519,28 +538,48 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
   const int64_t lo = geo.lo, hi = geo.hi;
   const int64_t wlo = lo + (int64_t)wib * 32 * kTilePerLane;
   __syncwarp();
-  // pass 1: load this lane's elements once, count the warp's bins
+  // pass 1: load this lane's elements once (every row's loads issued before
+  // any is used), count the warp's bins
   int64_t tk[kTilePerLane];
   int32_t bn[kTilePerLane], ax[kTilePerLane];
 #pragma unroll
   for (int r = 0; r < kTilePerLane; r++) {
     const int64_t i = wlo + r * 32 + lane;
-    bn[r] = -1 - lane;
     tk[r] = 0;
+    bn[r] = -1;
     ax[r] = 0;
     if (i < hi) {
-      const int32_t m = key[i];
       tk[r] = tick_in[i];
-      if (kMode != 2 && i > 0 && tk[r] < tick_in[i - 1])  // arrivals must be time-ordered
-        atomicMin(err + 1, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
-      if (kMode == 2 || (m >= 0 && m < M)) {  // unknown ids were reported by k_part_count
-        bn[r] = kMode == 1 ? shard_of_model[m] : m - geo.bin0;
-        if (kMode == 1) ax[r] = slot_of_model[m];
-        if (kMode == 2) ax[r] = aux_in[i];
-      }
+      bn[r] = key[i];
+      if (kMode == 2) ax[r] = aux_in[i];
     }
-    if (bn[r] >= 0) atomicAdd_block(&mine[bn[r]], 1);
   }
+  const int64_t before_warp = kMode != 2 && lane == 0 && wlo > 0 && wlo < hi ? tick_in[wlo - 1]
+                                                                            : INT64_MIN;
+#pragma unroll
+  for (int r = 0; r < kTilePerLane; r++) {
+    const int64_t i = wlo + r * 32 + lane;
+    const int32_t m = bn[r];
+    bn[r] = -1 - lane;
+    if (i < hi && (kMode == 2 || (m >= 0 && m < M))) {  // unknown ids: k_part_count
+      bn[r] = kMode == 1 ? shard_of_model[m] : m - geo.bin0;
+      if (kMode == 1) ax[r] = slot_of_model[m];
+    }
+  }
+  if (kMode != 2) {  // arrivals must be time-ordered: the previous element by shuffle
+#pragma unroll
+    for (int r = 0; r < kTilePerLane; r++) {
+      const int64_t i = wlo + r * 32 + lane;
+      int64_t prev = __shfl_up_sync(0xffffffffu, tk[r], 1);
+      const int64_t last_row = __shfl_sync(0xffffffffu, r > 0 ? tk[r > 0 ? r - 1 : 0] : 0, 31);
+      if (lane == 0) prev = r > 0 ? last_row : before_warp;
+      if (i < hi && i > 0 && tk[r] < prev)
+        atomicMin(err + 1, (int32_t)(i < INT32_MAX ? i : INT32_MAX));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kTilePerLane; r++)
+    if (bn[r] >= 0) atomicAdd_block(&mine[bn[r]], 1);
   __syncthreads();
   // per bin: warp offsets and the tile's count; local starts by a block scan
   {
@@ -609,12 +648,24 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
   }
   __syncthreads();
   const int32_t len = scratch[kTileWarps - 1];  // elements staged (valid ids)
-  for (int32_t e = threadIdx.x; e < len; e += blockDim.x) {  // bin runs
-    const int32_t b = st_b[e];
-    const int32_t pos = gbase[b] + (e - lstart[b]);
-    out_tick[pos] = st_t[e];
-    out_idx[pos] = st_i[e];
-    if (kAux) out_aux[pos] = st_a[e];
+  constexpr int kOutIlp = 4;  // independent shared-memory chains per thread
+  for (int32_t e0 = threadIdx.x; e0 < len; e0 += kOutIlp * blockDim.x) {  // bin runs
+    int32_t pos[kOutIlp];
+#pragma unroll
+    for (int k = 0; k < kOutIlp; k++) {
+      const int32_t e = e0 + k * blockDim.x;
+      const int32_t b = e < len ? st_b[e] : 0;
+      pos[k] = gbase[b] + (e - lstart[b]);
+    }
+#pragma unroll
+    for (int k = 0; k < kOutIlp; k++) {
+      const int32_t e = e0 + k * blockDim.x;
+      if (e < len) {
+        out_tick[pos[k]] = st_t[e];
+        out_idx[pos[k]] = st_i[e];
+        if (kAux) out_aux[pos[k]] = st_a[e];
+      }
+    }
   }
 }
 
