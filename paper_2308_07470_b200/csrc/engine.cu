@@ -768,6 +768,22 @@ __device__ __forceinline__ int32_t warp_slot_of_position(const ModelParam* __res
   return lo;
 }
 
+// Last index with a[idx] <= x over a non-decreasing int32 array (a[0] <= x):
+// a 32-ary search, one load per lane per level.
+__device__ __forceinline__ int32_t warp_last_le(const int32_t* __restrict__ a, int32_t M,
+                                                int64_t x, int lane) {
+  int32_t lo = 0, hi = M;
+  while (hi - lo > 1) {
+    const int32_t step = (hi - lo + 31) / 32;
+    const int32_t idx = lo + lane * step;
+    const bool le = idx < hi && (idx == lo || a[idx] <= x);
+    const unsigned b = __ballot_sync(0xffffffffu, le);
+    lo = lo + (31 - __clz(b)) * step;
+    hi = min(lo + step, hi);
+  }
+  return lo;
+}
+
 constexpr int kNxtTmaWarps = SYM_NXT_WARPS;
 constexpr int kNxtTmaBlocksPerSm = SYM_NXT_BPS;
 constexpr int kNxtTmaSmemBuf = kNxtTmaWarps * 2 * kNxtStage * 8;
@@ -1405,12 +1421,11 @@ k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_
              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
              uint32_t* __restrict__ fail, int tb) {
   const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // the warp's first batch locates its model by a 32-ary search (two loads
+  // per lane); a warp's 32 batches almost always share it
+  const int64_t d0 = __shfl_sync(0xffffffffu, d, 0);
+  int lo = warp_last_le(bbase, M, d0 < nt ? d0 : nt - 1, threadIdx.x & 31);
   if (d >= nt) return;
-  int lo = 0, hi = M;  // last model with bbase <= d
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (bbase[mid] <= d) lo = mid; else hi = mid;
-  }
   while (nb[lo] == 0 || bbase[lo] + nb[lo] <= d) lo++;
   const int s = shard_of_slot(slot_base, P, lo);
   const ModelParam& mp = mp_all[lo];

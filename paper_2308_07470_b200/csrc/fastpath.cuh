@@ -379,7 +379,9 @@ SYM_HD void lean_batch(const Shard& S, int32_t m, int32_t q, int32_t k, EvBatch&
   const int32_t len = k - q + 1, mb = P.max_batch;
   const int64_t d = tick[q] + P.slo, now = tick[k];
   const int64_t delay = S.d_ctrl + S.d_data * len;
-  const int64_t l_next = len < mb ? lat[len] : lat[mb - 1];
+  // affine rows need no table loads: l(b) = aff_a * b + aff_b
+  const int64_t l_next = P.affine ? P.aff_a * (len < mb ? len + 1 : mb) + P.aff_b
+                                  : (len < mb ? lat[len] : lat[mb - 1]);
   const int64_t exec = now + delay > d - l_next ? now + delay : d - l_next;
   const int64_t f = exec - delay;
   const int64_t fire = f < now ? now : f;
@@ -390,7 +392,7 @@ SYM_HD void lean_batch(const Shard& S, int32_t m, int32_t q, int32_t k, EvBatch&
   e.ap = aself_at(S, pos);
   e.chain = 0;
   e.exec = exec;
-  e.lat = lat[len - 1];
+  e.lat = P.affine ? P.aff_a * len + P.aff_b : lat[len - 1];
   e.size = len;
   e.first = P.off + q;
   e.model = m;
