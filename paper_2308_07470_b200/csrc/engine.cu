@@ -847,25 +847,33 @@ k_nxt_tma(const int64_t* __restrict__ tick, const Shard* __restrict__ shards,
         const int32_t ub = off + cnt < send ? off + cnt : send;  // this model's staged part
         for (int32_t e = a - t0 + lane; e < ub - t0; e += 32) u[e] += c1 * (t0 + e - off);
         __syncwarp();
+        // two positions per lane per iteration (p and p + 32): their searches
+        // interleave, so one's shared-memory latency hides behind the other's
+        auto finish = [&](int32_t pp, bool fast, int32_t x, int64_t uq, int64_t ukk) {
+          const int32_t v = fast ? (ukk <= uq + D2 ? pp + x + 1 : NX_UNSURE)
+                                 : lean_chain_next_affine(S, mk, pp - off);
+          nxt[pp] = v;
+          close_k[pp] = v >= 0 ? v - 1 - off : (v == NX_LAST ? cnt - 1 : -1);
+          if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = pp;
+        };
 #pragma unroll 1
-        for (int32_t p = a + lane; p < seg_end; p += 32) {
-          const int e = p - t0;
-          const int64_t uq = u[e];
-          const int64_t T = uq + D1;
-          int32_t v;
-          if (p <= pfull && u[e + kNxtWin] >= T) {
-            // the batch closes within 32 arrivals: first j in (p, p+32] with u_j >= T
-            int32_t x = 0;
+        for (int32_t p = a + lane; p < seg_end; p += 64) {
+          const int32_t p2 = p + 32;
+          const bool has2 = p2 < seg_end;
+          const int e = p - t0, e2 = e + 32;  // e2 + 32 < kNxtStage: always staged
+          const int64_t uq = u[e], uq2 = u[e2];
+          const int64_t T = uq + D1, T2 = uq2 + D1;
+          // the batch closes within 32 arrivals: first j in (p, p+32] with u_j >= T
+          const bool f1 = p <= pfull && u[e + kNxtWin] >= T;
+          const bool f2 = p2 <= pfull && u[e2 + kNxtWin] >= T2;
+          int32_t x = 0, x2 = 0;
 #pragma unroll
-            for (int st = kNxtWin / 2; st >= 1; st >>= 1)
-              if (u[e + x + st] < T) x += st;
-            v = u[e + x] <= uq + D2 ? p + x + 1 : NX_UNSURE;
-          } else {  // a long batch or the model's last arrivals: the scalar form
-            v = lean_chain_next_affine(S, mk, p - off);
+          for (int st = kNxtWin / 2; st >= 1; st >>= 1) {
+            if (u[e + x + st] < T) x += st;
+            if (u[e2 + x2 + st] < T2) x2 += st;
           }
-          nxt[p] = v;
-          close_k[p] = v >= 0 ? v - 1 - off : (v == NX_LAST ? cnt - 1 : -1);
-          if (v == NX_UNSURE) unsure[atomicAdd(unsure_n, 1)] = p;
+          finish(p, f1, x, uq, u[e + x]);
+          if (has2) finish(p2, f2, x2, uq2, u[e2 + x2]);
         }
       } else {  // other profiles / policies: the scalar lean forms
         const int32_t m = k - slot_base[sh];
