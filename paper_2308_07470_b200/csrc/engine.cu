@@ -1089,11 +1089,14 @@ __global__ void k_bid(const BatchRec* __restrict__ recs, const int64_t* __restri
     first = r.first;
     size = r.size;
   }
+#pragma unroll 4
   for (int b = 0; b < 32; b++) {
     const int32_t rb = __shfl_sync(0xffffffffu, ri, b);
     const int32_t fb = __shfl_sync(0xffffffffu, first, b);
     const int32_t sb = __shfl_sync(0xffffffffu, size, b);
-    for (int32_t j = lane; j < sb; j += 32) bid[fb + j] = rb;
+    if (lane < sb) bid[fb + lane] = rb;  // runs of at most 32: one predicated store
+    if (sb > 32)
+      for (int32_t j = lane + 32; j < sb; j += 32) bid[fb + j] = rb;
   }
 }
 
