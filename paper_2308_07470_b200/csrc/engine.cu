@@ -115,6 +115,7 @@ struct Ctx {
   int32_t *d_jC = nullptr;          // J_64 kept while J_256 is built
   int32_t *d_unsure = nullptr;      // [n] positions the lean pointer could not certify
   int32_t *d_unsure_n = nullptr;    // [1] their count
+  int32_t *d_cpoff = nullptr;       // [M+1] compact checkpoint offsets (k_cp_scan)
   int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
           *d_cp_model = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
@@ -1380,43 +1381,117 @@ __global__ void k_walk_fill(int32_t* __restrict__ cp_pos, int32_t* __restrict__ 
 // the fresh-start records along the chain, and add their drops.
 // One thread per kSub batches of a checkpoint (4 threads per J_64
 // checkpoint, started by J_16 hops): lists the batch starts in chain order.
-__global__ void k_walk_expand(const int32_t* __restrict__ cp_pos,
-                              const int32_t* __restrict__ cp_model, int64_t ncp,
-                              const ModelParam* __restrict__ mp_all,
-                              const int32_t* __restrict__ slot_base, int32_t P,
-                              const int32_t* __restrict__ nxt,
-                              const int32_t* __restrict__ j16,
-                              const int32_t* __restrict__ special,
-                              const Shard* __restrict__ shards,
-                              EvBatch* __restrict__ evb,
-                              unsigned long long* __restrict__ mdrops) {
-  constexpr int kPer = kJump / kSub;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t q = t / kPer;
-  const int sub = (int)(t % kPer);
-  if (q >= ncp) return;
-  const int32_t k = cp_model[q];
-  if (k < 0 || special[k]) return;
-  const ModelParam& mp = mp_all[k];
-  const int64_t c = q - (mp.off / kJump + k);  // checkpoint ordinal
-  const int s = shard_of_slot(slot_base, P, k);
-  int32_t p = cp_pos[q];
-  for (int h = 0; h < sub && p >= 0; h++) p = j16[p];
-  if (p < 0) return;  // the chain ends before this thread's batches
-  int64_t out = mp.off + c * kJump + sub * kSub;
-  for (int j = 0; j < kSub && p >= 0; j++) {
-    const int32_t v = nxt[p];
-    if (v == NX_NONE) {  // trailing all-dropped scan: count its drops
-      const FreshRec r = fresh_scan(shards[s], k - slot_base[s], p - mp.off, kFreshMaxSteps);
-      atomicAdd(&mdrops[k], (unsigned long long)r.drops);
-      break;
+// Compact checkpoint numbering for k_walk_expand: cpoff[k] = first compact
+// checkpoint of model k (exclusive scan of max(1, ceil(nb / kJump)) over the
+// models k_walk walked; special models have none), cpoff[M] = the total.
+// k_walk lays checkpoints out in per-model slot ranges sized by arrivals
+// (~10x the batches), so a launch over slots would leave 90 % of its threads
+// idle beside the few that walk.
+__global__ void __launch_bounds__(1024)
+k_cp_scan(const ModelParam* __restrict__ mp_all, int32_t M, const int32_t* __restrict__ nb,
+          const int32_t* __restrict__ special, int32_t* __restrict__ cpoff) {
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int32_t b0 = 0; b0 < M; b0 += 1024) {
+    const int32_t k = b0 + threadIdx.x;
+    int32_t v = 0;
+    if (k < M && mp_all[k].cnt > 0 && !special[k]) v = max(1, (nb[k] + kJump - 1) / kJump);
+    int32_t tot;
+    const int32_t ex = block_exclusive_scan(v, &tot);
+    const int32_t c = carry;
+    if (k < M) cpoff[k] = c + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cpoff[M] = carry;
+}
+
+// One warp per checkpoint (compact numbering), persistent: the checkpoint's
+// <= 64 batch starts lie in a short run of its model's positions, so the
+// chain pointers of kExpandWin positions from the checkpoint arrive in shared
+// memory by one bulk copy (cp.async.bulk on an mbarrier) issued one
+// checkpoint ahead into the warp's other buffer; lane 0 follows the chain
+// through shared memory (global loads only past the window), and the warp
+// writes the starts to bstart[] coalesced (k_chain_recs reads them there,
+// not from the 56-byte EvBatch records).
+constexpr int kExpandWin = 1024;
+constexpr int kExpandWarps = 8;
+constexpr int kExpandList = kJump + 4;  // batch starts | count
+constexpr int kExpandSmem = kExpandWarps * (2 * kExpandWin * 4 + kExpandList * 4 + 16);
+__global__ void __launch_bounds__(32 * kExpandWarps)
+k_walk_expand(const int32_t* __restrict__ cp_pos, const int32_t* __restrict__ cpoff, int32_t M,
+              const ModelParam* __restrict__ mp_all,
+              const int32_t* __restrict__ slot_base, int32_t P,
+              const int32_t* __restrict__ nxt, const Shard* __restrict__ shards,
+              int32_t* __restrict__ bstart, unsigned long long* __restrict__ mdrops) {
+  extern __shared__ __align__(128) unsigned char ex_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t(*win)[kExpandWin] =
+      reinterpret_cast<int32_t(*)[kExpandWin]>(ex_smem + w * 2 * kExpandWin * 4);
+  int32_t* lst = reinterpret_cast<int32_t*>(ex_smem + kExpandWarps * 2 * kExpandWin * 4) +
+                 w * kExpandList;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(
+                      ex_smem + kExpandWarps * (2 * kExpandWin + kExpandList) * 4) + w * 2;
+  const int32_t total = cpoff[M];
+  const int32_t W = gridDim.x * kExpandWarps;
+  int32_t c = blockIdx.x * kExpandWarps + w;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // checkpoint cc: model k, ordinal, first position, window base (16-byte aligned)
+  int32_t k = 0, ord = 0, p0 = 0, base = 0;
+  auto locate = [&](int32_t cc) {
+    k = warp_last_le(cpoff, M, cc, lane);  // cpoff[k] <= cc < cpoff[k+1]
+    ord = cc - cpoff[k];
+    p0 = cp_pos[mp_all[k].off / kJump + k + ord];
+    base = p0 & ~3;
+  };
+  // reads up to kExpandWin - 1 past n (capacity n + 1024); never used
+  auto issue = [&](int b) { bulk_load(win[b], nxt + base, kExpandWin * 4, &bar[b]); };
+  if (c < total) {
+    locate(c);
+    if (lane == 0) issue(0);
+  }
+  uint32_t phase = 0;
+  for (int b = 0; c < total; c += W, b ^= 1) {
+    const int32_t ck = k, cord = ord, cp0 = p0, cbase = base;
+    if (c + W < total) {  // the next checkpoint's window, one ahead
+      locate(c + W);
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(b ^ 1);
+      }
     }
-    if (v == NX_SPECIAL) break;
-    EvBatch& e = evb[out++];
-    e.first = p;  // batch fields filled by k_chain_recs
-    e.model = k - slot_base[s];
-    if (v == NX_LAST) break;
-    p = v;
+    const ModelParam& mp = mp_all[ck];
+    mbar_wait(&bar[b], (phase >> b) & 1);
+    phase ^= 1u << b;
+    if (lane == 0) {
+      int32_t p = cp0, cnt = 0;
+      for (int j = 0; j < kJump && p >= 0; j++) {
+        const int32_t v = p - cbase < kExpandWin ? win[b][p - cbase] : nxt[p];
+        if (v == NX_NONE) {  // trailing all-dropped scan: count its drops
+          const int s = shard_of_slot(slot_base, P, ck);
+          const FreshRec r = fresh_scan(shards[s], ck - slot_base[s], p - mp.off, kFreshMaxSteps);
+          atomicAdd(&mdrops[ck], (unsigned long long)r.drops);
+          break;
+        }
+        if (v == NX_SPECIAL) break;
+        lst[cnt++] = p;
+        if (v == NX_LAST) break;
+        p = v;
+      }
+      lst[kJump] = cnt;
+    }
+    __syncwarp();
+    const int32_t n_list = lst[kJump];
+    const int64_t out = mp.off + (int64_t)cord * kJump;  // this checkpoint's batch slots
+    for (int e = lane; e < n_list; e += 32) bstart[out + e] = lst[e];
+    __syncwarp();  // every lane is done with buffer b and the list before reuse
   }
 }
 
@@ -1429,6 +1504,7 @@ k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_
              const int32_t* __restrict__ nb, const int32_t* __restrict__ bbase,
              const int32_t* __restrict__ special, int64_t nt, EvBatch* __restrict__ evb,
              unsigned long long* __restrict__ mdrops, const int32_t* __restrict__ close_k,
+             const int32_t* __restrict__ bstart,
              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
              uint32_t* __restrict__ fail, int tb) {
   const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1444,11 +1520,12 @@ k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_
   EvBatch& e = evb[p];
   if (!special[lo]) {  // special models' records come from k_evolve
     const int32_t m = lo - slot_base[s];
-    const int32_t ck = close_k[e.first];
+    const int32_t first = bstart[p];  // listed by k_walk_expand
+    const int32_t ck = close_k[first];
     if (ck >= 0) {  // certified by the lean sweep: O(1) from (q, k)
-      lean_batch(shards[s], m, e.first - mp.off, ck, e);
+      lean_batch(shards[s], m, first - mp.off, ck, e);
     } else {
-      const FreshRec r = fresh_scan(shards[s], m, e.first - mp.off, kFreshMaxSteps);
+      const FreshRec r = fresh_scan(shards[s], m, first - mp.off, kFreshMaxSteps);
       e.t = r.mt_t;
       e.a = r.mt_a;
       e.tp = r.mt_tp;
@@ -1469,20 +1546,28 @@ k_chain_recs(const Shard* __restrict__ shards, const int32_t* __restrict__ slot_
   vals[d] = (uint32_t)p;
 }
 
-// K3b: dense batch numbering: bbase[k] per model, sbase[s] per shard
-__global__ void k_nb_scan(const int32_t* __restrict__ nb, int32_t M, int32_t P,
-                          const int32_t* __restrict__ slot_base,
-                          int32_t* __restrict__ bbase, int64_t* __restrict__ sbase) {
-  if (threadIdx.x != 0) return;
-  int64_t run = 0;
-  for (int s = 0; s < P; s++) {
-    sbase[s] = run;
-    for (int k = slot_base[s]; k < slot_base[s + 1]; k++) {
-      bbase[k] = (int32_t)run;
-      run += nb[k];
-    }
+// K3b: dense batch numbering: bbase[k] per model (slot order is
+// shard-major), sbase[s] per shard; one block scan
+__global__ void __launch_bounds__(1024)
+k_nb_scan(const int32_t* __restrict__ nb, int32_t M, int32_t P,
+          const int32_t* __restrict__ slot_base, int32_t* __restrict__ bbase,
+          int64_t* __restrict__ sbase) {
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int32_t b0 = 0; b0 < M; b0 += 1024) {
+    const int32_t k = b0 + threadIdx.x;
+    int32_t tot;
+    const int32_t ex = block_exclusive_scan(k < M ? nb[k] : 0, &tot);
+    const int32_t c = carry;
+    if (k < M) bbase[k] = c + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c + tot;
+    __syncthreads();
   }
-  sbase[P] = run;
+  const int32_t total = carry;
+  for (int32_t sh = threadIdx.x; sh <= P; sh += blockDim.x)
+    sbase[sh] = sh < P && slot_base[sh] < M ? bbase[slot_base[sh]] : total;
 }
 
 // K3c: (shard|tick) keys of every batch, value = its EvBatch index
@@ -2588,17 +2673,19 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                                          ctx->d_special));
     KL(k_walk_fill, nblk(ncp, 256), 256, 0, st>>>(ctx->d_cp_pos, ctx->d_cp_model, ncp,
                                                  ctx->d_jC));
-    KL(k_walk_expand, nblk(ncp * (kJump / kSub), 128), 128, 0, st>>>(
-        ctx->d_cp_pos, ctx->d_cp_model, ncp, ctx->d_mp, ctx->d_slot_base, P, ctx->d_nxt,
-        ctx->d_jB, ctx->d_special, ctx->d_shards, ctx->d_evb,
-        (unsigned long long*)ctx->d_mdrops));
+    KL(k_cp_scan, 1, 1024, 0, st>>>(ctx->d_mp, M, ctx->d_nb, ctx->d_special, ctx->d_cpoff));
+    // J_256 (jA) is dead after k_walk / k_walk_fill: it holds the batch starts
+    KL(k_walk_expand, (unsigned)std::min<int64_t>(nblk(ncp, kExpandWarps), (int64_t)ctx->n_sm * 3),
+       32 * kExpandWarps, kExpandSmem, st>>>(ctx->d_cp_pos, ctx->d_cpoff, M, ctx->d_mp,
+                                             ctx->d_slot_base, P, ctx->d_nxt, ctx->d_shards,
+                                             ctx->d_jA, (unsigned long long*)ctx->d_mdrops));
     // models whose chain needs the general (non-draining) evolution
     KL(k_evolve, nblk(M, 64), 64, 0, st>>>(ctx->d_shards, ctx->d_slot_base, P, M,
                                                      nullptr, ctx->d_evb, ctx->d_nb,
                                                      ctx->d_mdrops, ctx->d_fail,
                                                      ctx->d_special));
   pc.mark("evolve");
-    KL(k_nb_scan, 1, 32, 0, st>>>(ctx->d_nb, M, P, ctx->d_slot_base, ctx->d_bbase,
+    KL(k_nb_scan, 1, 1024, 0, st>>>(ctx->d_nb, M, P, ctx->d_slot_base, ctx->d_bbase,
                                             ctx->d_sbase));
     CK(cudaMemcpyAsync(sbase.data(), ctx->d_sbase, sizeof(int64_t) * (P + 1),
                        cudaMemcpyDeviceToHost, st));
@@ -2608,7 +2695,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
       KL(k_chain_recs, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_shards, ctx->d_slot_base, P, M, ctx->d_mp, ctx->d_nb, ctx->d_bbase,
           ctx->d_special, nt, ctx->d_evb, (unsigned long long*)ctx->d_mdrops, ctx->d_closek,
-          ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits));
+          ctx->d_jA, ctx->d_bkA, ctx->d_bvA, ctx->d_fail, tick_bits));
 
       // key = (shard << tick_bits) | tick: bits in use
       int bits = tick_bits;
@@ -3217,7 +3304,9 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   if ((e = cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, ctx->device)) !=
           cudaSuccess ||
       (e = cudaFuncSetAttribute(k_nxt_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kNxtTmaSmem)) != cudaSuccess)
+                                kNxtTmaSmem)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(k_walk_expand, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kExpandSmem)) != cudaSuccess)
     return fail("k_nxt_tma attributes", e);
   {  // keep pool memory mapped across synchronisations (no remap stalls)
     cudaMemPool_t pool;
@@ -3276,6 +3365,7 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_skip, P);
   ALLOC(ctx->d_changed, 4);
   ALLOC(ctx->d_unsure_n, 1);
+  ALLOC(ctx->d_cpoff, M + 1);
   ALLOC(ctx->d_seg, 4 * (P + 1));
   ALLOC(ctx->d_special, M);
   ALLOC(ctx->d_slo_model, M);
@@ -3392,7 +3482,7 @@ void sym_destroy(void* engine) {
                   ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
                   ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_jC,
-                  ctx->d_unsure, ctx->d_unsure_n, ctx->d_cp_pos, ctx->d_cp_model,
+                  ctx->d_unsure, ctx->d_unsure_n, ctx->d_cpoff, ctx->d_cp_pos, ctx->d_cp_model,
                   ctx->d_special, ctx->d_meta, ctx->d_req,
                   ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
                   ctx->d_net_vals, ctx->d_net_cdf, ctx->d_g_ticks, ctx->d_g_model,
