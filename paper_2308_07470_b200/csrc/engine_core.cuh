@@ -148,7 +148,7 @@ struct ModelState {
                       // the adoption table again (refresh_model)
 };
 
-struct BatchRec {
+struct alignas(16) BatchRec {
   int64_t emitted, start, finish;
   int64_t kt, ksub;   // processing position of the granting event (trace)
   int32_t ka;
