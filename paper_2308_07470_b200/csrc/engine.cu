@@ -391,8 +391,20 @@ __device__ __forceinline__ bool tile_geom(int64_t t, int64_t n, int32_t B, int64
   const int64_t* shard_off = seg + 2 * (P + 1);
   const int64_t* slot_base = seg + 3 * (P + 1);
   if (t >= tile_base[P]) return false;
+  // the tile's sub-cluster: every lane tests one boundary (one load latency,
+  // not a chain of P); called by whole warps
   int s = 0;
-  while (tile_base[s + 1] <= t) s++;
+  if (P <= 32) {
+    const int lane = threadIdx.x & 31;
+    s = __popc(__ballot_sync(0xffffffffu, lane < P && tile_base[lane + 1] <= t));
+  } else {
+    int lo = 0, hi = P;  // last s with tile_base[s] <= t
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (tile_base[mid] <= t) lo = mid; else hi = mid;
+    }
+    s = lo;
+  }
   const int64_t lt = t - tile_base[s];
   g.lo = shard_off[s] + lt * kTileI;
   g.hi = g.lo + kTileI < shard_off[s + 1] ? g.lo + kTileI : shard_off[s + 1];
@@ -534,8 +546,6 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
   int16_t* st_b = reinterpret_cast<int16_t*>(scratch + 32);
   int32_t* mine = wcnt + wib * B;
   for (int b = lane; b < B; b += 32) mine[b] = 0;
-  for (int b = threadIdx.x; b < B; b += blockDim.x)
-    gbase[b] = hist[geo.hbase + (int64_t)b * geo.hstride + geo.col];
   const int64_t lo = geo.lo, hi = geo.hi;
   const int64_t wlo = lo + (int64_t)wib * 32 * kTilePerLane;
   __syncwarp();
@@ -557,6 +567,10 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
   }
   const int64_t before_warp = kMode != 2 && lane == 0 && wlo > 0 && wlo < hi ? tick_in[wlo - 1]
                                                                             : INT64_MIN;
+  // the tile's bin bases (read after the counting barrier), loaded while the
+  // element loads are in flight
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    gbase[b] = hist[geo.hbase + (int64_t)b * geo.hstride + geo.col];
 #pragma unroll
   for (int r = 0; r < kTilePerLane; r++) {
     const int64_t i = wlo + r * 32 + lane;
