@@ -81,10 +81,10 @@ struct Ctx {
   // per-run buffers (grown)
   int64_t cap = 0;
   int64_t *d_ticks = nullptr, *d_s_tick = nullptr, *d_sh_tick = nullptr;
-  int32_t *d_inv = nullptr, *d_bid = nullptr;  // stream -> sorted position, position -> record
+  int32_t *d_bid = nullptr;         // stream index -> batch record (k_bid)
   int32_t *d_model = nullptr, *d_s_g = nullptr, *d_s_i = nullptr;
   int32_t* d_bins = nullptr;        // [B+1] (unused) | shard_off | model_of_slot | gpu_base
-  int32_t *d_sh_i = nullptr, *d_sh_slot = nullptr, *d_inv1 = nullptr;  // P > 1: level 1
+  int32_t *d_sh_i = nullptr, *d_sh_slot = nullptr;  // P > 1: level 1
   int32_t* d_hist = nullptr;        // [B][tiles] bin counts -> positions
   int32_t* d_hist_part = nullptr;   // block sums of its scan
   int32_t *d_bkt = nullptr, *d_bkt_part = nullptr;  // bucket sort counts / ends
@@ -350,11 +350,11 @@ k_scan_down(int32_t* __restrict__ a, int64_t len, const int32_t* __restrict__ pa
 // partitions with few bins each run far faster than one over M + P bins,
 // whose per-tile bin bookkeeping and shared memory (1016 bins for C4 on one
 // B200) starve the SMs.
-//   mode 0 (P = 1):  bin = model          out: s_tick, s_i = i, inv[i] = p
-//   mode 1 (level 1): bin = shard(model)  out: sh_tick, sh_i = i, sh_slot,
-//                                              inv1[i] = j
-//   mode 2 (level 2): bin = sh_slot       out: s_tick, s_g = j, s_i = sh_i[j],
-//                                              inv[j] = p
+//   mode 0 (P = 1):  bin = model          out: s_tick, s_i = i
+//   mode 1 (level 1): bin = shard(model)  out: sh_tick, sh_i = i, sh_slot
+//   mode 2 (level 2): bin = sh_slot       out: s_tick, s_g = j, s_i = sh_i[j]
+// (the inverse maps are optional outputs: the per-request results come from
+// k_bid's by-request record index, so the engine passes none)
 constexpr int kTileWarps = 8;
 constexpr int kTilePerLane = 8;
 constexpr int kTileI = kTileWarps * 32 * kTilePerLane;  // 2048 arrivals per tile
@@ -657,7 +657,7 @@ k_part(const int64_t* __restrict__ tick_in, const int32_t* __restrict__ key,
       st_i[le] = (int32_t)i;
       st_b[le] = (int16_t)bn[r];
       if (kAux) st_a[le] = ax[r];
-      inv_out[i] = gbase[bn[r]] + e;  // coalesced in i
+      if (inv_out) inv_out[i] = gbase[bn[r]] + e;  // coalesced in i
     }
     __syncwarp();
   }
@@ -1084,35 +1084,53 @@ __global__ void k_narrow(const int64_t* __restrict__ in, int64_t n, int32_t* __r
 
 
 // every batch stamps its record index on its member positions
+// Record index of every request, by stream index: bid[s_i[p]] = record for
+// each member position p of each batch record.  The records are interleaved
+// across sub-clusters (thread w: sub-cluster w mod P, its (w / P)-th record),
+// and each sub-cluster's records are in dispatch order, so the requests the
+// resident warps stamp at any moment lie in one short stretch of the stream
+// and their scattered 4-byte writes complete whole sectors in L2.  A warp
+// takes 32 records; each record's members are read (s_i, contiguous) and
+// stamped by the whole warp.  k_out then reads bid[i] coalesced instead of
+// the gather chain stream -> sub-cluster stream -> layout -> record.
 __global__ void k_bid(const BatchRec* __restrict__ recs, const int64_t* __restrict__ rec_base,
-                      const int64_t* __restrict__ rec_count, int32_t P, int64_t total,
-                      int32_t* __restrict__ bid) {
-  // a warp takes 32 records; each record's run of positions is written by
-  // the whole warp (one coalesced store per record) instead of by one lane
+                      const int64_t* __restrict__ rec_count, int32_t P, int64_t slots,
+                      const int32_t* __restrict__ s_i, int32_t* __restrict__ bid) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int32_t ri = -1, first = 0, size = 0;
-  if (w < total) {
-    int s = 0;
-    int64_t k = w;
-    while (s < P && k >= rec_count[s]) {
-      k -= rec_count[s];
-      s++;
+  if (w < slots) {
+    const int s = (int)(w % P);
+    const int64_t k = w / P;
+    if (k < rec_count[s]) {
+      ri = (int32_t)(rec_base[s] + k);
+      const BatchRec& r = recs[ri];
+      first = r.first;
+      size = r.size;
     }
-    ri = (int32_t)(rec_base[s] + k);
-    const BatchRec& r = recs[ri];
-    first = r.first;
-    size = r.size;
   }
-#pragma unroll 4
-  for (int b = 0; b < 32; b++) {
-    const int32_t rb = __shfl_sync(0xffffffffu, ri, b);
-    const int32_t fb = __shfl_sync(0xffffffffu, first, b);
-    const int32_t sb = __shfl_sync(0xffffffffu, size, b);
-    if (lane < sb) bid[fb + lane] = rb;  // runs of at most 32: one predicated store
-    if (sb > 32)
-      for (int32_t j = lane + 32; j < sb; j += 32) bid[fb + j] = rb;
+  // eight records at a time: their member loads are all issued before any
+  // store (one latency per eight records); runs beyond 32 members afterwards
+  for (int b0 = 0; b0 < 32; b0 += 8) {
+    int32_t tgt[8], rbv[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int32_t fb = __shfl_sync(0xffffffffu, first, b0 + q);
+      const int32_t sb = __shfl_sync(0xffffffffu, size, b0 + q);
+      rbv[q] = __shfl_sync(0xffffffffu, ri, b0 + q);
+      tgt[q] = lane < sb ? s_i[fb + lane] : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+      if (tgt[q] >= 0) bid[tgt[q]] = rbv[q];
   }
+  if (__any_sync(0xffffffffu, size > 32))
+    for (int b = 0; b < 32; b++) {
+      const int32_t rb = __shfl_sync(0xffffffffu, ri, b);
+      const int32_t fb = __shfl_sync(0xffffffffu, first, b);
+      const int32_t sb = __shfl_sync(0xffffffffu, size, b);
+      for (int32_t j = lane + 32; j < sb; j += 32) bid[s_i[fb + j]] = rb;
+    }
 }
 
 // RunResult arrays (simulator.py:74-78, 159-173, 249-258) in stream order:
@@ -1136,19 +1154,20 @@ __device__ __forceinline__ OutRow out_row(int32_t r, const BatchRec* __restrict_
     o.outc = 2;  // OUTCOME_DROPPED
     return o;
   }
-  const BatchRec& b = recs[r];
-  o.disp = b.emitted;
-  o.start = b.start;
-  o.fin = b.finish;
-  o.bat = b.size;
-  o.outc = b.finish <= dl ? 0 : 1;
+  // emitted | start, finish | size: two 16-byte gathers instead of four
+  const longlong2 w0 = __ldg(reinterpret_cast<const longlong2*>(recs + r));
+  const longlong2 w1 = __ldg(reinterpret_cast<const longlong2*>(recs + r) + 1);
+  o.disp = w0.x;
+  o.start = w0.y;
+  o.fin = w1.x;
+  o.bat = (int32_t)(w1.y & 0xffffffff);  // size: the low word (little-endian)
+  o.outc = w1.x <= dl ? 0 : 1;
   return o;
 }
 
 template <bool kVec>
 __global__ void __launch_bounds__(256)
-k_out(int64_t n, const int32_t* __restrict__ inv1, const int32_t* __restrict__ inv,
-      const int32_t* __restrict__ bid, const BatchRec* __restrict__ recs,
+k_out(int64_t n, const int32_t* __restrict__ bid, const BatchRec* __restrict__ recs,
       const int64_t* __restrict__ ticks, const int32_t* __restrict__ model,
       const int64_t* __restrict__ slo_by_model,
       int64_t* __restrict__ disp, int64_t* __restrict__ start,
@@ -1165,7 +1184,7 @@ k_out(int64_t n, const int32_t* __restrict__ inv1, const int32_t* __restrict__ i
       if (o_arr) o_arr[k] = tick;
       if (o_dl) o_dl[k] = dl;
       if (o_model) o_model[k] = mi;
-      const OutRow o = out_row(bid[inv[inv1 ? inv1[k] : (int32_t)k]], recs, dl);
+      const OutRow o = out_row(bid[k], recs, dl);
       disp[k] = o.disp;
       start[k] = o.start;
       fin[k] = o.fin;
@@ -1176,12 +1195,8 @@ k_out(int64_t n, const int32_t* __restrict__ inv1, const int32_t* __restrict__ i
   }
   const longlong2 t2 = *reinterpret_cast<const longlong2*>(ticks + i);
   const int2 m2 = *reinterpret_cast<const int2*>(model + i);
-  // sorted position: inv[i] (one sub-cluster) or inv[inv1[i]] (several:
-  // stream -> sub-cluster stream -> layout)
-  int2 j2 = make_int2((int32_t)i, (int32_t)i + 1);
-  if (inv1) j2 = *reinterpret_cast<const int2*>(inv1 + i);
-  const int32_t p0 = inv[j2.x], p1 = inv[j2.y];
-  const int32_t r0 = bid[p0], r1 = bid[p1];
+  const int2 r2 = *reinterpret_cast<const int2*>(bid + i);  // records, by request
+  const int32_t r0 = r2.x, r1 = r2.y;
   const int64_t dl0 = t2.x + slo_by_model[m2.x], dl1 = t2.y + slo_by_model[m2.y];
   const OutRow a = out_row(r0, recs, dl0), b = out_row(r1, recs, dl1);
   if (o_arr) *reinterpret_cast<longlong2*>(o_arr + i) = t2;
@@ -1859,7 +1874,8 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
   o.shrunk_from = 0;
   // four 16-byte stores instead of eleven field stores (the kernel is bound
   // by the LSU queue)
-  static_assert(sizeof(BatchRec) == 64, "BatchRec is four 16-byte words");
+  static_assert(sizeof(BatchRec) == 64 && offsetof(BatchRec, size) == 24,
+                "BatchRec is four 16-byte words, size in the second");
   const int4* src = reinterpret_cast<const int4*>(&o);
   int4* dst = reinterpret_cast<int4*>(recs + rec_base[s] + r);
 #pragma unroll
@@ -2333,9 +2349,8 @@ int ensure_capacity(Ctx* ctx, int64_t n) {
     if ((rc = grow(ctx, ctx->d_ticks, c)) || (rc = grow(ctx, ctx->d_model, c)) ||
         (rc = grow(ctx, ctx->d_s_tick, c)) || (rc = grow(ctx, ctx->d_sh_tick, c)) ||
         (rc = grow(ctx, ctx->d_s_g, c)) || (rc = grow(ctx, ctx->d_s_i, c)) ||
-        (rc = grow(ctx, ctx->d_inv, c)) || (rc = grow(ctx, ctx->d_bid, c)) ||
+        (rc = grow(ctx, ctx->d_bid, c)) ||
         (rc = grow(ctx, ctx->d_sh_i, c)) || (rc = grow(ctx, ctx->d_sh_slot, c)) ||
-        (rc = grow(ctx, ctx->d_inv1, c)) ||
         (rc = grow(ctx, ctx->d_scan_part,
                    ((c + kChunkR - 1) / kChunkR + 1) * kDigits / kScanItems + 2)) ||
         (rc = grow(ctx, ctx->d_fresh, c)) ||
@@ -2487,7 +2502,7 @@ struct IngestInfo {
 };
 
 // K1: stable partition of n time-ordered arrivals into the (shard, model)-
-// sorted layout (ctx->d_s_tick, d_s_g, d_s_i, d_sh_tick, d_inv;
+// sorted layout (ctx->d_s_tick, d_s_g, d_s_i, d_sh_tick;
 // per-slot off/cnt into mp_out).  Validates model ids (EPROTO) and the
 // time order (EINVAL) on the device.
 // One stable partition (k_part_count, flat_scan, k_part_binoff, k_part).
@@ -2547,15 +2562,15 @@ int ingest(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model, int64_t n,
     const int32_t zn[2] = {0, (int32_t)n};
     CK(cudaMemcpyAsync(shard_off, zn, sizeof zn, cudaMemcpyHostToDevice, st));
     if ((rc = partition<0>(ctx, d_ticks, d_model, nullptr, n, M, mp_out, nullptr,
-                           ctx->d_s_tick, ctx->d_s_i, nullptr, ctx->d_inv, kt, launches)))
+                           ctx->d_s_tick, ctx->d_s_i, nullptr, nullptr, kt, launches)))
       return rc;
   } else {
     // by sub-cluster (the sub-cluster streams), then each of them by model
     if ((rc = partition<1>(ctx, d_ticks, d_model, nullptr, n, P, nullptr, shard_off,
-                           ctx->d_sh_tick, ctx->d_sh_i, ctx->d_sh_slot, ctx->d_inv1, kt,
+                           ctx->d_sh_tick, ctx->d_sh_i, ctx->d_sh_slot, nullptr, kt,
                            launches)) ||
         (rc = partition<2>(ctx, ctx->d_sh_tick, ctx->d_sh_slot, ctx->d_sh_i, n, M, mp_out,
-                           nullptr, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i, ctx->d_inv, kt,
+                           nullptr, ctx->d_s_tick, ctx->d_s_g, ctx->d_s_i, nullptr, kt,
                            launches)))
       return rc;
   }
@@ -2890,11 +2905,13 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
   }
   const bool expand = !(flags & SYM_FLAG_NO_EXPAND) && out->req_dispatch;
   if (expand && n > 0) {
-    // every position starts as "no batch" (dropped); k_bid stamps the members
+    // every request starts as "no batch" (dropped); k_bid stamps the members
     CK(cudaMemsetAsync(ctx->d_bid, 0xff, sizeof(int32_t) * n, st));
+    int64_t most = 0;
+    for (int s2 = 0; s2 < P; s2++) most = std::max<int64_t>(most, rec_count[s2]);
     if (total > 0)
-      KL(k_bid, nblk(total, 256), 256, 0, st>>>(ctx->d_recs, d_meta, d_meta + P + 1, P, total,
-                                                ctx->d_bid));
+      KL(k_bid, nblk(most * P, 256), 256, 0, st>>>(ctx->d_recs, d_meta, d_meta + P + 1, P,
+                                                    most * P, ctx->d_s_i, ctx->d_bid));
     auto al16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
     const bool vec = al16(d_ticks) && ((uintptr_t)d_model & 7u) == 0 &&
                      al16(out->req_dispatch) && al16(out->req_start) &&
@@ -2902,12 +2919,12 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
                      al16(out->req_arrival) && al16(out->req_deadline) && al16(out->req_model);
     if (vec)
       KL(k_out<true>, nblk((n + 1) / 2, 256), 256, 0, st>>>(
-          n, P > 1 ? ctx->d_inv1 : nullptr, ctx->d_inv, ctx->d_bid, ctx->d_recs, d_ticks,
+          n, ctx->d_bid, ctx->d_recs, d_ticks,
           d_model, ctx->d_slo_model, out->req_dispatch, out->req_start, out->req_finish,
           out->req_batch, out->req_outcome, out->req_arrival, out->req_deadline, out->req_model));
     else
       KL(k_out<false>, nblk((n + 1) / 2, 256), 256, 0, st>>>(
-          n, P > 1 ? ctx->d_inv1 : nullptr, ctx->d_inv, ctx->d_bid, ctx->d_recs, d_ticks,
+          n, ctx->d_bid, ctx->d_recs, d_ticks,
           d_model, ctx->d_slo_model, out->req_dispatch, out->req_start, out->req_finish,
           out->req_batch, out->req_outcome, out->req_arrival, out->req_deadline, out->req_model));
   }
@@ -3494,9 +3511,9 @@ void sym_destroy(void* engine) {
                   ctx->d_pqt, ctx->d_gtf, ctx->d_mltv, ctx->d_mbtv,
                   ctx->d_shards, ctx->d_ticks, ctx->d_s_tick, ctx->d_sh_tick,
                   ctx->d_model, ctx->d_s_g,   ctx->d_s_i,
-                  ctx->d_inv, ctx->d_bid, ctx->d_scan_part, ctx->d_closek,
+                  ctx->d_bid, ctx->d_scan_part, ctx->d_closek,
                   ctx->d_bins,   ctx->d_err,   ctx->d_fresh, ctx->d_hist, ctx->d_hist_part, ctx->d_bkt, ctx->d_bkt_part, ctx->d_seg, ctx->d_sh_i,
-                  ctx->d_sh_slot, ctx->d_inv1,
+                  ctx->d_sh_slot,
                   ctx->d_recs, ctx->d_drop_t, ctx->d_drop_ks, ctx->d_drop_ka,
                   ctx->d_evb, ctx->d_bkA, ctx->d_bkB, ctx->d_tkA, ctx->d_tkB,
                   ctx->d_bvA, ctx->d_bvB, ctx->d_tvA, ctx->d_tvB, ctx->d_ptrA,

@@ -149,10 +149,13 @@ struct ModelState {
 };
 
 struct alignas(16) BatchRec {
+  // the first 32 bytes are what the per-request results need (k_out reads
+  // them as two 16-byte words)
   int64_t emitted, start, finish;
+  int32_t size, model;
   int64_t kt, ksub;   // processing position of the granting event (trace)
   int32_t ka;
-  int32_t model, gpu, size;
+  int32_t gpu;
   int32_t first;      // sorted-stream position of the first member
   int32_t shrunk_from;// pre-grant candidate size if it shrank, else 0
 };
