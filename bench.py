@@ -69,13 +69,14 @@ def design_bytes(kernel: str, n: int, nb: int, shards: int) -> float | None:
         "k_fresh": n * (8 + 4 + 4 + FRESH_REC_BYTES + 4),
         "k_nxt_general": 0,
         "k_chain_recs": n * (8 + 4 + 4) + nb * (4 + EV_BATCH_BYTES + 8 + 4),
-        "k_walk_expand": nb * (4 + EV_BATCH_BYTES),
+        "k_walk_expand": nb * (64 + 4),   # 4 KB pointer window per 64 batches + the start
+        "k_cp_scan": 0,
         "k_token_keys": nb * (4 + 8 + EV_BATCH_BYTES + 8 + 4),
         "k_jump4": n * (4 + 4),
         "k_bkt_scatter": nb * (12 + 12),
         "k_fast_emit": nb * (EV_BATCH_BYTES + 12 + 4 + 8 + BATCH_REC_BYTES),
-        "k_bid": nb * BATCH_REC_BYTES + n * 4,
-        "k_out": n * (4 + 4 + 8 + 4 + 5 * 8) + nb * BATCH_REC_BYTES,
+        "k_bid": nb * BATCH_REC_BYTES + n * (4 + 4),        # records, s_i, bid by request
+        "k_out": n * (8 + 4 + 4 + 5 * 8) + nb * BATCH_REC_BYTES,  # tick, model, bid; 5 results
         "k_copy_batches": nb * (BATCH_REC_BYTES + 4 + 64),
     }
     return table.get(kernel)
