@@ -116,6 +116,11 @@ struct Ctx {
   int32_t *d_unsure = nullptr;      // [n] positions the lean pointer could not certify
   int32_t *d_unsure_n = nullptr;    // [1] their count
   int32_t *d_cpoff = nullptr;       // [M+1] compact checkpoint offsets (k_cp_scan)
+  // tie groups (k_match_coop -> k_tie_fix -> k_fast_emit), per sub-cluster
+  int32_t *d_tie_cnt = nullptr, *d_tie_list = nullptr;
+  int4* d_tie_eff = nullptr;        // effective groups: R, E, pair offset, pair count
+  int2* d_tie_sig = nullptr;        // label pairs old -> new
+  uint32_t* d_tie_mask = nullptr;   // [P][32] hashed old labels
   int32_t *d_nxt = nullptr, *d_jA = nullptr, *d_jB = nullptr, *d_cp_pos = nullptr,
           *d_cp_model = nullptr;
   int64_t *d_drop_t = nullptr, *d_drop_ks = nullptr;
@@ -1755,80 +1760,174 @@ __global__ void k_token_keys(const uint32_t* __restrict__ bvals, int64_t nt,
   tvals[i] = (uint32_t)(i - sbase[s]);
 }
 
-// The whole matching phase in one cooperative launch: match (batch r pops
-// token r) -> pointer jumping to convergence -> re-sort equal-finish token
-// groups by the resolved gid, repeated until no group moves.  Grid-wide
-// syncs replace the host round trips; convergence flags alternate by parity
-// so a flag is reset one phase before it is written.
+constexpr int kTieMax = 256;    // tie groups listed per sub-cluster
+constexpr int kTieEff = 64;     // effective (re-sorted) groups per sub-cluster
+constexpr int kTieX = 256;      // sigma pairs (= explicit labels) per sub-cluster
+constexpr int kTieGroup = 64;   // tokens per tie group
+
+// The matching phase in one cooperative launch: match (batch r pops token
+// r) -> pointer jumping to convergence -> list the equal-finish token groups
+// (k_tie_fix orders them by gid; k_fast_emit applies the relabelling).
+// Grid-wide syncs replace host round trips.
 __global__ void __launch_bounds__(256)
 k_match_coop(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bvals,
              int64_t nt, const int64_t* __restrict__ sbase,
              const Shard* __restrict__ shards, const uint64_t* __restrict__ tkeys,
              uint32_t* __restrict__ tvals, int32_t* __restrict__ ptrA,
-             int32_t* __restrict__ flags, int tb) {
+             int32_t* __restrict__ flags, int tb, int32_t* __restrict__ tie_cnt,
+             int32_t* __restrict__ tie_list) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid0 == 0) flags[0] = flags[1] = flags[2] = flags[3] = 0;
-  grid.sync();
-  for (int it = 0; it < 16; it++) {
-    for (int64_t i = tid0; i < nt; i += stride) {  // match
-      const int s = (int)(bkeys[i] >> tb);
-      const int64_t r = i - sbase[s];
-      const int32_t G = shards[s].G;
-      if (r < G) {
-        ptrA[i] = -(int32_t)r - 1;
-      } else {
-        const int64_t c = tvals[sbase[s] + (r - G)];
-        ptrA[i] = c < r ? (int32_t)(sbase[s] + c) : -1;
-      }
+  (void)flags;
+  for (int64_t i = tid0; i < nt; i += stride) {  // match
+    const int s = (int)(bkeys[i] >> tb);
+    const int64_t r = i - sbase[s];
+    const int32_t G = shards[s].G;
+    if (r < G) {
+      ptrA[i] = -(int32_t)r - 1;
+    } else {
+      const int64_t c = tvals[sbase[s] + (r - G)];
+      ptrA[i] = c < r ? (int32_t)(sbase[s] + c) : -1;
     }
-    grid.sync();
-    // Resolve gids by pointer jumping IN PLACE and without barriers: every
-    // entry always holds an ancestor on its creator chain (or the resolved
-    // -gid-1), so reading a neighbour's stale or freshly jumped value is
-    // equally valid, and each jump strictly shortens the remaining chain.
-    // Loads bypass L1 (other SMs write these entries).  Each thread sweeps
-    // its entries until all are resolved: ~log2(depth) sweeps, one grid
-    // barrier in total instead of two per doubling round.
-    for (bool open = true; open;) {
-      open = false;
-      for (int64_t i = tid0; i < nt; i += stride) {
-        const int32_t v = __ldcg(ptrA + i);
-        if (v < 0) continue;
-        const int32_t w = __ldcg(ptrA + v);
-        __stcg(ptrA + i, w);
-        open |= w >= 0;
-      }
-    }
-    grid.sync();
-    if (tid0 == 0) flags[2 + ((it + 1) & 1)] = 0;
-    bool moved = false;
-    for (int64_t i = tid0; i < nt; i += stride) {  // equal-finish groups by gid
-      if (i > 0 && tkeys[i - 1] == tkeys[i]) continue;
-      if (i + 1 >= nt || tkeys[i + 1] != tkeys[i]) continue;
-      const int64_t base = sbase[tkeys[i] >> tb];
-      int64_t e = i + 1;
-      while (e < nt && tkeys[e] == tkeys[i]) e++;
-      for (int64_t a = i + 1; a < e; a++) {
-        const uint32_t v = tvals[a];
-        const int32_t gv = -ptrA[base + v] - 1;
-        int64_t b = a;
-        while (b > i && -ptrA[base + tvals[b - 1]] - 1 > gv) {
-          tvals[b] = tvals[b - 1];
-          b--;
-          moved = true;
-        }
-        tvals[b] = v;
-      }
-    }
-    if (moved) flags[2 + (it & 1)] = 1;
-    grid.sync();
-    if (tid0 == 0) flags[1] = it + 1;  // passes run (SYM_DEBUG_TIMING=1 prints it)
-    if (flags[2 + (it & 1)] == 0) break;
-    grid.sync();
   }
+  grid.sync();
+  // Resolve gids by pointer jumping IN PLACE and without barriers: every
+  // entry always holds an ancestor on its creator chain (or the resolved
+  // -gid-1), so reading a neighbour's stale or freshly jumped value is
+  // equally valid, and each jump strictly shortens the remaining chain.
+  // Loads bypass L1 (other SMs write these entries).  Each thread sweeps
+  // its entries until all are resolved: ~log2(depth) sweeps, one grid
+  // barrier in total instead of two per doubling round.
+  for (bool open = true; open;) {
+    open = false;
+    for (int64_t i = tid0; i < nt; i += stride) {
+      const int32_t v = __ldcg(ptrA + i);
+      if (v < 0) continue;
+      const int32_t w = __ldcg(ptrA + v);
+      __stcg(ptrA + i, w);
+      open |= w >= 0;
+    }
+  }
+  // equal-finish token groups: listed per sub-cluster for k_tie_fix (a
+  // handful per sub-cluster: C4 has 5-6 in 870k batches)
+  for (int64_t i = tid0; i < nt; i += stride) {
+    if (i > 0 && tkeys[i - 1] == tkeys[i]) continue;
+    if (i + 1 >= nt || tkeys[i + 1] != tkeys[i]) continue;
+    const int s = (int)(tkeys[i] >> tb);
+    const int32_t slot = atomicAdd(&tie_cnt[s], 1);
+    if (slot < kTieMax) tie_list[(int64_t)s * kTieMax + slot] = (int32_t)(i - sbase[s]);
+  }
+}
+
+// Equal-finish tokens must pop in gid order, but the gids depend on which
+// batch pops which token.  k_match_coop resolved the gids with each tie
+// group in creator order; here one thread per sub-cluster walks its tie
+// groups in rank order.  Re-sorting group g (tokens a..b, popped by the
+// batches R = a + G ... R + k - 1) by its creators' labels swaps which chain
+// continues through which of those batches: every later batch whose label
+// is one of the group's old labels L_j lies on that chain after R + j, so
+// its label becomes L'_j (sigma_g), and batch R + j itself gets L'_j.  A
+// batch's final label is its pass-one gid with the sigmas of the groups
+// below it applied in rank order (a few label pairs in all: C4 has 5-6 tie
+// groups per sub-cluster), so k_fast_emit reads every final gid in passing
+// instead of the match and the pointer jumping running again.  A creator inside its
+// own group, or more groups or pairs than the scratch holds, sends the
+// sub-cluster to the exact chain (FP_TOKEN_TIE); k_fast_emit re-checks every
+// tie against the final gids.
+__device__ __forceinline__ int32_t tie_label(int32_t x, int32_t lab,
+                                             const int4* __restrict__ eff, int32_t neff,
+                                             const int2* __restrict__ sig) {
+  for (int32_t m = 0; m < neff; m++) {
+    const int4 e = eff[m];  // R, E, pair offset, pair count (= E - R)
+    if (x < e.x) break;
+    if (x < e.y) return sig[e.z + (x - e.x)].y;  // a popping batch: explicit
+    for (int32_t j = 0; j < e.w; j++)
+      if (lab == sig[e.z + j].x) {
+        lab = sig[e.z + j].y;
+        break;
+      }
+  }
+  return lab;
+}
+
+__global__ void k_tie_fix(const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
+                          int32_t P, const uint64_t* __restrict__ tkeys,
+                          uint32_t* __restrict__ tvals, const int32_t* __restrict__ ptrA,
+                          int32_t* __restrict__ tie_cnt, int32_t* __restrict__ tie_list,
+                          int4* __restrict__ tie_eff, int2* __restrict__ tie_sig,
+                          uint32_t* __restrict__ tie_mask, uint32_t* __restrict__ fail) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= P) return;
+  const int32_t cnt = tie_cnt[s];
+  tie_cnt[s] = 0;  // becomes the effective-group count
+  uint32_t* mask = tie_mask + (int64_t)s * 32;  // old labels of every sigma, hashed
+  for (int q = 0; q < 32; q++) mask[q] = 0;
+  if (cnt == 0) return;
+  if (cnt > kTieMax) {
+    atomicOr(&fail[s], FP_TOKEN_TIE);
+    return;
+  }
+  int32_t* list = tie_list + (int64_t)s * kTieMax;
+  for (int32_t a = 1; a < cnt; a++) {  // group starts in rank order
+    const int32_t v = list[a];
+    int32_t b = a;
+    for (; b > 0 && list[b - 1] > v; b--) list[b] = list[b - 1];
+    list[b] = v;
+  }
+  const int64_t base = sbase[s];
+  const int32_t nb = (int32_t)(sbase[s + 1] - base), G = shards[s].G;
+  const int32_t* gid1 = ptrA + base;
+  int4* eff = tie_eff + (int64_t)s * kTieEff;
+  int2* sig = tie_sig + (int64_t)s * kTieX;
+  int32_t neff = 0, used = 0;
+  for (int32_t q = 0; q < cnt; q++) {
+    const int32_t a = list[q];
+    int32_t k = 1;
+    while (a + k < nb && tkeys[base + a + k] == tkeys[base + a]) k++;
+    const int32_t R = a + G;
+    const int32_t kp = R < nb ? min(k, nb - R) : 0;  // tokens some batch pops
+    if (k > kTieGroup) {
+      atomicOr(&fail[s], FP_TOKEN_TIE);
+      return;
+    }
+    int32_t cr[kTieGroup], lab[kTieGroup], ord[kTieGroup];
+    for (int32_t j = 0; j < k; j++) {
+      cr[j] = (int32_t)tvals[base + a + j];
+      if (kp > 0 && cr[j] >= R) {  // a creator inside its own group: the chain decides
+        atomicOr(&fail[s], FP_TOKEN_TIE);
+        return;
+      }
+      lab[j] = tie_label(cr[j], -gid1[cr[j]] - 1, eff, neff, sig);
+      ord[j] = j;
+    }
+    bool moved = false;
+    for (int32_t j = 1; j < k; j++) {  // insertion sort by label (distinct GPUs)
+      const int32_t v = ord[j];
+      int32_t b = j;
+      for (; b > 0 && lab[ord[b - 1]] > lab[v]; b--) {
+        ord[b] = ord[b - 1];
+        moved = true;
+      }
+      ord[b] = v;
+    }
+    if (!moved) continue;
+    for (int32_t j = 0; j < k; j++) tvals[base + a + j] = (uint32_t)cr[ord[j]];
+    if (kp == 0) continue;  // no batch pops these tokens: order only
+    if (neff == kTieEff || used + kp > kTieX) {
+      atomicOr(&fail[s], FP_TOKEN_TIE);
+      return;
+    }
+    for (int32_t j = 0; j < kp; j++) {
+      sig[used + j] = make_int2(lab[j], lab[ord[j]]);
+      mask[(lab[j] >> 5) & 31] |= 1u << (lab[j] & 31);
+    }
+    eff[neff] = make_int4(R, R + kp, used, kp);
+    neff++;
+    used += kp;
+  }
+  tie_cnt[s] = neff;
 }
 
 // K3g: token ties must pop in gid order; emit the BatchRec of every batch
@@ -1839,6 +1938,9 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
                             const uint64_t* __restrict__ tkeys,
                             const uint32_t* __restrict__ tvals,
                             const int32_t* __restrict__ gid,
+                            const int32_t* __restrict__ tie_neff,
+                            const int4* __restrict__ tie_eff, const int2* __restrict__ tie_sig,
+                            const uint32_t* __restrict__ tie_mask,
                             const int64_t* __restrict__ rec_base,
                             const Shard* __restrict__ shards,
                             BatchRec* __restrict__ recs, uint32_t* __restrict__ fail, int tb) {
@@ -1846,10 +1948,24 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
   if (i >= nt) return;
   const int s = (int)(bkeys[i] >> tb);
   const int64_t r = i - sbase[s];
+  // final gid of the sub-cluster's batch d: the pass-one gid, relabelled by
+  // the tie groups below d (k_tie_fix; usually none below)
+  const int32_t neff = tie_neff[s];
+  const int4* eff = tie_eff + (int64_t)s * kTieEff;
+  const int2* sig = tie_sig + (int64_t)s * kTieX;
+  const uint32_t* msk = tie_mask + (int64_t)s * 32;
+  auto final_gid = [&](int32_t d) {
+    const int32_t g = -gid[sbase[s] + d] - 1;
+    // a label no sigma takes as input never changes (and every popping
+    // batch of a group carries such an input label)
+    return neff > 0 && d >= eff[0].x && (msk[(g >> 5) & 31] >> (g & 31) & 1u)
+               ? tie_label(d, g, eff, neff, sig)
+               : g;
+  };
   // token i (shard order) vs token i+1: equal finish => gid order
   if (i + 1 < nt && tkeys[i + 1] == tkeys[i]) {
-    const int32_t g0 = -gid[sbase[s] + tvals[i]] - 1;
-    const int32_t g1 = -gid[sbase[s] + tvals[i + 1]] - 1;
+    const int32_t g0 = final_gid((int32_t)tvals[i]);
+    const int32_t g1 = final_gid((int32_t)tvals[i + 1]);
     if (g0 > g1) atomicOr(&fail[s], FP_TOKEN_TIE);
   }
   const EvBatch& e = evb[bvals[i]];
@@ -1868,7 +1984,7 @@ __global__ void k_fast_emit(const uint64_t* __restrict__ bkeys,
   o.ka = e.a;
   o.ksub = r;  // processing order = rank (the chain counter of the chain)
   o.model = e.model;
-  o.gpu = -gid[i] - 1;
+  o.gpu = final_gid((int32_t)r);
   o.size = e.size;
   o.first = e.first;
   o.shrunk_from = 0;
@@ -2775,25 +2891,28 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * nsm)));
         int64_t a_nt = nt;
         int a_tb = tick_bits;
+        CK(cudaMemsetAsync(ctx->d_tie_cnt, 0, sizeof(int32_t) * P, st));
         void* args[] = {&ctx->d_bkA, &ctx->d_bvA, &a_nt, &ctx->d_sbase, &ctx->d_shards,
-                        &ctx->d_tkA, &ctx->d_tvA, &ctx->d_ptrA, &ctx->d_changed, &a_tb};
+                        &ctx->d_tkA, &ctx->d_tvA, &ctx->d_ptrA, &ctx->d_changed, &a_tb,
+                        &ctx->d_tie_cnt, &ctx->d_tie_list};
         kt.begin("k_match_coop");
         ++launches;
         CK(cudaLaunchCooperativeKernel((void*)k_match_coop, grid, dim3(256), args, 0, st));
         kt.end();
       }
+      KL(k_tie_fix, nblk(P, 32), 32, 0, st>>>(ctx->d_sbase, ctx->d_shards, P, ctx->d_tkA,
+                                               ctx->d_tvA, ctx->d_ptrA, ctx->d_tie_cnt,
+                                               ctx->d_tie_list, ctx->d_tie_eff, ctx->d_tie_sig,
+                                               ctx->d_tie_mask, ctx->d_fail));
   pc.mark("match_loop");
-      if (pc.mode == 1) {
-        int32_t passes = 0;
-        cudaMemcpy(&passes, ctx->d_changed + 1, sizeof(int32_t), cudaMemcpyDeviceToHost);
-        fprintf(stderr, "[sym] match passes %d (%lld batches)\n", passes, (long long)nt);
-      }
       int64_t* d_rb = ctx->d_meta + 2 * (P + 1);
       CK(cudaMemcpyAsync(d_rb, rec_base.data(), sizeof(int64_t) * (P + 1),
                          cudaMemcpyHostToDevice, st));
       KL(k_fast_emit, nblk(nt, 256), 256, 0, st>>>(
           ctx->d_bkA, ctx->d_bvA, nt, ctx->d_evb, ctx->d_sbase, ctx->d_tkA, ctx->d_tvA,
-          ctx->d_ptrA, d_rb, ctx->d_shards, ctx->d_recs, ctx->d_fail, tick_bits));
+          ctx->d_ptrA, ctx->d_tie_cnt, ctx->d_tie_eff, ctx->d_tie_sig, ctx->d_tie_mask, d_rb,
+          ctx->d_shards,
+          ctx->d_recs, ctx->d_fail, tick_bits));
     }
     CK(cudaMemcpyAsync(fail.data(), ctx->d_fail, sizeof(uint32_t) * P,
                        cudaMemcpyDeviceToHost, st));
@@ -3404,6 +3523,11 @@ void* sym_create(const sym_config* cfg, int32_t* status) {
   ALLOC(ctx->d_changed, 4);
   ALLOC(ctx->d_unsure_n, 1);
   ALLOC(ctx->d_cpoff, M + 1);
+  ALLOC(ctx->d_tie_cnt, P);
+  ALLOC(ctx->d_tie_list, (int64_t)P * kTieMax);
+  ALLOC(ctx->d_tie_eff, (int64_t)P * kTieEff);
+  ALLOC(ctx->d_tie_sig, (int64_t)P * kTieX);
+  ALLOC(ctx->d_tie_mask, (int64_t)P * 32);
   ALLOC(ctx->d_seg, 4 * (P + 1));
   ALLOC(ctx->d_special, M);
   ALLOC(ctx->d_slo_model, M);
@@ -3520,7 +3644,8 @@ void sym_destroy(void* engine) {
                   ctx->d_rhist, ctx->d_nb, ctx->d_bbase,
                   ctx->d_changed, ctx->d_mdrops, ctx->d_sbase, ctx->d_fail,
                   ctx->d_skip, ctx->d_nxt, ctx->d_jA, ctx->d_jB, ctx->d_jC,
-                  ctx->d_unsure, ctx->d_unsure_n, ctx->d_cpoff, ctx->d_cp_pos, ctx->d_cp_model,
+                  ctx->d_unsure, ctx->d_unsure_n, ctx->d_cpoff, ctx->d_tie_cnt, ctx->d_tie_list, ctx->d_tie_eff,
+                  ctx->d_tie_sig, ctx->d_tie_mask, ctx->d_cp_pos, ctx->d_cp_model,
                   ctx->d_special, ctx->d_meta, ctx->d_req,
                   ctx->d_drop, ctx->d_dka, ctx->d_bat, ctx->d_slo_model,
                   ctx->d_net_vals, ctx->d_net_cdf, ctx->d_g_ticks, ctx->d_g_model,
