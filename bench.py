@@ -72,6 +72,7 @@ def design_bytes(kernel: str, n: int, nb: int, shards: int) -> float | None:
         "k_walk_expand": nb * (64 + 4),   # 4 KB pointer window per 64 batches + the start
         "k_cp_scan": 0,
         "k_tie_fix": 0,
+        "k_match_iter": 0,
         "k_token_keys": nb * (4 + 8 + EV_BATCH_BYTES + 8 + 4),
         "k_jump4": n * (4 + 4),
         "k_bkt_scatter": nb * (12 + 12),
@@ -477,9 +478,9 @@ def run_b200(args, rank, world, local_rank):
                          "bytes_per_launch": kern[name]["bytes_per_launch"]}
     if "K3" in k123 and "k_tie_fix" in kern:  # the matching phase: the match + the tie groups
         ms3 = sum(kern[k]["ms_per_launch"] * kern[k]["launches_per_step"]
-                  for k in ("k_match_coop", "k_tie_fix"))
+                  for k in ("k_match_coop", "k_tie_fix", "k_match_iter") if k in kern)
         b3 = k123["K3"]["bytes_per_launch"]
-        k123["K3"]["phase"] = {"kernels": "k_match_coop + k_tie_fix", "ms": ms3,
+        k123["K3"]["phase"] = {"kernels": "k_match_coop + k_tie_fix + k_match_iter", "ms": ms3,
                                "achieved_gbs": b3 / (ms3 / 1e3) / 1e9,
                                "frac": b3 / (ms3 / 1e3) / 1e9 / peak}
     if "K1" in k123:  # the whole ingest phase (counts, scans, passes, readback) vs 24 B/request

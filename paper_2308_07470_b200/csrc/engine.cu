@@ -1857,7 +1857,7 @@ __global__ void k_tie_fix(const int64_t* __restrict__ sbase, const Shard* __rest
                           uint32_t* __restrict__ tvals, const int32_t* __restrict__ ptrA,
                           int32_t* __restrict__ tie_cnt, int32_t* __restrict__ tie_list,
                           int4* __restrict__ tie_eff, int2* __restrict__ tie_sig,
-                          uint32_t* __restrict__ tie_mask, uint32_t* __restrict__ fail) {
+                          uint32_t* __restrict__ tie_mask, int32_t* __restrict__ overflow) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= P) return;
   const int32_t cnt = tie_cnt[s];
@@ -1866,7 +1866,7 @@ __global__ void k_tie_fix(const int64_t* __restrict__ sbase, const Shard* __rest
   for (int q = 0; q < 32; q++) mask[q] = 0;
   if (cnt == 0) return;
   if (cnt > kTieMax) {
-    atomicOr(&fail[s], FP_TOKEN_TIE);
+    *overflow = 1;  // k_match_iter redoes the matching
     return;
   }
   int32_t* list = tie_list + (int64_t)s * kTieMax;
@@ -1889,14 +1889,14 @@ __global__ void k_tie_fix(const int64_t* __restrict__ sbase, const Shard* __rest
     const int32_t R = a + G;
     const int32_t kp = R < nb ? min(k, nb - R) : 0;  // tokens some batch pops
     if (k > kTieGroup) {
-      atomicOr(&fail[s], FP_TOKEN_TIE);
+      *overflow = 1;  // k_match_iter redoes the matching
       return;
     }
     int32_t cr[kTieGroup], lab[kTieGroup], ord[kTieGroup];
     for (int32_t j = 0; j < k; j++) {
       cr[j] = (int32_t)tvals[base + a + j];
       if (kp > 0 && cr[j] >= R) {  // a creator inside its own group: the chain decides
-        atomicOr(&fail[s], FP_TOKEN_TIE);
+        *overflow = 1;  // k_match_iter redoes the matching
         return;
       }
       lab[j] = tie_label(cr[j], -gid1[cr[j]] - 1, eff, neff, sig);
@@ -1916,7 +1916,7 @@ __global__ void k_tie_fix(const int64_t* __restrict__ sbase, const Shard* __rest
     for (int32_t j = 0; j < k; j++) tvals[base + a + j] = (uint32_t)cr[ord[j]];
     if (kp == 0) continue;  // no batch pops these tokens: order only
     if (neff == kTieEff || used + kp > kTieX) {
-      atomicOr(&fail[s], FP_TOKEN_TIE);
+      *overflow = 1;  // k_match_iter redoes the matching
       return;
     }
     for (int32_t j = 0; j < kp; j++) {
@@ -1928,6 +1928,87 @@ __global__ void k_tie_fix(const int64_t* __restrict__ sbase, const Shard* __rest
     used += kp;
   }
   tie_cnt[s] = neff;
+}
+
+// Fallback for tie-heavy runs (more tie groups, relabelled labels or
+// group tokens than k_tie_fix's scratch holds, or a creator inside its own
+// group: e.g. C3's 50 % same-tick arrivals): the whole matching phase again,
+// iterated -- match, pointer jumping, re-sort every equal-finish group by
+// gid -- until no group moves.  Launched every run; returns at once unless
+// k_tie_fix raised the overflow flag.
+__global__ void __launch_bounds__(256)
+k_match_iter(const uint64_t* __restrict__ bkeys, const uint32_t* __restrict__ bvals,
+             int64_t nt, const int64_t* __restrict__ sbase,
+             const Shard* __restrict__ shards, const uint64_t* __restrict__ tkeys,
+             uint32_t* __restrict__ tvals, int32_t* __restrict__ ptrA,
+             int32_t* __restrict__ flags, int tb, int32_t* __restrict__ tie_neff,
+             int32_t P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (flags[0] == 0) return;  // no sub-cluster overflowed k_tie_fix (grid-uniform)
+  grid.sync();                 // every thread has read the flag
+  if (tid0 == 0) flags[0] = flags[1] = flags[2] = flags[3] = 0;
+  if (tid0 < P) tie_neff[tid0] = 0;  // the gids below are final: no relabelling
+  grid.sync();
+  for (int it = 0; it < 16; it++) {
+    for (int64_t i = tid0; i < nt; i += stride) {  // match
+      const int s = (int)(bkeys[i] >> tb);
+      const int64_t r = i - sbase[s];
+      const int32_t G = shards[s].G;
+      if (r < G) {
+        ptrA[i] = -(int32_t)r - 1;
+      } else {
+        const int64_t c = tvals[sbase[s] + (r - G)];
+        ptrA[i] = c < r ? (int32_t)(sbase[s] + c) : -1;
+      }
+    }
+    grid.sync();
+    // Resolve gids by pointer jumping IN PLACE and without barriers: every
+    // entry always holds an ancestor on its creator chain (or the resolved
+    // -gid-1), so reading a neighbour's stale or freshly jumped value is
+    // equally valid, and each jump strictly shortens the remaining chain.
+    // Loads bypass L1 (other SMs write these entries).  Each thread sweeps
+    // its entries until all are resolved: ~log2(depth) sweeps, one grid
+    // barrier in total instead of two per doubling round.
+    for (bool open = true; open;) {
+      open = false;
+      for (int64_t i = tid0; i < nt; i += stride) {
+        const int32_t v = __ldcg(ptrA + i);
+        if (v < 0) continue;
+        const int32_t w = __ldcg(ptrA + v);
+        __stcg(ptrA + i, w);
+        open |= w >= 0;
+      }
+    }
+    grid.sync();
+    if (tid0 == 0) flags[2 + ((it + 1) & 1)] = 0;
+    bool moved = false;
+    for (int64_t i = tid0; i < nt; i += stride) {  // equal-finish groups by gid
+      if (i > 0 && tkeys[i - 1] == tkeys[i]) continue;
+      if (i + 1 >= nt || tkeys[i + 1] != tkeys[i]) continue;
+      const int64_t base = sbase[tkeys[i] >> tb];
+      int64_t e = i + 1;
+      while (e < nt && tkeys[e] == tkeys[i]) e++;
+      for (int64_t a = i + 1; a < e; a++) {
+        const uint32_t v = tvals[a];
+        const int32_t gv = -ptrA[base + v] - 1;
+        int64_t b = a;
+        while (b > i && -ptrA[base + tvals[b - 1]] - 1 > gv) {
+          tvals[b] = tvals[b - 1];
+          b--;
+          moved = true;
+        }
+        tvals[b] = v;
+      }
+    }
+    if (moved) flags[2 + (it & 1)] = 1;
+    grid.sync();
+    if (tid0 == 0) flags[1] = it + 1;  // passes run (SYM_DEBUG_TIMING=1 prints it)
+    if (flags[2 + (it & 1)] == 0) break;
+    grid.sync();
+  }
 }
 
 // K3g: token ties must pop in gid order; emit the BatchRec of every batch
@@ -2892,6 +2973,7 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         int64_t a_nt = nt;
         int a_tb = tick_bits;
         CK(cudaMemsetAsync(ctx->d_tie_cnt, 0, sizeof(int32_t) * P, st));
+        CK(cudaMemsetAsync(ctx->d_changed, 0, sizeof(int32_t) * 4, st));  // [0]: overflow
         void* args[] = {&ctx->d_bkA, &ctx->d_bvA, &a_nt, &ctx->d_sbase, &ctx->d_shards,
                         &ctx->d_tkA, &ctx->d_tvA, &ctx->d_ptrA, &ctx->d_changed, &a_tb,
                         &ctx->d_tie_cnt, &ctx->d_tie_list};
@@ -2903,7 +2985,22 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
       KL(k_tie_fix, nblk(P, 32), 32, 0, st>>>(ctx->d_sbase, ctx->d_shards, P, ctx->d_tkA,
                                                ctx->d_tvA, ctx->d_ptrA, ctx->d_tie_cnt,
                                                ctx->d_tie_list, ctx->d_tie_eff, ctx->d_tie_sig,
-                                               ctx->d_tie_mask, ctx->d_fail));
+                                               ctx->d_tie_mask, ctx->d_changed));
+      {  // tie-heavy runs only (returns at once otherwise)
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_match_iter, 256, 0);
+        const int64_t want = (nt + 255) / 256;
+        dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)bps * ctx->n_sm)));
+        int64_t a_nt = nt;
+        int a_tb = tick_bits, a_P = P;
+        void* args[] = {&ctx->d_bkA, &ctx->d_bvA, &a_nt, &ctx->d_sbase, &ctx->d_shards,
+                        &ctx->d_tkA, &ctx->d_tvA, &ctx->d_ptrA, &ctx->d_changed, &a_tb,
+                        &ctx->d_tie_cnt, &a_P};
+        kt.begin("k_match_iter");
+        ++launches;
+        CK(cudaLaunchCooperativeKernel((void*)k_match_iter, grid, dim3(256), args, 0, st));
+        kt.end();
+      }
   pc.mark("match_loop");
       int64_t* d_rb = ctx->d_meta + 2 * (P + 1);
       CK(cudaMemcpyAsync(d_rb, rec_base.data(), sizeof(int64_t) * (P + 1),
