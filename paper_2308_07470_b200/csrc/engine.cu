@@ -1,15 +1,15 @@
 // engine.cu -- B200 (sm_100a) kernels and the C ABI of include/symphony_b200.h.
 //
 // Pipeline of one run (all on the engine's stream, inputs resident in HBM):
-//   K1a k_hist      per-block-chunk histograms of (slot, shard) of the stream
-//   K1b k_scan_*    flat exclusive scan of the bin-major histogram -> stable bases
-//   K1c k_binoff    per-model ModelParam.off/cnt, shard offsets
-//   K1d k_scatter   stable scatter to the (shard, model)-sorted layout with
-//                   warp __match_any_sync ranking (per-warp offsets keep
-//                   stream order without any global atomics)
+//   K1  k_part_count / flat scan / k_part_binoff / k_part
+//                   stable partition to the (shard, model)-sorted layout
+//                   (two passes with several sub-clusters: by sub-cluster,
+//                   then by model), warp __match_any_sync ranking
 //   (A' of an arrival -- same-tick cascades -- is derived on the fly, aself_at)
-//   K2  k_fresh     fresh-start pre-scan (chain fallback only)
-//   K3  k_nxt_pp ... k_fast_emit  the parallel validated path (fastpath.cuh)
+//   K2  k_nxt_tma   batch-chain pointers (bulk-copied tiles, binary search)
+//   K3  k_jump4 / k_walk / k_walk_expand / k_chain_recs / bucket sorts /
+//       k_match_coop / k_tie_fix / k_fast_emit   the parallel validated path
+//       (fastpath.cuh); k_fresh / k_chain for sub-clusters that fail it
 //   K4  k_chain     one CTA per sub-cluster runs the live-event chain
 //   K5  k_bid / k_out  per-request RunResult arrays from batch records
 // The chain (engine_core.cuh) is the only sequential part; everything else is
@@ -936,7 +936,7 @@ k_nxt_general(const Shard* __restrict__ shards, const int32_t* __restrict__ slot
               const ModelParam* __restrict__ mp_all, int32_t P,
               const int32_t* __restrict__ unsure, const int32_t* __restrict__ unsure_n,
               int32_t* __restrict__ nxt, int32_t* __restrict__ close_k) {
-  const int32_t cnt = *unsure_n;  // listed by k_nxt_pp; usually none
+  const int32_t cnt = *unsure_n;  // listed by k_nxt_tma; usually none
   for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < cnt; u += gridDim.x * blockDim.x)
     nxt_general_one(shards, slot_base, mp_all, P, unsure[u], nxt, close_k);
 }
