@@ -1411,10 +1411,6 @@ __global__ void k_walk_fill(int32_t* __restrict__ cp_pos, int32_t* __restrict__ 
   }
 }
 
-// One thread per checkpoint: materialise up to 64 batches (EvBatch) from
-// the fresh-start records along the chain, and add their drops.
-// One thread per kSub batches of a checkpoint (4 threads per J_64
-// checkpoint, started by J_16 hops): lists the batch starts in chain order.
 // Compact checkpoint numbering for k_walk_expand: cpoff[k] = first compact
 // checkpoint of model k (exclusive scan of max(1, ceil(nb / kJump)) over the
 // models k_walk walked; special models have none), cpoff[M] = the total.
@@ -1444,30 +1440,44 @@ k_cp_scan(const ModelParam* __restrict__ mp_all, int32_t M, const int32_t* __res
 
 // One warp per checkpoint (compact numbering), persistent: the checkpoint's
 // <= 64 batch starts lie in a short run of its model's positions, so the
-// chain pointers of kExpandWin positions from the checkpoint arrive in shared
-// memory by one bulk copy (cp.async.bulk on an mbarrier) issued one
-// checkpoint ahead into the warp's other buffer; lane 0 follows the chain
-// through shared memory (global loads only past the window), and the warp
-// writes the starts to bstart[] coalesced (k_chain_recs reads them there,
-// not from the 56-byte EvBatch records).
+// chain pointers (J_1) and the J_16 pointers of kExpandWin positions from the
+// checkpoint arrive in shared memory by bulk copies (cp.async.bulk on one
+// mbarrier) issued one checkpoint ahead into the warp's other buffer.  Lanes
+// 0..3 take J_16 hops to batches 0, 16, 32, 48 and each follows 16 chain
+// pointers through shared memory (global loads only past the window); they
+// write the starts to bstart[] (k_chain_recs reads them there, not from the
+// 56-byte EvBatch records).
 constexpr int kExpandWin = 1024;
-constexpr int kExpandWarps = 8;
-constexpr int kExpandList = kJump + 4;  // batch starts | count
-constexpr int kExpandSmem = kExpandWarps * (2 * kExpandWin * 4 + kExpandList * 4 + 16);
+constexpr int kExpandWarps = 4;
+constexpr int kExpandSmem = kExpandWarps * (4 * kExpandWin * 4 + 16);
+__device__ __forceinline__ void bulk_load2(void* dst0, const void* src0, void* dst1,
+                                           const void* src1, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(2 * bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst0)), "l"(src0), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst1)), "l"(src1), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __global__ void __launch_bounds__(32 * kExpandWarps)
 k_walk_expand(const int32_t* __restrict__ cp_pos, const int32_t* __restrict__ cpoff, int32_t M,
               const ModelParam* __restrict__ mp_all,
               const int32_t* __restrict__ slot_base, int32_t P,
-              const int32_t* __restrict__ nxt, const Shard* __restrict__ shards,
+              const int32_t* __restrict__ nxt, const int32_t* __restrict__ j16,
+              const Shard* __restrict__ shards,
               int32_t* __restrict__ bstart, unsigned long long* __restrict__ mdrops) {
   extern __shared__ __align__(128) unsigned char ex_smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int32_t(*win)[kExpandWin] =
-      reinterpret_cast<int32_t(*)[kExpandWin]>(ex_smem + w * 2 * kExpandWin * 4);
-  int32_t* lst = reinterpret_cast<int32_t*>(ex_smem + kExpandWarps * 2 * kExpandWin * 4) +
-                 w * kExpandList;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(
-                      ex_smem + kExpandWarps * (2 * kExpandWin + kExpandList) * 4) + w * 2;
+  // per warp: [buffer][J_1 | J_16][kExpandWin]
+  int32_t(*win)[2][kExpandWin] =
+      reinterpret_cast<int32_t(*)[2][kExpandWin]>(ex_smem + w * 4 * kExpandWin * 4);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ex_smem + kExpandWarps * 4 * kExpandWin * 4) + w * 2;
   const int32_t total = cpoff[M];
   const int32_t W = gridDim.x * kExpandWarps;
   int32_t c = blockIdx.x * kExpandWarps + w;
@@ -1486,7 +1496,9 @@ k_walk_expand(const int32_t* __restrict__ cp_pos, const int32_t* __restrict__ cp
     base = p0 & ~3;
   };
   // reads up to kExpandWin - 1 past n (capacity n + 1024); never used
-  auto issue = [&](int b) { bulk_load(win[b], nxt + base, kExpandWin * 4, &bar[b]); };
+  auto issue = [&](int b) {
+    bulk_load2(win[b][0], nxt + base, win[b][1], j16 + base, kExpandWin * 4, &bar[b]);
+  };
   if (c < total) {
     locate(c);
     if (lane == 0) issue(0);
@@ -1494,7 +1506,7 @@ k_walk_expand(const int32_t* __restrict__ cp_pos, const int32_t* __restrict__ cp
   uint32_t phase = 0;
   for (int b = 0; c < total; c += W, b ^= 1) {
     const int32_t ck = k, cord = ord, cp0 = p0, cbase = base;
-    if (c + W < total) {  // the next checkpoint's window, one ahead
+    if (c + W < total) {  // the next checkpoint's windows, one ahead
       locate(c + W);
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1504,28 +1516,31 @@ k_walk_expand(const int32_t* __restrict__ cp_pos, const int32_t* __restrict__ cp
     const ModelParam& mp = mp_all[ck];
     mbar_wait(&bar[b], (phase >> b) & 1);
     phase ^= 1u << b;
-    if (lane == 0) {
-      int32_t p = cp0, cnt = 0;
-      for (int j = 0; j < kJump && p >= 0; j++) {
-        const int32_t v = p - cbase < kExpandWin ? win[b][p - cbase] : nxt[p];
-        if (v == NX_NONE) {  // trailing all-dropped scan: count its drops
-          const int s = shard_of_slot(slot_base, P, ck);
-          const FreshRec r = fresh_scan(shards[s], ck - slot_base[s], p - mp.off, kFreshMaxSteps);
-          atomicAdd(&mdrops[ck], (unsigned long long)r.drops);
-          break;
+    if (lane < kJump / kSub) {
+      const int32_t* w1 = win[b][0];
+      const int32_t* w16 = win[b][1];
+      int32_t p = cp0;
+      for (int h = 0; h < lane && p >= 0; h++)
+        p = p - cbase < kExpandWin ? w16[p - cbase] : j16[p];
+      if (p >= 0) {
+        int64_t out = mp.off + (int64_t)cord * kJump + lane * kSub;
+        for (int j = 0; j < kSub && p >= 0; j++) {
+          const int32_t v = p - cbase < kExpandWin ? w1[p - cbase] : nxt[p];
+          if (v == NX_NONE) {  // trailing all-dropped scan: count its drops
+            const int s = shard_of_slot(slot_base, P, ck);
+            const FreshRec r =
+                fresh_scan(shards[s], ck - slot_base[s], p - mp.off, kFreshMaxSteps);
+            atomicAdd(&mdrops[ck], (unsigned long long)r.drops);
+            break;
+          }
+          if (v == NX_SPECIAL) break;
+          bstart[out++] = p;
+          if (v == NX_LAST) break;
+          p = v;
         }
-        if (v == NX_SPECIAL) break;
-        lst[cnt++] = p;
-        if (v == NX_LAST) break;
-        p = v;
       }
-      lst[kJump] = cnt;
     }
-    __syncwarp();
-    const int32_t n_list = lst[kJump];
-    const int64_t out = mp.off + (int64_t)cord * kJump;  // this checkpoint's batch slots
-    for (int e = lane; e < n_list; e += 32) bstart[out + e] = lst[e];
-    __syncwarp();  // every lane is done with buffer b and the list before reuse
+    __syncwarp();  // every lane is done with buffer b before it is refilled
   }
 }
 
@@ -2910,8 +2925,9 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
     // J_256 (jA) is dead after k_walk / k_walk_fill: it holds the batch starts
     KL(k_walk_expand, (unsigned)std::min<int64_t>(nblk(ncp, kExpandWarps), (int64_t)ctx->n_sm * 3),
        32 * kExpandWarps, kExpandSmem, st>>>(ctx->d_cp_pos, ctx->d_cpoff, M, ctx->d_mp,
-                                             ctx->d_slot_base, P, ctx->d_nxt, ctx->d_shards,
-                                             ctx->d_jA, (unsigned long long*)ctx->d_mdrops));
+                                             ctx->d_slot_base, P, ctx->d_nxt, ctx->d_jB,
+                                             ctx->d_shards, ctx->d_jA,
+                                             (unsigned long long*)ctx->d_mdrops));
     // models whose chain needs the general (non-draining) evolution
     KL(k_evolve, nblk(M, 64), 64, 0, st>>>(ctx->d_shards, ctx->d_slot_base, P, M,
                                                      nullptr, ctx->d_evb, ctx->d_nb,
