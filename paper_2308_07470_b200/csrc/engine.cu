@@ -1778,7 +1778,6 @@ __global__ void k_token_keys(const uint32_t* __restrict__ bvals, int64_t nt,
 constexpr int kTieMax = 256;    // tie groups listed per sub-cluster
 constexpr int kTieEff = 64;     // effective (re-sorted) groups per sub-cluster
 constexpr int kTieX = 256;      // sigma pairs (= explicit labels) per sub-cluster
-constexpr int kTieGroup = 64;   // tokens per tie group
 
 // The matching phase in one cooperative launch: match (batch r pops token
 // r) -> pointer jumping to convergence -> list the equal-finish token groups
@@ -1867,82 +1866,135 @@ __device__ __forceinline__ int32_t tie_label(int32_t x, int32_t lab,
   return lab;
 }
 
-__global__ void k_tie_fix(const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
-                          int32_t P, const uint64_t* __restrict__ tkeys,
-                          uint32_t* __restrict__ tvals, const int32_t* __restrict__ ptrA,
-                          int32_t* __restrict__ tie_cnt, int32_t* __restrict__ tie_list,
-                          int4* __restrict__ tie_eff, int2* __restrict__ tie_sig,
-                          uint32_t* __restrict__ tie_mask, int32_t* __restrict__ overflow) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int kTieGroupS = 8;   // tokens per tie group held for the relabelling
+constexpr int kTieThreads = 256;
+static_assert(kTieThreads >= kTieMax, "one thread per listed tie group");
+
+// One block per sub-cluster: the groups' tokens, creators and pass-one gids
+// are loaded in parallel (one thread per group), thread 0 walks the groups
+// in rank order through shared memory, and the block writes the results.
+__global__ void __launch_bounds__(kTieThreads)
+k_tie_fix(const int64_t* __restrict__ sbase, const Shard* __restrict__ shards,
+          int32_t P, const uint64_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
+          const int32_t* __restrict__ ptrA, int32_t* __restrict__ tie_cnt,
+          const int32_t* __restrict__ tie_list, int4* __restrict__ tie_eff,
+          int2* __restrict__ tie_sig, uint32_t* __restrict__ tie_mask,
+          int32_t* __restrict__ overflow) {
+  __shared__ int32_t s_list[kTieMax], g_a[kTieMax], g_k[kTieMax];
+  __shared__ int32_t g_cr[kTieMax][kTieGroupS], g_g1[kTieMax][kTieGroupS];
+  __shared__ int32_t g_ord[kTieMax][kTieGroupS];
+  __shared__ int32_t g_moved[kTieMax];
+  __shared__ int4 e_sm[kTieEff];
+  __shared__ int2 sig_sm[kTieX];
+  __shared__ uint32_t mask_sm[32];
+  __shared__ int32_t s_cnt, s_bad, s_neff, s_used;
+  const int s = blockIdx.x, t = threadIdx.x;
   if (s >= P) return;
-  const int32_t cnt = tie_cnt[s];
-  tie_cnt[s] = 0;  // becomes the effective-group count
-  uint32_t* mask = tie_mask + (int64_t)s * 32;  // old labels of every sigma, hashed
-  for (int q = 0; q < 32; q++) mask[q] = 0;
-  if (cnt == 0) return;
-  if (cnt > kTieMax) {
-    *overflow = 1;  // k_match_iter redoes the matching
-    return;
+  if (t == 0) {
+    s_cnt = tie_cnt[s];
+    s_bad = s_cnt > kTieMax;
+    s_neff = s_used = 0;
   }
-  int32_t* list = tie_list + (int64_t)s * kTieMax;
-  for (int32_t a = 1; a < cnt; a++) {  // group starts in rank order
-    const int32_t v = list[a];
-    int32_t b = a;
-    for (; b > 0 && list[b - 1] > v; b--) list[b] = list[b - 1];
-    list[b] = v;
+  if (t < 32) mask_sm[t] = 0;
+  __syncthreads();
+  const int32_t cnt = s_cnt;
+  if (s_bad) {
+    if (t == 0) {
+      tie_cnt[s] = 0;
+      *overflow = 1;  // k_match_iter redoes the matching
+    }
+    if (t < 32) tie_mask[(int64_t)s * 32 + t] = 0;
+    return;
   }
   const int64_t base = sbase[s];
   const int32_t nb = (int32_t)(sbase[s + 1] - base), G = shards[s].G;
-  const int32_t* gid1 = ptrA + base;
-  int4* eff = tie_eff + (int64_t)s * kTieEff;
-  int2* sig = tie_sig + (int64_t)s * kTieX;
-  int32_t neff = 0, used = 0;
-  for (int32_t q = 0; q < cnt; q++) {
-    const int32_t a = list[q];
-    int32_t k = 1;
-    while (a + k < nb && tkeys[base + a + k] == tkeys[base + a]) k++;
-    const int32_t R = a + G;
-    const int32_t kp = R < nb ? min(k, nb - R) : 0;  // tokens some batch pops
-    if (k > kTieGroup) {
-      *overflow = 1;  // k_match_iter redoes the matching
-      return;
-    }
-    int32_t cr[kTieGroup], lab[kTieGroup], ord[kTieGroup];
-    for (int32_t j = 0; j < k; j++) {
-      cr[j] = (int32_t)tvals[base + a + j];
-      if (kp > 0 && cr[j] >= R) {  // a creator inside its own group: the chain decides
-        *overflow = 1;  // k_match_iter redoes the matching
-        return;
-      }
-      lab[j] = tie_label(cr[j], -gid1[cr[j]] - 1, eff, neff, sig);
-      ord[j] = j;
-    }
-    bool moved = false;
-    for (int32_t j = 1; j < k; j++) {  // insertion sort by label (distinct GPUs)
-      const int32_t v = ord[j];
-      int32_t b = j;
-      for (; b > 0 && lab[ord[b - 1]] > lab[v]; b--) {
-        ord[b] = ord[b - 1];
-        moved = true;
-      }
-      ord[b] = v;
-    }
-    if (!moved) continue;
-    for (int32_t j = 0; j < k; j++) tvals[base + a + j] = (uint32_t)cr[ord[j]];
-    if (kp == 0) continue;  // no batch pops these tokens: order only
-    if (neff == kTieEff || used + kp > kTieX) {
-      *overflow = 1;  // k_match_iter redoes the matching
-      return;
-    }
-    for (int32_t j = 0; j < kp; j++) {
-      sig[used + j] = make_int2(lab[j], lab[ord[j]]);
-      mask[(lab[j] >> 5) & 31] |= 1u << (lab[j] & 31);
-    }
-    eff[neff] = make_int4(R, R + kp, used, kp);
-    neff++;
-    used += kp;
+  if (t < cnt) s_list[t] = tie_list[(int64_t)s * kTieMax + t];
+  __syncthreads();
+  if (t < cnt) {  // rank order of the group starts (distinct)
+    const int32_t a = s_list[t];
+    int32_t pos = 0;
+    for (int32_t u = 0; u < cnt; u++) pos += s_list[u] < a;
+    g_a[pos] = a;
   }
-  tie_cnt[s] = neff;
+  __syncthreads();
+  if (t < cnt) {  // this group's tokens: extent, creators, pass-one gids
+    const int32_t a = g_a[t];
+    int32_t k = 1;
+    while (k <= kTieGroupS && a + k < nb && tkeys[base + a + k] == tkeys[base + a]) k++;
+    const int32_t R = a + G;
+    bool bad = k > kTieGroupS;
+    for (int32_t j = 0; j < k && !bad; j++) {
+      const int32_t c = (int32_t)tvals[base + a + j];
+      g_cr[t][j] = c;
+      if (R < nb && c >= R) bad = true;  // a creator inside its own group
+      else g_g1[t][j] = -ptrA[base + c] - 1;
+    }
+    g_k[t] = k;
+    if (bad) atomicExch(&s_bad, 1);
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (t == 0) {
+      tie_cnt[s] = 0;
+      *overflow = 1;
+    }
+    if (t < 32) tie_mask[(int64_t)s * 32 + t] = 0;
+    return;
+  }
+  if (t == 0) {  // the groups in rank order
+    int32_t neff = 0, used = 0;
+    for (int32_t q = 0; q < cnt && !s_bad; q++) {
+      const int32_t a = g_a[q], k = g_k[q], R = a + G;
+      const int32_t kp = R < nb ? min(k, nb - R) : 0;  // tokens some batch pops
+      int32_t lab[kTieGroupS];
+      for (int32_t j = 0; j < k; j++) {
+        lab[j] = tie_label(g_cr[q][j], g_g1[q][j], e_sm, neff, sig_sm);
+        g_ord[q][j] = j;
+      }
+      bool moved = false;
+      for (int32_t j = 1; j < k; j++) {  // insertion sort by label (distinct GPUs)
+        const int32_t v = g_ord[q][j];
+        int32_t b = j;
+        for (; b > 0 && lab[g_ord[q][b - 1]] > lab[v]; b--) {
+          g_ord[q][b] = g_ord[q][b - 1];
+          moved = true;
+        }
+        g_ord[q][b] = v;
+      }
+      g_moved[q] = moved;
+      if (!moved || kp == 0) continue;  // unpopped tokens: order only
+      if (neff == kTieEff || used + kp > kTieX) {
+        s_bad = 1;
+        break;
+      }
+      for (int32_t j = 0; j < kp; j++) {
+        sig_sm[used + j] = make_int2(lab[j], lab[g_ord[q][j]]);
+        mask_sm[(lab[j] >> 5) & 31] |= 1u << (lab[j] & 31);
+      }
+      e_sm[neff] = make_int4(R, R + kp, used, kp);
+      neff++;
+      used += kp;
+    }
+    s_neff = neff;
+    s_used = used;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (t == 0) {
+      tie_cnt[s] = 0;
+      *overflow = 1;
+    }
+    if (t < 32) tie_mask[(int64_t)s * 32 + t] = 0;
+    return;
+  }
+  if (t < cnt && g_moved[t]) {  // re-sorted tokens
+    const int32_t a = g_a[t];
+    for (int32_t j = 0; j < g_k[t]; j++) tvals[base + a + j] = (uint32_t)g_cr[t][g_ord[t][j]];
+  }
+  for (int32_t q = t; q < s_neff; q += blockDim.x) tie_eff[(int64_t)s * kTieEff + q] = e_sm[q];
+  for (int32_t q = t; q < s_used; q += blockDim.x) tie_sig[(int64_t)s * kTieX + q] = sig_sm[q];
+  if (t < 32) tie_mask[(int64_t)s * 32 + t] = mask_sm[t];
+  if (t == 0) tie_cnt[s] = s_neff;
 }
 
 // Fallback for tie-heavy runs (more tie groups, relabelled labels or
@@ -2998,10 +3050,10 @@ int run_device(Ctx* ctx, const int64_t* d_ticks, const int32_t* d_model,
         CK(cudaLaunchCooperativeKernel((void*)k_match_coop, grid, dim3(256), args, 0, st));
         kt.end();
       }
-      KL(k_tie_fix, nblk(P, 32), 32, 0, st>>>(ctx->d_sbase, ctx->d_shards, P, ctx->d_tkA,
-                                               ctx->d_tvA, ctx->d_ptrA, ctx->d_tie_cnt,
-                                               ctx->d_tie_list, ctx->d_tie_eff, ctx->d_tie_sig,
-                                               ctx->d_tie_mask, ctx->d_changed));
+      KL(k_tie_fix, P, kTieThreads, 0, st>>>(ctx->d_sbase, ctx->d_shards, P, ctx->d_tkA,
+                                              ctx->d_tvA, ctx->d_ptrA, ctx->d_tie_cnt,
+                                              ctx->d_tie_list, ctx->d_tie_eff, ctx->d_tie_sig,
+                                              ctx->d_tie_mask, ctx->d_changed));
       {  // tie-heavy runs only (returns at once otherwise)
         int bps = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_match_iter, 256, 0);
