@@ -363,6 +363,8 @@ def run_b200(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     dev_ms, batches, launches = 0.0, 0, 0
+    phase_keys = ("ms_ingest", "ms_fresh", "ms_fast", "ms_chain", "ms_expand")
+    phase_sum = dict.fromkeys(phase_keys, 0.0)
     t0 = time.perf_counter()
     w0 = time.time()
     for _ in range(args.steps):
@@ -371,6 +373,8 @@ def run_b200(args, rank, world, local_rank):
         dev_ms += cnt["ms_total"]
         batches += cnt["n_batches"]
         launches += cnt["launches"]
+        for k in phase_keys:
+            phase_sum[k] += cnt[k]
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     clk.window = (w0, time.time())
@@ -378,6 +382,7 @@ def run_b200(args, rank, world, local_rank):
         dist.barrier()
     clk.stop()
     stats = dict(cnt)
+    stats.update({k: v / args.steps for k, v in phase_sum.items()})  # phases: mean over the K steps
     host_outs = {k: v.cpu().numpy() for k, v in outs.items()}
 
     # per-kernel device time: the same K steps again with every launch
